@@ -1,0 +1,303 @@
+/*
+ * tsb_capi.h — C ABI of the B200-native CALVO KV-ingest path (libtsb.so).
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary.  Every entry
+ * point returns a tsb_status; on failure tsb_last_error() (thread-local) holds the message,
+ * worded like the reference's throw sites so the C++ shim (include/tiersim/*.hpp) and the
+ * Python mirror can rethrow the matching error.hpp class.
+ *
+ * Each declaration cites the reference interface it replaces (paths relative to
+ * /root/reference/proj/).  The reference has no device or process boundary (SURVEY.md 0,
+ * 8(b)); the L2->L1 hop it models in engine.cpp:206-207 / :427-446 is the one this ABI
+ * makes real.
+ *
+ * Threading: one host thread per device issues calls; device work is asynchronous on the
+ * caller's stream (a cudaStream_t passed as void*, NULL = legacy default stream) unless the
+ * function says it synchronises.  Objects are not thread-safe (like TierLedger,
+ * engine.hpp:48-52).
+ */
+#ifndef TSB_CAPI_H_
+#define TSB_CAPI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  Mapping to reference exceptions (core/include/tiersim/error.hpp:13-71). */
+typedef enum {
+  TSB_OK = 0,
+  TSB_VALIDATION = 1,       /* ValidationError */
+  TSB_CAPACITY = 2,         /* CapacityError */
+  TSB_MISSING_DEADLINE = 3, /* MissingDeadline */
+  TSB_DEGENERATE_FIT = 4,   /* DegenerateFit */
+  TSB_CUDA = 5,             /* CUDA runtime failure (tiersim::Error) */
+  TSB_UNSUPPORTED = 6       /* shape/option not supported by the kernels */
+} tsb_status;
+
+const char* tsb_last_error(void);
+const char* tsb_version(void);
+/* Number of device kernels this library has launched since load (evidence counter). */
+uint64_t tsb_kernel_launch_count(void);
+
+/* ------------------------------------------------------------------------------------ */
+/* Cluster calibration: field-for-field tiersim::ClusterConfig (types.hpp:82-97).          */
+/* ------------------------------------------------------------------------------------ */
+typedef struct {
+  double network_bandwidth;
+  double pcie_bandwidth;
+  double transfer_base_latency;
+  int64_t l1_capacity;
+  int64_t l2_capacity;
+  int64_t bytes_per_token;
+  int64_t block_size_tokens;
+  double compute_base;
+  double compute_per_token;
+  double compute_quadratic;
+  int32_t allocation_mode; /* 0 Proactive, 1 Reactive (types.hpp:70) */
+  int32_t control_mode;    /* 0 Coupled, 1 Decoupled (types.hpp:71) */
+} tsb_cluster;
+
+/* Defaults of ClusterConfig (types.hpp:83-94). */
+void tsb_cluster_default(tsb_cluster* out);
+/* ClusterConfig::validate (types.cpp:56-71). */
+tsb_status tsb_cluster_validate(const tsb_cluster* c);
+
+/* ------------------------------------------------------------------------------------ */
+/* KV geometry and chunk plan (types.cpp:73-118)                                           */
+/* ------------------------------------------------------------------------------------ */
+typedef struct {
+  int64_t layers;       /* L */
+  int64_t kv_heads;     /* H (all ranks) */
+  int64_t head_dim;     /* D */
+  int64_t dtype_bytes;  /* E (2 = bf16) */
+  int64_t chunk_tokens; /* KVBlock tokens = ClusterConfig::block_size_tokens (256) */
+  int64_t page_tokens;  /* vLLM block_size (16) */
+  int64_t tp_size;      /* KV-head shards; H % tp_size == 0 */
+  int64_t tp_rank;      /* this GPU keeps heads [tp_rank*H/tp_size, (tp_rank+1)*H/tp_size) */
+} tsb_kv_shape;
+
+/* kv_bytes_per_token (types.cpp:113-118): 2*L*H*D*E; VALIDATION if any arg < 1. */
+tsb_status tsb_kv_bytes_per_token(int64_t layers, int64_t kv_heads, int64_t head_dim,
+                                  int64_t dtype_bytes, int64_t* out);
+/* Validates a shape; returns full chunk bytes (L*2*C*H*D*E, the L2 slot size), local page
+ * bytes (one page across all layers, K and V, this rank's heads) and local chunk bytes. */
+tsb_status tsb_kv_shape_info(const tsb_kv_shape* s, int64_t* chunk_bytes,
+                             int64_t* local_page_bytes, int64_t* local_chunk_bytes);
+
+/* Struct-of-arrays queue of tiersim::RequestSpec (types.hpp:52-64). */
+enum { TSB_HAS_DEADLINE = 1, TSB_HAS_MEASURED = 2 };
+typedef struct {
+  const int64_t* id;
+  const double* arrival;
+  const int64_t* context_tokens;
+  const int64_t* query_tokens;
+  const double* cache_hit_ratio;
+  const uint8_t* flags; /* TSB_HAS_DEADLINE | TSB_HAS_MEASURED */
+  const double* deadline;
+  const double* measured_t_load;
+  const double* measured_t_comp;
+} tsb_queue;
+
+/* RequestSpec::validate (types.cpp:40-54) for entry i. */
+tsb_status tsb_request_validate(const tsb_queue* q, int64_t i);
+/* cached_token_count / compute_token_count / derive_block_plan (types.cpp:73-101) for
+ * entry i: the plan is n_blocks full chunks of block_tokens tokens and block_bytes bytes. */
+tsb_status tsb_derive_block_plan(const tsb_queue* q, int64_t i, const tsb_cluster* c,
+                                 int64_t* cached_tokens, int64_t* compute_tokens,
+                                 int64_t* n_blocks, int64_t* block_tokens,
+                                 int64_t* block_bytes);
+
+/* ------------------------------------------------------------------------------------ */
+/* Cost model (cost_model.cpp:14-85)                                                      */
+/* models[4] = {load.slope, load.intercept, comp.slope, comp.intercept}                    */
+/* ------------------------------------------------------------------------------------ */
+void tsb_cost_models_from_config(const tsb_cluster* c, double models[4]);
+double tsb_predict(double slope, double intercept, int64_t tokens);
+tsb_status tsb_fit_linear(int64_t n, const int64_t* tokens, const double* seconds,
+                          double* slope, double* intercept, int* slope_clamped,
+                          int* intercept_clamped);
+/* Scalar host forms for single-request callers (planning arithmetic, not the batched path):
+ * estimate_service_cost (cost_model.cpp:56-71) and priority_key (scheduler.cpp:45-73) of
+ * entry i.  tsb_priority_key returns MISSING_DEADLINE for EDF/LSTF without a deadline. */
+tsb_status tsb_estimate_service_cost(const tsb_queue* q, int64_t i, const double models[4],
+                                     const tsb_cluster* c, double* t_load, double* t_comp);
+tsb_status tsb_priority_key(const tsb_queue* q, int64_t i, int policy, double t_load,
+                            double t_comp, double* primary);
+
+/* ------------------------------------------------------------------------------------ */
+/* Batched scorer + schedule order (K4, K5).                                              */
+/* Replaces estimate_service_cost (cost_model.cpp:56-71), priority_key (scheduler.cpp:45-73) */
+/* and the pick_next drain (scheduler.cpp:75-100): order[k] is the queue index picked k-th. */
+/* ------------------------------------------------------------------------------------ */
+typedef enum {
+  TSB_FIFO = 0,
+  TSB_SJF_PT = 1,
+  TSB_SJF_COST = 2,
+  TSB_EDF = 3,
+  TSB_LSTF = 4
+} tsb_policy; /* PolicyKind order, scheduler.hpp:23 */
+
+/* Device-pointer variant: every array in q and the outputs live in device memory.  Fully
+ * asynchronous on `stream` except for the error check, which needs err_index: pass a host
+ * pointer to get a synchronous check (MISSING_DEADLINE / VALIDATION with the first
+ * offending queue index, as best_request_index would throw at scheduler.cpp:79-84), or
+ * NULL to skip it (errors then surface at the next tsb_scorer_check). order may be NULL. */
+typedef struct tsb_scorer tsb_scorer;
+tsb_status tsb_scorer_create(int device, int64_t capacity, tsb_scorer** out);
+void tsb_scorer_destroy(tsb_scorer* s);
+tsb_status tsb_score_queue_device(tsb_scorer* s, void* stream, int64_t n, const tsb_queue* q,
+                                  int policy, const double models[4], const tsb_cluster* c,
+                                  double* t_load, double* t_comp, double* primary,
+                                  int64_t* order, int64_t* err_index);
+tsb_status tsb_scorer_check(tsb_scorer* s, void* stream, int64_t* err_index);
+/* Host-pointer variant (the drop-in for a CPU caller): copies q in, runs K4+K5, copies
+ * the results out, synchronises.  Any output may be NULL. */
+tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_queue* q,
+                           int policy, const double models[4], const tsb_cluster* c,
+                           double* t_load, double* t_comp, double* primary, int64_t* order);
+
+/* ------------------------------------------------------------------------------------ */
+/* Prefix chunk hasher (K3).  Definition in oracle/tsb_oracle.c (orc_hash_prefix_chunks);   */
+/* the reference's only hash primitive is FNV-1a-64 (engine.cpp:500-534).                   */
+/* Request r owns tokens [offsets[r], offsets[r+1]) and writes floor(len/256) chained chunk */
+/* hashes at out[chunk_offsets[r] ...].                                                     */
+/* ------------------------------------------------------------------------------------ */
+tsb_status tsb_hash_prefix_chunks_device(void* stream, int64_t n_req, const int64_t* offsets,
+                                         const int32_t* tokens, const int64_t* chunk_offsets,
+                                         uint64_t* out);
+/* Host-pointer variant: H2D tokens, hash, D2H hashes, synchronise. */
+tsb_status tsb_hash_prefix_chunks(void* stream, int64_t n_req, const int64_t* offsets,
+                                  const int32_t* tokens, uint64_t* out, int64_t* n_hashes);
+/* Synthetic token ids on device (harness; same generator as orc_gen_tokens). */
+tsb_status tsb_gen_tokens_device(void* stream, uint64_t seed, int64_t n_req,
+                                 const int64_t* offsets, const int64_t* doc,
+                                 const int64_t* shared_len, int32_t* out);
+
+/* ------------------------------------------------------------------------------------ */
+/* L2 chunk pool: pinned, portable, mapped host memory (replaces TierLedger(L2) as a byte   */
+/* store; engine.cpp:18-49 stays the accounting).  Slot s holds one full chunk             */
+/* [L][2][C][H][D] at host address base + s*chunk_bytes.                                   */
+/* ------------------------------------------------------------------------------------ */
+typedef struct tsb_pool tsb_pool;
+tsb_status tsb_pool_create(const tsb_kv_shape* shape, int64_t n_slots, tsb_pool** out);
+/* Adopt caller-owned memory instead (must be page-locked, e.g. cudaHostRegister'ed). */
+tsb_status tsb_pool_wrap(const tsb_kv_shape* shape, void* host_base, int64_t n_slots,
+                         tsb_pool** out);
+void tsb_pool_destroy(tsb_pool* p);
+void* tsb_pool_slot_ptr(tsb_pool* p, int64_t slot);
+int64_t tsb_pool_slots(const tsb_pool* p);
+int64_t tsb_pool_chunk_bytes(const tsb_pool* p);
+/* Harness: fill slots [first, first+n) with the synthetic bf16 pattern (orc_synth_word)
+ * from a device kernel writing through the mapped pointer; synchronises. */
+tsb_status tsb_pool_fill_synthetic(tsb_pool* p, uint64_t seed, int64_t first, int64_t n,
+                                   void* stream);
+
+/* ------------------------------------------------------------------------------------ */
+/* L1 paged allocator + block_table.                                                        */
+/* Byte accounting is exactly TierLedger (engine.cpp:18-49): a chunk reservation is        */
+/* granted iff no older reservation waits and it fits, else deferred; releases grant FIFO. */
+/* Capacity = num_pages * local_page_bytes.  On grant the chunk's pages are taken from a   */
+/* FIFO free list and written into block_table[row(request)][chunk*pages_per_chunk + j].   */
+/* The KV arena is per layer [2][num_pages][page_tokens][H_local][D] (vLLM flash-attn).     */
+/* ------------------------------------------------------------------------------------ */
+typedef struct tsb_l1 tsb_l1;
+typedef struct {
+  int64_t request_id;
+  int32_t block_index;
+  int32_t bt_row; /* -1 for the standalone byte ledger */
+  int64_t bytes;
+} tsb_grant;
+
+/* Standalone byte ledger: TierLedger (engine.hpp:22-53) with identical decisions and messages;
+ * the L1 allocator below runs the same ledger object.  tier: 0 L3, 1 L2, 2 L1. */
+typedef struct tsb_ledger tsb_ledger;
+tsb_status tsb_ledger_create(int tier, int64_t capacity, tsb_ledger** out);
+void tsb_ledger_destroy(tsb_ledger* l);
+tsb_status tsb_ledger_request(tsb_ledger* l, int64_t request_id, int32_t block_index,
+                              int64_t bytes, int* granted);
+/* TierLedger::release: grants are written to out[0..min(n,cap)). */
+tsb_status tsb_ledger_release(tsb_ledger* l, int64_t bytes, tsb_grant* out, int64_t cap,
+                              int64_t* n);
+int64_t tsb_ledger_reserved(const tsb_ledger* l);
+int64_t tsb_ledger_capacity(const tsb_ledger* l);
+int64_t tsb_ledger_deferred(const tsb_ledger* l);
+
+/* arena: device pointer of L*2*num_pages*page_tokens*H_local*D*E bytes, or NULL to allocate
+ * internally.  max_rows = concurrent requests; max_chunks = chunk columns per row. */
+tsb_status tsb_l1_create(int device, const tsb_kv_shape* shape, int64_t num_pages,
+                         int64_t max_rows, int64_t max_chunks, void* arena, tsb_l1** out);
+void tsb_l1_destroy(tsb_l1* l1);
+/* TierLedger::request (engine.cpp:22-36).  bytes must be a whole number of local pages
+ * (a chunk: chunk_tokens * local bytes/token).  *granted = 1 when granted now; *bt_row gets
+ * the request's block_table row (assigned at its first reservation). */
+tsb_status tsb_l1_request(tsb_l1* l1, int64_t request_id, int32_t block_index, int64_t bytes,
+                          int* granted, int32_t* bt_row);
+/* Releases every page of a request (ComputeDone release, engine.cpp:280-282) and grants
+ * waiting reservations FIFO while they fit (TierLedger::release, engine.cpp:38-49).  The
+ * grants are written to out[0..min(n,cap)). */
+tsb_status tsb_l1_release_request(tsb_l1* l1, int64_t request_id, tsb_grant* out, int64_t cap,
+                                  int64_t* n);
+int64_t tsb_l1_reserved(const tsb_l1* l1);
+int64_t tsb_l1_capacity(const tsb_l1* l1);
+int64_t tsb_l1_deferred(const tsb_l1* l1);
+int64_t tsb_l1_free_pages(const tsb_l1* l1);
+int64_t tsb_l1_num_pages(const tsb_l1* l1);
+int64_t tsb_l1_page_bytes(const tsb_l1* l1);
+void* tsb_l1_arena(tsb_l1* l1);
+void* tsb_l1_layer_ptr(tsb_l1* l1, int64_t layer);
+/* Host (pinned) mirror of the block table, [max_rows][max_chunks*pages_per_chunk] int32,
+ * -1 = unassigned, and its device copy. */
+const int32_t* tsb_l1_block_table_host(const tsb_l1* l1);
+const int32_t* tsb_l1_block_table_device(const tsb_l1* l1);
+int64_t tsb_l1_block_table_stride(const tsb_l1* l1);
+/* Copies the host block table to the device copy on `stream` (async). */
+tsb_status tsb_l1_sync_block_table(tsb_l1* l1, void* stream);
+
+/* ------------------------------------------------------------------------------------ */
+/* L2 -> L1 ingest (K1 / CE+K2).  The real pcie_dispatch hop (engine.cpp:427-446, duration  */
+/* model engine.cpp:206-207).  One call moves every (item, layer in [layer_lo, layer_hi))   */
+/* of the batch; `done_event` (cudaEvent_t as void*, may be NULL) is recorded after it.     */
+/* ------------------------------------------------------------------------------------ */
+typedef struct {
+  int64_t src_slot;    /* L2 pool slot holding the chunk */
+  int32_t bt_row;      /* block_table row of the owning request */
+  int32_t chunk_index; /* KVBlock::block_index within the request */
+} tsb_ingest_item;
+
+typedef enum {
+  TSB_INGEST_AUTO = 0,     /* best measured mode for the shape */
+  TSB_INGEST_ZEROCOPY = 1, /* K1: SM 16B loads from mapped host memory, scatter to pages */
+  TSB_INGEST_BULK = 2,     /* K1b: cp.async.bulk host->smem->pages, one issuing lane/CTA */
+  TSB_INGEST_CE = 3        /* copy-engine H2D into an HBM staging ring, then K2 scatter */
+} tsb_ingest_mode;
+
+/* items: host array (copied into a pinned ring internally, so it may be reused on return).
+ * All grants for the items must already be in the block table (tsb_l1_sync_block_table). */
+tsb_status tsb_ingest(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
+                      int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
+                      void* done_event);
+/* Device-items variant (items already in device memory). */
+tsb_status tsb_ingest_device(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items_dev,
+                             int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
+                             void* stream, void* done_event);
+/* K2 alone: scatter chunks already staged contiguously in HBM (src_slot indexes `staging`,
+ * each slot = one full chunk, layers [layer_lo, layer_hi) only). */
+tsb_status tsb_scatter_device(tsb_l1* l1, const void* staging, const tsb_ingest_item* items_dev,
+                              int64_t n_items, int64_t layer_lo, int64_t layer_hi, void* stream);
+/* Tuning knobs for measurement (0 = default). */
+tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas);
+
+/* Harness check: counts bytes of the items' pages (layers [lo,hi)) that differ from the
+ * synthetic pattern of their source slot (as filled by tsb_pool_fill_synthetic with `seed`);
+ * synchronises. */
+tsb_status tsb_l1_verify_synthetic(tsb_l1* l1, const tsb_ingest_item* items, int64_t n_items,
+                                   int64_t layer_lo, int64_t layer_hi, uint64_t seed,
+                                   int64_t pool_chunk_bytes, void* stream, uint64_t* mismatches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

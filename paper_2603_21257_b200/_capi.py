@@ -1,0 +1,158 @@
+"""ctypes binding of libtsb.so (include/tsb_capi.h).
+
+This is the reference-side binding a Python caller would add (INTEGRATION.md shows the same
+declarations); every higher-level module in the package goes through it.  There is no
+fallback: importing the package without the built library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("TSB_LIB", _HERE / "libtsb.so"))
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"libtsb.so not found at {LIB_PATH}: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "or `make -C paper_2603_21257_b200` (no CPU fallback exists)."
+    )
+
+lib = C.CDLL(str(LIB_PATH))
+
+# ---- status -------------------------------------------------------------------------------
+TSB_OK, TSB_VALIDATION, TSB_CAPACITY, TSB_MISSING_DEADLINE, TSB_DEGENERATE_FIT, TSB_CUDA, TSB_UNSUPPORTED = range(7)
+
+i64, u64, f64, i32, u8 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint8
+P = C.POINTER
+vp = C.c_void_p
+
+
+class Cluster(C.Structure):
+    """tsb_cluster == tiersim::ClusterConfig (types.hpp:82-97)."""
+
+    _fields_ = [
+        ("network_bandwidth", f64),
+        ("pcie_bandwidth", f64),
+        ("transfer_base_latency", f64),
+        ("l1_capacity", i64),
+        ("l2_capacity", i64),
+        ("bytes_per_token", i64),
+        ("block_size_tokens", i64),
+        ("compute_base", f64),
+        ("compute_per_token", f64),
+        ("compute_quadratic", f64),
+        ("allocation_mode", i32),
+        ("control_mode", i32),
+    ]
+
+
+class KvShape(C.Structure):
+    _fields_ = [
+        ("layers", i64),
+        ("kv_heads", i64),
+        ("head_dim", i64),
+        ("dtype_bytes", i64),
+        ("chunk_tokens", i64),
+        ("page_tokens", i64),
+        ("tp_size", i64),
+        ("tp_rank", i64),
+    ]
+
+
+class Queue(C.Structure):
+    """tsb_queue: struct-of-arrays RequestSpec queue (pointers may be host or device)."""
+
+    _fields_ = [
+        ("id", vp),
+        ("arrival", vp),
+        ("context_tokens", vp),
+        ("query_tokens", vp),
+        ("cache_hit_ratio", vp),
+        ("flags", vp),
+        ("deadline", vp),
+        ("measured_t_load", vp),
+        ("measured_t_comp", vp),
+    ]
+
+
+class Grant(C.Structure):
+    _fields_ = [("request_id", i64), ("block_index", i32), ("bt_row", i32), ("bytes", i64)]
+
+
+class IngestItem(C.Structure):
+    _fields_ = [("src_slot", i64), ("bt_row", i32), ("chunk_index", i32)]
+
+
+HAS_DEADLINE, HAS_MEASURED = 1, 2
+INGEST_AUTO, INGEST_ZEROCOPY, INGEST_BULK, INGEST_CE = range(4)
+
+
+def _decl(name, restype, *argtypes):
+    f = getattr(lib, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+    return f
+
+
+st = C.c_int
+_decl("tsb_last_error", C.c_char_p)
+_decl("tsb_version", C.c_char_p)
+_decl("tsb_kernel_launch_count", u64)
+_decl("tsb_cluster_default", None, P(Cluster))
+_decl("tsb_cluster_validate", st, P(Cluster))
+_decl("tsb_kv_bytes_per_token", st, i64, i64, i64, i64, P(i64))
+_decl("tsb_kv_shape_info", st, P(KvShape), P(i64), P(i64), P(i64))
+_decl("tsb_request_validate", st, P(Queue), i64)
+_decl("tsb_derive_block_plan", st, P(Queue), i64, P(Cluster), P(i64), P(i64), P(i64), P(i64), P(i64))
+_decl("tsb_cost_models_from_config", None, P(Cluster), P(f64))
+_decl("tsb_predict", f64, f64, f64, i64)
+_decl("tsb_fit_linear", st, i64, vp, vp, P(f64), P(f64), P(C.c_int), P(C.c_int))
+_decl("tsb_estimate_service_cost", st, P(Queue), i64, P(f64), P(Cluster), P(f64), P(f64))
+_decl("tsb_priority_key", st, P(Queue), i64, C.c_int, f64, f64, P(f64))
+_decl("tsb_scorer_create", st, C.c_int, i64, P(vp))
+_decl("tsb_scorer_destroy", None, vp)
+_decl("tsb_score_queue_device", st, vp, vp, i64, P(Queue), C.c_int, P(f64), P(Cluster), vp, vp, vp, vp, P(i64))
+_decl("tsb_scorer_check", st, vp, vp, P(i64))
+_decl("tsb_score_queue", st, vp, vp, i64, P(Queue), C.c_int, P(f64), P(Cluster), vp, vp, vp, vp)
+_decl("tsb_hash_prefix_chunks_device", st, vp, i64, vp, vp, vp, vp)
+_decl("tsb_hash_prefix_chunks", st, vp, i64, vp, vp, vp, P(i64))
+_decl("tsb_gen_tokens_device", st, vp, u64, i64, vp, vp, vp, vp)
+_decl("tsb_pool_create", st, P(KvShape), i64, P(vp))
+_decl("tsb_pool_wrap", st, P(KvShape), vp, i64, P(vp))
+_decl("tsb_pool_destroy", None, vp)
+_decl("tsb_pool_slot_ptr", vp, vp, i64)
+_decl("tsb_pool_slots", i64, vp)
+_decl("tsb_pool_chunk_bytes", i64, vp)
+_decl("tsb_pool_fill_synthetic", st, vp, u64, i64, i64, vp)
+_decl("tsb_ledger_create", st, C.c_int, i64, P(vp))
+_decl("tsb_ledger_destroy", None, vp)
+_decl("tsb_ledger_request", st, vp, i64, i32, i64, P(C.c_int))
+_decl("tsb_ledger_release", st, vp, i64, P(Grant), i64, P(i64))
+for _n in ("reserved", "capacity", "deferred"):
+    _decl(f"tsb_ledger_{_n}", i64, vp)
+_decl("tsb_l1_create", st, C.c_int, P(KvShape), i64, i64, i64, vp, P(vp))
+_decl("tsb_l1_destroy", None, vp)
+_decl("tsb_l1_request", st, vp, i64, i32, i64, P(C.c_int), P(i32))
+_decl("tsb_l1_release_request", st, vp, i64, P(Grant), i64, P(i64))
+for _n in ("reserved", "capacity", "deferred", "free_pages", "num_pages", "page_bytes", "block_table_stride"):
+    _decl(f"tsb_l1_{_n}", i64, vp)
+_decl("tsb_l1_arena", vp, vp)
+_decl("tsb_l1_layer_ptr", vp, vp, i64)
+_decl("tsb_l1_block_table_host", vp, vp)
+_decl("tsb_l1_block_table_device", vp, vp)
+_decl("tsb_l1_sync_block_table", st, vp, vp)
+_decl("tsb_ingest", st, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, vp)
+_decl("tsb_ingest_device", st, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp)
+_decl("tsb_scatter_device", st, vp, vp, vp, i64, i64, i64, vp)
+_decl("tsb_ingest_set_grid", st, C.c_int, C.c_int, C.c_int)
+_decl("tsb_l1_verify_synthetic", st, vp, P(IngestItem), i64, i64, i64, u64, i64, vp, P(u64))
+
+EXPORTED = sorted(
+    n for n in dir(lib) if n.startswith("tsb_")
+)  # populated lazily by ctypes; tests read the header instead
+
+
+def last_error() -> str:
+    return lib.tsb_last_error().decode()

@@ -1,0 +1,641 @@
+// capi_ingest.cpp — C ABI: L2 pinned chunk pool, L1 paged allocator + block_table, and the
+// L2->L1 ingest launcher (K1 zero-copy / K1b bulk / CE + K2 scatter).
+//
+// The L1 allocator keeps TierLedger's byte semantics exactly (engine.cpp:18-49): reservations
+// are granted iff nothing older waits and they fit; release grants the waiting queue strictly
+// FIFO while reservations fit.  What the reference cannot express -- WHICH memory a grant
+// gets -- is a FIFO free list of page ids (restated as alloc_ref in oracle/tsb_oracle.c) and a
+// per-request block_table row, mirrored in pinned host memory and copied to the device by
+// dirty row ranges.
+//
+// Block-table protocol: rows are only rewritten by grants (-1 -> page) while a request is
+// live, and cleared by release, which the caller issues only after the request's device work
+// has completed (the reference releases L1 at ComputeDone, engine.cpp:280-282).  Therefore an
+// in-flight async copy of a row can never hand a kernel a stale page id.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "ledger.h"
+
+using tsb::fail;
+
+namespace {
+
+struct Knobs {
+  int zerocopy_ctas = 32;
+  int bulk_ctas = 16;
+  int scatter_ctas = 148 * 4;
+};
+Knobs g_knobs;
+
+// Small pinned->device upload ring for item lists (16 slots; each slot reused only after the
+// event recorded behind its consumer has completed).
+struct UploadRing {
+  static constexpr int kSlots = 16;
+  static constexpr size_t kSlotBytes = 4u << 20;
+  uint8_t* host = nullptr;
+  uint8_t* dev = nullptr;
+  cudaEvent_t ev[kSlots] = {};
+  bool used[kSlots] = {};
+  int next = 0;
+
+  tsb_status init() {
+    TSB_CUDA_TRY(cudaMallocHost(&host, kSlots * kSlotBytes));
+    TSB_CUDA_TRY(cudaMalloc(&dev, kSlots * kSlotBytes));
+    for (auto& e : ev) TSB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return TSB_OK;
+  }
+  void destroy() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    cudaFreeHost(host);
+    cudaFree(dev);
+  }
+  // Copies `bytes` (<= kSlotBytes) to a device slot on `st`; returns its device address.
+  tsb_status stage(const void* src, size_t bytes, cudaStream_t st, void** dptr, int* slot) {
+    const int s = next;
+    next = (next + 1) % kSlots;
+    if (used[s]) TSB_CUDA_TRY(cudaEventSynchronize(ev[s]));
+    std::memcpy(host + s * kSlotBytes, src, bytes);
+    TSB_CUDA_TRY(cudaMemcpyAsync(dev + s * kSlotBytes, host + s * kSlotBytes, bytes,
+                                 cudaMemcpyHostToDevice, st));
+    *dptr = dev + s * kSlotBytes;
+    *slot = s;
+    return TSB_OK;
+  }
+  tsb_status fence(int slot, cudaStream_t st) {
+    used[slot] = true;
+    TSB_CUDA_TRY(cudaEventRecord(ev[slot], st));
+    return TSB_OK;
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// L2 pool
+// ---------------------------------------------------------------------------------------
+struct tsb_pool {
+  tsb_kv_shape shape{};
+  uint8_t* host = nullptr;  // host address
+  uint8_t* dev = nullptr;   // device (UVA) alias of the same memory
+  int64_t slots = 0;
+  int64_t chunk_bytes = 0;
+  bool owned = false;
+};
+
+extern "C" {
+
+tsb_status tsb_pool_create(const tsb_kv_shape* shape, int64_t n_slots, tsb_pool** out) {
+  int64_t cb = 0;
+  TSB_TRY(tsb_kv_shape_info(shape, &cb, nullptr, nullptr));
+  if (n_slots < 1) return fail(TSB_VALIDATION, "pool: n_slots must be >= 1");
+  auto* p = new tsb_pool();
+  p->shape = *shape;
+  p->slots = n_slots;
+  p->chunk_bytes = cb;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p->host),
+                                static_cast<size_t>(cb) * n_slots,
+                                cudaHostAllocPortable | cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->dev), p->host, 0);
+  if (e != cudaSuccess) {
+    if (p->host) cudaFreeHost(p->host);
+    delete p;
+    return tsb::cuda_fail(e, "tsb_pool_create (cudaHostAlloc portable|mapped)");
+  }
+  p->owned = true;
+  *out = p;
+  return TSB_OK;
+}
+
+tsb_status tsb_pool_wrap(const tsb_kv_shape* shape, void* host_base, int64_t n_slots,
+                         tsb_pool** out) {
+  int64_t cb = 0;
+  TSB_TRY(tsb_kv_shape_info(shape, &cb, nullptr, nullptr));
+  auto* p = new tsb_pool();
+  p->shape = *shape;
+  p->slots = n_slots;
+  p->chunk_bytes = cb;
+  p->host = static_cast<uint8_t*>(host_base);
+  cudaError_t e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->dev), host_base, 0);
+  if (e != cudaSuccess) {
+    delete p;
+    return tsb::cuda_fail(e, "tsb_pool_wrap (memory must be page-locked and mapped)");
+  }
+  *out = p;
+  return TSB_OK;
+}
+
+void tsb_pool_destroy(tsb_pool* p) {
+  if (!p) return;
+  if (p->owned) cudaFreeHost(p->host);
+  delete p;
+}
+
+void* tsb_pool_slot_ptr(tsb_pool* p, int64_t slot) { return p->host + slot * p->chunk_bytes; }
+int64_t tsb_pool_slots(const tsb_pool* p) { return p->slots; }
+int64_t tsb_pool_chunk_bytes(const tsb_pool* p) { return p->chunk_bytes; }
+
+tsb_status tsb_pool_fill_synthetic(tsb_pool* p, uint64_t seed, int64_t first, int64_t n,
+                                   void* stream) {
+  if (first < 0 || n < 0 || first + n > p->slots)
+    return fail(TSB_VALIDATION, "pool_fill_synthetic: slot range out of bounds");
+  auto st = static_cast<cudaStream_t>(stream);
+  const uint64_t w0 = static_cast<uint64_t>(first) * p->chunk_bytes / 8;
+  const uint64_t nw = static_cast<uint64_t>(n) * p->chunk_bytes / 8;
+  auto* dst = reinterpret_cast<uint64_t*>(p->dev + first * p->chunk_bytes);
+  TSB_CUDA_TRY(tsb::launch_fill_synth(dst, w0, nw, seed, st));
+  TSB_CUDA_TRY(cudaStreamSynchronize(st));
+  return TSB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// L1 paged allocator
+// ---------------------------------------------------------------------------------------
+struct tsb_l1 {
+  int device = 0;
+  tsb_kv_shape shape{};
+  int64_t num_pages = 0;
+  int64_t page_bytes = 0;  // local bytes of one page across all layers (K and V)
+  int64_t ppc = 0;         // pages per chunk
+  tsb::Ledger ledger{2, 1};  // TierLedger(L1) byte accounting; capacity = pages * page_bytes
+  // FIFO free list of page ids
+  std::vector<int32_t> ring;
+  int64_t head = 0, free_len = 0;
+  // block table
+  int64_t rows = 0, max_chunks = 0, stride = 0;
+  int32_t* bt_host = nullptr;
+  int32_t* bt_dev = nullptr;
+  std::vector<uint8_t> row_dirty;
+  std::unordered_map<int64_t, int32_t> row_of;
+  std::vector<int32_t> free_rows;
+  std::vector<std::vector<int32_t>> row_pages;  // pages held per row, grant order
+  std::vector<int64_t> row_bytes;
+  std::vector<int64_t> row_waiting;  // deferred reservations per row
+  // arena
+  uint8_t* arena = nullptr;
+  bool arena_owned = false;
+  int64_t layer_bytes = 0;
+  // ingest state
+  UploadRing ring_items;
+  uint8_t* staging = nullptr;  // CE staging (lazy)
+  int64_t staging_bytes = 0;
+  cudaStream_t ce_stream = nullptr;
+  cudaEvent_t ev_ce[2] = {};
+  cudaEvent_t ev_k2[2] = {};
+  bool k2_used[2] = {};
+  unsigned long long* verify_ctr = nullptr;
+};
+
+namespace {
+
+void l1_free(tsb_l1* l) {
+  if (!l) return;
+  l->ring_items.destroy();
+  if (l->arena_owned) cudaFree(l->arena);
+  cudaFreeHost(l->bt_host);
+  cudaFree(l->bt_dev);
+  cudaFree(l->staging);
+  cudaFree(l->verify_ctr);
+  for (auto& e : l->ev_ce)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : l->ev_k2)
+    if (e) cudaEventDestroy(e);
+  if (l->ce_stream) cudaStreamDestroy(l->ce_stream);
+}
+
+// Grants one reservation: takes pages from the free-list front into the block table row.
+void grant(tsb_l1* l, int32_t block_index, int64_t bytes, int32_t row) {
+  const int64_t n = bytes / l->page_bytes;
+  int32_t* dst = l->bt_host + row * l->stride + static_cast<int64_t>(block_index) * l->ppc;
+  const int64_t cap = static_cast<int64_t>(l->ring.size());
+  for (int64_t k = 0; k < n; ++k) {
+    const int32_t page = l->ring[(l->head + k) % cap];
+    dst[k] = page;
+    l->row_pages[row].push_back(page);
+  }
+  l->head = (l->head + n) % cap;
+  l->free_len -= n;
+  l->row_bytes[row] += bytes;
+  l->row_dirty[row] = 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+tsb_status tsb_l1_create(int device, const tsb_kv_shape* shape, int64_t num_pages,
+                         int64_t max_rows, int64_t max_chunks, void* arena, tsb_l1** out) {
+  int64_t cb = 0, pb = 0, lcb = 0;
+  TSB_TRY(tsb_kv_shape_info(shape, &cb, &pb, &lcb));
+  if (num_pages < 1 || num_pages > INT32_MAX)
+    return fail(TSB_VALIDATION, "l1: num_pages must be in [1, 2^31)");
+  if (max_rows < 1 || max_chunks < 1) return fail(TSB_VALIDATION, "l1: max_rows/max_chunks must be >= 1");
+  TSB_CUDA_TRY(cudaSetDevice(device));
+  auto* l = new tsb_l1();
+  l->device = device;
+  l->shape = *shape;
+  l->num_pages = num_pages;
+  l->page_bytes = pb;
+  l->ppc = shape->chunk_tokens / shape->page_tokens;
+  l->ledger = tsb::Ledger(2, num_pages * pb);
+  l->ring.resize(static_cast<size_t>(num_pages));
+  for (int64_t i = 0; i < num_pages; ++i) l->ring[i] = static_cast<int32_t>(i);
+  l->free_len = num_pages;
+  l->rows = max_rows;
+  l->max_chunks = max_chunks;
+  l->stride = max_chunks * l->ppc;
+  l->row_dirty.assign(static_cast<size_t>(max_rows), 0);
+  l->row_pages.resize(static_cast<size_t>(max_rows));
+  l->row_bytes.assign(static_cast<size_t>(max_rows), 0);
+  l->row_waiting.assign(static_cast<size_t>(max_rows), 0);
+  for (int64_t r = max_rows - 1; r >= 0; --r) l->free_rows.push_back(static_cast<int32_t>(r));
+  const int64_t Hl = shape->kv_heads / shape->tp_size;
+  l->layer_bytes = 2 * num_pages * shape->page_tokens * Hl * shape->head_dim * shape->dtype_bytes;
+  const size_t bt_bytes = sizeof(int32_t) * static_cast<size_t>(max_rows * l->stride);
+  cudaError_t e = cudaMallocHost(&l->bt_host, bt_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&l->bt_dev, bt_bytes);
+  if (e == cudaSuccess) {
+    std::memset(l->bt_host, 0xff, bt_bytes);
+    e = cudaMemset(l->bt_dev, 0xff, bt_bytes);
+  }
+  if (e == cudaSuccess && arena == nullptr) {
+    e = cudaMalloc(&l->arena, static_cast<size_t>(l->layer_bytes) * shape->layers);
+    l->arena_owned = e == cudaSuccess;
+  } else {
+    l->arena = static_cast<uint8_t*>(arena);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&l->verify_ctr, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    l1_free(l);
+    delete l;
+    return tsb::cuda_fail(e, "tsb_l1_create");
+  }
+  tsb_status st = l->ring_items.init();
+  if (st != TSB_OK) {
+    l1_free(l);
+    delete l;
+    return st;
+  }
+  *out = l;
+  return TSB_OK;
+}
+
+void tsb_l1_destroy(tsb_l1* l) {
+  l1_free(l);
+  delete l;
+}
+
+// TierLedger::request (engine.cpp:22-36) at page granularity.
+tsb_status tsb_l1_request(tsb_l1* l, int64_t request_id, int32_t block_index, int64_t bytes,
+                          int* granted, int32_t* bt_row) {
+  std::string msg;
+  if (bytes > 0 && bytes <= l->ledger.capacity()) {
+    if (bytes % l->page_bytes != 0)
+      return fail(TSB_VALIDATION, "l1: reservation of " + std::to_string(bytes) +
+                                      " bytes is not a whole number of " +
+                                      std::to_string(l->page_bytes) + "-byte pages");
+    const int64_t n_pages = bytes / l->page_bytes;
+    if (block_index < 0 || (static_cast<int64_t>(block_index) * l->ppc + n_pages) > l->stride)
+      return fail(TSB_VALIDATION, "l1: block_index " + std::to_string(block_index) +
+                                      " outside the block_table row (" +
+                                      std::to_string(l->max_chunks) + " chunks)");
+    if (!l->row_of.count(request_id) && l->free_rows.empty())
+      return fail(TSB_CAPACITY, "l1: block_table has no free row for request " +
+                                    std::to_string(request_id));
+  }
+  bool ok = false;
+  const tsb_status st = l->ledger.request(request_id, block_index, bytes, &ok, &msg);
+  if (st != TSB_OK) return fail(st, msg);
+  int32_t row;
+  auto it = l->row_of.find(request_id);
+  if (it != l->row_of.end()) {
+    row = it->second;
+  } else {
+    row = l->free_rows.back();
+    l->free_rows.pop_back();
+    l->row_of.emplace(request_id, row);
+  }
+  if (bt_row) *bt_row = row;
+  if (ok) {
+    grant(l, block_index, bytes, row);
+  } else {
+    l->row_waiting[row] += 1;
+  }
+  *granted = ok ? 1 : 0;
+  return TSB_OK;
+}
+
+// ComputeDone release (engine.cpp:280-282) + TierLedger::release FIFO grants (:38-49).
+tsb_status tsb_l1_release_request(tsb_l1* l, int64_t request_id, tsb_grant* out, int64_t cap,
+                                  int64_t* n) {
+  *n = 0;
+  auto it = l->row_of.find(request_id);
+  if (it == l->row_of.end())
+    return fail(TSB_VALIDATION, "TierLedger: releasing more than reserved (request " +
+                                    std::to_string(request_id) + " holds nothing)");
+  const int32_t row = it->second;
+  if (l->row_waiting[row] > 0)
+    return fail(TSB_VALIDATION, "l1: request " + std::to_string(request_id) +
+                                    " still has deferred reservations");
+  // Return pages to the back of the free list in grant order.
+  const int64_t ringcap = static_cast<int64_t>(l->ring.size());
+  for (int32_t page : l->row_pages[row]) {
+    l->ring[(l->head + l->free_len) % ringcap] = page;
+    ++l->free_len;
+  }
+  const int64_t bytes = l->row_bytes[row];
+  l->row_pages[row].clear();
+  l->row_bytes[row] = 0;
+  std::fill(l->bt_host + row * l->stride, l->bt_host + (row + 1) * l->stride, -1);
+  l->row_dirty[row] = 1;
+  l->row_of.erase(it);
+  l->free_rows.push_back(row);
+  std::string msg;
+  const tsb_status st = l->ledger.release(
+      bytes,
+      [&](const tsb::Ledger::Pending& p) {
+        const int32_t prow = l->row_of.at(p.request_id);
+        l->row_waiting[prow] -= 1;
+        grant(l, p.block_index, p.bytes, prow);
+        if (*n < cap) out[*n] = tsb_grant{p.request_id, p.block_index, prow, p.bytes};
+        ++*n;
+      },
+      &msg);
+  if (st != TSB_OK) return fail(st, msg);
+  return TSB_OK;
+}
+
+int64_t tsb_l1_reserved(const tsb_l1* l) { return l->ledger.reserved(); }
+int64_t tsb_l1_capacity(const tsb_l1* l) { return l->ledger.capacity(); }
+int64_t tsb_l1_deferred(const tsb_l1* l) { return l->ledger.deferred(); }
+int64_t tsb_l1_free_pages(const tsb_l1* l) { return l->free_len; }
+int64_t tsb_l1_num_pages(const tsb_l1* l) { return l->num_pages; }
+int64_t tsb_l1_page_bytes(const tsb_l1* l) { return l->page_bytes; }
+void* tsb_l1_arena(tsb_l1* l) { return l->arena; }
+void* tsb_l1_layer_ptr(tsb_l1* l, int64_t layer) { return l->arena + layer * l->layer_bytes; }
+const int32_t* tsb_l1_block_table_host(const tsb_l1* l) { return l->bt_host; }
+const int32_t* tsb_l1_block_table_device(const tsb_l1* l) { return l->bt_dev; }
+int64_t tsb_l1_block_table_stride(const tsb_l1* l) { return l->stride; }
+
+tsb_status tsb_l1_sync_block_table(tsb_l1* l, void* stream) {
+  auto st = static_cast<cudaStream_t>(stream);
+  int64_t r = 0;
+  while (r < l->rows) {
+    if (!l->row_dirty[r]) {
+      ++r;
+      continue;
+    }
+    int64_t e = r;
+    while (e < l->rows && l->row_dirty[e]) l->row_dirty[e++] = 0;
+    TSB_CUDA_TRY(cudaMemcpyAsync(l->bt_dev + r * l->stride, l->bt_host + r * l->stride,
+                                 sizeof(int32_t) * (e - r) * l->stride, cudaMemcpyHostToDevice,
+                                 st));
+    r = e;
+  }
+  return TSB_OK;
+}
+
+tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas) {
+  g_knobs.zerocopy_ctas = zerocopy_ctas > 0 ? zerocopy_ctas : 32;
+  g_knobs.bulk_ctas = bulk_ctas > 0 ? bulk_ctas : 16;
+  g_knobs.scatter_ctas = scatter_ctas > 0 ? scatter_ctas : 148 * 4;
+  return TSB_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+tsb::IngestGeom make_geom(const tsb_l1* l, int64_t layer_lo, int64_t layer_hi) {
+  const tsb_kv_shape& s = l->shape;
+  tsb::IngestGeom g{};
+  const int64_t Hl = s.kv_heads / s.tp_size;
+  g.row = s.kv_heads * s.head_dim * s.dtype_bytes;
+  g.run = Hl * s.head_dim * s.dtype_bytes;
+  g.head_off = s.tp_rank * g.run;
+  g.chunk_bytes = s.layers * 2 * s.chunk_tokens * g.row;
+  g.kv_src = s.chunk_tokens * g.row;
+  g.layer_src = 2 * g.kv_src;
+  g.P = s.page_tokens;
+  g.ppc = l->ppc;
+  g.seg_bytes = g.P * g.run;
+  g.num_pages = l->num_pages;
+  g.kv_dst = l->num_pages * g.seg_bytes;
+  g.layer_dst = 2 * g.kv_dst;
+  g.bt_stride = l->stride;
+  g.layer_lo = static_cast<int32_t>(layer_lo);
+  g.n_layers = static_cast<int32_t>(layer_hi - layer_lo);
+  g.staged = 0;
+  g.item_stride = 0;
+  return g;
+}
+
+int resolve_mode(const tsb_l1* l, int mode) {
+  if (mode != TSB_INGEST_AUTO) return mode;
+  return TSB_INGEST_BULK;
+}
+
+tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
+                     const tsb_ingest_item* items_host, int64_t n_items, int64_t lo, int64_t hi,
+                     cudaStream_t st) {
+  if (l->shape.tp_size != 1)
+    return fail(TSB_UNSUPPORTED, "ingest CE mode copies whole chunks; use zerocopy/bulk when tp_size > 1");
+  if (!items_host)
+    return fail(TSB_UNSUPPORTED, "ingest CE mode needs host-visible items (use tsb_ingest)");
+  tsb::IngestGeom g = make_geom(l, lo, hi);
+  const int64_t item_bytes = (hi - lo) * g.layer_src;
+  if (!l->staging) {
+    l->staging_bytes = std::max<int64_t>(256ll << 20, 4 * g.chunk_bytes);
+    TSB_CUDA_TRY(cudaMalloc(&l->staging, l->staging_bytes));
+    TSB_CUDA_TRY(cudaStreamCreateWithFlags(&l->ce_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_ce[b], cudaEventDisableTiming));
+      TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_k2[b], cudaEventDisableTiming));
+    }
+  }
+  const int64_t half = l->staging_bytes / 2;
+  const int64_t per_group = std::max<int64_t>(1, half / item_bytes);
+  if (item_bytes > half) return fail(TSB_UNSUPPORTED, "ingest CE: chunk range exceeds staging");
+  g.staged = 1;
+  g.item_stride = item_bytes;
+  // The CE stream must not run ahead of work the caller already queued on `st`.
+  TSB_CUDA_TRY(cudaEventRecord(l->ev_ce[0], st));
+  TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_ce[0], 0));
+  int buf = 0;
+  for (int64_t i0 = 0; i0 < n_items; i0 += per_group, buf ^= 1) {
+    const int64_t n = std::min(per_group, n_items - i0);
+    uint8_t* stage = l->staging + buf * half;
+    if (l->k2_used[buf]) TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_k2[buf], 0));
+    for (int64_t i = 0; i < n; ++i) {
+      const tsb_ingest_item& it = items_host[i0 + i];
+      const uint8_t* src = pool->host + it.src_slot * g.chunk_bytes + lo * g.layer_src;
+      TSB_CUDA_TRY(cudaMemcpyAsync(stage + i * item_bytes, src, item_bytes,
+                                   cudaMemcpyHostToDevice, l->ce_stream));
+    }
+    TSB_CUDA_TRY(cudaEventRecord(l->ev_ce[buf], l->ce_stream));
+    TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_ce[buf], 0));
+    TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, stage, l->arena, items_dev + i0, l->bt_dev, n,
+                                        g_knobs.scatter_ctas, st));
+    TSB_CUDA_TRY(cudaEventRecord(l->ev_k2[buf], st));
+    l->k2_used[buf] = true;
+  }
+  return TSB_OK;
+}
+
+tsb_status ingest_impl(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
+                       const tsb_ingest_item* items_host, int64_t n_items, int64_t lo, int64_t hi,
+                       int mode, cudaStream_t st) {
+  if (lo < 0 || hi > l->shape.layers || lo >= hi)
+    return fail(TSB_VALIDATION, "ingest: layer range must satisfy 0 <= lo < hi <= layers");
+  if (pool->chunk_bytes != make_geom(l, 0, 1).chunk_bytes)
+    return fail(TSB_VALIDATION, "ingest: pool chunk geometry differs from the L1 shape");
+  if (n_items == 0) return TSB_OK;
+  mode = resolve_mode(l, mode);
+  const tsb::IngestGeom g = make_geom(l, lo, hi);
+  switch (mode) {
+    case TSB_INGEST_ZEROCOPY:
+      TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
+                                          g_knobs.zerocopy_ctas, st));
+      return TSB_OK;
+    case TSB_INGEST_BULK:
+      if (g.seg_bytes * 6 > 200 * 1024)
+        return fail(TSB_UNSUPPORTED, "ingest bulk: page segment too large for the smem ring");
+      TSB_CUDA_TRY(tsb::launch_ingest_bulk(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
+                                           g_knobs.bulk_ctas, st));
+      return TSB_OK;
+    case TSB_INGEST_CE:
+      return ingest_ce(l, pool, items_dev, items_host, n_items, lo, hi, st);
+    default:
+      return fail(TSB_VALIDATION, "ingest: unknown mode " + std::to_string(mode));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
+                      int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
+                      void* done_event) {
+  auto st = static_cast<cudaStream_t>(stream);
+  const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb_ingest_item));
+  for (int64_t i0 = 0; i0 < n_items; i0 += per) {
+    const int64_t n = std::min(per, n_items - i0);
+    void* dptr = nullptr;
+    int slot = 0;
+    TSB_TRY(l->ring_items.stage(items + i0, sizeof(tsb_ingest_item) * n, st, &dptr, &slot));
+    TSB_TRY(ingest_impl(l, pool, static_cast<const tsb_ingest_item*>(dptr), items + i0, n,
+                        layer_lo, layer_hi, mode, st));
+    TSB_TRY(l->ring_items.fence(slot, st));
+  }
+  if (done_event) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(done_event), st));
+  return TSB_OK;
+}
+
+tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
+                             int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
+                             void* stream, void* done_event) {
+  auto st = static_cast<cudaStream_t>(stream);
+  TSB_TRY(ingest_impl(l, pool, items_dev, nullptr, n_items, layer_lo, layer_hi, mode, st));
+  if (done_event) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(done_event), st));
+  return TSB_OK;
+}
+
+tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_item* items_dev,
+                              int64_t n_items, int64_t layer_lo, int64_t layer_hi,
+                              void* stream) {
+  if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
+    return fail(TSB_VALIDATION, "scatter: layer range must satisfy 0 <= lo < hi <= layers");
+  tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
+  TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, static_cast<const uint8_t*>(staging), l->arena,
+                                      items_dev, l->bt_dev, n_items, g_knobs.scatter_ctas,
+                                      static_cast<cudaStream_t>(stream)));
+  return TSB_OK;
+}
+
+tsb_status tsb_l1_verify_synthetic(tsb_l1* l, const tsb_ingest_item* items, int64_t n_items,
+                                   int64_t layer_lo, int64_t layer_hi, uint64_t seed,
+                                   int64_t pool_chunk_bytes, void* stream,
+                                   uint64_t* mismatches) {
+  auto st = static_cast<cudaStream_t>(stream);
+  tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
+  if (pool_chunk_bytes != g.chunk_bytes)
+    return fail(TSB_VALIDATION, "verify: pool chunk bytes differ from the L1 shape");
+  TSB_CUDA_TRY(cudaMemsetAsync(l->verify_ctr, 0, sizeof(unsigned long long), st));
+  const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb_ingest_item));
+  for (int64_t i0 = 0; i0 < n_items; i0 += per) {
+    const int64_t n = std::min(per, n_items - i0);
+    void* dptr = nullptr;
+    int slot = 0;
+    TSB_TRY(l->ring_items.stage(items + i0, sizeof(tsb_ingest_item) * n, st, &dptr, &slot));
+    TSB_CUDA_TRY(tsb::launch_verify_synth(g, l->arena, static_cast<const tsb_ingest_item*>(dptr),
+                                          l->bt_dev, n, seed, l->verify_ctr, st));
+    TSB_TRY(l->ring_items.fence(slot, st));
+  }
+  unsigned long long h = 0;
+  TSB_CUDA_TRY(cudaMemcpyAsync(&h, l->verify_ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  TSB_CUDA_TRY(cudaStreamSynchronize(st));
+  *mismatches = h;
+  return TSB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// Standalone TierLedger (engine.hpp:22-53) over the same tsb::Ledger the L1 allocator uses.
+// ---------------------------------------------------------------------------------------
+struct tsb_ledger {
+  tsb::Ledger l;
+};
+
+extern "C" {
+
+tsb_status tsb_ledger_create(int tier, int64_t capacity, tsb_ledger** out) {
+  if (capacity <= 0) return fail(TSB_VALIDATION, "TierLedger: capacity must be > 0");
+  *out = new tsb_ledger{tsb::Ledger(tier, capacity)};
+  return TSB_OK;
+}
+
+void tsb_ledger_destroy(tsb_ledger* l) { delete l; }
+
+tsb_status tsb_ledger_request(tsb_ledger* l, int64_t request_id, int32_t block_index,
+                              int64_t bytes, int* granted) {
+  std::string msg;
+  bool ok = false;
+  const tsb_status st = l->l.request(request_id, block_index, bytes, &ok, &msg);
+  if (st != TSB_OK) return fail(st, msg);
+  *granted = ok ? 1 : 0;
+  return TSB_OK;
+}
+
+tsb_status tsb_ledger_release(tsb_ledger* l, int64_t bytes, tsb_grant* out, int64_t cap,
+                              int64_t* n) {
+  std::string msg;
+  *n = 0;
+  const tsb_status st = l->l.release(
+      bytes,
+      [&](const tsb::Ledger::Pending& p) {
+        if (*n < cap) out[*n] = tsb_grant{p.request_id, p.block_index, -1, p.bytes};
+        ++*n;
+      },
+      &msg);
+  if (st != TSB_OK) return fail(st, msg);
+  return TSB_OK;
+}
+
+int64_t tsb_ledger_reserved(const tsb_ledger* l) { return l->l.reserved(); }
+int64_t tsb_ledger_capacity(const tsb_ledger* l) { return l->l.capacity(); }
+int64_t tsb_ledger_deferred(const tsb_ledger* l) { return l->l.deferred(); }
+
+}  // extern "C"

@@ -1,0 +1,235 @@
+// ingest.cu — K1 (zero-copy / bulk) and K2 (staged scatter) ingest kernels for sm_100a.
+//
+// The L2->L1 hop the reference only models as `transfer_base_latency + bytes/pcie_bandwidth`
+// per chunk (engine.cpp:206-207), dispatched one chunk at a time by pcie_dispatch
+// (engine.cpp:427-446).  Here one launch moves a batch of chunks x a layer range.  Work unit:
+// a segment = (item, layer, K|V, page j) = page_tokens rows of `run` bytes gathered from the
+// chunk [L][2][C][H][D] and written contiguously into page block_table[row][chunk*ppc + j]
+// of the layer's [2][num_pages][P][H_local][D] arena.  Segments are numbered so consecutive
+// ids read consecutive source bytes (layer-major inside a chunk), which keeps host reads
+// sequential.  No tensor cores: a pure gather/scatter bounded by the host link (K1) or HBM (K2).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tsb {
+namespace {
+
+struct SegAddr {
+  const uint8_t* src;
+  uint8_t* dst;
+  bool ok;
+};
+
+__device__ __forceinline__ SegAddr seg_addr(const IngestGeom& g, const uint8_t* src,
+                                            uint8_t* arena, const tsb_ingest_item* items,
+                                            const int32_t* bt, int64_t s) {
+  const int64_t spi = static_cast<int64_t>(g.n_layers) * 2 * g.ppc;
+  const int64_t i = s / spi;
+  const int64_t r = s - i * spi;
+  const int64_t l = r / (2 * g.ppc);
+  const int64_t kv = (r / g.ppc) & 1;
+  const int64_t j = r % g.ppc;
+  const tsb_ingest_item it = items[i];
+  const int32_t page = bt[static_cast<int64_t>(it.bt_row) * g.bt_stride +
+                          static_cast<int64_t>(it.chunk_index) * g.ppc + j];
+  SegAddr a;
+  const int64_t base = g.staged ? i * g.item_stride
+                                : it.src_slot * g.chunk_bytes + g.layer_lo * g.layer_src;
+  a.src = src + base + l * g.layer_src + kv * g.kv_src + j * g.P * g.row + g.head_off;
+  a.dst = arena + (g.layer_lo + l) * g.layer_dst + kv * g.kv_dst +
+          static_cast<int64_t>(page) * g.seg_bytes;
+  a.ok = page >= 0 && page < g.num_pages;
+  return a;
+}
+
+// K1 / K2: one warp per segment, 16-byte streaming loads, U loads in flight per lane before
+// the stores.  Source may be mapped host memory (K1, zero-copy over PCIe) or an HBM staging
+// buffer (K2).
+template <bool kContig, int U>
+__global__ void __launch_bounds__(256) k_ingest_ldg(IngestGeom g, const uint8_t* __restrict__ src,
+                                                    uint8_t* __restrict__ arena,
+                                                    const tsb_ingest_item* __restrict__ items,
+                                                    const int32_t* __restrict__ bt,
+                                                    int64_t nseg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int vpr = static_cast<int>(g.run >> 4);
+  const int nvec = static_cast<int>(g.P) * vpr;
+  for (int64_t s = warp; s < nseg; s += nwarps) {
+    const SegAddr a = seg_addr(g, src, arena, items, bt, s);
+    if (!a.ok) continue;
+    for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+      int4 buf[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32;
+        if (v < nvec) {
+          const int64_t off = kContig ? static_cast<int64_t>(v) * 16
+                                      : (v / vpr) * g.row + (v % vpr) * 16;
+          buf[u] = ld_stream(a.src + off);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32;
+        if (v < nvec) st_stream(a.dst + static_cast<int64_t>(v) * 16, buf[u]);
+      }
+    }
+  }
+}
+
+// K1b: the TMA/bulk-copy engine does the moving.  One warp per CTA; a ring of kStages
+// segment buffers in shared memory.  Lane 0 (or lanes 0..P-1 for head-sharded runs) issues
+// cp.async.bulk host->smem completing on the stage mbarrier, then one cp.async.bulk
+// smem->HBM per segment.  Almost no SM issue bandwidth is used, so prefill keeps the SMs.
+template <int kStages>
+__global__ void __launch_bounds__(32) k_ingest_bulk(IngestGeom g, const uint8_t* __restrict__ src,
+                                                    uint8_t* __restrict__ arena,
+                                                    const tsb_ingest_item* __restrict__ items,
+                                                    const int32_t* __restrict__ bt,
+                                                    int64_t nseg) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kStages];
+  const int lane = threadIdx.x;
+  const bool contig = g.run == g.row;
+  const uint32_t seg = static_cast<uint32_t>(g.seg_bytes);
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+
+  auto issue = [&](int64_t s, int stage) {
+    const SegAddr a = seg_addr(g, src, arena, items, bt, s);
+    uint8_t* buf = smem + static_cast<int64_t>(stage) * seg;
+    if (lane == 0) mbar_arrive_expect_tx(&full[stage], seg);
+    __syncwarp();
+    if (contig) {
+      if (lane == 0) bulk_g2s(buf, a.src, seg, &full[stage]);
+    } else {
+      for (int t = lane; t < g.P; t += 32)
+        bulk_g2s(buf + t * g.run, a.src + t * g.row, static_cast<uint32_t>(g.run), &full[stage]);
+    }
+  };
+
+  int64_t next = blockIdx.x;
+  for (int st = 0; st < kStages && next < nseg; ++st, next += gridDim.x) issue(next, st);
+  int k = 0;
+  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x, ++k) {
+    const int stage = k % kStages;
+    mbar_wait(&full[stage], (k / kStages) & 1);
+    if (lane == 0) {
+      const SegAddr a = seg_addr(g, src, arena, items, bt, s);
+      if (a.ok) bulk_s2g(a.dst, smem + static_cast<int64_t>(stage) * seg, seg);
+      bulk_commit();
+    }
+    if (next < nseg) {
+      if (lane == 0) bulk_wait_read0();  // the stage's smem has been read by the store
+      __syncwarp();
+      issue(next, stage);
+      next += gridDim.x;
+    }
+  }
+  if (lane == 0) bulk_wait0();
+}
+
+__global__ void k_fill_synth(uint64_t* __restrict__ dst, uint64_t first_word, uint64_t n_words,
+                             uint64_t seed) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t npairs = n_words / 2;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < npairs;
+       p += stride) {
+    const uint64_t w = first_word + 2 * p;
+    const uint64_t a = synth_word(seed, w), b = synth_word(seed, w + 1);
+    int4 v;
+    v.x = static_cast<int>(a);
+    v.y = static_cast<int>(a >> 32);
+    v.z = static_cast<int>(b);
+    v.w = static_cast<int>(b >> 32);
+    *reinterpret_cast<int4*>(dst + 2 * p) = v;
+  }
+  if ((n_words & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+    dst[n_words - 1] = synth_word(seed, first_word + n_words - 1);
+}
+
+// Harness check: every 8-byte word of every page of the items must equal the synthetic word
+// of the source position it was gathered from (slot mode geometry).
+__global__ void k_verify_synth(IngestGeom g, const uint8_t* __restrict__ arena,
+                               const tsb_ingest_item* __restrict__ items,
+                               const int32_t* __restrict__ bt, int64_t nseg, uint64_t seed,
+                               unsigned long long* mismatches) {
+  const int64_t words_per_run = g.run / 8;
+  const int64_t words = g.P * words_per_run;
+  unsigned long long bad = 0;
+  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    const SegAddr a = seg_addr(g, nullptr, const_cast<uint8_t*>(arena), items, bt, s);
+    if (!a.ok) {
+      if (threadIdx.x == 0) bad += words;
+      continue;
+    }
+    const int64_t src_off = reinterpret_cast<int64_t>(a.src);  // src base was nullptr
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) {
+      const int64_t t = w / words_per_run, c = w % words_per_run;
+      const uint64_t expect =
+          synth_word(seed, static_cast<uint64_t>(src_off + t * g.row + c * 8) / 8);
+      bad += reinterpret_cast<const uint64_t*>(a.dst)[w] != expect;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
+}
+
+}  // namespace
+
+cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
+                              const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
+                              int grid, cudaStream_t st) {
+  const int64_t nseg = n_items * g.n_layers * 2 * g.ppc;
+  if (nseg == 0) return cudaSuccess;
+  if (g.run == g.row)
+    k_ingest_ldg<true, 8><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+  else
+    k_ingest_ldg<false, 8><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ingest_bulk(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
+                               const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
+                               int grid, cudaStream_t st) {
+  const int64_t nseg = n_items * g.n_layers * 2 * g.ppc;
+  if (nseg == 0) return cudaSuccess;
+  constexpr int kStages = 6;
+  const size_t smem = static_cast<size_t>(kStages) * g.seg_bytes;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_ingest_bulk<kStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_ingest_bulk<kStages><<<grid, 32, smem, st>>>(g, src, arena, items, bt, nseg);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_synth(uint64_t* dst, uint64_t first_word, uint64_t n_words, uint64_t seed,
+                              cudaStream_t st) {
+  if (n_words == 0) return cudaSuccess;
+  k_fill_synth<<<148 * 8, 256, 0, st>>>(dst, first_word, n_words, seed);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_verify_synth(const IngestGeom& g, const uint8_t* arena,
+                                const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
+                                uint64_t seed, unsigned long long* mismatches, cudaStream_t st) {
+  const int64_t nseg = n_items * g.n_layers * 2 * g.ppc;
+  if (nseg == 0) return cudaSuccess;
+  k_verify_synth<<<148 * 8, 256, 0, st>>>(g, arena, items, bt, nseg, seed, mismatches);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace tsb

@@ -1,0 +1,72 @@
+// kernels.h — launch interface of the sm_100a kernels (internal to libtsb.so).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tsb_capi.h"
+
+namespace tsb {
+
+// Geometry of one ingest launch.  A "segment" is one (item, layer, K|V, page) unit: P token
+// rows of `run` bytes read at stride `row` from the chunk, written contiguously to one page.
+struct IngestGeom {
+  int64_t row;          // H*D*E: one token's K (or V) across all heads in the chunk
+  int64_t run;          // H_local*D*E: this rank's slice of that row
+  int64_t head_off;     // tp_rank*H_local*D*E
+  int64_t chunk_bytes;  // L*2*C*row: one L2 slot
+  int64_t kv_src;       // C*row: K->V stride inside a chunk layer
+  int64_t layer_src;    // 2*C*row
+  int64_t P;            // page tokens
+  int64_t ppc;          // pages per chunk (C/P)
+  int64_t seg_bytes;    // P*run
+  int64_t num_pages;
+  int64_t kv_dst;       // num_pages*seg_bytes
+  int64_t layer_dst;    // 2*kv_dst
+  int64_t bt_stride;    // block_table row stride (int32 entries)
+  int32_t layer_lo;     // first layer of the launch
+  int32_t n_layers;     // layers in the launch
+  // Source addressing: slot mode (src = base + slot*chunk_bytes + layer_lo*layer_src) for the
+  // L2 pool, or staged mode (src = base + item_rank*item_stride) for a CE staging buffer that
+  // holds only layers [layer_lo, layer_lo+n_layers) of each item.
+  int32_t staged;
+  int64_t item_stride;
+};
+
+cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
+                              const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
+                              int grid, cudaStream_t st);
+cudaError_t launch_ingest_bulk(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
+                               const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
+                               int grid, cudaStream_t st);
+cudaError_t launch_fill_synth(uint64_t* dst, uint64_t first_word, uint64_t n_words, uint64_t seed,
+                              cudaStream_t st);
+cudaError_t launch_verify_synth(const IngestGeom& g, const uint8_t* arena,
+                                const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
+                                uint64_t seed, unsigned long long* mismatches, cudaStream_t st);
+
+// Scorer (K4) and order (K5).
+struct ScoreParams {
+  int policy;
+  double load_slope, load_icpt, comp_slope, comp_icpt;
+  double quadratic;
+  int64_t block;
+};
+cudaError_t launch_score(int64_t n, tsb_queue q, ScoreParams p, double* t_load, double* t_comp,
+                         double* primary, uint64_t* kp, uint64_t* ka, uint64_t* ki,
+                         unsigned long long* err_missing, unsigned long long* err_nan,
+                         cudaStream_t st);
+// Sorts (kp, ka, ki) ascending, producing the permutation in order_out.  Scratch must hold
+// 2 * n of each key array plus 2 * n int64 indices.
+cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, int64_t* idx,
+                         uint64_t* kp2, uint64_t* ka2, uint64_t* ki2, int64_t* idx2,
+                         int64_t* order_out, cudaStream_t st);
+
+// Prefix hasher (K3) and token generator.
+cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
+                               const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st);
+cudaError_t launch_gen_tokens(uint64_t seed, int64_t n_req, const int64_t* offsets,
+                              const int64_t* doc, const int64_t* shared_len, int32_t* out,
+                              cudaStream_t st);
+
+}  // namespace tsb

@@ -1,0 +1,248 @@
+"""L2 pinned chunk pool, L1 paged KV cache + block_table, and the L2->L1 ingest (K1/K1b/CE+K2).
+
+Python face of tsb_pool_* / tsb_l1_* / tsb_ingest*.  The reference models this hop only as a
+duration (engine.cpp:206-207, pcie_dispatch engine.cpp:427-446); here it moves real bytes:
+LMCache-style chunks [layer][K/V][token][kv_head][dim] in pinned host memory are scattered
+into vLLM-style paged HBM blocks [2][num_pages][page_tokens][kv_heads_local][head_dim] per
+layer through the block table.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _capi as capi
+from ._capi import lib
+from .tiersim import Tier, check
+
+ZEROCOPY, BULK, CE, AUTO = capi.INGEST_ZEROCOPY, capi.INGEST_BULK, capi.INGEST_CE, capi.INGEST_AUTO
+MODES = {"auto": AUTO, "zerocopy": ZEROCOPY, "bulk": BULK, "ce": CE}
+
+
+@dataclass(frozen=True)
+class KVShape:
+    layers: int
+    kv_heads: int
+    head_dim: int
+    dtype_bytes: int = 2
+    chunk_tokens: int = 256
+    page_tokens: int = 16
+    tp_size: int = 1
+    tp_rank: int = 0
+
+    def struct(self) -> capi.KvShape:
+        return capi.KvShape(self.layers, self.kv_heads, self.head_dim, self.dtype_bytes, self.chunk_tokens,
+                            self.page_tokens, self.tp_size, self.tp_rank)
+
+    def info(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.tsb_kv_shape_info(C.byref(self.struct()), C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    @property
+    def chunk_bytes(self) -> int:
+        return self.info()[0]
+
+    @property
+    def page_bytes(self) -> int:
+        """Local bytes of one page across all layers (K and V, this rank's heads)."""
+        return self.info()[1]
+
+    @property
+    def local_chunk_bytes(self) -> int:
+        return self.info()[2]
+
+    @property
+    def heads_local(self) -> int:
+        return self.kv_heads // self.tp_size
+
+    @property
+    def pages_per_chunk(self) -> int:
+        return self.chunk_tokens // self.page_tokens
+
+    def with_rank(self, tp_size: int, tp_rank: int) -> "KVShape":
+        return KVShape(self.layers, self.kv_heads, self.head_dim, self.dtype_bytes, self.chunk_tokens,
+                       self.page_tokens, tp_size, tp_rank)
+
+
+# Model shapes of BASELINE.json (public configs).
+LLAMA31_8B = KVShape(layers=32, kv_heads=8, head_dim=128)
+QWEN25_32B = KVShape(layers=64, kv_heads=8, head_dim=128)
+LLAMA3_70B = KVShape(layers=80, kv_heads=8, head_dim=128)
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class ChunkPool:
+    """L2 tier: pinned + portable + mapped host memory, one full chunk per slot."""
+
+    def __init__(self, shape: KVShape, n_slots: int):
+        self.shape = shape
+        h = C.c_void_p()
+        check(lib.tsb_pool_create(C.byref(shape.struct()), int(n_slots), C.byref(h)))
+        self._h = h
+        self.n_slots = n_slots
+        self.chunk_bytes = lib.tsb_pool_chunk_bytes(h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tsb_pool_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def slot_ptr(self, slot: int) -> int:
+        return lib.tsb_pool_slot_ptr(self._h, int(slot))
+
+    def slot_view(self, slot: int, count: int = 1) -> np.ndarray:
+        """Writable uint8 numpy view of `count` slots (host memory)."""
+        buf = (C.c_uint8 * (self.chunk_bytes * count)).from_address(self.slot_ptr(slot))
+        return np.frombuffer(buf, dtype=np.uint8)
+
+    def fill_synthetic(self, seed: int, first: int = 0, n: Optional[int] = None, stream=None):
+        n = self.n_slots - first if n is None else n
+        check(lib.tsb_pool_fill_synthetic(self._h, int(seed), int(first), int(n), _stream(stream)))
+
+
+class PagedKVCache:
+    """L1 tier: paged HBM arena + block_table, allocated with TierLedger semantics.
+
+    request()/release_request() mirror TierLedger::request/release (engine.cpp:22-49) with
+    capacity = num_pages * page_bytes; each granted chunk gets pages_per_chunk pages from a FIFO
+    free list, written into the request's block_table row."""
+
+    def __init__(self, shape: KVShape, num_pages: int, max_rows: int, max_chunks: int, device: int = 0,
+                 arena: Optional[torch.Tensor] = None):
+        self.shape = shape
+        self.device = device
+        self.num_pages = num_pages
+        layer_bytes = 2 * num_pages * shape.page_tokens * shape.heads_local * shape.head_dim * shape.dtype_bytes
+        if arena is None:
+            arena = torch.empty(shape.layers * layer_bytes, dtype=torch.uint8, device=torch.device("cuda", device))
+        if arena.numel() < shape.layers * layer_bytes or not arena.is_cuda:
+            raise ValueError("arena must be a CUDA uint8 tensor of layers*2*num_pages*page*heads*dim*dtype bytes")
+        self.arena = arena
+        self.layer_bytes = layer_bytes
+        h = C.c_void_p()
+        check(lib.tsb_l1_create(device, C.byref(shape.struct()), int(num_pages), int(max_rows), int(max_chunks),
+                                arena.data_ptr(), C.byref(h)))
+        self._h = h
+        self.max_rows, self.max_chunks = max_rows, max_chunks
+        self.stride = lib.tsb_l1_block_table_stride(h)
+        self.page_bytes = lib.tsb_l1_page_bytes(h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tsb_l1_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def tier(self) -> Tier:
+        return Tier.L1
+
+    def request(self, request_id: int, block_index: int, nbytes: int):
+        g, row = C.c_int(), C.c_int32()
+        check(lib.tsb_l1_request(self._h, int(request_id), int(block_index), int(nbytes), C.byref(g), C.byref(row)))
+        return bool(g.value), row.value
+
+    def release_request(self, request_id: int):
+        cap = max(64, self.deferred_count())
+        out = (capi.Grant * cap)()
+        n = C.c_int64()
+        check(lib.tsb_l1_release_request(self._h, int(request_id), out, cap, C.byref(n)))
+        return [(out[i].request_id, out[i].block_index, out[i].bt_row, out[i].bytes) for i in range(min(n.value, cap))]
+
+    def capacity(self) -> int:
+        return lib.tsb_l1_capacity(self._h)
+
+    def reserved(self) -> int:
+        return lib.tsb_l1_reserved(self._h)
+
+    def deferred_count(self) -> int:
+        return lib.tsb_l1_deferred(self._h)
+
+    def free_pages(self) -> int:
+        return lib.tsb_l1_free_pages(self._h)
+
+    def block_table(self) -> np.ndarray:
+        """Host (pinned) mirror [max_rows, max_chunks*pages_per_chunk] int32 (a view)."""
+        n = self.max_rows * self.stride
+        buf = (C.c_int32 * n).from_address(lib.tsb_l1_block_table_host(self._h))
+        return np.frombuffer(buf, dtype=np.int32).reshape(self.max_rows, self.stride)
+
+    def sync_block_table(self, stream=None):
+        check(lib.tsb_l1_sync_block_table(self._h, _stream(stream)))
+
+    def layer(self, layer: int, dtype=torch.bfloat16) -> torch.Tensor:
+        """vLLM flash-attn view of one layer: [2, num_pages, page_tokens, heads_local, head_dim]."""
+        s = self.shape
+        t = self.arena[layer * self.layer_bytes:(layer + 1) * self.layer_bytes]
+        return t.view(dtype).view(2, self.num_pages, s.page_tokens, s.heads_local, s.head_dim)
+
+
+def items_array(rows: Sequence) -> "C.Array":
+    """[(src_slot, bt_row, chunk_index), ...] -> tsb_ingest_item[]"""
+    arr = (capi.IngestItem * len(rows))()
+    for i, (slot, row, chunk) in enumerate(rows):
+        arr[i].src_slot, arr[i].bt_row, arr[i].chunk_index = int(slot), int(row), int(chunk)
+    return arr
+
+
+def items_numpy(src_slot, bt_row, chunk_index) -> np.ndarray:
+    dt = np.dtype([("src_slot", np.int64), ("bt_row", np.int32), ("chunk_index", np.int32)])
+    a = np.empty(len(src_slot), dtype=dt)
+    a["src_slot"], a["bt_row"], a["chunk_index"] = src_slot, bt_row, chunk_index
+    return a
+
+
+def _items_ptr(items):
+    if isinstance(items, np.ndarray):
+        return C.cast(items.ctypes.data, C.POINTER(capi.IngestItem)), len(items)
+    return items, len(items)
+
+
+def ingest(l1: PagedKVCache, pool: ChunkPool, items, layer_lo: int = 0, layer_hi: Optional[int] = None,
+           mode: int = AUTO, stream=None, done_event: Optional[torch.cuda.Event] = None):
+    """tsb_ingest: moves every (item, layer in [layer_lo, layer_hi)) L2 -> L1 (async)."""
+    layer_hi = l1.shape.layers if layer_hi is None else layer_hi
+    ptr, n = _items_ptr(items)
+    ev = done_event.cuda_event if done_event is not None else None
+    check(lib.tsb_ingest(l1.handle, pool.handle, ptr, n, layer_lo, layer_hi, int(mode), _stream(stream), ev))
+
+
+def ingest_device(l1: PagedKVCache, pool: ChunkPool, items_dev: torch.Tensor, n_items: int, layer_lo: int = 0,
+                  layer_hi: Optional[int] = None, mode: int = AUTO, stream=None, done_event=None):
+    layer_hi = l1.shape.layers if layer_hi is None else layer_hi
+    ev = done_event.cuda_event if done_event is not None else None
+    check(lib.tsb_ingest_device(l1.handle, pool.handle, items_dev.data_ptr(), int(n_items), layer_lo, layer_hi,
+                                int(mode), _stream(stream), ev))
+
+
+def verify_synthetic(l1: PagedKVCache, pool: ChunkPool, items, seed: int, layer_lo: int = 0,
+                     layer_hi: Optional[int] = None, stream=None) -> int:
+    layer_hi = l1.shape.layers if layer_hi is None else layer_hi
+    ptr, n = _items_ptr(items)
+    out = C.c_uint64()
+    check(lib.tsb_l1_verify_synthetic(l1.handle, ptr, n, layer_lo, layer_hi, int(seed), pool.chunk_bytes,
+                                      _stream(stream), C.byref(out)))
+    return out.value
+
+
+def set_grid(zerocopy_ctas: int = 0, bulk_ctas: int = 0, scatter_ctas: int = 0):
+    check(lib.tsb_ingest_set_grid(zerocopy_ctas, bulk_ctas, scatter_ctas))

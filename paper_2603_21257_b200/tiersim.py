@@ -1,0 +1,432 @@
+"""Reference-shaped Python mirror of the kept tiersim API, over libtsb.so.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/core/include/tiersim/
+(types.hpp, cost_model.hpp, scheduler.hpp, engine.hpp TierLedger, error.hpp) so that parity tests
+read like the reference's own doctest suites.  Scalar planning helpers run as host arithmetic
+inside libtsb.so; everything batched (scorer, order, hashing, ingest) runs on the GPU through
+the C ABI -- there is no CPU fallback in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import _capi as capi
+from ._capi import lib
+
+
+# ---- error.hpp:13-71 -----------------------------------------------------------------------
+class Error(RuntimeError):
+    """tiersim::Error"""
+
+
+class ValidationError(Error):
+    pass
+
+
+class DegenerateFit(Error):
+    pass
+
+
+class MissingDeadline(Error):
+    pass
+
+
+class CapacityError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class Unsupported(Error):
+    pass
+
+
+_STATUS = {
+    capi.TSB_VALIDATION: ValidationError,
+    capi.TSB_CAPACITY: CapacityError,
+    capi.TSB_MISSING_DEADLINE: MissingDeadline,
+    capi.TSB_DEGENERATE_FIT: DegenerateFit,
+    capi.TSB_CUDA: CudaError,
+    capi.TSB_UNSUPPORTED: Unsupported,
+}
+
+
+def check(status: int) -> None:
+    if status != capi.TSB_OK:
+        raise _STATUS.get(status, Error)(capi.last_error())
+
+
+# ---- types.hpp -------------------------------------------------------------------------------
+class Tier(enum.IntEnum):
+    L3 = 0
+    L2 = 1
+    L1 = 2
+
+
+class AllocationMode(enum.IntEnum):
+    Proactive = 0
+    Reactive = 1
+
+
+class ControlMode(enum.IntEnum):
+    Coupled = 0
+    Decoupled = 1
+
+
+@dataclass
+class MeasuredCost:
+    t_load: float = 0.0
+    t_comp: float = 0.0
+
+
+@dataclass
+class RequestSpec:
+    """types.hpp:52-64"""
+
+    id: int = 0
+    arrival_time: float = 0.0
+    context_tokens: int = 0
+    query_tokens: int = 1
+    cache_hit_ratio: float = 1.0
+    deadline: Optional[float] = None
+    measured_cost: Optional[MeasuredCost] = None
+    dataset_tag: str = ""
+
+    def validate(self) -> None:
+        q = QueueArrays.from_specs([self])
+        check(lib.tsb_request_validate(C.byref(q.struct()), 0))
+
+
+@dataclass
+class ClusterConfig:
+    """types.hpp:82-97 (same defaults)."""
+
+    network_bandwidth: float = 50e9
+    pcie_bandwidth: float = 64e9
+    transfer_base_latency: float = 10e-6
+    l1_capacity: int = 80_000_000_000
+    l2_capacity: int = 128_000_000_000
+    bytes_per_token: int = 131072
+    block_size_tokens: int = 256
+    compute_base: float = 2e-3
+    compute_per_token: float = 4e-5
+    compute_quadratic: float = 0.0
+    allocation_mode: AllocationMode = AllocationMode.Proactive
+    control_mode: ControlMode = ControlMode.Decoupled
+
+    def struct(self) -> capi.Cluster:
+        c = capi.Cluster()
+        for name, _ in capi.Cluster._fields_:
+            setattr(c, name, int(getattr(self, name)) if name.endswith("mode") else getattr(self, name))
+        return c
+
+    def validate(self) -> None:
+        check(lib.tsb_cluster_validate(C.byref(self.struct())))
+
+
+@dataclass
+class KVBlock:
+    """types.hpp:104-111"""
+
+    request_id: int = 0
+    block_index: int = 0
+    tokens: int = 0
+    bytes: int = 0
+    residency: Tier = Tier.L3
+
+
+class QueueArrays:
+    """Struct-of-arrays RequestSpec queue (numpy, host) matching tsb_queue."""
+
+    FIELDS = (
+        ("id", np.int64),
+        ("arrival", np.float64),
+        ("context_tokens", np.int64),
+        ("query_tokens", np.int64),
+        ("cache_hit_ratio", np.float64),
+        ("flags", np.uint8),
+        ("deadline", np.float64),
+        ("measured_t_load", np.float64),
+        ("measured_t_comp", np.float64),
+    )
+
+    def __init__(self, n: int = 0, **arrays):
+        for name, dt in self.FIELDS:
+            a = arrays.get(name)
+            setattr(self, name, np.ascontiguousarray(a, dtype=dt) if a is not None else np.zeros(n, dtype=dt))
+        self.n = len(self.id)
+
+    @classmethod
+    def from_specs(cls, specs: Sequence[RequestSpec], costs: Optional[dict] = None) -> "QueueArrays":
+        n = len(specs)
+        q = cls(n)
+        for i, s in enumerate(specs):
+            q.id[i] = s.id
+            q.arrival[i] = s.arrival_time
+            q.context_tokens[i] = s.context_tokens
+            q.query_tokens[i] = s.query_tokens
+            q.cache_hit_ratio[i] = s.cache_hit_ratio
+            fl = 0
+            if s.deadline is not None:
+                fl |= capi.HAS_DEADLINE
+                q.deadline[i] = s.deadline
+            mc = s.measured_cost
+            if costs is not None:  # CostMap semantics (scheduler.cpp:82-83): missing id -> zero
+                mc = costs.get(s.id, ServiceCost())
+            if mc is not None:
+                fl |= capi.HAS_MEASURED
+                q.measured_t_load[i] = mc.t_load
+                q.measured_t_comp[i] = mc.t_comp
+            q.flags[i] = fl
+        return q
+
+    def struct(self) -> capi.Queue:
+        s = capi.Queue()
+        for name, _ in self.FIELDS:
+            setattr(s, name, getattr(self, name).ctypes.data)
+        return s
+
+
+def _q1(spec: RequestSpec):
+    q = QueueArrays.from_specs([spec])
+    return q, q.struct()
+
+
+def kv_bytes_per_token(layers: int, kv_heads: int, head_dim: int, dtype_bytes: int) -> int:
+    out = C.c_int64()
+    check(lib.tsb_kv_bytes_per_token(layers, kv_heads, head_dim, dtype_bytes, C.byref(out)))
+    return out.value
+
+
+def _plan(spec: RequestSpec, config: ClusterConfig):
+    q, s = _q1(spec)
+    vals = [C.c_int64() for _ in range(5)]
+    check(lib.tsb_derive_block_plan(C.byref(s), 0, C.byref(config.struct()), *[C.byref(v) for v in vals]))
+    return [v.value for v in vals]
+
+
+def cached_token_count(spec: RequestSpec, config: ClusterConfig) -> int:
+    return _plan(spec, config)[0]
+
+
+def compute_token_count(spec: RequestSpec, config: ClusterConfig) -> int:
+    return _plan(spec, config)[1]
+
+
+def derive_block_plan(spec: RequestSpec, config: ClusterConfig) -> list[KVBlock]:
+    cached, _, n, tokens, nbytes = _plan(spec, config)
+    return [KVBlock(spec.id, i, tokens, nbytes) for i in range(n)]
+
+
+# ---- cost_model.hpp --------------------------------------------------------------------------
+@dataclass
+class LinearCostModel:
+    slope: float = 0.0
+    intercept: float = 0.0
+
+
+@dataclass
+class LinearFit:
+    model: LinearCostModel
+    slope_clamped: bool = False
+    intercept_clamped: bool = False
+
+
+@dataclass
+class ServiceCost:
+    t_load: float = 0.0
+    t_comp: float = 0.0
+
+    def total(self) -> float:
+        return self.t_load + self.t_comp
+
+
+@dataclass
+class CostModelPair:
+    load: LinearCostModel = field(default_factory=LinearCostModel)
+    comp: LinearCostModel = field(default_factory=LinearCostModel)
+
+    def array(self):
+        return (C.c_double * 4)(self.load.slope, self.load.intercept, self.comp.slope, self.comp.intercept)
+
+
+def cost_models_from_config(config: ClusterConfig) -> CostModelPair:
+    m = (C.c_double * 4)()
+    lib.tsb_cost_models_from_config(C.byref(config.struct()), m)
+    return CostModelPair(LinearCostModel(m[0], m[1]), LinearCostModel(m[2], m[3]))
+
+
+def predict(model: LinearCostModel, tokens: int) -> float:
+    return lib.tsb_predict(model.slope, model.intercept, int(tokens))
+
+
+def fit_linear(samples: Iterable) -> LinearFit:
+    samples = list(samples)
+    tok = np.array([s[0] for s in samples], dtype=np.int64)
+    sec = np.array([s[1] for s in samples], dtype=np.float64)
+    a, b = C.c_double(), C.c_double()
+    ca, cb = C.c_int(), C.c_int()
+    check(lib.tsb_fit_linear(len(samples), tok.ctypes.data, sec.ctypes.data, C.byref(a), C.byref(b), C.byref(ca), C.byref(cb)))
+    return LinearFit(LinearCostModel(a.value, b.value), bool(ca.value), bool(cb.value))
+
+
+def estimate_service_cost(spec: RequestSpec, load_model: LinearCostModel, comp_model: LinearCostModel,
+                          config: ClusterConfig) -> ServiceCost:
+    q, s = _q1(spec)
+    m = CostModelPair(load_model, comp_model).array()
+    a, b = C.c_double(), C.c_double()
+    check(lib.tsb_estimate_service_cost(C.byref(s), 0, m, C.byref(config.struct()), C.byref(a), C.byref(b)))
+    return ServiceCost(a.value, b.value)
+
+
+# ---- scheduler.hpp ---------------------------------------------------------------------------
+class PolicyKind(enum.IntEnum):
+    Fifo = 0
+    SjfPt = 1
+    SjfCost = 2
+    Edf = 3
+    Lstf = 4
+
+
+_POLICY_NAMES = {"fifo": PolicyKind.Fifo, "sjf-pt": PolicyKind.SjfPt, "sjf-cost": PolicyKind.SjfCost,
+                 "edf": PolicyKind.Edf, "lstf": PolicyKind.Lstf}
+
+
+def policy_from_name(name: str) -> Optional[PolicyKind]:
+    return _POLICY_NAMES.get(name)
+
+
+def policy_name(policy: PolicyKind) -> str:
+    return {v: k for k, v in _POLICY_NAMES.items()}[PolicyKind(policy)]
+
+
+def all_policies() -> list[PolicyKind]:
+    return list(PolicyKind)
+
+
+@dataclass(frozen=True, order=False)
+class PriorityKey:
+    primary: float = 0.0
+    arrival: float = 0.0
+    id: int = 0
+
+    def __lt__(self, other: "PriorityKey") -> bool:  # scheduler.hpp:38-42
+        if self.primary != other.primary:
+            return self.primary < other.primary
+        if self.arrival != other.arrival:
+            return self.arrival < other.arrival
+        return self.id < other.id
+
+
+def prefill_token_estimate(spec: RequestSpec) -> float:
+    q, s = _q1(spec)
+    out = C.c_double()
+    check(lib.tsb_priority_key(C.byref(s), 0, int(PolicyKind.SjfPt), 0.0, 0.0, C.byref(out)))
+    return out.value
+
+
+def priority_key(spec: RequestSpec, policy: PolicyKind, cost: ServiceCost, now: float = 0.0) -> PriorityKey:
+    q, s = _q1(spec)
+    out = C.c_double()
+    check(lib.tsb_priority_key(C.byref(s), 0, int(policy), cost.t_load, cost.t_comp, C.byref(out)))
+    return PriorityKey(out.value, spec.arrival_time, spec.id)
+
+
+# The batched GPU scorer (K4+K5) backs the queue operations below.
+_default_scorer = None
+
+
+def default_scorer():
+    global _default_scorer
+    if _default_scorer is None:
+        from .scorer import BatchScorer
+
+        _default_scorer = BatchScorer(device=0)
+    return _default_scorer
+
+
+def best_request_index(queue: Sequence[RequestSpec], policy: PolicyKind, costs: dict, now: float = 0.0):
+    """scheduler.cpp:75-91 -- on the GPU: order[0] of the batched scorer with CostMap costs."""
+    if not queue:
+        return None
+    order = default_scorer().order_specs(queue, policy, costs=costs)
+    return int(order[0])
+
+
+def pick_next(queue: list, policy: PolicyKind, costs: dict, now: float = 0.0):
+    """scheduler.cpp:93-100: removes and returns the minimum-key request (None when empty)."""
+    idx = best_request_index(queue, policy, costs, now)
+    if idx is None:
+        return None
+    return queue.pop(idx)
+
+
+def schedule_order(queue: Sequence[RequestSpec], policy: PolicyKind, costs: Optional[dict] = None,
+                   models: Optional[CostModelPair] = None, config: Optional[ClusterConfig] = None) -> list[int]:
+    """The full pick_next drain of a fixed queue as one GPU sort: returns request ids in pick order."""
+    order = default_scorer().order_specs(queue, policy, costs=costs, models=models, config=config)
+    return [queue[int(i)].id for i in order]
+
+
+# ---- engine.hpp TierLedger --------------------------------------------------------------------
+class TierLedger:
+    """engine.hpp:22-53 -- the libtsb byte ledger (tsb_ledger_*), the same object the L1 paged
+    allocator (ingest.PagedKVCache) runs its grant/defer decisions through."""
+
+    class Outcome(enum.IntEnum):
+        Granted = 0
+        Deferred = 1
+
+    Granted, Deferred = Outcome.Granted, Outcome.Deferred
+
+    def __init__(self, tier: Tier, capacity: int):
+        h = C.c_void_p()
+        check(lib.tsb_ledger_create(int(tier), int(capacity), C.byref(h)))
+        self._h = h
+        self._tier = Tier(tier)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.tsb_ledger_destroy(h)
+            self._h = None
+
+    def request(self, request_id: int, block_index: int, nbytes: int) -> "TierLedger.Outcome":
+        g = C.c_int()
+        check(lib.tsb_ledger_request(self._h, int(request_id), int(block_index), int(nbytes), C.byref(g)))
+        return self.Granted if g.value else self.Deferred
+
+    def release(self, nbytes: int) -> list:
+        n = C.c_int64()
+        cap = max(16, self.deferred_count())
+        out = (capi.Grant * cap)()
+        check(lib.tsb_ledger_release(self._h, int(nbytes), out, cap, C.byref(n)))
+        return [Pending(out[i].request_id, out[i].block_index, out[i].bytes) for i in range(n.value)]
+
+    def tier(self) -> Tier:
+        return self._tier
+
+    def capacity(self) -> int:
+        return lib.tsb_ledger_capacity(self._h)
+
+    def reserved(self) -> int:
+        return lib.tsb_ledger_reserved(self._h)
+
+    def deferred_count(self) -> int:
+        return lib.tsb_ledger_deferred(self._h)
+
+
+@dataclass
+class Pending:
+    """TierLedger::Pending (engine.hpp:26-30)"""
+
+    request_id: int
+    block_index: int
+    bytes: int

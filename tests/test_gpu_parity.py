@@ -1,0 +1,355 @@
+"""GPU parity: the CUDA path through the C ABI vs the pinned CPU oracle (bit-exact).
+
+Runs on a B200 (`pytest -m gpu`).  Every comparison is against tests/golden (generated from the
+compiled reference) or the oracle restatement pinned to it in test_oracle_pins.py.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import pyoracle as po
+from conftest import has_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+from paper_2603_21257_b200 import _capi  # noqa: E402
+from paper_2603_21257_b200 import hasher, ingest  # noqa: E402
+from paper_2603_21257_b200 import tiersim as t  # noqa: E402
+from paper_2603_21257_b200.scorer import BatchScorer, DeviceQueue  # noqa: E402
+
+CFGS = {"default": t.ClusterConfig(), "quad": t.ClusterConfig(compute_quadratic=1e-9, block_size_tokens=128)}
+
+
+@pytest.fixture(scope="module")
+def scorer():
+    return BatchScorer(device=0)
+
+
+def golden_queue(g, sl=slice(None)):
+    return t.QueueArrays(**{k: np.array(g[k][sl]) for k, _ in t.QueueArrays.FIELDS})
+
+
+# ---------------------------------------------------------------------------------------------
+# K4 + K5: scorer and schedule order
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cname", sorted(CFGS))
+@pytest.mark.parametrize("policy", range(5))
+def test_scores_and_order_bit_exact_vs_reference(golden, scorer, cname, policy):
+    g = golden("ref_queue.npz")
+    q = golden_queue(g)
+    cfg = CFGS[cname]
+    models = t.cost_models_from_config(cfg)
+    assert np.array_equal(np.array([models.load.slope, models.load.intercept, models.comp.slope,
+                                    models.comp.intercept]), g[f"{cname}_models"])
+    tl, tc, pr, order = scorer.score(q, policy, models, cfg)
+    assert np.array_equal(tl.view(np.uint64), g[f"{cname}_p{policy}_t_load"])
+    assert np.array_equal(tc.view(np.uint64), g[f"{cname}_p{policy}_t_comp"])
+    assert np.array_equal(pr.view(np.uint64), g[f"{cname}_p{policy}_primary"])
+    assert np.array_equal(order, g[f"{cname}_p{policy}_order"])
+    # device-resident variant
+    out = scorer.score_device(DeviceQueue(q), policy, models, cfg)
+    assert out["err_index"] == -1
+    assert np.array_equal(out["primary"].cpu().numpy().view(np.uint64), g[f"{cname}_p{policy}_primary"])
+    assert np.array_equal(out["order"].cpu().numpy(), g[f"{cname}_p{policy}_order"])
+
+
+@pytest.mark.parametrize("policy", range(5))
+def test_order_equals_reference_pick_next_drain(golden, scorer, policy):
+    g = golden("ref_queue.npz")
+    q = golden_queue(g, slice(0, 300))
+    order = scorer.score(q, policy, t.cost_models_from_config(CFGS["default"]), CFGS["default"])[3]
+    assert np.array_equal(order, g[f"drain300_p{policy}"])
+
+
+def _req(i, arrival, deadline=None):
+    return t.RequestSpec(id=i, arrival_time=arrival, context_tokens=1000, query_tokens=10, deadline=deadline)
+
+
+def drain(queue, policy, costs):
+    """test_scheduler.cpp:26-31 -- repeated pick_next, here backed by the GPU scorer."""
+    queue = list(queue)
+    out = []
+    while (p := t.pick_next(queue, policy, costs, 0.0)) is not None:
+        out.append(p.id)
+    return out
+
+
+def test_reference_scheduler_cases_on_gpu():
+    """test_scheduler.cpp:42-89"""
+    costs = {1: t.ServiceCost(0.361, 0.019), 2: t.ServiceCost(0.199, 0.025)}
+    q = [_req(1, 0.0), _req(2, 0.0)]
+    assert drain(q, t.PolicyKind.SjfCost, costs) == [2, 1]
+    assert drain(q, t.PolicyKind.Fifo, costs) == [1, 2]
+    a, b = _req(1, 0.0, 1.0), _req(2, 0.0, 0.8)
+    costs = {1: t.ServiceCost(0.4, 0.1), 2: t.ServiceCost(0.05, 0.05)}
+    assert drain([a, b], t.PolicyKind.Lstf, costs) == [1, 2]
+    assert drain([a, b], t.PolicyKind.Edf, costs) == [2, 1]
+    costs = {i: t.ServiceCost(0.1, 0.1) for i in (7, 9, 11)}
+    assert drain([_req(7, 2.0), _req(9, 1.0)], t.PolicyKind.SjfCost, costs) == [9, 7]
+    assert drain([_req(11, 1.0), _req(7, 1.0), _req(9, 1.0)], t.PolicyKind.SjfCost, costs) == [7, 9, 11]
+    assert t.pick_next([], t.PolicyKind.Fifo, {}, 0.0) is None
+    with pytest.raises(t.MissingDeadline, match="edf: request 1 has no deadline"):
+        drain([_req(1, 0.0), _req(2, 0.0, 3.0)], t.PolicyKind.Edf, {})
+
+
+def test_missing_deadline_reports_first_queue_index(golden, scorer):
+    g = golden("ref_queue.npz")
+    q = golden_queue(g)
+    q.flags[[17, 40, 900]] &= np.uint8(0xFE)
+    for pol in (t.PolicyKind.Edf, t.PolicyKind.Lstf):
+        with pytest.raises(t.MissingDeadline, match=f"request {int(q.id[17])} has no deadline"):
+            scorer.score(q, pol, t.cost_models_from_config(CFGS["default"]), CFGS["default"])
+        out = None
+        with pytest.raises(t.MissingDeadline):
+            out = scorer.score_device(DeviceQueue(q), pol, t.cost_models_from_config(CFGS["default"]), CFGS["default"])
+        assert out is None
+
+
+def random_queue(n, seed):
+    rng = np.random.default_rng(seed)
+    q = t.QueueArrays(
+        n,
+        id=rng.permutation(n).astype(np.int64) * 3 - 7,
+        arrival=np.round(rng.random(n) * 1000, 1),
+        context_tokens=rng.integers(0, 200_000, n),
+        query_tokens=rng.integers(1, 4000, n),
+        cache_hit_ratio=rng.choice([0.0, 0.25, 0.5, 0.75, 0.9, 1.0, 0.3333333333333333], n),
+        flags=np.where(rng.random(n) < 0.03, 3, 1).astype(np.uint8),
+        deadline=np.round(rng.random(n) * 1000, 1) + 1000.0,
+        measured_t_load=np.round(rng.random(n), 2),
+        measured_t_comp=np.round(rng.random(n) * 0.1, 2),
+    )
+    q.arrival[100:2000] = 5.0  # heavy ties on arrival
+    return q
+
+
+@pytest.mark.parametrize("n", [1, 2, 2047, 2048, 2049, 4097, 100_000])
+@pytest.mark.parametrize("policy", [t.PolicyKind.Fifo, t.PolicyKind.SjfPt, t.PolicyKind.Lstf])
+def test_large_queue_matches_oracle(scorer, oracle, n, policy):
+    q = random_queue(n, n)
+    cfg = CFGS["default"]
+    m = t.cost_models_from_config(cfg)
+    tl, tc, pr, order = scorer.score(q, policy, m, cfg)
+    st, err, otl, otc, opr = oracle.score_queue(q, int(policy), [m.load.slope, m.load.intercept, m.comp.slope,
+                                                                 m.comp.intercept], cfg)
+    assert st == 0
+    assert np.array_equal(pr.view(np.uint64), opr.view(np.uint64))
+    assert np.array_equal(tl.view(np.uint64), otl.view(np.uint64))
+    assert np.array_equal(order, oracle.sort_order(opr, q.arrival, q.id))
+
+
+def test_signed_zero_and_infinite_keys_order(scorer, oracle):
+    q = t.QueueArrays(4, id=np.array([4, 3, 2, 1]), arrival=np.array([0.0, -0.0, 0.0, 1.0]),
+                      context_tokens=np.zeros(4, np.int64), query_tokens=np.ones(4, np.int64),
+                      cache_hit_ratio=np.ones(4), flags=np.array([3, 3, 3, 3], np.uint8),
+                      deadline=np.array([np.inf, 1.0, 1.0, np.inf]), measured_t_load=np.zeros(4),
+                      measured_t_comp=np.array([0.0, 1.0, 1.0, 0.0]))
+    for pol in range(5):
+        _, _, pr, order = scorer.score(q, pol, t.CostModelPair(), t.ClusterConfig())
+        assert np.array_equal(order, oracle.sort_order(pr, q.arrival, q.id)), pol
+
+
+# ---------------------------------------------------------------------------------------------
+# K3: prefix hasher
+# ---------------------------------------------------------------------------------------------
+def test_hash_frozen_vectors(golden):
+    g = golden("hash_frozen.npz")
+    assert np.array_equal(hasher.hash_prefix_chunks(g["offsets"], g["tokens"]), g["hashes"])
+
+
+def test_hash_random_and_unaligned_vs_oracle(oracle):
+    rng = np.random.default_rng(5)
+    lens = rng.integers(0, 3000, 400)
+    lens[:5] = [0, 255, 256, 257, 131072]
+    offs = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=offs[1:])  # arbitrary (mostly unaligned) request starts
+    doc = rng.integers(0, 7, len(lens))
+    shared = rng.integers(0, 3000, len(lens))
+    toks = oracle.gen_tokens(99, offs, doc, shared)
+    assert np.array_equal(hasher.hash_prefix_chunks(offs, toks), oracle.hash_prefix_chunks(offs, toks))
+
+
+def test_hash_device_path_and_token_generator(oracle):
+    rng = np.random.default_rng(6)
+    lens = (rng.integers(1, 600, 1000) * 4).astype(np.int64)
+    offs = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=offs[1:])
+    doc = rng.integers(0, 16, len(lens)).astype(np.int64)
+    shared = rng.integers(0, 2000, len(lens)).astype(np.int64)
+    dev = torch.device("cuda", 0)
+    d_offs, d_doc, d_sh = (torch.from_numpy(x).to(dev) for x in (offs, doc, shared))
+    d_tok = torch.empty(int(offs[-1]), dtype=torch.int32, device=dev)
+    hasher.gen_tokens_device(3, d_offs, d_doc, d_sh, d_tok)
+    want_tok = oracle.gen_tokens(3, offs, doc, shared)
+    assert np.array_equal(d_tok.cpu().numpy(), want_tok)
+    coff = hasher.chunk_offsets(offs)
+    d_out = torch.empty(int(coff[-1]), dtype=torch.int64, device=dev)
+    hasher.hash_prefix_chunks_device(d_offs, d_tok, torch.from_numpy(coff).to(dev), d_out)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy().view(np.uint64), oracle.hash_prefix_chunks(offs, want_tok))
+
+
+# ---------------------------------------------------------------------------------------------
+# K1 / K1b / CE+K2: L2 -> L1 ingest through the paged allocator
+# ---------------------------------------------------------------------------------------------
+SMALL = ingest.KVShape(layers=4, kv_heads=8, head_dim=128, chunk_tokens=256, page_tokens=16)
+
+
+def build_scenario(shape, n_slots=8, num_pages=200, seed=17):
+    """Pool of synthetic chunks; three requests through the L1 ledger (one deferred, then granted
+    after a release) so the block table is a non-trivial permutation of pages."""
+    pool = ingest.ChunkPool(shape, n_slots)
+    pool.fill_synthetic(seed)
+    arena = torch.zeros(shape.layers * 2 * num_pages * shape.page_tokens * shape.heads_local * shape.head_dim * 2,
+                        dtype=torch.uint8, device="cuda")
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=4, max_chunks=12, arena=arena)
+    cb = shape.page_bytes * shape.pages_per_chunk
+    items = []
+    # request 10: 6 chunks; request 11: 5 chunks; release 10; request 12: 7 chunks (partly deferred)
+    for c in range(6):
+        assert l1.request(10, c, cb)[0]
+    for c in range(5):
+        g, row11 = l1.request(11, c, cb)
+        assert g
+    granted_12 = []
+    for c in range(7):
+        g, row12 = l1.request(12, c, cb)
+        if g:
+            granted_12.append(c)
+    assert l1.deferred_count() > 0  # 18 chunks x 16 pages > 200 pages
+    grants = l1.release_request(10)
+    granted_12 += [b for (rid, b, row, nb) in grants if rid == 12]
+    assert l1.deferred_count() == 0 and sorted(granted_12) == list(range(7))
+    rng = np.random.default_rng(seed)
+    for c in range(5):
+        items.append((int(rng.integers(n_slots)), row11, c))
+    for c in range(7):
+        items.append((int(rng.integers(n_slots)), row12, c))
+    l1.sync_block_table()
+    return pool, l1, ingest.items_numpy(*zip(*items))
+
+
+def alloc_ref_block_table(shape, num_pages):
+    """alloc_ref (orc_pages FIFO free list) driven by the same ledger decisions as build_scenario."""
+    lib = po.restate()
+    pages = lib.orc_pages_new(num_pages)
+    ppc = shape.pages_per_chunk
+    rows = {}
+    buf = (C.c_int32 * ppc)()
+    def take(rid, c):
+        assert lib.orc_pages_take(pages, ppc, buf) == ppc
+        rows.setdefault(rid, {})[c] = list(buf)
+    for c in range(6):
+        take(10, c)
+    for c in range(5):
+        take(11, c)
+    pending = []
+    for c in range(7):
+        if lib.orc_pages_available(pages) >= ppc and not pending:
+            take(12, c)
+        else:
+            pending.append(c)
+    freed = [p for c in range(6) for p in rows.pop(10)[c]]
+    arr = (C.c_int32 * len(freed))(*freed)
+    lib.orc_pages_give(pages, len(freed), arr)
+    for c in pending:
+        take(12, c)
+    lib.orc_pages_free(pages)
+    return rows
+
+
+def test_page_ids_match_alloc_ref():
+    pool, l1, items = build_scenario(SMALL)
+    bt = l1.block_table()
+    want = alloc_ref_block_table(SMALL, l1.num_pages)
+    rows = {11: items["bt_row"][0], 12: items["bt_row"][-1]}
+    for rid, chunks in want.items():
+        for c, pages in chunks.items():
+            assert list(bt[rows[rid], c * 16:(c + 1) * 16]) == pages
+
+
+@pytest.mark.parametrize("mode", ["zerocopy", "bulk", "ce", "auto"])
+def test_ingest_bit_exact_vs_scatter_ref(oracle, mode):
+    pool, l1, items = build_scenario(SMALL)
+    ingest.ingest(l1, pool, items, mode=ingest.MODES[mode])
+    torch.cuda.synchronize()
+    got = l1.arena.cpu().numpy()
+    want = oracle.scatter_ref(SMALL, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
+    assert np.array_equal(got, want)
+    assert ingest.verify_synthetic(l1, pool, items, seed=17) == 0
+
+
+@pytest.mark.parametrize("tp", [(2, 0), (2, 1), (4, 3), (8, 5)])
+@pytest.mark.parametrize("mode", ["zerocopy", "bulk"])
+def test_ingest_head_sharded_bit_exact(oracle, tp, mode):
+    shape = SMALL.with_rank(*tp)
+    pool, l1, items = build_scenario(shape)
+    ingest.ingest(l1, pool, items, mode=ingest.MODES[mode])
+    torch.cuda.synchronize()
+    want = oracle.scatter_ref(shape, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+
+
+def test_ingest_per_layer_with_events_equals_whole(oracle):
+    pool, l1, items = build_scenario(SMALL)
+    s = torch.cuda.Stream()
+    evs = [torch.cuda.Event() for _ in range(SMALL.layers)]
+    with torch.cuda.stream(s):
+        for layer in range(SMALL.layers):
+            ingest.ingest(l1, pool, items, layer, layer + 1, mode=ingest.BULK, stream=s, done_event=evs[layer])
+    evs[-1].synchronize()
+    want = oracle.scatter_ref(SMALL, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+    # vLLM flash-attn view: [2, num_pages, page_tokens, heads, head_dim]
+    assert tuple(l1.layer(0).shape) == (2, 200, 16, 8, 128)
+
+
+def test_ingest_errors_fail_loudly():
+    pool, l1, items = build_scenario(SMALL)
+    with pytest.raises(t.ValidationError):
+        ingest.ingest(l1, pool, items, 3, 3)
+    with pytest.raises(t.Unsupported):
+        shp = SMALL.with_rank(2, 0)
+        p2, l2, it2 = build_scenario(shp)
+        ingest.ingest(l2, p2, it2, mode=ingest.CE)
+    with pytest.raises(t.CapacityError):
+        l1.request(99, 0, 10**15)
+    with pytest.raises(t.ValidationError):
+        l1.request(99, 0, 12345)  # not a whole number of pages
+    with pytest.raises(t.ValidationError):
+        l1.release_request(4242)
+
+
+@pytest.mark.parametrize("mode", ["bulk", "ce"])
+def test_config1_full_size_llama8b_32k(mode):
+    """configs[0]: Llama-3.1-8B KV, one 32K prefix = 128 chunks (4.29 GB) -> 2048 pages, per layer.
+    Size-independent checks: every byte of every page equals the synthetic word of the source
+    position it must come from (verify kernel), plus sampled segments compared on the host."""
+    shape = ingest.LLAMA31_8B
+    pool = ingest.ChunkPool(shape, 128)
+    pool.fill_synthetic(5)
+    l1 = ingest.PagedKVCache(shape, 2048, max_rows=1, max_chunks=128)
+    cb = shape.page_bytes * 16
+    rows = []
+    for c in range(128):
+        g, row = l1.request(1, c, cb)
+        assert g
+    assert l1.free_pages() == 0
+    items = ingest.items_numpy(np.random.default_rng(1).permutation(128), [row] * 128, np.arange(128))
+    l1.sync_block_table()
+    for layer in range(shape.layers):
+        ingest.ingest(l1, pool, items, layer, layer + 1, mode=ingest.MODES[mode])
+    torch.cuda.synchronize()
+    assert ingest.verify_synthetic(l1, pool, items, seed=5) == 0
+    bt = l1.block_table()
+    rng = np.random.default_rng(2)
+    poolv = pool.slot_view(0, 128).view(np.uint16).reshape(128, 32, 2, 256, 8, 128)
+    for _ in range(64):
+        i, layer, kv, j = rng.integers(128), rng.integers(32), rng.integers(2), rng.integers(16)
+        page = bt[row, items["chunk_index"][i] * 16 + j]
+        got = l1.layer(layer, torch.int16)[kv, page].cpu().numpy().view(np.uint16)
+        want = poolv[items["src_slot"][i], layer, kv, j * 16:(j + 1) * 16]
+        assert np.array_equal(got, want)
+    assert l1.release_request(1) == [] and l1.free_pages() == 2048
