@@ -257,9 +257,12 @@ int64_t tsb_l1_block_table_stride(const tsb_l1* l1);
 tsb_status tsb_l1_sync_block_table(tsb_l1* l1, void* stream);
 
 /* ------------------------------------------------------------------------------------ */
-/* L2 -> L1 ingest (K1 / CE+K2).  The real pcie_dispatch hop (engine.cpp:427-446, duration  */
-/* model engine.cpp:206-207).  One call moves every (item, layer in [layer_lo, layer_hi))   */
-/* of the batch; `done_event` (cudaEvent_t as void*, may be NULL) is recorded after it.     */
+/* L2 -> L1 ingest (K1 / K1b / CE+K2).  The real pcie_dispatch hop (engine.cpp:427-446,     */
+/* duration model engine.cpp:206-207).  One call moves every (item, layer in               */
+/* [layer_lo, layer_hi)) of the batch, layer by layer.  layer_events (NULL, or an array of  */
+/* layer_hi-layer_lo cudaEvent_t passed as void*, entries may be NULL): event k is recorded */
+/* on `stream` once layer layer_lo+k of every item is resident in L1 -- the per-layer fence */
+/* a prefill consumer waits on with cudaStreamWaitEvent.                                    */
 /* ------------------------------------------------------------------------------------ */
 typedef struct {
   int64_t src_slot;    /* L2 pool slot holding the chunk */
@@ -268,27 +271,34 @@ typedef struct {
 } tsb_ingest_item;
 
 typedef enum {
-  TSB_INGEST_AUTO = 0,     /* best measured mode for the shape */
+  TSB_INGEST_AUTO = 0,     /* CE for full-head shapes, ZEROCOPY for head-sharded shapes */
   TSB_INGEST_ZEROCOPY = 1, /* K1: SM 16B loads from mapped host memory, scatter to pages */
   TSB_INGEST_BULK = 2,     /* K1b: cp.async.bulk host->smem->pages, one issuing lane/CTA */
-  TSB_INGEST_CE = 3        /* copy-engine H2D into an HBM staging ring, then K2 scatter */
+  TSB_INGEST_CE = 3        /* copy engine H2D into an HBM staging ring, then K2 scatter;
+                              host reads run on an internal copy stream ordered after the
+                              work queued on `stream` before the call (tp_size == 1 only) */
 } tsb_ingest_mode;
 
 /* items: host array (copied into a pinned ring internally, so it may be reused on return).
  * All grants for the items must already be in the block table (tsb_l1_sync_block_table). */
 tsb_status tsb_ingest(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
                       int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
-                      void* done_event);
-/* Device-items variant (items already in device memory). */
+                      void* const* layer_events);
+/* Device-items variant (items already in device memory; CE mode needs host items and returns
+ * UNSUPPORTED here). */
 tsb_status tsb_ingest_device(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items_dev,
                              int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
-                             void* stream, void* done_event);
+                             void* stream, void* const* layer_events);
 /* K2 alone: scatter chunks already staged contiguously in HBM (src_slot indexes `staging`,
  * each slot = one full chunk, layers [layer_lo, layer_hi) only). */
 tsb_status tsb_scatter_device(tsb_l1* l1, const void* staging, const tsb_ingest_item* items_dev,
                               int64_t n_items, int64_t layer_lo, int64_t layer_hi, void* stream);
 /* Tuning knobs for measurement (0 = default). */
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas);
+/* CE copy strategy: 0 = one cudaMemcpyAsync per (item, layer range), 1 = one
+ * cudaMemcpy2DAsync per run of consecutive pool slots (default), 2 = cudaMemcpyBatchAsync.
+ * staging_bytes: HBM staging ring size (0 = default 512 MiB). */
+tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes);
 
 /* Harness check: counts bytes of the items' pages (layers [lo,hi)) that differ from the
  * synthetic pattern of their source slot (as filled by tsb_pool_fill_synthetic with `seed`);

@@ -143,8 +143,9 @@ _decl("tsb_l1_layer_ptr", vp, vp, i64)
 _decl("tsb_l1_block_table_host", vp, vp)
 _decl("tsb_l1_block_table_device", vp, vp)
 _decl("tsb_l1_sync_block_table", st, vp, vp)
-_decl("tsb_ingest", st, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, vp)
-_decl("tsb_ingest_device", st, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp)
+_decl("tsb_ingest", st, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, P(vp))
+_decl("tsb_ingest_device", st, vp, vp, vp, i64, i64, i64, C.c_int, vp, P(vp))
+_decl("tsb_ingest_set_ce", st, C.c_int, i64)
 _decl("tsb_scatter_device", st, vp, vp, vp, i64, i64, i64, vp)
 _decl("tsb_ingest_set_grid", st, C.c_int, C.c_int, C.c_int)
 _decl("tsb_l1_verify_synthetic", st, vp, P(IngestItem), i64, i64, i64, u64, i64, vp, P(u64))

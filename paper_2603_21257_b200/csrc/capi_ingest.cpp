@@ -30,9 +30,11 @@ using tsb::fail;
 namespace {
 
 struct Knobs {
-  int zerocopy_ctas = 32;
-  int bulk_ctas = 16;
+  int zerocopy_ctas = 64;
+  int bulk_ctas = 64;
   int scatter_ctas = 148 * 4;
+  int ce_variant = 1;
+  int64_t staging_bytes = 512ll << 20;
 };
 Knobs g_knobs;
 
@@ -191,9 +193,11 @@ struct tsb_l1 {
   uint8_t* staging = nullptr;  // CE staging (lazy)
   int64_t staging_bytes = 0;
   cudaStream_t ce_stream = nullptr;
+  cudaEvent_t ev_fence = nullptr;
   cudaEvent_t ev_ce[2] = {};
   cudaEvent_t ev_k2[2] = {};
   bool k2_used[2] = {};
+  int next_buf = 0;
   unsigned long long* verify_ctr = nullptr;
 };
 
@@ -207,6 +211,7 @@ void l1_free(tsb_l1* l) {
   cudaFree(l->bt_dev);
   cudaFree(l->staging);
   cudaFree(l->verify_ctr);
+  if (l->ev_fence) cudaEventDestroy(l->ev_fence);
   for (auto& e : l->ev_ce)
     if (e) cudaEventDestroy(e);
   for (auto& e : l->ev_k2)
@@ -407,8 +412,8 @@ tsb_status tsb_l1_sync_block_table(tsb_l1* l, void* stream) {
 }
 
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas) {
-  g_knobs.zerocopy_ctas = zerocopy_ctas > 0 ? zerocopy_ctas : 32;
-  g_knobs.bulk_ctas = bulk_ctas > 0 ? bulk_ctas : 16;
+  g_knobs.zerocopy_ctas = zerocopy_ctas > 0 ? zerocopy_ctas : 64;
+  g_knobs.bulk_ctas = bulk_ctas > 0 ? bulk_ctas : 64;
   g_knobs.scatter_ctas = scatter_ctas > 0 ? scatter_ctas : 148 * 4;
   return TSB_OK;
 }
@@ -441,81 +446,154 @@ tsb::IngestGeom make_geom(const tsb_l1* l, int64_t layer_lo, int64_t layer_hi) {
   return g;
 }
 
-int resolve_mode(const tsb_l1* l, int mode) {
+int resolve_mode(const tsb_l1* l, int mode, bool host_items) {
   if (mode != TSB_INGEST_AUTO) return mode;
-  return TSB_INGEST_BULK;
+  // Measured on B200 (profiles/r01_*): SM-initiated host reads plateau at ~92.6% of the copy
+  // engines' H2D rate, so full-head chunks go through CE + K2; head-sharded chunks have
+  // 256 B - 1 KiB runs that only the SM path reads without moving other ranks' heads.
+  return (l->shape.tp_size == 1 && host_items) ? TSB_INGEST_CE : TSB_INGEST_ZEROCOPY;
 }
 
-tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
-                     const tsb_ingest_item* items_host, int64_t n_items, int64_t lo, int64_t hi,
-                     cudaStream_t st) {
-  if (l->shape.tp_size != 1)
-    return fail(TSB_UNSUPPORTED, "ingest CE mode copies whole chunks; use zerocopy/bulk when tp_size > 1");
-  if (!items_host)
-    return fail(TSB_UNSUPPORTED, "ingest CE mode needs host-visible items (use tsb_ingest)");
-  tsb::IngestGeom g = make_geom(l, lo, hi);
-  const int64_t item_bytes = (hi - lo) * g.layer_src;
-  if (!l->staging) {
-    l->staging_bytes = std::max<int64_t>(256ll << 20, 4 * g.chunk_bytes);
-    TSB_CUDA_TRY(cudaMalloc(&l->staging, l->staging_bytes));
-    TSB_CUDA_TRY(cudaStreamCreateWithFlags(&l->ce_stream, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
-      TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_ce[b], cudaEventDisableTiming));
-      TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_k2[b], cudaEventDisableTiming));
+tsb_status ensure_staging(tsb_l1* l) {
+  if (l->staging) return TSB_OK;
+  l->staging_bytes = g_knobs.staging_bytes;
+  TSB_CUDA_TRY(cudaMalloc(&l->staging, l->staging_bytes));
+  TSB_CUDA_TRY(cudaStreamCreateWithFlags(&l->ce_stream, cudaStreamNonBlocking));
+  TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_fence, cudaEventDisableTiming));
+  for (int b = 0; b < 2; ++b) {
+    TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_ce[b], cudaEventDisableTiming));
+    TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_k2[b], cudaEventDisableTiming));
+  }
+  return TSB_OK;
+}
+
+// Copies layer `layer` of items [0, n) into stage (item k at stage + k*layer_bytes) on the
+// copy-engine stream.
+tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, int64_t n,
+                         int64_t layer, const tsb::IngestGeom& g, uint8_t* stage) {
+  const int64_t lb = g.layer_src;
+  const uint8_t* base = pool->host + layer * lb;
+  switch (g_knobs.ce_variant) {
+    case 0:
+      for (int64_t k = 0; k < n; ++k)
+        TSB_CUDA_TRY(cudaMemcpyAsync(stage + k * lb, base + it[k].src_slot * g.chunk_bytes, lb,
+                                     cudaMemcpyHostToDevice, l->ce_stream));
+      return TSB_OK;
+    case 2: {
+      std::vector<void*> dst(n), src(n);
+      std::vector<size_t> sz(n, static_cast<size_t>(lb));
+      for (int64_t k = 0; k < n; ++k) {
+        dst[k] = stage + k * lb;
+        src[k] = const_cast<uint8_t*>(base + it[k].src_slot * g.chunk_bytes);
+      }
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      attr.srcLocHint.type = cudaMemLocationTypeHost;
+      attr.dstLocHint.type = cudaMemLocationTypeDevice;
+      attr.dstLocHint.id = l->device;
+      size_t idx = 0, fail_idx = 0;
+      TSB_CUDA_TRY(cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), static_cast<size_t>(n),
+                                        &attr, &idx, 1, &fail_idx, l->ce_stream));
+      return TSB_OK;
+    }
+    default: {  // one 2D copy per run of consecutive pool slots (pitch = chunk bytes)
+      int64_t k = 0;
+      while (k < n) {
+        int64_t e = k + 1;
+        while (e < n && it[e].src_slot == it[e - 1].src_slot + 1) ++e;
+        TSB_CUDA_TRY(cudaMemcpy2DAsync(stage + k * lb, lb, base + it[k].src_slot * g.chunk_bytes,
+                                       g.chunk_bytes, lb, e - k, cudaMemcpyHostToDevice,
+                                       l->ce_stream));
+        k = e;
+      }
+      return TSB_OK;
     }
   }
+}
+
+// CE + K2: per layer and per staging group, the copy engine lands the items' layer slices in
+// one half of the HBM staging ring while K2 scatters the other half into pages.
+tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
+                     const tsb_ingest_item* items_host, int64_t n_items, int64_t lo, int64_t hi,
+                     cudaStream_t st, void* const* layer_events) {
+  if (l->shape.tp_size != 1)
+    return fail(TSB_UNSUPPORTED,
+                "ingest CE mode copies whole token rows; use zerocopy/bulk when tp_size > 1");
+  if (!items_host)
+    return fail(TSB_UNSUPPORTED, "ingest CE mode needs host-visible items (use tsb_ingest)");
+  TSB_TRY(ensure_staging(l));
+  tsb::IngestGeom g = make_geom(l, lo, lo + 1);
+  const int64_t lb = g.layer_src;
   const int64_t half = l->staging_bytes / 2;
-  const int64_t per_group = std::max<int64_t>(1, half / item_bytes);
-  if (item_bytes > half) return fail(TSB_UNSUPPORTED, "ingest CE: chunk range exceeds staging");
-  g.staged = 1;
-  g.item_stride = item_bytes;
-  // The CE stream must not run ahead of work the caller already queued on `st`.
-  TSB_CUDA_TRY(cudaEventRecord(l->ev_ce[0], st));
-  TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_ce[0], 0));
-  int buf = 0;
-  for (int64_t i0 = 0; i0 < n_items; i0 += per_group, buf ^= 1) {
-    const int64_t n = std::min(per_group, n_items - i0);
-    uint8_t* stage = l->staging + buf * half;
-    if (l->k2_used[buf]) TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_k2[buf], 0));
-    for (int64_t i = 0; i < n; ++i) {
-      const tsb_ingest_item& it = items_host[i0 + i];
-      const uint8_t* src = pool->host + it.src_slot * g.chunk_bytes + lo * g.layer_src;
-      TSB_CUDA_TRY(cudaMemcpyAsync(stage + i * item_bytes, src, item_bytes,
-                                   cudaMemcpyHostToDevice, l->ce_stream));
+  if (lb > half) return fail(TSB_UNSUPPORTED, "ingest CE: one chunk layer exceeds the staging ring");
+  const int64_t per_group = half / lb;
+  // Host reads are ordered after the work already queued on `st` (stream semantics).
+  TSB_CUDA_TRY(cudaEventRecord(l->ev_fence, st));
+  TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_fence, 0));
+  for (int64_t layer = lo; layer < hi; ++layer) {
+    g = make_geom(l, layer, layer + 1);
+    g.staged = 1;
+    g.item_stride = lb;
+    for (int64_t i0 = 0; i0 < n_items; i0 += per_group) {
+      const int64_t n = std::min(per_group, n_items - i0);
+      const int b = l->next_buf;
+      l->next_buf ^= 1;
+      uint8_t* stage = l->staging + b * half;
+      if (l->k2_used[b]) TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_k2[b], 0));
+      TSB_TRY(ce_copy_layer(l, pool, items_host + i0, n, layer, g, stage));
+      TSB_CUDA_TRY(cudaEventRecord(l->ev_ce[b], l->ce_stream));
+      TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_ce[b], 0));
+      TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, stage, l->arena, items_dev + i0, l->bt_dev, n,
+                                          g_knobs.scatter_ctas, st));
+      TSB_CUDA_TRY(cudaEventRecord(l->ev_k2[b], st));
+      l->k2_used[b] = true;
     }
-    TSB_CUDA_TRY(cudaEventRecord(l->ev_ce[buf], l->ce_stream));
-    TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_ce[buf], 0));
-    TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, stage, l->arena, items_dev + i0, l->bt_dev, n,
-                                        g_knobs.scatter_ctas, st));
-    TSB_CUDA_TRY(cudaEventRecord(l->ev_k2[buf], st));
-    l->k2_used[buf] = true;
+    if (layer_events && layer_events[layer - lo])
+      TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[layer - lo]), st));
+  }
+  return TSB_OK;
+}
+
+tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev, int64_t n_items,
+                     int64_t lo, int64_t hi, int mode, cudaStream_t st, void* const* layer_events) {
+  // One launch per layer when the caller wants per-layer fences, else one launch in total.
+  const int64_t step = layer_events ? 1 : hi - lo;
+  for (int64_t l0 = lo; l0 < hi; l0 += step) {
+    const tsb::IngestGeom g = make_geom(l, l0, l0 + step);
+    if (mode == TSB_INGEST_ZEROCOPY) {
+      TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
+                                          g_knobs.zerocopy_ctas, st));
+    } else {
+      if (g.seg_bytes * 6 > 200 * 1024)
+        return fail(TSB_UNSUPPORTED, "ingest bulk: page segment too large for the smem ring");
+      TSB_CUDA_TRY(tsb::launch_ingest_bulk(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
+                                           g_knobs.bulk_ctas, st));
+    }
+    if (layer_events && layer_events[l0 - lo])
+      TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[l0 - lo]), st));
   }
   return TSB_OK;
 }
 
 tsb_status ingest_impl(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
                        const tsb_ingest_item* items_host, int64_t n_items, int64_t lo, int64_t hi,
-                       int mode, cudaStream_t st) {
+                       int mode, cudaStream_t st, void* const* layer_events) {
   if (lo < 0 || hi > l->shape.layers || lo >= hi)
     return fail(TSB_VALIDATION, "ingest: layer range must satisfy 0 <= lo < hi <= layers");
   if (pool->chunk_bytes != make_geom(l, 0, 1).chunk_bytes)
     return fail(TSB_VALIDATION, "ingest: pool chunk geometry differs from the L1 shape");
-  if (n_items == 0) return TSB_OK;
-  mode = resolve_mode(l, mode);
-  const tsb::IngestGeom g = make_geom(l, lo, hi);
+  mode = resolve_mode(l, mode, items_host != nullptr);
+  if (n_items == 0) {
+    for (int64_t k = 0; layer_events && k < hi - lo; ++k)
+      if (layer_events[k]) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[k]), st));
+    return TSB_OK;
+  }
   switch (mode) {
     case TSB_INGEST_ZEROCOPY:
-      TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
-                                          g_knobs.zerocopy_ctas, st));
-      return TSB_OK;
     case TSB_INGEST_BULK:
-      if (g.seg_bytes * 6 > 200 * 1024)
-        return fail(TSB_UNSUPPORTED, "ingest bulk: page segment too large for the smem ring");
-      TSB_CUDA_TRY(tsb::launch_ingest_bulk(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
-                                           g_knobs.bulk_ctas, st));
-      return TSB_OK;
+      return ingest_sm(l, pool, items_dev, n_items, lo, hi, mode, st, layer_events);
     case TSB_INGEST_CE:
-      return ingest_ce(l, pool, items_dev, items_host, n_items, lo, hi, st);
+      return ingest_ce(l, pool, items_dev, items_host, n_items, lo, hi, st, layer_events);
     default:
       return fail(TSB_VALIDATION, "ingest: unknown mode " + std::to_string(mode));
   }
@@ -527,28 +605,32 @@ extern "C" {
 
 tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
                       int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
-                      void* done_event) {
+                      void* const* layer_events) {
   auto st = static_cast<cudaStream_t>(stream);
   const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb_ingest_item));
-  for (int64_t i0 = 0; i0 < n_items; i0 += per) {
-    const int64_t n = std::min(per, n_items - i0);
-    void* dptr = nullptr;
-    int slot = 0;
-    TSB_TRY(l->ring_items.stage(items + i0, sizeof(tsb_ingest_item) * n, st, &dptr, &slot));
-    TSB_TRY(ingest_impl(l, pool, static_cast<const tsb_ingest_item*>(dptr), items + i0, n,
-                        layer_lo, layer_hi, mode, st));
-    TSB_TRY(l->ring_items.fence(slot, st));
-  }
-  if (done_event) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(done_event), st));
+  if (n_items > per)
+    return fail(TSB_VALIDATION, "ingest: at most " + std::to_string(per) + " items per call");
+  void* dptr = nullptr;
+  int slot = 0;
+  if (n_items > 0)
+    TSB_TRY(l->ring_items.stage(items, sizeof(tsb_ingest_item) * n_items, st, &dptr, &slot));
+  TSB_TRY(ingest_impl(l, pool, static_cast<const tsb_ingest_item*>(dptr), items, n_items,
+                      layer_lo, layer_hi, mode, st, layer_events));
+  if (n_items > 0) TSB_TRY(l->ring_items.fence(slot, st));
   return TSB_OK;
 }
 
 tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
                              int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
-                             void* stream, void* done_event) {
-  auto st = static_cast<cudaStream_t>(stream);
-  TSB_TRY(ingest_impl(l, pool, items_dev, nullptr, n_items, layer_lo, layer_hi, mode, st));
-  if (done_event) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(done_event), st));
+                             void* stream, void* const* layer_events) {
+  return ingest_impl(l, pool, items_dev, nullptr, n_items, layer_lo, layer_hi, mode,
+                     static_cast<cudaStream_t>(stream), layer_events);
+}
+
+tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes) {
+  if (variant < 0 || variant > 2) return fail(TSB_VALIDATION, "ingest_set_ce: variant must be 0, 1 or 2");
+  g_knobs.ce_variant = variant;
+  g_knobs.staging_bytes = staging_bytes > 0 ? staging_bytes : (512ll << 20);
   return TSB_OK;
 }
 

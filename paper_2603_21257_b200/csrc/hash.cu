@@ -5,8 +5,7 @@
 // oracle/tsb_oracle.c (orc_hash_prefix_chunks) keeps FNV-1a's constants and step but makes a
 // 256-token chunk warp-parallel: lane j folds tokens [8j, 8j+8) as 64-bit FNV words, a 5-level
 // shuffle tree pairs the 32 leaves, and the chunk digests are chained per request so hash c
-// names the whole prefix [0, 256(c+1)).  One CTA per request; 4 warps compute digests of a
-// window of chunks (two chunks per warp in flight), then one thread chains the window.
+// names the whole prefix [0, 256(c+1)).  One warp per request, kUnroll chunks in flight.
 // HBM-bound: 4 B/token read + 8 B/chunk written.
 #include "common.cuh"
 #include "kernels.h"
@@ -19,9 +18,8 @@ __device__ __forceinline__ uint64_t fpair(uint64_t a, uint64_t b) {
   return fstep(fstep(kFnvOffset, a), b);
 }
 
-constexpr int kHashThreads = 128;
+constexpr int kHashThreads = 256;
 constexpr int kHashWarps = kHashThreads / 32;
-constexpr int kWin = 512;
 
 __device__ __forceinline__ uint64_t leaf8(const int32_t (&t)[8]) {
   uint64_t h = kFnvOffset;
@@ -51,43 +49,40 @@ __device__ __forceinline__ void load8(const int32_t* p, bool aligned, int32_t (&
   }
 }
 
-__global__ void __launch_bounds__(kHashThreads) k_hash_prefix(const int64_t* __restrict__ offsets,
+// One warp per request: chunks are processed kUnroll at a time (all their loads issued before
+// any is consumed), lane 0 folds each digest into the request's chain as it goes and stores the
+// running hash.  No block-level synchronisation; ~kUnroll KiB in flight per warp.
+constexpr int kUnroll = 4;
+
+__global__ void __launch_bounds__(kHashThreads) k_hash_prefix(int64_t n_req,
+                                                              const int64_t* __restrict__ offsets,
                                                               const int32_t* __restrict__ tokens,
                                                               const int64_t* __restrict__ chunk_offsets,
                                                               uint64_t* __restrict__ out) {
-  __shared__ uint64_t dig[kWin];
-  const int64_t r = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(kHashWarps) + (threadIdx.x >> 5);
+  if (r >= n_req) return;
+  const int lane = threadIdx.x & 31;
   const int64_t t0 = offsets[r];
   const int64_t nchunks = (offsets[r + 1] - t0) / 256;
   const int64_t c0 = chunk_offsets[r];
   const bool aligned = (t0 & 3) == 0;
+  const int32_t* base = tokens + t0 + lane * 8;
   uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
-  for (int64_t w0 = 0; w0 < nchunks; w0 += kWin) {
-    const int wn = static_cast<int>(nchunks - w0 < kWin ? nchunks - w0 : kWin);
-    for (int c = warp * 2; c < wn; c += kHashWarps * 2) {
-      const bool two = c + 1 < wn;
-      int32_t ta[8], tb[8];
-      const int32_t* base = tokens + t0 + (w0 + c) * 256 + lane * 8;
-      load8(base, aligned, ta);
-      if (two) load8(base + 256, aligned, tb);
-      const uint64_t da = tree32(leaf8(ta), lane);
-      const uint64_t db = two ? tree32(leaf8(tb), lane) : 0;
-      if (lane == 0) {
-        dig[c] = da;
-        if (two) dig[c + 1] = db;
+  for (int64_t c = 0; c < nchunks; c += kUnroll) {
+    int32_t tk[kUnroll][8];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (c + u < nchunks) load8(base + (c + u) * 256, aligned, tk[u]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (c + u < nchunks) {
+        const uint64_t d = tree32(leaf8(tk[u]), lane);
+        if (lane == 0) {
+          h = fpair(h, d);
+          out[c0 + c + u] = h;
+        }
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int c = 0; c < wn; ++c) {
-        h = fpair(h, dig[c]);
-        dig[c] = h;
-      }
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < wn; c += kHashThreads) out[c0 + w0 + c] = dig[c];
-    __syncthreads();
   }
 }
 
@@ -112,9 +107,9 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
-  // grid.x limit is 2^31-1: one CTA per request.
-  k_hash_prefix<<<static_cast<unsigned>(n_req), kHashThreads, 0, st>>>(offsets, tokens,
-                                                                      chunk_offsets, out);
+  const int64_t grid = (n_req + kHashWarps - 1) / kHashWarps;
+  k_hash_prefix<<<static_cast<unsigned>(grid), kHashThreads, 0, st>>>(n_req, offsets, tokens,
+                                                                     chunk_offsets, out);
   count_launch();
   return cudaGetLastError();
 }

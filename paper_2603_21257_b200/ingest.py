@@ -217,21 +217,31 @@ def _items_ptr(items):
     return items, len(items)
 
 
+def _events(layer_events, n_layers):
+    if layer_events is None:
+        return None
+    assert len(layer_events) == n_layers, "one event (or None) per layer of the range"
+    arr = (C.c_void_p * n_layers)()
+    for i, e in enumerate(layer_events):
+        arr[i] = e.cuda_event if e is not None else None
+    return arr
+
+
 def ingest(l1: PagedKVCache, pool: ChunkPool, items, layer_lo: int = 0, layer_hi: Optional[int] = None,
-           mode: int = AUTO, stream=None, done_event: Optional[torch.cuda.Event] = None):
-    """tsb_ingest: moves every (item, layer in [layer_lo, layer_hi)) L2 -> L1 (async)."""
+           mode: int = AUTO, stream=None, layer_events: Optional[Sequence] = None):
+    """tsb_ingest: moves every (item, layer in [layer_lo, layer_hi)) L2 -> L1 (async on `stream`);
+    layer_events[k] (torch.cuda.Event or None) is recorded once layer layer_lo+k is resident."""
     layer_hi = l1.shape.layers if layer_hi is None else layer_hi
     ptr, n = _items_ptr(items)
-    ev = done_event.cuda_event if done_event is not None else None
-    check(lib.tsb_ingest(l1.handle, pool.handle, ptr, n, layer_lo, layer_hi, int(mode), _stream(stream), ev))
+    check(lib.tsb_ingest(l1.handle, pool.handle, ptr, n, layer_lo, layer_hi, int(mode), _stream(stream),
+                         _events(layer_events, layer_hi - layer_lo)))
 
 
 def ingest_device(l1: PagedKVCache, pool: ChunkPool, items_dev: torch.Tensor, n_items: int, layer_lo: int = 0,
-                  layer_hi: Optional[int] = None, mode: int = AUTO, stream=None, done_event=None):
+                  layer_hi: Optional[int] = None, mode: int = AUTO, stream=None, layer_events=None):
     layer_hi = l1.shape.layers if layer_hi is None else layer_hi
-    ev = done_event.cuda_event if done_event is not None else None
     check(lib.tsb_ingest_device(l1.handle, pool.handle, items_dev.data_ptr(), int(n_items), layer_lo, layer_hi,
-                                int(mode), _stream(stream), ev))
+                                int(mode), _stream(stream), _events(layer_events, layer_hi - layer_lo)))
 
 
 def verify_synthetic(l1: PagedKVCache, pool: ChunkPool, items, seed: int, layer_lo: int = 0,
@@ -246,3 +256,8 @@ def verify_synthetic(l1: PagedKVCache, pool: ChunkPool, items, seed: int, layer_
 
 def set_grid(zerocopy_ctas: int = 0, bulk_ctas: int = 0, scatter_ctas: int = 0):
     check(lib.tsb_ingest_set_grid(zerocopy_ctas, bulk_ctas, scatter_ctas))
+
+
+def set_ce(variant: int = 1, staging_bytes: int = 0):
+    """CE copy strategy: 0 per-item memcpy, 1 2D per consecutive-slot run (default), 2 batch API."""
+    check(lib.tsb_ingest_set_ce(variant, staging_bytes))

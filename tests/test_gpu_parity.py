@@ -251,7 +251,8 @@ def alloc_ref_block_table(shape, num_pages):
             take(12, c)
         else:
             pending.append(c)
-    freed = [p for c in range(6) for p in rows.pop(10)[c]]
+    rows10 = rows.pop(10)
+    freed = [p for c in range(6) for p in rows10[c]]
     arr = (C.c_int32 * len(freed))(*freed)
     lib.orc_pages_give(pages, len(freed), arr)
     for c in pending:
@@ -281,6 +282,22 @@ def test_ingest_bit_exact_vs_scatter_ref(oracle, mode):
     assert ingest.verify_synthetic(l1, pool, items, seed=17) == 0
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_ingest_ce_copy_variants_bit_exact(oracle, variant):
+    """CE strategies: per-item memcpy, 2D copy per run of consecutive slots, batched memcpy."""
+    pool, l1, items = build_scenario(SMALL)
+    items["src_slot"] = (np.arange(len(items)) + 2) % pool.n_slots  # runs 2..7, 0..5
+    ingest.set_ce(variant)
+    try:
+        ingest.ingest(l1, pool, items, mode=ingest.CE)
+        ingest.ingest(l1, pool, items[::-1].copy(), 1, 3, mode=ingest.CE)
+        torch.cuda.synchronize()
+    finally:
+        ingest.set_ce(1)
+    want = oracle.scatter_ref(SMALL, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("tp", [(2, 0), (2, 1), (4, 3), (8, 5)])
 @pytest.mark.parametrize("mode", ["zerocopy", "bulk"])
 def test_ingest_head_sharded_bit_exact(oracle, tp, mode):
@@ -295,13 +312,21 @@ def test_ingest_head_sharded_bit_exact(oracle, tp, mode):
 def test_ingest_per_layer_with_events_equals_whole(oracle):
     pool, l1, items = build_scenario(SMALL)
     s = torch.cuda.Stream()
-    evs = [torch.cuda.Event() for _ in range(SMALL.layers)]
-    with torch.cuda.stream(s):
-        for layer in range(SMALL.layers):
-            ingest.ingest(l1, pool, items, layer, layer + 1, mode=ingest.BULK, stream=s, done_event=evs[layer])
-    evs[-1].synchronize()
     want = oracle.scatter_ref(SMALL, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
-    assert np.array_equal(l1.arena.cpu().numpy(), want)
+    for mode in (ingest.BULK, ingest.ZEROCOPY, ingest.CE):
+        l1.arena.zero_()
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event() for _ in range(SMALL.layers)]
+        with torch.cuda.stream(s):
+            ingest.ingest(l1, pool, items, 0, 2, mode=mode, stream=s, layer_events=evs[:2])
+            for layer in range(2, SMALL.layers):
+                ingest.ingest(l1, pool, items, layer, layer + 1, mode=mode, stream=s, layer_events=[evs[layer]])
+        for layer, e in enumerate(evs):
+            e.synchronize()
+            page0 = l1.block_table()[items["bt_row"][0], items["chunk_index"][0] * 16]
+            assert l1.layer(layer, torch.int16)[0, page0].abs().sum().item() > 0
+        evs[-1].synchronize()
+        assert np.array_equal(l1.arena.cpu().numpy(), want), mode
     # vLLM flash-attn view: [2, num_pages, page_tokens, heads, head_dim]
     assert tuple(l1.layer(0).shape) == (2, 200, 16, 8, 128)
 

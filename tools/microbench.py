@@ -36,7 +36,7 @@ def timed(fn, reps=5, warm=2, stream=None):
     return min(ts), float(np.median(ts))
 
 
-def bench_ingest(shape, n_chunks, modes, per_layer, grids=None):
+def bench_ingest(shape, n_chunks, modes, per_layer, grids=None, ce_variants=(1,), slots=None):
     res = []
     pool = ingest.ChunkPool(shape, n_chunks)
     pool.fill_synthetic(3)
@@ -45,30 +45,25 @@ def bench_ingest(shape, n_chunks, modes, per_layer, grids=None):
     for c in range(n_chunks):
         g, row = l1.request(1, c, cb)
     l1.sync_block_table()
-    items = ingest.items_numpy(np.arange(n_chunks), [row] * n_chunks, np.arange(n_chunks))
-    dev_items = torch.from_numpy(items.view(np.uint8).copy()).cuda()
+    src = np.arange(n_chunks) if slots is None else slots
+    items = ingest.items_numpy(src, [row] * n_chunks, np.arange(n_chunks))
     payload = n_chunks * shape.local_chunk_bytes
+    evs = [torch.cuda.Event() for _ in range(shape.layers)] if per_layer else None
     for mode in modes:
         for g in (grids or [0]):
-            if mode == "zerocopy":
-                ingest.set_grid(zerocopy_ctas=g)
-            elif mode == "bulk":
-                ingest.set_grid(bulk_ctas=g)
-            if mode == "ce":
-                fn = (lambda: [ingest.ingest(l1, pool, items, l, l + 1, mode=ingest.CE) for l in range(shape.layers)]) \
-                    if per_layer else (lambda: ingest.ingest(l1, pool, items, mode=ingest.CE))
-            else:
+            for v in (ce_variants if mode == "ce" else (1,)):
+                ingest.set_grid(zerocopy_ctas=g if mode == "zerocopy" else 0, bulk_ctas=g if mode == "bulk" else 0)
+                ingest.set_ce(v)
                 m = ingest.MODES[mode]
-                fn = (lambda: [ingest.ingest_device(l1, pool, dev_items, n_chunks, l, l + 1, mode=m)
-                               for l in range(shape.layers)]) if per_layer else \
-                    (lambda: ingest.ingest_device(l1, pool, dev_items, n_chunks, mode=m))
-            best, med = timed(fn, reps=3, warm=1)
-            ok = ingest.verify_synthetic(l1, pool, items, 3)
-            res.append(dict(shape=f"L{shape.layers}H{shape.kv_heads}tp{shape.tp_size}", chunks=n_chunks, mode=mode,
-                            grid=g, per_layer=per_layer, GBps=payload / best / 1e9, med_GBps=payload / med / 1e9,
-                            mismatches=ok))
-            print(json.dumps(res[-1]), flush=True)
+                fn = lambda: ingest.ingest(l1, pool, items, mode=m, layer_events=evs)
+                best, med = timed(fn, reps=3, warm=1)
+                ok = ingest.verify_synthetic(l1, pool, items, 3)
+                res.append(dict(shape=f"L{shape.layers}H{shape.kv_heads}tp{shape.tp_size}", chunks=n_chunks,
+                                mode=mode, ce_variant=v, grid=g, per_layer=per_layer, GBps=payload / best / 1e9,
+                                med_GBps=payload / med / 1e9, mismatches=ok))
+                print(json.dumps(res[-1]), flush=True)
     ingest.set_grid()
+    ingest.set_ce()
     pool.close()
     l1.close()
     return res
@@ -125,13 +120,14 @@ if __name__ == "__main__":
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
     bench_ce_peak()
-    bench_scorer()
-    bench_hash()
-    bench_ingest(ingest.LLAMA31_8B, 128, ["bulk", "zerocopy", "ce"], per_layer=True)
+    bench_ingest(ingest.LLAMA31_8B, 128, ["ce"], per_layer=True, ce_variants=(0, 1, 2))
+    bench_ingest(ingest.LLAMA31_8B, 128, ["ce"], per_layer=True, ce_variants=(0, 1, 2),
+                 slots=np.random.default_rng(0).permutation(128))
     bench_ingest(ingest.LLAMA31_8B, 128, ["bulk", "zerocopy", "ce"], per_layer=False)
-    bench_ingest(ingest.LLAMA31_8B, 128, ["bulk"], per_layer=False, grids=[4, 8, 16, 32, 64])
-    bench_ingest(ingest.LLAMA31_8B, 128, ["zerocopy"], per_layer=False, grids=[8, 16, 32, 64, 148])
+    bench_ingest(ingest.QWEN25_32B, 460, ["ce", "bulk"], per_layer=True)
     for tp in (2, 4, 8):
         shp = ingest.LLAMA3_70B.with_rank(tp, tp - 1)
-        bench_ingest(shp, 128, ["bulk", "zerocopy"], per_layer=True)
-        bench_ingest(shp, 128, ["bulk", "zerocopy"], per_layer=False, grids=[16, 64])
+        bench_ingest(shp, 128, ["bulk", "zerocopy"], per_layer=True, grids=[32, 64, 128])
+    if not a.quick:
+        bench_scorer()
+        bench_hash()

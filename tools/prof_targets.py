@@ -1,0 +1,51 @@
+"""Small, single-purpose workloads for ncu (one GPU, short):  python tools/prof_targets.py <what>
+
+what: scorer | hash | ingest-ce | ingest-bulk | ingest-zerocopy | ingest-tp8
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tools"))
+from microbench import bench_hash, bench_scorer  # noqa: E402
+from paper_2603_21257_b200 import ingest  # noqa: E402
+
+
+def ingest_once(shape, n_chunks, mode, reps=2):
+    pool = ingest.ChunkPool(shape, n_chunks)
+    pool.fill_synthetic(3)
+    l1 = ingest.PagedKVCache(shape, n_chunks * shape.pages_per_chunk, 1, n_chunks)
+    cb = shape.page_bytes * shape.pages_per_chunk
+    for c in range(n_chunks):
+        g, row = l1.request(1, c, cb)
+    l1.sync_block_table()
+    items = ingest.items_numpy(np.arange(n_chunks), [row] * n_chunks, np.arange(n_chunks))
+    evs = [torch.cuda.Event() for _ in range(shape.layers)]
+    for _ in range(reps):
+        ingest.ingest(l1, pool, items, mode=mode, layer_events=evs)
+    torch.cuda.synchronize()
+    assert ingest.verify_synthetic(l1, pool, items, 3) == 0
+
+
+if __name__ == "__main__":
+    what = sys.argv[1]
+    if what == "scorer":
+        bench_scorer()
+    elif what == "hash":
+        bench_hash()
+    elif what == "ingest-ce":
+        ingest_once(ingest.LLAMA31_8B, 128, ingest.CE)
+    elif what == "ingest-bulk":
+        ingest_once(ingest.LLAMA31_8B, 128, ingest.BULK)
+    elif what == "ingest-zerocopy":
+        ingest_once(ingest.LLAMA31_8B, 128, ingest.ZEROCOPY)
+    elif what == "ingest-tp8":
+        ingest_once(ingest.LLAMA3_70B.with_rank(8, 7), 128, ingest.ZEROCOPY)
+    else:
+        raise SystemExit(__doc__)
