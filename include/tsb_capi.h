@@ -246,6 +246,8 @@ int64_t tsb_l1_deferred(const tsb_l1* l1);
 int64_t tsb_l1_free_pages(const tsb_l1* l1);
 int64_t tsb_l1_num_pages(const tsb_l1* l1);
 int64_t tsb_l1_page_bytes(const tsb_l1* l1);
+int tsb_l1_device(const tsb_l1* l1);
+tsb_status tsb_l1_shape(const tsb_l1* l1, tsb_kv_shape* out);
 void* tsb_l1_arena(tsb_l1* l1);
 void* tsb_l1_layer_ptr(tsb_l1* l1, int64_t layer);
 /* Host (pinned) mirror of the block table, [max_rows][max_chunks*pages_per_chunk] int32,
@@ -299,6 +301,79 @@ tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_cta
  * cudaMemcpy2DAsync per run of consecutive pool slots (default), 2 = cudaMemcpyBatchAsync.
  * staging_bytes: HBM staging ring size (0 = default 512 MiB). */
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes);
+
+/* ------------------------------------------------------------------------------------ */
+/* Load stage: the real-time L2->L1 dispatcher.  Follows SimEngine's dispatch semantics    */
+/* (engine.cpp:290-302 pump, :341-355 admit, :405-425 proactive L1 reservation at dispatch, */
+/* :427-446 pcie_dispatch, :258-272 PcieDone, :280-282 L1 release at ComputeDone) with real */
+/* bytes and real time: requests are scored and ordered on the GPU (K4/K5), admitted in     */
+/* pick order, every planned chunk reserves L1 pages through the TierLedger-semantics        */
+/* allocator (grant-before-hop; deferred reservations are granted FIFO as earlier requests  */
+/* release), granted chunks are ingested per request in pick order, and a request's pages   */
+/* are released when its ingest (and optional synthetic prefill) completes.                 */
+/* ------------------------------------------------------------------------------------ */
+typedef struct tsb_stage tsb_stage;
+
+typedef struct {
+  int32_t mode;         /* tsb_ingest_mode */
+  int32_t policy;       /* tsb_policy used for the admission (pick) order */
+  int32_t layer_events; /* 1: per-layer fences per request (layer-pipelined prefill) */
+  int32_t prefill;      /* 1: synthetic prefill K6 per request after/with its ingest, lasting
+                           compute_base + compute_per_token*n + compute_quadratic*n^2 seconds
+                           (engine.cpp:210-212); 0: pages are released once resident */
+  int32_t prefill_ctas; /* CTAs per K6 launch (0 = 148) */
+  int32_t record_trace; /* 1: keep TraceEvent-schema rows (events.hpp:33-42) for the run */
+  uint64_t verify_seed; /* harness check, 0 = off: before a request's pages are released, count
+                           page words differing from tsb_pool_fill_synthetic(verify_seed) */
+} tsb_stage_options;
+
+typedef struct {
+  int64_t request_id;
+  int32_t pick_position;   /* index in the admission order */
+  int32_t deferred_chunks; /* chunk reservations that waited for a release */
+  int64_t chunks;          /* chunks ingested (derive_block_plan size) */
+  int64_t bytes;           /* bytes moved L2 -> L1 for this request on this GPU */
+  double first_layer_ms;   /* run start -> layer lo of every chunk resident (CUDA events) */
+  double resident_ms;      /* run start -> all layers resident (Timestamps::l1_resident) */
+  double done_ms;          /* run start -> prefill done / pages released */
+} tsb_stage_request;
+
+typedef struct {
+  int64_t bytes;           /* total L2 -> L1 bytes of the run */
+  double device_ms;        /* first ingest start -> last request resident (CUDA events) */
+  double wall_ms;          /* host wall time of tsb_stage_run */
+  int64_t ingest_calls;
+  int64_t deferred_chunks;
+  int64_t releases;
+  int64_t kernel_launches; /* libtsb kernels launched during the run */
+  uint64_t verify_mismatches; /* with verify_seed != 0 */
+} tsb_stage_stats;
+
+/* TraceEvent row (events.hpp:33-42): kind 1 TransferDone, 2 AllocationGrant, 4 DispatchWake;
+ * stage 1 Pcie, 2 Compute; tier 2 L1 (or -1); time in seconds from run start (host clock for
+ * dispatch/grant rows, CUDA events for TransferDone rows). */
+typedef struct {
+  double time;
+  uint64_t seq;
+  int32_t kind;
+  int32_t stage;
+  int32_t tier;
+  int32_t block_index;
+  int64_t request_id;
+  int64_t bytes;
+} tsb_trace_row;
+
+tsb_status tsb_stage_create(tsb_l1* l1, tsb_pool* pool, tsb_stage** out);
+void tsb_stage_destroy(tsb_stage* s);
+/* Runs one batch to completion (synchronises).  Request i's planned chunk c is stored in pool
+ * slot slots[slot_offsets[i] + c]; slot_offsets has n+1 entries and each request must list
+ * exactly derive_block_plan(spec_i).size() slots.  results may be NULL. */
+tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_cluster* c,
+                         const double models[4], const int64_t* slot_offsets,
+                         const int64_t* slots, const tsb_stage_options* opt, void* stream,
+                         tsb_stage_request* results, tsb_stage_stats* stats);
+/* Trace of the last run (when record_trace was set): copies min(n, cap) rows. */
+tsb_status tsb_stage_trace(tsb_stage* s, tsb_trace_row* out, int64_t cap, int64_t* n);
 
 /* Harness check: counts bytes of the items' pages (layers [lo,hi)) that differ from the
  * synthetic pattern of their source slot (as filled by tsb_pool_fill_synthetic with `seed`);

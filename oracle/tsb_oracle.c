@@ -410,9 +410,12 @@ void orc_gen_tokens(uint64_t seed, int64_t n_req, const int64_t* offsets, const 
 /* (engine.cpp:500-507, seeded with 0xcbf29ce484222325 at :518); it has no     */
 /* prefix hasher.  Definition (frozen here, GPU must match): */
 /*   step(h, w)  = (h ^ w) * FNV_PRIME           (FNV-1a on a 64-bit word)     */
-/*   leaf j      = fold step over tokens [8j, 8j+8) of the chunk from FNV_OFFSET */
+/*   word k      = u32 tok[2k] | u32 tok[2k+1] << 32 (the little-endian 8-byte  */
+/*                 image of two consecutive int32 token ids)                   */
+/*   leaf j      = fold step over words [8j, 8j+8) of the chunk from FNV_OFFSET */
+/*                 (j = 0..15, i.e. 16 tokens per leaf)                         */
 /*   pair(a, b)  = step(step(FNV_OFFSET, a), b)                                 */
-/*   digest      = 5-level pairwise tree of pair() over the 32 leaves, lane order */
+/*   digest      = 4-level pairwise tree of pair() over the 16 leaves, in order */
 /*   H_c         = pair(H_{c-1}, digest_c),  H_{-1} = rotl(FNV_OFFSET, 32)       */
 /* Only full 256-token chunks are hashed (floor rule, types.cpp:73-79).        */
 /* ------------------------------------------------------------------------ */
@@ -431,13 +434,16 @@ static inline uint64_t step(uint64_t h, uint64_t w) { return (h ^ w) * FNV_PRIME
 static inline uint64_t pair(uint64_t a, uint64_t b) { return step(step(FNV_OFFSET, a), b); }
 
 uint64_t orc_chunk_digest(const int32_t* tok) {
-  uint64_t node[32];
-  for (int j = 0; j < 32; ++j) {
+  uint64_t node[16];
+  for (int j = 0; j < 16; ++j) {
     uint64_t h = FNV_OFFSET;
-    for (int t = 0; t < 8; ++t) h = step(h, (uint64_t)(uint32_t)tok[8 * j + t]);
+    for (int k = 0; k < 8; ++k) {
+      const int t = 16 * j + 2 * k;
+      h = step(h, (uint64_t)(uint32_t)tok[t] | ((uint64_t)(uint32_t)tok[t + 1] << 32));
+    }
     node[j] = h;
   }
-  for (int width = 16; width >= 1; width /= 2)
+  for (int width = 8; width >= 1; width /= 2)
     for (int i = 0; i < width; ++i) node[i] = pair(node[2 * i], node[2 * i + 1]);
   return node[0];
 }

@@ -85,6 +85,26 @@ class IngestItem(C.Structure):
     _fields_ = [("src_slot", i64), ("bt_row", i32), ("chunk_index", i32)]
 
 
+class StageOptions(C.Structure):
+    _fields_ = [("mode", i32), ("policy", i32), ("layer_events", i32), ("prefill", i32), ("prefill_ctas", i32),
+                ("record_trace", i32), ("verify_seed", u64)]
+
+
+class StageRequest(C.Structure):
+    _fields_ = [("request_id", i64), ("pick_position", i32), ("deferred_chunks", i32), ("chunks", i64),
+                ("bytes", i64), ("first_layer_ms", f64), ("resident_ms", f64), ("done_ms", f64)]
+
+
+class StageStats(C.Structure):
+    _fields_ = [("bytes", i64), ("device_ms", f64), ("wall_ms", f64), ("ingest_calls", i64),
+                ("deferred_chunks", i64), ("releases", i64), ("kernel_launches", i64), ("verify_mismatches", u64)]
+
+
+class TraceRow(C.Structure):
+    _fields_ = [("time", f64), ("seq", u64), ("kind", i32), ("stage", i32), ("tier", i32), ("block_index", i32),
+                ("request_id", i64), ("bytes", i64)]
+
+
 HAS_DEADLINE, HAS_MEASURED = 1, 2
 INGEST_AUTO, INGEST_ZEROCOPY, INGEST_BULK, INGEST_CE = range(4)
 
@@ -148,6 +168,13 @@ _decl("tsb_ingest_device", st, vp, vp, vp, i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_set_ce", st, C.c_int, i64)
 _decl("tsb_scatter_device", st, vp, vp, vp, i64, i64, i64, vp)
 _decl("tsb_ingest_set_grid", st, C.c_int, C.c_int, C.c_int)
+_decl("tsb_l1_device", C.c_int, vp)
+_decl("tsb_l1_shape", st, vp, P(KvShape))
+_decl("tsb_stage_create", st, vp, vp, P(vp))
+_decl("tsb_stage_destroy", None, vp)
+_decl("tsb_stage_run", st, vp, i64, P(Queue), P(Cluster), P(f64), vp, vp, P(StageOptions), vp, P(StageRequest),
+      P(StageStats))
+_decl("tsb_stage_trace", st, vp, P(TraceRow), i64, P(i64))
 _decl("tsb_l1_verify_synthetic", st, vp, P(IngestItem), i64, i64, i64, u64, i64, vp, P(u64))
 
 EXPORTED = sorted(

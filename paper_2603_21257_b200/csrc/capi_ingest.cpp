@@ -387,6 +387,11 @@ int64_t tsb_l1_deferred(const tsb_l1* l) { return l->ledger.deferred(); }
 int64_t tsb_l1_free_pages(const tsb_l1* l) { return l->free_len; }
 int64_t tsb_l1_num_pages(const tsb_l1* l) { return l->num_pages; }
 int64_t tsb_l1_page_bytes(const tsb_l1* l) { return l->page_bytes; }
+int tsb_l1_device(const tsb_l1* l) { return l->device; }
+tsb_status tsb_l1_shape(const tsb_l1* l, tsb_kv_shape* out) {
+  *out = l->shape;
+  return TSB_OK;
+}
 void* tsb_l1_arena(tsb_l1* l) { return l->arena; }
 void* tsb_l1_layer_ptr(tsb_l1* l, int64_t layer) { return l->arena + layer * l->layer_bytes; }
 const int32_t* tsb_l1_block_table_host(const tsb_l1* l) { return l->bt_host; }

@@ -2,11 +2,14 @@
 //
 // The reference's only hash is byte-serial FNV-1a-64 (engine.cpp:500-507), used for a config
 // fingerprint; it has no prefix hasher.  The definition frozen in
-// oracle/tsb_oracle.c (orc_hash_prefix_chunks) keeps FNV-1a's constants and step but makes a
-// 256-token chunk warp-parallel: lane j folds tokens [8j, 8j+8) as 64-bit FNV words, a 5-level
-// shuffle tree pairs the 32 leaves, and the chunk digests are chained per request so hash c
-// names the whole prefix [0, 256(c+1)).  One warp per request, kUnroll chunks in flight.
-// HBM-bound: 4 B/token read + 8 B/chunk written.
+// oracle/tsb_oracle.c (orc_hash_prefix_chunks) keeps FNV-1a's constants and step, applied to
+// 64-bit words (two int32 token ids each): 16 leaves of 8 words per 256-token chunk, a 4-level
+// pairwise tree, and a per-request chain so hash c names the whole prefix [0, 256(c+1)).
+//
+// Mapping: one warp per request; each half-warp owns one chunk per round (lane j of the half
+// folds leaf j = tokens [16j, 16j+16), 64 contiguous bytes), two rounds are loaded before any
+// is consumed (4 chunks = 4 KiB in flight per warp), the tree is 4 shuffle levels inside the
+// half-warp, and lane 0 folds both digests into the chain.  HBM-bound: 4 B/token + 8 B/chunk.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -20,66 +23,80 @@ __device__ __forceinline__ uint64_t fpair(uint64_t a, uint64_t b) {
 
 constexpr int kHashThreads = 256;
 constexpr int kHashWarps = kHashThreads / 32;
+constexpr int kRounds = 2;  // rounds of 2 chunks loaded ahead per warp
 
-__device__ __forceinline__ uint64_t leaf8(const int32_t (&t)[8]) {
+struct Leaf {
+  int4 v[4];  // 16 int32 tokens
+};
+
+__device__ __forceinline__ void load_leaf(const int32_t* p, bool aligned, Leaf& f) {
+  if (aligned) {
+    const int4* q = reinterpret_cast<const int4*>(p);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) f.v[k] = __ldg(q + k);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      f.v[k] = make_int4(__ldg(p + 4 * k), __ldg(p + 4 * k + 1), __ldg(p + 4 * k + 2),
+                         __ldg(p + 4 * k + 3));
+  }
+}
+
+__device__ __forceinline__ uint64_t word(int lo, int hi) {
+  return static_cast<uint64_t>(static_cast<uint32_t>(lo)) |
+         (static_cast<uint64_t>(static_cast<uint32_t>(hi)) << 32);
+}
+
+__device__ __forceinline__ uint64_t fold_leaf(const Leaf& f) {
   uint64_t h = kFnvOffset;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) h = fstep(h, static_cast<uint64_t>(static_cast<uint32_t>(t[k])));
+  for (int k = 0; k < 4; ++k) {
+    h = fstep(h, word(f.v[k].x, f.v[k].y));
+    h = fstep(h, word(f.v[k].z, f.v[k].w));
+  }
   return h;
 }
 
-__device__ __forceinline__ uint64_t tree32(uint64_t v, int lane) {
+// 4-level pairwise tree over the 16 leaves of each half-warp; result in lanes 0 and 16.
+__device__ __forceinline__ uint64_t tree16(uint64_t v, int j) {
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint64_t o = __shfl_down_sync(0xffffffffu, v, d);
-    if ((lane & (2 * d - 1)) == 0) v = fpair(v, o);
+  for (int d = 1; d < 16; d <<= 1) {
+    const uint64_t o = __shfl_down_sync(0xffffffffu, v, d, 16);
+    if ((j & (2 * d - 1)) == 0) v = fpair(v, o);
   }
-  return v;  // valid in lane 0
+  return v;
 }
 
-__device__ __forceinline__ void load8(const int32_t* p, bool aligned, int32_t (&t)[8]) {
-  if (aligned) {
-    const int4 a = __ldg(reinterpret_cast<const int4*>(p));
-    const int4 b = __ldg(reinterpret_cast<const int4*>(p) + 1);
-    t[0] = a.x; t[1] = a.y; t[2] = a.z; t[3] = a.w;
-    t[4] = b.x; t[5] = b.y; t[6] = b.z; t[7] = b.w;
-  } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t[k] = __ldg(p + k);
-  }
-}
-
-// One warp per request: chunks are processed kUnroll at a time (all their loads issued before
-// any is consumed), lane 0 folds each digest into the request's chain as it goes and stores the
-// running hash.  No block-level synchronisation; ~kUnroll KiB in flight per warp.
-constexpr int kUnroll = 4;
-
-__global__ void __launch_bounds__(kHashThreads) k_hash_prefix(int64_t n_req,
-                                                              const int64_t* __restrict__ offsets,
-                                                              const int32_t* __restrict__ tokens,
-                                                              const int64_t* __restrict__ chunk_offsets,
-                                                              uint64_t* __restrict__ out) {
+__global__ void __launch_bounds__(kHashThreads, 4) k_hash_prefix(
+    int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
+    const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(kHashWarps) + (threadIdx.x >> 5);
   if (r >= n_req) return;
   const int lane = threadIdx.x & 31;
+  const int half = lane >> 4, j = lane & 15;
   const int64_t t0 = offsets[r];
   const int64_t nchunks = (offsets[r + 1] - t0) / 256;
-  const int64_t c0 = chunk_offsets[r];
+  uint64_t* dst = out + chunk_offsets[r];
   const bool aligned = (t0 & 3) == 0;
-  const int32_t* base = tokens + t0 + lane * 8;
+  const int32_t* base = tokens + t0 + half * 256 + j * 16;
   uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
-  for (int64_t c = 0; c < nchunks; c += kUnroll) {
-    int32_t tk[kUnroll][8];
+  for (int64_t c = 0; c < nchunks; c += 2 * kRounds) {
+    Leaf f[kRounds];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      if (c + u < nchunks) load8(base + (c + u) * 256, aligned, tk[u]);
+    for (int u = 0; u < kRounds; ++u)
+      if (c + 2 * u + half < nchunks) load_leaf(base + (c + 2 * u) * 256, aligned, f[u]);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (c + u < nchunks) {
-        const uint64_t d = tree32(leaf8(tk[u]), lane);
-        if (lane == 0) {
-          h = fpair(h, d);
-          out[c0 + c + u] = h;
+    for (int u = 0; u < kRounds; ++u) {
+      const int64_t ca = c + 2 * u;
+      if (ca >= nchunks) break;
+      const uint64_t d = tree16(fold_leaf(f[u]), j);
+      const uint64_t db = __shfl_sync(0xffffffffu, d, 16);
+      if (lane == 0) {
+        h = fpair(h, d);
+        dst[ca] = h;
+        if (ca + 1 < nchunks) {
+          h = fpair(h, db);
+          dst[ca + 1] = h;
         }
       }
     }

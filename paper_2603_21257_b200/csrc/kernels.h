@@ -69,4 +69,7 @@ cudaError_t launch_gen_tokens(uint64_t seed, int64_t n_req, const int64_t* offse
                               const int64_t* doc, const int64_t* shared_len, int32_t* out,
                               cudaStream_t st);
 
+// Synthetic prefill burner (K6, harness).
+cudaError_t launch_prefill_burn(uint64_t ns, int ctas, unsigned long long* sink, cudaStream_t st);
+
 }  // namespace tsb

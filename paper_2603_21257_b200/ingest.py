@@ -223,6 +223,8 @@ def _events(layer_events, n_layers):
     assert len(layer_events) == n_layers, "one event (or None) per layer of the range"
     arr = (C.c_void_p * n_layers)()
     for i, e in enumerate(layer_events):
+        if e is not None and not e.cuda_event:
+            e.record()  # torch creates the cudaEvent_t lazily on first record
         arr[i] = e.cuda_event if e is not None else None
     return arr
 

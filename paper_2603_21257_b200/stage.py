@@ -1,0 +1,71 @@
+"""Load stage: the real-time L2->L1 dispatcher (tsb_stage_*), SimEngine's dispatch semantics with
+real bytes (engine.cpp:290-302, 341-355, 405-446, 258-282)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _capi as capi
+from ._capi import lib
+from .ingest import AUTO, ChunkPool, PagedKVCache
+from .tiersim import ClusterConfig, CostModelPair, PolicyKind, QueueArrays, check, cost_models_from_config
+
+TRACE_KINDS = {0: "arrival", 1: "transfer_done", 2: "allocation_grant", 3: "compute_done", 4: "dispatch_wake"}
+
+
+@dataclass
+class StageResult:
+    requests: np.ndarray  # structured: request_id, pick_position, deferred_chunks, chunks, bytes, *_ms
+    stats: dict
+    trace: Optional[np.ndarray] = None
+
+
+class LoadStage:
+    def __init__(self, l1: PagedKVCache, pool: ChunkPool):
+        h = C.c_void_p()
+        check(lib.tsb_stage_create(l1.handle, pool.handle, C.byref(h)))
+        self._h = h
+        self.l1, self.pool = l1, pool
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tsb_stage_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def run(self, queue: QueueArrays, slot_lists: Sequence[Sequence[int]], config: ClusterConfig,
+            models: Optional[CostModelPair] = None, policy: int = PolicyKind.Fifo, mode: int = AUTO,
+            layer_events: bool = False, prefill: bool = False, prefill_ctas: int = 0, record_trace: bool = False,
+            verify_seed: int = 0, stream=None) -> StageResult:
+        models = models or cost_models_from_config(config)
+        offs = np.zeros(len(slot_lists) + 1, np.int64)
+        np.cumsum([len(s) for s in slot_lists], out=offs[1:])
+        slots = np.concatenate([np.asarray(s, np.int64) for s in slot_lists]) if len(slot_lists) else np.zeros(0, np.int64)
+        slots = np.ascontiguousarray(slots, np.int64)
+        opt = capi.StageOptions(int(mode), int(policy), int(layer_events), int(prefill), int(prefill_ctas),
+                                int(record_trace), int(verify_seed))
+        res = (capi.StageRequest * max(queue.n, 1))()
+        stats = capi.StageStats()
+        qs = queue.struct()
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        check(lib.tsb_stage_run(self._h, queue.n, C.byref(qs), C.byref(config.struct()), models.array(),
+                                offs.ctypes.data, slots.ctypes.data, C.byref(opt), s, res, C.byref(stats)))
+        dt = np.dtype([(n, np.int64 if t in (capi.i64,) else np.int32 if t is capi.i32 else np.float64)
+                       for n, t in capi.StageRequest._fields_])
+        arr = np.frombuffer(bytes(res), dtype=dt, count=queue.n) if queue.n else np.zeros(0, dt)
+        st = {n: getattr(stats, n) for n, _ in capi.StageStats._fields_}
+        trace = None
+        if record_trace:
+            n = C.c_int64()
+            check(lib.tsb_stage_trace(self._h, None, 0, C.byref(n)))
+            rows = (capi.TraceRow * max(n.value, 1))()
+            check(lib.tsb_stage_trace(self._h, rows, n.value, C.byref(n)))
+            tdt = np.dtype([(f, np.float64 if t is capi.f64 else np.uint64 if t is capi.u64 else
+                             np.int64 if t is capi.i64 else np.int32) for f, t in capi.TraceRow._fields_])
+            trace = np.frombuffer(bytes(rows), dtype=tdt, count=n.value)
+        return StageResult(arr, st, trace)

@@ -1,0 +1,146 @@
+"""GPU: the real-time load stage (tsb_stage_run) under L1 pressure.
+
+Data parity: every request's pages are checked against the synthetic source pattern before they
+are released (verify_seed), and a no-deferral run is compared byte-for-byte with scatter_ref.
+Control parity: the TraceEvent-schema log must satisfy the reference's run invariants
+(proj/tests/trace_checks.hpp:93-143 -- grant-before-hop, exactly one hop per block, byte
+conservation, L1 ledger bound) and the admission order must equal the oracle's pick order.
+"""
+import numpy as np
+import pytest
+import torch
+
+import pyoracle as po
+from conftest import has_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+from paper_2603_21257_b200 import ingest  # noqa: E402
+from paper_2603_21257_b200 import tiersim as t  # noqa: E402
+from paper_2603_21257_b200.stage import LoadStage  # noqa: E402
+
+SHAPE = ingest.KVShape(layers=4, kv_heads=8, head_dim=128)
+KIND = {"transfer_done": 1, "grant": 2, "compute_done": 3, "dispatch": 4}
+
+
+def make_queue(n, seed):
+    rng = np.random.default_rng(seed)
+    ctx = rng.integers(256, 256 * 9, n)
+    q = t.QueueArrays(n, id=np.arange(100, 100 + n), arrival=np.round(rng.random(n), 2), context_tokens=ctx,
+                      query_tokens=rng.integers(1, 50, n), cache_hit_ratio=rng.choice([0.5, 0.9, 1.0], n),
+                      flags=np.ones(n, np.uint8), deadline=5.0 + rng.random(n))
+    return q
+
+
+def slot_lists(q, cfg, n_slots, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(q.n):
+        spec = t.RequestSpec(id=int(q.id[i]), context_tokens=int(q.context_tokens[i]),
+                             query_tokens=int(q.query_tokens[i]), cache_hit_ratio=float(q.cache_hit_ratio[i]))
+        nb = len(t.derive_block_plan(spec, cfg))
+        start = int(rng.integers(n_slots))
+        out.append([(start + k) % n_slots for k in range(nb)])  # a document's chunks, stored in order
+    return out
+
+
+def check_trace_invariants(tr, chunk_bytes, capacity, plans):
+    tr = tr[np.argsort(tr["seq"])]
+    grants, dispatch, done = {}, {}, {}
+    held, reserved, peak = {}, 0, 0
+    for r in tr:
+        key = (int(r["request_id"]), int(r["block_index"]))
+        if r["kind"] == KIND["grant"]:
+            assert key not in grants, "one grant per block"
+            grants[key] = r["seq"]
+            reserved += int(r["bytes"])
+            held[key[0]] = held.get(key[0], 0) + int(r["bytes"])
+            peak = max(peak, reserved)
+            assert reserved <= capacity, "L1 ledger bound"
+        elif r["kind"] == KIND["dispatch"]:
+            assert key in grants and grants[key] < r["seq"], "grant-before-hop"
+            assert key not in dispatch, "exactly one hop per block"
+            dispatch[key] = r["seq"]
+        elif r["kind"] == KIND["transfer_done"]:
+            assert key in dispatch and key not in done
+            done[key] = r["time"]
+            assert r["bytes"] == chunk_bytes
+        elif r["kind"] == KIND["compute_done"]:
+            reserved -= held.pop(key[0], 0)
+    want = {(rid, b) for rid, nb in plans.items() for b in range(nb)}
+    assert set(grants) == set(dispatch) == set(done) == want, "byte conservation: every planned block moved once"
+    return peak
+
+
+@pytest.mark.parametrize("mode", ["ce", "bulk", "zerocopy"])
+@pytest.mark.parametrize("policy", [t.PolicyKind.Fifo, t.PolicyKind.Lstf])
+def test_stage_under_l1_pressure(oracle, mode, policy):
+    n_slots, num_pages = 24, 10 * 16  # L1 holds 10 chunks; the batch needs ~50
+    pool = ingest.ChunkPool(SHAPE, n_slots)
+    pool.fill_synthetic(77)
+    l1 = ingest.PagedKVCache(SHAPE, num_pages, max_rows=16, max_chunks=16)
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(4, 8, 128, 2), block_size_tokens=256)
+    q = make_queue(12, 3)
+    slots = slot_lists(q, cfg, n_slots, 4)
+    stage = LoadStage(l1, pool)
+    res = stage.run(q, slots, cfg, policy=policy, mode=ingest.MODES[mode], layer_events=True,
+                    record_trace=True, verify_seed=77)
+    assert res.stats["verify_mismatches"] == 0
+    assert res.stats["deferred_chunks"] > 0
+    assert res.stats["bytes"] == sum(len(s) for s in slots) * SHAPE.local_chunk_bytes
+    assert l1.reserved() == 0 and l1.free_pages() == num_pages
+    plans = {int(q.id[i]): len(slots[i]) for i in range(q.n)}
+    check_trace_invariants(res.trace, SHAPE.local_chunk_bytes, l1.capacity(), plans)
+    # admission order == the oracle's pick order for this policy
+    m = t.cost_models_from_config(cfg)
+    st, err, tl, tc, pr = oracle.score_queue(q, int(policy), [m.load.slope, m.load.intercept, m.comp.slope,
+                                                              m.comp.intercept], cfg)
+    order = oracle.sort_order(pr, q.arrival, q.id)
+    assert np.array_equal(np.argsort(res.requests["pick_position"]), order)
+    # requests become resident in pick order (FIFO grants, single dispatcher)
+    resident = res.requests["resident_ms"][order]
+    assert np.all(np.diff(resident) >= 0)
+    assert np.all(res.requests["first_layer_ms"] <= res.requests["resident_ms"])
+
+
+def test_stage_no_pressure_and_errors():
+    pool = ingest.ChunkPool(SHAPE, 16)
+    pool.fill_synthetic(5)
+    l1 = ingest.PagedKVCache(SHAPE, 512, max_rows=8, max_chunks=16)
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(4, 8, 128, 2))
+    q = make_queue(4, 9)
+    slots = slot_lists(q, cfg, 16, 10)
+    stage = LoadStage(l1, pool)
+    res = stage.run(q, slots, cfg, mode=ingest.CE, verify_seed=5)
+    assert res.stats["verify_mismatches"] == 0 and res.stats["deferred_chunks"] == 0
+    assert res.stats["kernel_launches"] > 0
+    with pytest.raises(t.ValidationError, match="pool slots for a plan"):
+        stage.run(q, [s[:-1] if s else s for s in slots], cfg)
+    small = ingest.PagedKVCache(SHAPE, 16, max_rows=8, max_chunks=16)
+    with pytest.raises(t.CapacityError, match="can never fit"):
+        LoadStage(small, pool).run(q, slots, cfg)
+    with pytest.raises(t.MissingDeadline):
+        q2 = make_queue(4, 9)
+        q2.flags[:] = 0
+        stage.run(q2, slots, cfg, policy=t.PolicyKind.Edf)
+
+
+def test_stage_synthetic_prefill_overlap():
+    """With K6 prefill on a lower-priority stream, ingest of later requests overlaps earlier
+    prefills: the batch finishes well before sum(ingest) + sum(prefill)."""
+    shape = ingest.KVShape(layers=8, kv_heads=8, head_dim=128)
+    pool = ingest.ChunkPool(shape, 64)
+    pool.fill_synthetic(1)
+    l1 = ingest.PagedKVCache(shape, 64 * 16, max_rows=8, max_chunks=64)
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(8, 8, 128, 2), compute_base=2e-3,
+                          compute_per_token=2e-6)
+    q = t.QueueArrays(6, id=np.arange(6), arrival=np.zeros(6), context_tokens=np.full(6, 256 * 40),
+                      query_tokens=np.full(6, 500), cache_hit_ratio=np.ones(6), flags=np.zeros(6, np.uint8))
+    slots = [list(range(40))] * 6
+    stage = LoadStage(l1, pool)
+    res = stage.run(q, slots, cfg, mode=ingest.CE, layer_events=True, prefill=True, verify_seed=1)
+    assert res.stats["verify_mismatches"] == 0
+    r = res.requests
+    assert np.all(r["done_ms"] >= r["resident_ms"])
+    prefill_s = cfg.compute_base + cfg.compute_per_token * 500
+    assert r["done_ms"].max() * 1e-3 >= 6 * prefill_s * 0.9
