@@ -412,8 +412,9 @@ void orc_gen_tokens(uint64_t seed, int64_t n_req, const int64_t* offsets, const 
 /*   step(h, w)  = (h ^ w) * FNV_PRIME           (FNV-1a on a 64-bit word)     */
 /*   word k      = u32 tok[2k] | u32 tok[2k+1] << 32 (the little-endian 8-byte  */
 /*                 image of two consecutive int32 token ids)                   */
-/*   leaf j      = fold step over words [8j, 8j+8) of the chunk from FNV_OFFSET */
-/*                 (j = 0..15, i.e. 16 tokens per leaf)                         */
+/*   leaf j      = fold step, from FNV_OFFSET, over the 8 words                   */
+/*                 32k + 2j, 32k + 2j + 1 for k = 0..3 (j = 0..15): the words a */
+/*                 16-lane group reads with four fully coalesced 16-byte loads  */
 /*   pair(a, b)  = step(step(FNV_OFFSET, a), b)                                 */
 /*   digest      = 4-level pairwise tree of pair() over the 16 leaves, in order */
 /*   H_c         = pair(H_{c-1}, digest_c),  H_{-1} = rotl(FNV_OFFSET, 32)       */
@@ -437,9 +438,11 @@ uint64_t orc_chunk_digest(const int32_t* tok) {
   uint64_t node[16];
   for (int j = 0; j < 16; ++j) {
     uint64_t h = FNV_OFFSET;
-    for (int k = 0; k < 8; ++k) {
-      const int t = 16 * j + 2 * k;
-      h = step(h, (uint64_t)(uint32_t)tok[t] | ((uint64_t)(uint32_t)tok[t + 1] << 32));
+    for (int k = 0; k < 4; ++k) {
+      for (int e = 0; e < 2; ++e) {
+        const int t = 2 * (32 * k + 2 * j + e); /* first token of word 32k + 2j + e */
+        h = step(h, (uint64_t)(uint32_t)tok[t] | ((uint64_t)(uint32_t)tok[t + 1] << 32));
+      }
     }
     node[j] = h;
   }

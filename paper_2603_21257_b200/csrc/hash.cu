@@ -7,7 +7,8 @@
 // pairwise tree, and a per-request chain so hash c names the whole prefix [0, 256(c+1)).
 //
 // Mapping: one warp per request; each half-warp owns one chunk per round (lane j of the half
-// folds leaf j = tokens [16j, 16j+16), 64 contiguous bytes), two rounds are loaded before any
+// folds leaf j = words 32k+2j, 32k+2j+1 for k = 0..3, so each of the four 16-byte load
+// instructions reads 2 x 256 contiguous bytes -- fully coalesced), two rounds are loaded before any
 // is consumed (4 chunks = 4 KiB in flight per warp), the tree is 4 shuffle levels inside the
 // half-warp, and lane 0 folds both digests into the chain.  HBM-bound: 4 B/token + 8 B/chunk.
 #include "common.cuh"
@@ -29,16 +30,17 @@ struct Leaf {
   int4 v[4];  // 16 int32 tokens
 };
 
+// Lane j of a half-warp loads tokens [64k + 4j, 64k + 4j + 4) for k = 0..3: every 16-byte load
+// instruction of the warp reads two contiguous 256-byte runs (one per chunk).
 __device__ __forceinline__ void load_leaf(const int32_t* p, bool aligned, Leaf& f) {
   if (aligned) {
-    const int4* q = reinterpret_cast<const int4*>(p);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) f.v[k] = __ldg(q + k);
+    for (int k = 0; k < 4; ++k) f.v[k] = ld_stream(p + 64 * k);
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      f.v[k] = make_int4(__ldg(p + 4 * k), __ldg(p + 4 * k + 1), __ldg(p + 4 * k + 2),
-                         __ldg(p + 4 * k + 3));
+      f.v[k] = make_int4(__ldg(p + 64 * k), __ldg(p + 64 * k + 1), __ldg(p + 64 * k + 2),
+                         __ldg(p + 64 * k + 3));
   }
 }
 
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_hash_prefix(
   const int64_t nchunks = (offsets[r + 1] - t0) / 256;
   uint64_t* dst = out + chunk_offsets[r];
   const bool aligned = (t0 & 3) == 0;
-  const int32_t* base = tokens + t0 + half * 256 + j * 16;
+  const int32_t* base = tokens + t0 + half * 256 + j * 4;
   uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
   for (int64_t c = 0; c < nchunks; c += 2 * kRounds) {
     Leaf f[kRounds];

@@ -98,7 +98,8 @@ def test_stage_under_l1_pressure(oracle, mode, policy):
     order = oracle.sort_order(pr, q.arrival, q.id)
     assert np.array_equal(np.argsort(res.requests["pick_position"]), order)
     # requests become resident in pick order (FIFO grants, single dispatcher)
-    resident = res.requests["resident_ms"][order]
+    loaded = [i for i in order if res.requests["chunks"][i] > 0]  # empty plans are resident at admit
+    resident = res.requests["resident_ms"][loaded]
     assert np.all(np.diff(resident) >= 0)
     assert np.all(res.requests["first_layer_ms"] <= res.requests["resident_ms"])
 
