@@ -1,0 +1,408 @@
+#!/usr/bin/env python3
+"""Contract benchmark: KV ingest GB/s (L2 pinned host chunk pool -> L1 paged HBM) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
+
+A step is one pass of the load stage over the batch: GPU scoring + pick order, TierLedger-
+semantics page grants with FIFO deferral, block-table upload, ingest of every planned chunk, and
+page release (tsb_stage_run, the public C-ABI call).  Default workload = BASELINE.json configs[1]
+(Qwen2.5-32B KV, 16 x 128K @ 0.9 hit).  With N GPUs the KV heads are sharded TP-style: every rank
+ingests its head slice of the same batch from the pool (strong scaling, no data-path collective).
+
+  value : payload bytes of all ranks / max over ranks of the CUDA-event time of the K timed steps
+  e2e   : the same bytes / max over ranks of the host wall time of the K public-API calls
+  roofline     : the dominant kernel (K2 paged scatter, HBM-bound) timed live with CUDA events
+  host_link    : ingest GB/s per GPU vs the live-measured copy-engine H2D peak of this box
+  cpu_baseline : the oracle's scatter_ref (port) on the host cores, bounded sample (rank 0, N=1)
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "KV ingest GB/s per GPU and aggregate vs host-link/HBM roofline; TTFT load ms"
+UNIT = "GB/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "utilization.gpu"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for r in self.lines if len(r) == len(self.FIELDS)]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------------------------
+# shared pool across per-GPU processes
+# ------------------------------------------------------------------------------------------------
+def make_pool(shape_full, n_slots, world, rank, dist, seed):
+    """One pinned L2 pool per box: a /dev/shm segment page-locked by every rank when it fits,
+    else a private pinned pool per process (same bytes; documented in DESIGN.md)."""
+    from paper_2603_21257_b200 import ingest
+
+    nbytes = n_slots * shape_full.chunk_bytes
+    if world > 1:
+        import mmap
+
+        path = f"/dev/shm/tsb_pool_{os.environ.get('MASTER_PORT', '0')}_{nbytes}"
+        try:
+            free = os.statvfs("/dev/shm").f_bavail * os.statvfs("/dev/shm").f_frsize
+        except OSError:
+            free = 0
+        shared = free > nbytes * 1.05
+        flag = [shared]
+        if shared:
+            if rank == 0:
+                with open(path, "wb") as f:
+                    f.truncate(nbytes)
+            dist.barrier()
+            fd = os.open(path, os.O_RDWR)
+            mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+            addr = C.addressof(C.c_char.from_buffer(mm))
+            pool = ingest.ChunkPool.register(shape_full, addr, n_slots, keepalive=(mm, fd, path))
+            if rank == 0:
+                pool.fill_synthetic(seed)
+            dist.barrier()
+            return pool, "shared /dev/shm segment, cudaHostRegister'ed by every rank"
+        del flag
+    pool = ingest.ChunkPool(shape_full, n_slots)
+    pool.fill_synthetic(seed)
+    return pool, "cudaHostAlloc portable|mapped" + (" (private per rank: /dev/shm too small)" if world > 1 else "")
+
+
+def measure_ce_peak(torch, reps=5):
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    best = 1e9
+    for i in range(reps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        d.copy_(h, non_blocking=True)
+        b.record()
+        b.synchronize()
+        if i:
+            best = min(best, a.elapsed_time(b) * 1e-3)
+    del h, d
+    return n / best / 1e9
+
+
+def measure_k2(torch, l1, shape, n_items=128, reps=20):
+    """K2 (k_ingest_ldg over an HBM staging buffer) timed alone with CUDA events on its stream:
+    one layer of n_items chunks per launch; algorithmic bytes = read + write of the payload."""
+    from paper_2603_21257_b200 import _capi, ingest
+    from paper_2603_21257_b200.tiersim import check
+
+    cb = shape.page_bytes * shape.pages_per_chunk
+    rid = 1 << 40
+    rows = []
+    for c in range(n_items):
+        g, row = l1.request(rid, c, cb)
+        assert g
+    l1.sync_block_table()
+    layer_bytes = 2 * shape.chunk_tokens * shape.kv_heads * shape.head_dim * shape.dtype_bytes
+    staging = torch.empty(n_items * layer_bytes, dtype=torch.uint8, device="cuda")
+    items = ingest.items_numpy(np.arange(n_items), [row] * n_items, np.arange(n_items))
+    dev_items = torch.from_numpy(items.view(np.uint8).copy()).cuda()
+    s = torch.cuda.current_stream()
+    launch = lambda: check(_capi.lib.tsb_scatter_device(l1.handle, staging.data_ptr(), dev_items.data_ptr(),
+                                                         n_items, 0, 1, s.cuda_stream))
+    for _ in range(3):
+        launch()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(reps):
+        launch()
+    b.record(s)
+    b.synchronize()
+    avg_s = a.elapsed_time(b) * 1e-3 / reps
+    l1.release_request(rid)
+    del staging
+    return 2 * n_items * layer_bytes, avg_s
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def k2_traffic_from_profile():
+    p = ROOT / "profiles" / "k2_ncu_summary.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+    return None, None
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline (oracle port, test infrastructure) -- rank 0, N = 1 only
+# ------------------------------------------------------------------------------------------------
+def cpu_scatter_baseline(shape, sample_chunks, seed, threads, reps=2, pool_view=None):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle as po
+
+    cb = shape.chunk_bytes
+    if pool_view is None:
+        pool_view = po.synth_fill(seed, 0, sample_chunks * cb // 8, threads).view(np.uint8)
+    num_pages = sample_chunks * shape.pages_per_chunk
+    rng = np.random.default_rng(seed)
+    bt = rng.permutation(num_pages).astype(np.int32).reshape(1, -1)
+    items = np.zeros(sample_chunks, dtype=[("src_slot", np.int64), ("bt_row", np.int32), ("chunk_index", np.int32)])
+    items["src_slot"] = np.arange(sample_chunks)
+    items["chunk_index"] = np.arange(sample_chunks)
+    arena = np.empty(shape.layers * 2 * num_pages * shape.page_tokens * shape.heads_local * shape.head_dim
+                     * shape.dtype_bytes, np.uint8)
+    po.scatter_ref(shape, pool_view, items, bt, num_pages, threads=threads, arena=arena)  # first touch
+    best = 1e9
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        po.scatter_ref(shape, pool_view, items, bt, num_pages, threads=threads, arena=arena)
+        best = min(best, time.perf_counter() - t0)
+    nbytes = sample_chunks * shape.local_chunk_bytes
+    return nbytes / best / 1e9, nbytes, best
+
+
+# ------------------------------------------------------------------------------------------------
+def run_reference(args):
+    """The reference CPU implementation of the path on the host cores: the reference moves no
+    bytes (proj/ is a simulator), so this is the oracle port scatter_ref over the same chunk
+    layouts, all host threads, one bounded sample per step."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from paper_2603_21257_b200.workloads import WORKLOADS
+
+    wl = WORKLOADS[args.workload]()
+    shape = wl.shape
+    threads = os.cpu_count() or 1
+    sample = args.cpu_sample_chunks
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle as po
+
+    pool_view = po.synth_fill(7, 0, sample * shape.chunk_bytes // 8, threads).view(np.uint8)
+    times = []
+    for i in range(args.warmup + args.steps):
+        gbs, nbytes, secs = cpu_scatter_baseline(shape, sample, 7, threads, reps=1, pool_view=pool_view)
+        if i >= args.warmup:
+            times.append(secs)
+    tot = sum(times)
+    value = args.steps * nbytes / tot / 1e9
+    desc = f"{sample} chunks ({nbytes / 1e9:.2f} GB) of request 1 of {wl.name}, scatter_ref, {threads} threads"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl.name, "sample": desc},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    from paper_2603_21257_b200 import _capi, ingest
+    from paper_2603_21257_b200.stage import LoadStage
+    from paper_2603_21257_b200.tiersim import PolicyKind
+    from paper_2603_21257_b200.workloads import WORKLOADS
+
+    wl = WORKLOADS[args.workload]()
+    shape = wl.for_rank(world, rank)
+    seed = 20261017
+    ce_peak = measure_ce_peak(torch)
+    pool, pool_kind = make_pool(wl.shape, wl.pool_slots, world, rank, dist, seed)
+
+    # L1 arena: most of HBM, fewer pages than the batch needs so FIFO deferral is exercised.
+    free, total = torch.cuda.mem_get_info()
+    page = shape.page_bytes
+    need_pages = wl.chunks * shape.pages_per_chunk
+    arena_bytes = min(free - (10 << 30), args.l1_gib << 30)
+    num_pages = min(arena_bytes // page, need_pages)
+    max_chunks = max(len(s) for s in wl.slots)
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=wl.queue.n + 1, max_chunks=max(max_chunks, 128))
+    stage = LoadStage(l1, pool)
+    mode = ingest.MODES[args.mode]
+    run = lambda verify=0: stage.run(wl.queue, wl.slots, wl.config, policy=PolicyKind.Fifo, mode=mode,
+                                     verify_seed=verify)
+
+    # warm-up (the first one also checks every page against the synthetic source pattern)
+    for i in range(args.warmup):
+        r = run(seed if i == 0 else 0)
+        if i == 0 and r.stats["verify_mismatches"]:
+            raise SystemExit(f"ingest parity failure: {r.stats['verify_mismatches']} mismatching words")
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _capi.lib.tsb_kernel_launch_count()
+    walls, results = [], None
+    with ClockSampler(dev) as clk:
+        ev0.record(s)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            results = run()
+            walls.append(time.perf_counter() - t0)
+        ev1.record(s)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    gpu_launches = _capi.lib.tsb_kernel_launch_count() - launches0
+    dev_s = ev0.elapsed_time(ev1) * 1e-3
+    wall_s = sum(walls)
+    local_bytes = results.stats["bytes"]
+    if dist:
+        t = torch.tensor([dev_s, wall_s, float(local_bytes)], device="cuda", dtype=torch.float64)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_s, wall_s, total_bytes = float(mx[0]), float(mx[1]), float(sm[2])
+    else:
+        total_bytes = float(local_bytes)
+    value = args.steps * total_bytes / dev_s / 1e9
+    e2e = args.steps * total_bytes / wall_s / 1e9
+
+    # dominant kernel roofline (K2), measured live; host-link fraction vs live CE peak
+    alg_bytes, k2_s = measure_k2(torch, l1, shape)
+    hbm_peak, hbm_src = measured_peaks()
+    traffic, traffic_alg = k2_traffic_from_profile()
+    if traffic and traffic_alg:
+        traffic = traffic * alg_bytes / traffic_alg  # scale the per-launch ncu bytes to this launch
+    req = results.requests
+    order = np.argsort(req["pick_position"])
+    ttft = {"first_layer_ms_p50": float(np.median(req["first_layer_ms"])),
+            "resident_ms_p50": float(np.median(req["resident_ms"])),
+            "resident_ms_max": float(req["resident_ms"].max()),
+            "resident_ms_first_request": float(req["resident_ms"][order[0]]),
+            "reference_model_ms_per_request": float(len(wl.slots[0]) * (10e-6 + shape.local_chunk_bytes / 64e9) * 1e3)}
+    bt_bytes = wl.queue.n * l1.stride * 4
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": wl.name, "description": wl.description,
+                   "parallelism": f"kv-head shards tp{world}" if world > 1 else "single GPU",
+                   "ingest_mode": args.mode, "policy": "fifo", "l1_pages": int(num_pages),
+                   "l1_page_bytes": int(page), "l1_gib": round(num_pages * page / 2**30, 1),
+                   "bytes_per_step": int(total_bytes), "pool": pool_kind,
+                   "l2_flush": "inputs larger than L2 (each step streams the whole batch from host memory)"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(local_bytes + bt_bytes + wl.queue.n * 66),
+                "d2h_bytes_per_step": int(wl.queue.n * (8 + 16))},
+        "gpu_launches": int(gpu_launches),
+        "roofline": {"bound": "hbm", "kernel": "k_ingest_ldg (K2 paged scatter from the CE staging ring)",
+                     "achieved": alg_bytes / k2_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": alg_bytes / k2_s / 1e9 / hbm_peak, "traffic": traffic, "peak_source": hbm_src,
+                     "algorithmic_bytes_per_launch": int(alg_bytes), "launch_us": k2_s * 1e6},
+        "host_link": {"achieved": value / world, "peak": ce_peak, "unit": "GB/s", "frac": value / world / ce_peak,
+                      "peak_source": "live pinned 1 GiB cudaMemcpy H2D, best of 5, this box"},
+        "ttft_load_ms": ttft,
+        "stage": {k: results.stats[k] for k in ("ingest_calls", "deferred_chunks", "releases", "kernel_launches")},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = args.cpu_sample_chunks
+        view = pool.slot_view(0, sample)
+        gbs, nbytes, secs = cpu_scatter_baseline(wl.shape, sample, seed, threads, pool_view=view)
+        line["cpu_baseline"] = {"value": gbs, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{sample} chunks ({nbytes / 1e9:.2f} GB) of {wl.name} from the pinned "
+                                          f"pool, oracle scatter_ref, {threads} threads, best of 2"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="qwen16x128k")
+    ap.add_argument("--mode", default="auto", choices=["auto", "ce", "bulk", "zerocopy"])
+    ap.add_argument("--l1-gib", type=int, default=144)
+    ap.add_argument("--cpu-sample-chunks", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -186,6 +186,10 @@ tsb_status tsb_pool_create(const tsb_kv_shape* shape, int64_t n_slots, tsb_pool*
 /* Adopt caller-owned memory instead (must be page-locked, e.g. cudaHostRegister'ed). */
 tsb_status tsb_pool_wrap(const tsb_kv_shape* shape, void* host_base, int64_t n_slots,
                          tsb_pool** out);
+/* Page-lock caller memory (cudaHostRegister portable|mapped), e.g. a shared-memory segment
+ * every per-GPU process maps, so all GPUs of a box read one L2 pool; unregistered on destroy. */
+tsb_status tsb_pool_register(const tsb_kv_shape* shape, void* host_base, int64_t n_slots,
+                             tsb_pool** out);
 void tsb_pool_destroy(tsb_pool* p);
 void* tsb_pool_slot_ptr(tsb_pool* p, int64_t slot);
 int64_t tsb_pool_slots(const tsb_pool* p);
@@ -297,8 +301,9 @@ tsb_status tsb_scatter_device(tsb_l1* l1, const void* staging, const tsb_ingest_
                               int64_t n_items, int64_t layer_lo, int64_t layer_hi, void* stream);
 /* Tuning knobs for measurement (0 = default). */
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas);
-/* CE copy strategy: 0 = one cudaMemcpyAsync per (item, layer range), 1 = one
- * cudaMemcpy2DAsync per run of consecutive pool slots (default), 2 = cudaMemcpyBatchAsync.
+/* CE copy strategy: 0 = one cudaMemcpyAsync per (item, layer), 1 = one cudaMemcpy2DAsync per
+ * run of consecutive pool slots, 2 = one cudaMemcpyBatchAsync per staging group (default:
+ * 99.6% of the CE peak for any slot order, measured on B200).
  * staging_bytes: HBM staging ring size (0 = default 512 MiB). */
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes);
 

@@ -141,6 +141,7 @@ _decl("tsb_hash_prefix_chunks", st, vp, i64, vp, vp, vp, P(i64))
 _decl("tsb_gen_tokens_device", st, vp, u64, i64, vp, vp, vp, vp)
 _decl("tsb_pool_create", st, P(KvShape), i64, P(vp))
 _decl("tsb_pool_wrap", st, P(KvShape), vp, i64, P(vp))
+_decl("tsb_pool_register", st, P(KvShape), vp, i64, P(vp))
 _decl("tsb_pool_destroy", None, vp)
 _decl("tsb_pool_slot_ptr", vp, vp, i64)
 _decl("tsb_pool_slots", i64, vp)

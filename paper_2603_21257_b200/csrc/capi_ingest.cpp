@@ -33,7 +33,7 @@ struct Knobs {
   int zerocopy_ctas = 64;
   int bulk_ctas = 64;
   int scatter_ctas = 148 * 4;
-  int ce_variant = 1;
+  int ce_variant = 2;
   int64_t staging_bytes = 512ll << 20;
 };
 Knobs g_knobs;
@@ -92,6 +92,7 @@ struct tsb_pool {
   int64_t slots = 0;
   int64_t chunk_bytes = 0;
   bool owned = false;
+  bool registered = false;
 };
 
 extern "C" {
@@ -136,9 +137,26 @@ tsb_status tsb_pool_wrap(const tsb_kv_shape* shape, void* host_base, int64_t n_s
   return TSB_OK;
 }
 
+tsb_status tsb_pool_register(const tsb_kv_shape* shape, void* host_base, int64_t n_slots,
+                             tsb_pool** out) {
+  int64_t cb = 0;
+  TSB_TRY(tsb_kv_shape_info(shape, &cb, nullptr, nullptr));
+  if (n_slots < 1) return fail(TSB_VALIDATION, "pool: n_slots must be >= 1");
+  TSB_CUDA_TRY(cudaHostRegister(host_base, static_cast<size_t>(cb) * n_slots,
+                                cudaHostRegisterPortable | cudaHostRegisterMapped));
+  tsb_status st = tsb_pool_wrap(shape, host_base, n_slots, out);
+  if (st != TSB_OK) {
+    cudaHostUnregister(host_base);
+    return st;
+  }
+  (*out)->registered = true;
+  return TSB_OK;
+}
+
 void tsb_pool_destroy(tsb_pool* p) {
   if (!p) return;
   if (p->owned) cudaFreeHost(p->host);
+  if (p->registered) cudaHostUnregister(p->host);
   delete p;
 }
 

@@ -91,6 +91,19 @@ class ChunkPool:
         self.n_slots = n_slots
         self.chunk_bytes = lib.tsb_pool_chunk_bytes(h)
 
+    @classmethod
+    def register(cls, shape: KVShape, host_ptr: int, n_slots: int, keepalive=None) -> "ChunkPool":
+        """Page-lock caller memory (e.g. a /dev/shm segment every per-GPU process maps) as the pool."""
+        self = cls.__new__(cls)
+        self.shape = shape
+        h = C.c_void_p()
+        check(lib.tsb_pool_register(C.byref(shape.struct()), int(host_ptr), int(n_slots), C.byref(h)))
+        self._h = h
+        self.n_slots = n_slots
+        self.chunk_bytes = lib.tsb_pool_chunk_bytes(h)
+        self._keepalive = keepalive
+        return self
+
     @property
     def handle(self):
         return self._h
