@@ -295,8 +295,9 @@ tsb_status tsb_ingest(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items, 
 tsb_status tsb_ingest_device(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items_dev,
                              int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
                              void* stream, void* const* layer_events);
-/* K2 alone: scatter chunks already staged contiguously in HBM (src_slot indexes `staging`,
- * each slot = one full chunk, layers [layer_lo, layer_hi) only). */
+/* K2 alone: scatter chunks already staged in HBM: item i's layers [layer_lo, layer_hi), laid out
+ * as in the chunk ([layer][K/V][token][kv_head][dim]), start at staging + i*(hi-lo)*2*C*H*D*E
+ * (src_slot is ignored). */
 tsb_status tsb_scatter_device(tsb_l1* l1, const void* staging, const tsb_ingest_item* items_dev,
                               int64_t n_items, int64_t layer_lo, int64_t layer_hi, void* stream);
 /* Tuning knobs for measurement (0 = default). */

@@ -663,6 +663,8 @@ tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_i
   if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
     return fail(TSB_VALIDATION, "scatter: layer range must satisfy 0 <= lo < hi <= layers");
   tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
+  g.staged = 1;  // item i's layers [lo, hi) at staging + i * (hi - lo) * layer bytes
+  g.item_stride = (layer_hi - layer_lo) * g.layer_src;
   TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, static_cast<const uint8_t*>(staging), l->arena,
                                       items_dev, l->bt_dev, n_items, g_knobs.scatter_ctas,
                                       static_cast<cudaStream_t>(stream)));

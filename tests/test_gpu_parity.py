@@ -282,6 +282,20 @@ def test_ingest_bit_exact_vs_scatter_ref(oracle, mode):
     assert ingest.verify_synthetic(l1, pool, items, seed=17) == 0
 
 
+def test_k2_scatter_alone_bit_exact(oracle):
+    """tsb_scatter_device: K2 from an HBM staging buffer holding layers [1, 3) of each item."""
+    pool, l1, items = build_scenario(SMALL)
+    lo, hi = 1, 3
+    chunks = pool.slot_view(0, pool.n_slots).reshape(pool.n_slots, SMALL.layers, -1)
+    staging = torch.from_numpy(np.ascontiguousarray(chunks[items["src_slot"], lo:hi]).reshape(-1)).cuda()
+    dev_items = torch.from_numpy(items.view(np.uint8).copy()).cuda()
+    t.check(_capi.lib.tsb_scatter_device(l1.handle, staging.data_ptr(), dev_items.data_ptr(), len(items), lo, hi,
+                                         torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = oracle.scatter_ref(SMALL, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages, lo, hi)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2])
 def test_ingest_ce_copy_variants_bit_exact(oracle, variant):
     """CE strategies: per-item memcpy, 2D copy per run of consecutive slots, batched memcpy."""
