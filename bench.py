@@ -97,34 +97,30 @@ def make_pool(shape_full, n_slots, world, rank, dist, seed):
     else a private pinned pool per process (same bytes; documented in DESIGN.md)."""
     from paper_2603_21257_b200 import ingest
 
+    from paper_2603_21257_b200.multirank import SharedSegment
+
     nbytes = n_slots * shape_full.chunk_bytes
     if world > 1:
-        import mmap
-
-        path = f"/dev/shm/tsb_pool_{os.environ.get('MASTER_PORT', '0')}_{nbytes}"
-        try:
-            free = os.statvfs("/dev/shm").f_bavail * os.statvfs("/dev/shm").f_frsize
-        except OSError:
-            free = 0
-        shared = free > nbytes * 1.05
-        flag = [shared]
+        shared = torch_tensor_flag(SharedSegment.fits(nbytes), dist)
         if shared:
-            if rank == 0:
-                with open(path, "wb") as f:
-                    f.truncate(nbytes)
-            dist.barrier()
-            fd = os.open(path, os.O_RDWR)
-            mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
-            addr = C.addressof(C.c_char.from_buffer(mm))
-            pool = ingest.ChunkPool.register(shape_full, addr, n_slots, keepalive=(mm, fd, path))
+            seg = SharedSegment(f"tsb_pool_{os.environ.get('MASTER_PORT', '0')}_{nbytes}", nbytes, rank, dist.barrier)
+            pool = ingest.ChunkPool.register(shape_full, seg.address(), n_slots, keepalive=seg)
             if rank == 0:
                 pool.fill_synthetic(seed)
             dist.barrier()
             return pool, "shared /dev/shm segment, cudaHostRegister'ed by every rank"
-        del flag
     pool = ingest.ChunkPool(shape_full, n_slots)
     pool.fill_synthetic(seed)
     return pool, "cudaHostAlloc portable|mapped" + (" (private per rank: /dev/shm too small)" if world > 1 else "")
+
+
+def torch_tensor_flag(flag: bool, dist) -> bool:
+    """All ranks agree on a boolean (logical AND over ranks)."""
+    import torch
+
+    t = torch.tensor([1 if flag else 0], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
 
 
 def measure_ce_peak(torch, reps=5):
@@ -322,15 +318,9 @@ def run_ours(args):
     dev_s = ev0.elapsed_time(ev1) * 1e-3
     wall_s = sum(walls)
     local_bytes = results.stats["bytes"]
-    if dist:
-        t = torch.tensor([dev_s, wall_s, float(local_bytes)], device="cuda", dtype=torch.float64)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        dev_s, wall_s, total_bytes = float(mx[0]), float(mx[1]), float(sm[2])
-    else:
-        total_bytes = float(local_bytes)
+    from paper_2603_21257_b200.multirank import reduce_timing
+
+    dev_s, wall_s, total_bytes = reduce_timing(dist, dev_s, wall_s, float(local_bytes), device="cuda")
     value = args.steps * total_bytes / dev_s / 1e9
     e2e = args.steps * total_bytes / wall_s / 1e9
 
