@@ -302,6 +302,8 @@ tsb_status tsb_scatter_device(tsb_l1* l1, const void* staging, const tsb_ingest_
                               int64_t n_items, int64_t layer_lo, int64_t layer_hi, void* stream);
 /* Tuning knobs for measurement (0 = default). */
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas);
+/* K2 implementation: 0 = SM 16-byte load/store warps (default), 1 = cp.async.bulk ring. */
+tsb_status tsb_ingest_set_scatter(int impl, int ctas);
 /* CE copy strategy: 0 = one cudaMemcpyAsync per (item, layer), 1 = one cudaMemcpy2DAsync per
  * run of consecutive pool slots, 2 = one cudaMemcpyBatchAsync per staging group (default:
  * 99.6% of the CE peak for any slot order, measured on B200).

@@ -33,6 +33,7 @@ struct Knobs {
   int zerocopy_ctas = 64;
   int bulk_ctas = 64;
   int scatter_ctas = 148 * 4;
+  int scatter_impl = 0;  // K2: 0 = SM load/store warps, 1 = bulk-copy (TMA engine)
   int ce_variant = 2;
   int64_t staging_bytes = 512ll << 20;
 };
@@ -441,7 +442,27 @@ tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_cta
   return TSB_OK;
 }
 
+tsb_status tsb_ingest_set_scatter(int impl, int ctas) {
+  if (impl < 0 || impl > 1) return fail(TSB_VALIDATION, "ingest_set_scatter: impl must be 0 or 1");
+  g_knobs.scatter_impl = impl;
+  g_knobs.scatter_ctas = ctas > 0 ? ctas : (impl == 0 ? 148 * 4 : 148 * 2);
+  return TSB_OK;
+}
+
 }  // extern "C"
+
+namespace {
+
+// K2: HBM staging -> pages, with the SM load/store kernel or the bulk-copy (TMA engine) kernel.
+cudaError_t launch_scatter(const tsb::IngestGeom& g, const uint8_t* src, uint8_t* arena,
+                           const tsb_ingest_item* items, const int32_t* bt, int64_t n,
+                           cudaStream_t st) {
+  if (g_knobs.scatter_impl == 1 && g.seg_bytes * 6 <= 200 * 1024)
+    return tsb::launch_ingest_bulk(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st);
+  return tsb::launch_ingest_ldg(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st);
+}
+
+}  // namespace
 
 namespace {
 
@@ -566,8 +587,7 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
       TSB_TRY(ce_copy_layer(l, pool, items_host + i0, n, layer, g, stage));
       TSB_CUDA_TRY(cudaEventRecord(l->ev_ce[b], l->ce_stream));
       TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_ce[b], 0));
-      TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, stage, l->arena, items_dev + i0, l->bt_dev, n,
-                                          g_knobs.scatter_ctas, st));
+      TSB_CUDA_TRY(launch_scatter(g, stage, l->arena, items_dev + i0, l->bt_dev, n, st));
       TSB_CUDA_TRY(cudaEventRecord(l->ev_k2[b], st));
       l->k2_used[b] = true;
     }
@@ -665,9 +685,8 @@ tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_i
   tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
   g.staged = 1;  // item i's layers [lo, hi) at staging + i * (hi - lo) * layer bytes
   g.item_stride = (layer_hi - layer_lo) * g.layer_src;
-  TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, static_cast<const uint8_t*>(staging), l->arena,
-                                      items_dev, l->bt_dev, n_items, g_knobs.scatter_ctas,
-                                      static_cast<cudaStream_t>(stream)));
+  TSB_CUDA_TRY(launch_scatter(g, static_cast<const uint8_t*>(staging), l->arena, items_dev,
+                              l->bt_dev, n_items, static_cast<cudaStream_t>(stream)));
   return TSB_OK;
 }
 
