@@ -325,7 +325,9 @@ def run_ours(args):
     e2e = args.steps * total_bytes / wall_s / 1e9
 
     # dominant kernel roofline (K2), measured live; host-link fraction vs live CE peak
-    alg_bytes, k2_s = measure_k2(torch, l1, shape)
+    layer_bytes = 2 * shape.chunk_tokens * shape.kv_heads * shape.head_dim * shape.dtype_bytes
+    k2_items = min((512 << 20) // layer_bytes, max_chunks)  # the stage's K2 group: one staging half
+    alg_bytes, k2_s = measure_k2(torch, l1, shape, n_items=k2_items)
     hbm_peak, hbm_src = measured_peaks()
     traffic, traffic_alg = k2_traffic_from_profile()
     if traffic and traffic_alg:

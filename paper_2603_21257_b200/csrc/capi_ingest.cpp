@@ -32,10 +32,10 @@ namespace {
 struct Knobs {
   int zerocopy_ctas = 64;
   int bulk_ctas = 64;
-  int scatter_ctas = 148 * 4;
+  int scatter_ctas = 148 * 8;  // K2 sweep (r01): 5.6-5.9 TB/s from 592 CTAs up, 8 warps each
   int scatter_impl = 0;  // K2: 0 = SM load/store warps, 1 = bulk-copy (TMA engine)
   int ce_variant = 2;
-  int64_t staging_bytes = 512ll << 20;
+  int64_t staging_bytes = 1ll << 30;  // 2 x 512 MiB: one K2 launch per layer of a 460-chunk request
 };
 Knobs g_knobs;
 
@@ -438,14 +438,14 @@ tsb_status tsb_l1_sync_block_table(tsb_l1* l, void* stream) {
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas) {
   g_knobs.zerocopy_ctas = zerocopy_ctas > 0 ? zerocopy_ctas : 64;
   g_knobs.bulk_ctas = bulk_ctas > 0 ? bulk_ctas : 64;
-  g_knobs.scatter_ctas = scatter_ctas > 0 ? scatter_ctas : 148 * 4;
+  g_knobs.scatter_ctas = scatter_ctas > 0 ? scatter_ctas : 148 * 8;
   return TSB_OK;
 }
 
 tsb_status tsb_ingest_set_scatter(int impl, int ctas) {
   if (impl < 0 || impl > 1) return fail(TSB_VALIDATION, "ingest_set_scatter: impl must be 0 or 1");
   g_knobs.scatter_impl = impl;
-  g_knobs.scatter_ctas = ctas > 0 ? ctas : (impl == 0 ? 148 * 4 : 148 * 2);
+  g_knobs.scatter_ctas = ctas > 0 ? ctas : (impl == 0 ? 148 * 8 : 148);
   return TSB_OK;
 }
 
@@ -673,7 +673,7 @@ tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* i
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes) {
   if (variant < 0 || variant > 2) return fail(TSB_VALIDATION, "ingest_set_ce: variant must be 0, 1 or 2");
   g_knobs.ce_variant = variant;
-  g_knobs.staging_bytes = staging_bytes > 0 ? staging_bytes : (512ll << 20);
+  g_knobs.staging_bytes = staging_bytes > 0 ? staging_bytes : (1ll << 30);
   return TSB_OK;
 }
 
