@@ -3,7 +3,7 @@
  *
  * Plain pointers and sizes only; no torch or C++ types cross this boundary.  Every entry
  * point returns a tsb_status; on failure tsb_last_error() (thread-local) holds the message,
- * worded like the reference's throw sites so the C++ shim (include/tiersim/*.hpp) and the
+ * worded like the reference's throw sites so the C++ shim (include/tiersim/ headers) and the
  * Python mirror can rethrow the matching error.hpp class.
  *
  * Each declaration cites the reference interface it replaces (paths relative to
