@@ -264,6 +264,7 @@ struct tsb_scorer {
   void* qdev = nullptr;
   double* outdev = nullptr;
   int64_t* orderdev = nullptr;
+  int64_t host_cap = 0;  // capacity of qdev/outdev/orderdev in requests
 };
 
 namespace {
@@ -388,16 +389,21 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
   if (n == 0) return TSB_OK;
   // Pack the SoA queue into one device block: 7 x 8-byte arrays + flags.
   const size_t w = sizeof(int64_t) * static_cast<size_t>(n);
-  const size_t qbytes = 8 * w + static_cast<size_t>(n);
-  cudaFree(s->qdev);
-  cudaFree(s->outdev);
-  cudaFree(s->orderdev);
-  s->qdev = nullptr;
-  s->outdev = nullptr;
-  s->orderdev = nullptr;
-  TSB_CUDA_TRY(cudaMalloc(&s->qdev, qbytes));
-  TSB_CUDA_TRY(cudaMalloc(&s->outdev, 3 * w));
-  TSB_CUDA_TRY(cudaMalloc(&s->orderdev, w));
+  if (n > s->host_cap) {  // grow-only device buffers: no allocation (and no implicit sync) per call
+    const int64_t cap = std::max<int64_t>(n, 4096);
+    const size_t wc = sizeof(int64_t) * static_cast<size_t>(cap);
+    cudaFree(s->qdev);
+    cudaFree(s->outdev);
+    cudaFree(s->orderdev);
+    s->qdev = nullptr;
+    s->outdev = nullptr;
+    s->orderdev = nullptr;
+    s->host_cap = 0;
+    TSB_CUDA_TRY(cudaMalloc(&s->qdev, 8 * wc + static_cast<size_t>(cap)));
+    TSB_CUDA_TRY(cudaMalloc(&s->outdev, 3 * wc));
+    TSB_CUDA_TRY(cudaMalloc(&s->orderdev, wc));
+    s->host_cap = cap;
+  }
   auto* b = static_cast<uint8_t*>(s->qdev);
   tsb_queue dq;
   dq.id = reinterpret_cast<const int64_t*>(b + 0 * w);
