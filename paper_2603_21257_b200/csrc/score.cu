@@ -8,10 +8,14 @@
 // K5 replaces the O(N^2) pick_next drain (scheduler.cpp:75-100) with a sort under
 // PriorityKey::operator< (scheduler.hpp:38-42).  Keys ignore `now` (scheduler.cpp:47), so for
 // a fixed queue the drain order IS the sorted order.  Keys are encoded as order-preserving
-// u64 triples (primary, arrival, id); -0.0 is canonicalised to +0.0 (equal under operator<).
-// Sort = bitonic sort of 2048-key tiles in shared memory, then stable merge passes in which
-// each element finds its output slot by binary search in the sibling run.  Latency-bound at
-// 100K requests (~3 MB of keys): the point is microseconds instead of the CPU's milliseconds.
+// u64 triples (primary, arrival, id); -0.0 is canonicalised to +0.0 (equal under operator<); the
+// original queue index breaks any remaining tie (first-minimum wins, scheduler.cpp:85).
+// Sort = merge sort: each 512-thread CTA sorts a 2048-record tile (4 records per thread sorted
+// by a register network, then 9 merge-path rounds in shared memory), then one merge-path pass
+// per doubling of the run width, in which every CTA produces 2048 outputs: one warp finds each
+// end of the CTA's output window with a 32-ary search over global memory, the window's inputs
+// are staged in shared memory, and each thread merges 4 outputs.  Latency-bound at 100K
+// requests (~3 MB of keys).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -85,111 +89,186 @@ __global__ void k_score(int64_t n, tsb_queue q, ScoreParams p, double* __restric
   ki[i] = enc_i64(q.id[i]);
 }
 
-struct Key {
+// ---- K5 -----------------------------------------------------------------------------------------
+struct Rec {
   uint64_t p, a, i;
+  int64_t x;  // original queue index
 };
 
-__device__ __forceinline__ bool key_less(const Key& x, const Key& y) {
-  if (x.p != y.p) return x.p < y.p;
-  if (x.a != y.a) return x.a < y.a;
-  return x.i < y.i;
+__device__ __forceinline__ bool rec_less(const Rec& u, const Rec& v) {
+  if (u.p != v.p) return u.p < v.p;
+  if (u.a != v.a) return u.a < v.a;
+  if (u.i != v.i) return u.i < v.i;
+  return u.x < v.x;
 }
 
-constexpr int kTile = 2048;
-constexpr int kTileThreads = 1024;
+__device__ __forceinline__ void cswap(Rec& u, Rec& v) {
+  if (rec_less(v, u)) {
+    const Rec t = u;
+    u = v;
+    v = t;
+  }
+}
 
-// Bitonic sort of one tile in shared memory; pads with +inf keys.
-__global__ void __launch_bounds__(kTileThreads) k_tile_sort(
+constexpr int kItems = 4;
+constexpr int kThreads = 512;
+constexpr int kTileN = kItems * kThreads;  // 2048 records per CTA
+constexpr Rec kPad = {~0ull, ~0ull, ~0ull, 0x7fffffffffffffffll};
+
+__device__ __forceinline__ Rec load_rec(const uint64_t* kp, const uint64_t* ka, const uint64_t* ki,
+                                        const int64_t* idx, int64_t g) {
+  return Rec{kp[g], ka[g], ki[g], idx ? idx[g] : g};
+}
+
+// Merge path inside shared memory: number of A records among the first d merged outputs.
+__device__ __forceinline__ int merge_path(const Rec* A, int alen, const Rec* B, int blen, int d) {
+  int lo = max(0, d - blen), hi = min(d, alen);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (rec_less(A[mid], B[d - 1 - mid])) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Serial merge of kItems outputs starting at (A + ai, B + bi).
+__device__ __forceinline__ void merge_items(const Rec* A, int alen, const Rec* B, int blen, int ai,
+                                            int bi, Rec (&r)[kItems]) {
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const bool take_a = bi >= blen || (ai < alen && rec_less(A[ai], B[bi]));
+    r[k] = take_a ? A[ai++] : B[bi++];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_tile_sort(
     int64_t n, const uint64_t* __restrict__ kp, const uint64_t* __restrict__ ka,
     const uint64_t* __restrict__ ki, uint64_t* __restrict__ okp, uint64_t* __restrict__ oka,
     uint64_t* __restrict__ oki, int64_t* __restrict__ oidx, int64_t* __restrict__ order_out) {
-  extern __shared__ __align__(16) uint64_t tile_smem[];
-  uint64_t* sp = tile_smem;
-  uint64_t* sa = sp + kTile;
-  uint64_t* si = sa + kTile;
-  int32_t* sx = reinterpret_cast<int32_t*>(si + kTile);
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
-  for (int t = threadIdx.x; t < kTile; t += kTileThreads) {
-    const int64_t g = base + t;
-    if (g < n) {
-      sp[t] = kp[g];
-      sa[t] = ka[g];
-      si[t] = ki[g];
-    } else {
-      sp[t] = sa[t] = si[t] = ~0ull;
-    }
-    sx[t] = t;
+  extern __shared__ __align__(16) uint8_t sbuf[];
+  Rec* s = reinterpret_cast<Rec*>(sbuf);
+  const int t = threadIdx.x;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileN;
+  // striped (coalesced) load into shared memory, then each thread takes 4 consecutive records
+  for (int e = t; e < kTileN; e += kThreads) {
+    const int64_t g = base + e;
+    s[e] = g < n ? load_rec(kp, ka, ki, nullptr, g) : kPad;
   }
   __syncthreads();
-  for (int k = 2; k <= kTile; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const int t = threadIdx.x;
-      const int lo = 2 * t - (t & (j - 1));  // index with bit j clear
-      const int hi = lo + j;
-      const bool up = (lo & k) == 0;
-      const Key x{sp[lo], sa[lo], si[lo]};
-      const Key y{sp[hi], sa[hi], si[hi]};
-      // Ties (duplicate keys) keep the lower original index first: stable.
-      const bool gt = key_less(y, x) || (!key_less(x, y) && sx[lo] > sx[hi]);
-      if (gt == up) {
-        sp[lo] = y.p; sa[lo] = y.a; si[lo] = y.i;
-        sp[hi] = x.p; sa[hi] = x.a; si[hi] = x.i;
-        const int32_t tx = sx[lo];
-        sx[lo] = sx[hi];
-        sx[hi] = tx;
-      }
-      __syncthreads();
-    }
+  Rec r[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) r[k] = s[t * kItems + k];
+  // 4-record sorting network
+  cswap(r[0], r[1]);
+  cswap(r[2], r[3]);
+  cswap(r[0], r[2]);
+  cswap(r[1], r[3]);
+  cswap(r[1], r[2]);
+  for (int w = kItems; w < kTileN; w <<= 1) {
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) s[t * kItems + k] = r[k];
+    __syncthreads();
+    const int start = (t * kItems) & ~(2 * w - 1);
+    const int d = t * kItems - start;
+    const int ai = merge_path(s + start, w, s + start + w, w, d);
+    merge_items(s + start, w, s + start + w, w, ai, d - ai, r);
   }
-  for (int t = threadIdx.x; t < kTile; t += kTileThreads) {
-    const int64_t g = base + t;
-    if (g < n) {
-      if (order_out) {
-        order_out[g] = base + sx[t];
-      } else {
-        okp[g] = sp[t];
-        oka[g] = sa[t];
-        oki[g] = si[t];
-        oidx[g] = base + sx[t];
-      }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) s[t * kItems + k] = r[k];
+  __syncthreads();
+  for (int e = t; e < kTileN; e += kThreads) {
+    const int64_t g = base + e;
+    if (g >= n) continue;
+    const Rec v = s[e];
+    if (order_out) {
+      order_out[g] = v.x;
+    } else {
+      okp[g] = v.p;
+      oka[g] = v.a;
+      oki[g] = v.i;
+      oidx[g] = v.x;
     }
   }
 }
 
-// One stable merge pass of runs of `width`: element e of run A lands at
-// (e - startA) + #{b in B : b < e}; element of run B at (e - startB) + #{a in A : a <= e}.
-__global__ void k_merge_pass(int64_t n, int64_t width, const uint64_t* __restrict__ kp,
-                             const uint64_t* __restrict__ ka, const uint64_t* __restrict__ ki,
-                             const int64_t* __restrict__ idx, uint64_t* __restrict__ okp,
-                             uint64_t* __restrict__ oka, uint64_t* __restrict__ oki,
-                             int64_t* __restrict__ oidx, int64_t* __restrict__ order_out) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= n) return;
-  const int64_t pair_base = (e / (2 * width)) * (2 * width);
-  const int64_t mid = min(pair_base + width, n);
-  const int64_t end = min(pair_base + 2 * width, n);
-  const bool in_a = e < mid;
-  const Key x{kp[e], ka[e], ki[e]};
-  int64_t lo = in_a ? mid : pair_base;
-  int64_t hi = in_a ? end : mid;
-  // lower_bound (A side counts strictly-less B keys) / upper_bound (B counts <= A keys)
-  while (lo < hi) {
-    const int64_t m = (lo + hi) >> 1;
-    const Key y{kp[m], ka[m], ki[m]};
-    const bool go_right = in_a ? key_less(y, x) : !key_less(x, y);
-    if (go_right) lo = m + 1;
-    else hi = m;
+// 32-ary merge-path search over global memory by one warp: number of A records among the first
+// d outputs of merge(A, B).
+__device__ int warp_merge_path(const uint64_t* kp, const uint64_t* ka, const uint64_t* ki,
+                               const int64_t* idx, int64_t a0, int64_t alen, int64_t b0,
+                               int64_t blen, int64_t d) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = d - blen > 0 ? d - blen : 0, hi = d < alen ? d : alen;
+  while (hi > lo) {
+    const int64_t span = hi - lo;
+    const int64_t step = span <= 32 ? 1 : (span + 31) / 32;
+    const int64_t i = lo + lane * step;
+    bool f = false;
+    if (i < hi)
+      f = rec_less(load_rec(kp, ka, ki, idx, a0 + i), load_rec(kp, ka, ki, idx, b0 + d - 1 - i));
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    const int k = __popc(b);
+    if (step == 1) return static_cast<int>(lo + k);
+    if (k == 0) return static_cast<int>(lo);
+    const int64_t nlo = lo + (k - 1) * step + 1;
+    const int64_t ik = lo + k * step;
+    if (k < 32 && ik < hi) hi = ik;
+    lo = nlo;
   }
-  const int64_t other_start = in_a ? mid : pair_base;
-  const int64_t own_start = in_a ? pair_base : mid;
-  const int64_t dst = pair_base + (e - own_start) + (lo - other_start);
-  if (order_out) {
-    order_out[dst] = idx[e];
-  } else {
-    okp[dst] = x.p;
-    oka[dst] = x.a;
-    oki[dst] = x.i;
-    oidx[dst] = idx[e];
+  return static_cast<int>(lo);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_merge_pass(
+    int64_t n, int64_t width, const uint64_t* __restrict__ kp, const uint64_t* __restrict__ ka,
+    const uint64_t* __restrict__ ki, const int64_t* __restrict__ idx, uint64_t* __restrict__ okp,
+    uint64_t* __restrict__ oka, uint64_t* __restrict__ oki, int64_t* __restrict__ oidx,
+    int64_t* __restrict__ order_out) {
+  extern __shared__ __align__(16) uint8_t sbuf[];
+  Rec* s = reinterpret_cast<Rec*>(sbuf);
+  __shared__ int split[2];
+  const int t = threadIdx.x, warp = t >> 5;
+  const int64_t out_begin = static_cast<int64_t>(blockIdx.x) * kTileN;
+  const int64_t pair_base = (out_begin / (2 * width)) * (2 * width);
+  const int64_t a0 = pair_base, alen = min(width, n - pair_base);
+  const int64_t b0 = a0 + alen;
+  const int64_t brem = n - b0 < width ? n - b0 : width;
+  const int64_t blen = brem > 0 ? brem : 0;
+  const int64_t d0 = out_begin - pair_base;
+  const int64_t d1 = d0 + kTileN < alen + blen ? d0 + kTileN : alen + blen;
+  if (warp < 2) {
+    const int sp = warp_merge_path(kp, ka, ki, idx, a0, alen, b0, blen, warp == 0 ? d0 : d1);
+    if ((t & 31) == 0) split[warp] = sp;
+  }
+  __syncthreads();
+  const int s0 = split[0], s1 = split[1];
+  const int wa = s1 - s0, wb = static_cast<int>((d1 - s1) - (d0 - s0));
+  Rec* A = s;
+  Rec* B = s + wa;
+  for (int e = t; e < wa + wb; e += kThreads) {
+    s[e] = e < wa ? load_rec(kp, ka, ki, idx, a0 + s0 + e)
+                  : load_rec(kp, ka, ki, idx, b0 + (d0 - s0) + (e - wa));
+  }
+  __syncthreads();
+  const int dt = t * kItems;
+  const int total = wa + wb;
+  if (dt < total) {
+    const int ai = merge_path(A, wa, B, wb, dt);
+    Rec r[kItems];
+    merge_items(A, wa, B, wb, ai, dt - ai, r);
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      if (dt + k >= total) break;
+      const int64_t g = pair_base + d0 + dt + k;
+      if (order_out) {
+        order_out[g] = r[k].x;
+      } else {
+        okp[g] = r[k].p;
+        oka[g] = r[k].a;
+        oki[g] = r[k].i;
+        oidx[g] = r[k].x;
+      }
+    }
   }
 }
 
@@ -210,29 +289,32 @@ cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, in
                          uint64_t* kp2, uint64_t* ka2, uint64_t* ki2, int64_t* idx2,
                          int64_t* order_out, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  const int tiles = ceil_div(n, kTile);
-  constexpr size_t kTileSmem = kTile * (3 * sizeof(uint64_t) + sizeof(int32_t));
+  constexpr size_t kSmem = sizeof(Rec) * kTileN;  // 64 KiB
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kTileSmem));
+                                         static_cast<int>(kSmem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_merge_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  const int tiles = ceil_div(n, kTileN);
   if (tiles == 1) {
-    k_tile_sort<<<1, kTileThreads, kTileSmem, st>>>(n, kp, ka, ki, nullptr, nullptr, nullptr, nullptr,
+    k_tile_sort<<<1, kThreads, kSmem, st>>>(n, kp, ka, ki, nullptr, nullptr, nullptr, nullptr,
                                             order_out);
     count_launch();
     return cudaGetLastError();
   }
-  k_tile_sort<<<tiles, kTileThreads, kTileSmem, st>>>(n, kp, ka, ki, kp2, ka2, ki2, idx2, nullptr);
+  k_tile_sort<<<tiles, kThreads, kSmem, st>>>(n, kp, ka, ki, kp2, ka2, ki2, idx2, nullptr);
   count_launch();
   uint64_t *sp = kp2, *sa = ka2, *si = ki2, *dp = kp, *da = ka, *di = ki;
   int64_t *sx = idx2, *dx = idx;
-  for (int64_t width = kTile; width < n; width *= 2) {
+  for (int64_t width = kTileN; width < n; width *= 2) {
     const bool last = width * 2 >= n;
-    k_merge_pass<<<ceil_div(n, 256), 256, 0, st>>>(n, width, sp, sa, si, sx, dp, da, di, dx,
-                                                   last ? order_out : nullptr);
+    k_merge_pass<<<tiles, kThreads, kSmem, st>>>(n, width, sp, sa, si, sx, dp, da, di, dx,
+                                                 last ? order_out : nullptr);
     count_launch();
     std::swap(sp, dp);
     std::swap(sa, da);
