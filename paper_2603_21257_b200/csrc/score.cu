@@ -12,7 +12,7 @@
 // original queue index breaks any remaining tie (first-minimum wins, scheduler.cpp:85).
 // Sort = merge sort: each 512-thread CTA sorts a 2048-record tile (4 records per thread sorted
 // by a register network, then 9 merge-path rounds in shared memory), then one merge-path pass
-// per doubling of the run width, in which every CTA produces 2048 outputs: one warp finds each
+// per doubling of the run width, in which every CTA produces 1024 outputs: one warp finds each
 // end of the CTA's output window with a 32-ary search over global memory, the window's inputs
 // are staged in shared memory, and each thread merges 4 outputs.  Latency-bound at 100K
 // requests (~3 MB of keys).
@@ -112,32 +112,43 @@ __device__ __forceinline__ void cswap(Rec& u, Rec& v) {
 
 constexpr int kItems = 4;
 constexpr int kThreads = 512;
-constexpr int kTileN = kItems * kThreads;  // 2048 records per CTA
+constexpr int kTileN = kItems * kThreads;  // 2048 records per tile-sort CTA
+constexpr int kMergeThreads = 256;
+constexpr int kMergeN = kItems * kMergeThreads;  // 1024 outputs per merge-pass CTA
 constexpr Rec kPad = {~0ull, ~0ull, ~0ull, 0x7fffffffffffffffll};
+
+// Shared-memory record L lives at byte L*32 + (L/4)*8: the 8-byte pad after every 4 records
+// makes both the blocked (thread t <-> records 4t..4t+3) and the striped (lane <-> record)
+// access patterns 2-way instead of 32-way / 8-way bank-conflicted.
+constexpr size_t smem_bytes(int n) { return static_cast<size_t>(n) * 32 + static_cast<size_t>(n / 4) * 8; }
+__device__ __forceinline__ Rec& sat(uint8_t* sb, int L) {
+  return *reinterpret_cast<Rec*>(sb + static_cast<size_t>(L) * 32 + static_cast<size_t>(L >> 2) * 8);
+}
 
 __device__ __forceinline__ Rec load_rec(const uint64_t* kp, const uint64_t* ka, const uint64_t* ki,
                                         const int64_t* idx, int64_t g) {
   return Rec{kp[g], ka[g], ki[g], idx ? idx[g] : g};
 }
 
-// Merge path inside shared memory: number of A records among the first d merged outputs.
-__device__ __forceinline__ int merge_path(const Rec* A, int alen, const Rec* B, int blen, int d) {
+// Merge path inside shared memory (runs A = [a, a+alen), B = [b, b+blen) in record indices):
+// number of A records among the first d merged outputs.
+__device__ __forceinline__ int merge_path(uint8_t* sb, int a, int alen, int b, int blen, int d) {
   int lo = max(0, d - blen), hi = min(d, alen);
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (rec_less(A[mid], B[d - 1 - mid])) lo = mid + 1;
+    if (rec_less(sat(sb, a + mid), sat(sb, b + d - 1 - mid))) lo = mid + 1;
     else hi = mid;
   }
   return lo;
 }
 
-// Serial merge of kItems outputs starting at (A + ai, B + bi).
-__device__ __forceinline__ void merge_items(const Rec* A, int alen, const Rec* B, int blen, int ai,
+// Serial merge of kItems outputs starting at A + ai, B + bi.
+__device__ __forceinline__ void merge_items(uint8_t* sb, int a, int alen, int b, int blen, int ai,
                                             int bi, Rec (&r)[kItems]) {
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
-    const bool take_a = bi >= blen || (ai < alen && rec_less(A[ai], B[bi]));
-    r[k] = take_a ? A[ai++] : B[bi++];
+    const bool take_a = bi >= blen || (ai < alen && rec_less(sat(sb, a + ai), sat(sb, b + bi)));
+    r[k] = take_a ? sat(sb, a + ai++) : sat(sb, b + bi++);
   }
 }
 
@@ -146,18 +157,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_sort(
     const uint64_t* __restrict__ ki, uint64_t* __restrict__ okp, uint64_t* __restrict__ oka,
     uint64_t* __restrict__ oki, int64_t* __restrict__ oidx, int64_t* __restrict__ order_out) {
   extern __shared__ __align__(16) uint8_t sbuf[];
-  Rec* s = reinterpret_cast<Rec*>(sbuf);
   const int t = threadIdx.x;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileN;
   // striped (coalesced) load into shared memory, then each thread takes 4 consecutive records
   for (int e = t; e < kTileN; e += kThreads) {
     const int64_t g = base + e;
-    s[e] = g < n ? load_rec(kp, ka, ki, nullptr, g) : kPad;
+    sat(sbuf, e) = g < n ? load_rec(kp, ka, ki, nullptr, g) : kPad;
   }
   __syncthreads();
   Rec r[kItems];
 #pragma unroll
-  for (int k = 0; k < kItems; ++k) r[k] = s[t * kItems + k];
+  for (int k = 0; k < kItems; ++k) r[k] = sat(sbuf, t * kItems + k);
   // 4-record sorting network
   cswap(r[0], r[1]);
   cswap(r[2], r[3]);
@@ -167,21 +177,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_sort(
   for (int w = kItems; w < kTileN; w <<= 1) {
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) s[t * kItems + k] = r[k];
+    for (int k = 0; k < kItems; ++k) sat(sbuf, t * kItems + k) = r[k];
     __syncthreads();
     const int start = (t * kItems) & ~(2 * w - 1);
     const int d = t * kItems - start;
-    const int ai = merge_path(s + start, w, s + start + w, w, d);
-    merge_items(s + start, w, s + start + w, w, ai, d - ai, r);
+    const int ai = merge_path(sbuf, start, w, start + w, w, d);
+    merge_items(sbuf, start, w, start + w, w, ai, d - ai, r);
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kItems; ++k) s[t * kItems + k] = r[k];
+  for (int k = 0; k < kItems; ++k) sat(sbuf, t * kItems + k) = r[k];
   __syncthreads();
   for (int e = t; e < kTileN; e += kThreads) {
     const int64_t g = base + e;
     if (g >= n) continue;
-    const Rec v = s[e];
+    const Rec v = sat(sbuf, e);
     if (order_out) {
       order_out[g] = v.x;
     } else {
@@ -219,23 +229,22 @@ __device__ int warp_merge_path(const uint64_t* kp, const uint64_t* ka, const uin
   return static_cast<int>(lo);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_merge_pass(
+__global__ void __launch_bounds__(kMergeThreads) k_merge_pass(
     int64_t n, int64_t width, const uint64_t* __restrict__ kp, const uint64_t* __restrict__ ka,
     const uint64_t* __restrict__ ki, const int64_t* __restrict__ idx, uint64_t* __restrict__ okp,
     uint64_t* __restrict__ oka, uint64_t* __restrict__ oki, int64_t* __restrict__ oidx,
     int64_t* __restrict__ order_out) {
   extern __shared__ __align__(16) uint8_t sbuf[];
-  Rec* s = reinterpret_cast<Rec*>(sbuf);
   __shared__ int split[2];
   const int t = threadIdx.x, warp = t >> 5;
-  const int64_t out_begin = static_cast<int64_t>(blockIdx.x) * kTileN;
+  const int64_t out_begin = static_cast<int64_t>(blockIdx.x) * kMergeN;
   const int64_t pair_base = (out_begin / (2 * width)) * (2 * width);
   const int64_t a0 = pair_base, alen = min(width, n - pair_base);
   const int64_t b0 = a0 + alen;
   const int64_t brem = n - b0 < width ? n - b0 : width;
   const int64_t blen = brem > 0 ? brem : 0;
   const int64_t d0 = out_begin - pair_base;
-  const int64_t d1 = d0 + kTileN < alen + blen ? d0 + kTileN : alen + blen;
+  const int64_t d1 = d0 + kMergeN < alen + blen ? d0 + kMergeN : alen + blen;
   if (warp < 2) {
     const int sp = warp_merge_path(kp, ka, ki, idx, a0, alen, b0, blen, warp == 0 ? d0 : d1);
     if ((t & 31) == 0) split[warp] = sp;
@@ -243,19 +252,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_pass(
   __syncthreads();
   const int s0 = split[0], s1 = split[1];
   const int wa = s1 - s0, wb = static_cast<int>((d1 - s1) - (d0 - s0));
-  Rec* A = s;
-  Rec* B = s + wa;
-  for (int e = t; e < wa + wb; e += kThreads) {
-    s[e] = e < wa ? load_rec(kp, ka, ki, idx, a0 + s0 + e)
-                  : load_rec(kp, ka, ki, idx, b0 + (d0 - s0) + (e - wa));
+  for (int e = t; e < wa + wb; e += kMergeThreads) {
+    sat(sbuf, e) = e < wa ? load_rec(kp, ka, ki, idx, a0 + s0 + e)
+                          : load_rec(kp, ka, ki, idx, b0 + (d0 - s0) + (e - wa));
   }
   __syncthreads();
   const int dt = t * kItems;
   const int total = wa + wb;
   if (dt < total) {
-    const int ai = merge_path(A, wa, B, wb, dt);
+    const int ai = merge_path(sbuf, 0, wa, wa, wb, dt);
     Rec r[kItems];
-    merge_items(A, wa, B, wb, ai, dt - ai, r);
+    merge_items(sbuf, 0, wa, wa, wb, ai, dt - ai, r);
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       if (dt + k >= total) break;
@@ -289,14 +296,15 @@ cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, in
                          uint64_t* kp2, uint64_t* ka2, uint64_t* ki2, int64_t* idx2,
                          int64_t* order_out, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  constexpr size_t kSmem = sizeof(Rec) * kTileN;  // 64 KiB
+  constexpr size_t kSmem = smem_bytes(kTileN);       // 68 KiB
+  constexpr size_t kMergeSmem = smem_bytes(kMergeN);  // 34 KiB
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kSmem));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_merge_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(kSmem));
+                               static_cast<int>(kMergeSmem));
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -313,8 +321,8 @@ cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, in
   int64_t *sx = idx2, *dx = idx;
   for (int64_t width = kTileN; width < n; width *= 2) {
     const bool last = width * 2 >= n;
-    k_merge_pass<<<tiles, kThreads, kSmem, st>>>(n, width, sp, sa, si, sx, dp, da, di, dx,
-                                                 last ? order_out : nullptr);
+    k_merge_pass<<<ceil_div(n, kMergeN), kMergeThreads, kMergeSmem, st>>>(
+        n, width, sp, sa, si, sx, dp, da, di, dx, last ? order_out : nullptr);
     count_launch();
     std::swap(sp, dp);
     std::swap(sa, da);
