@@ -6,11 +6,13 @@
 // 64-bit words (two int32 token ids each): 16 leaves of 8 words per 256-token chunk, a 4-level
 // pairwise tree, and a per-request chain so hash c names the whole prefix [0, 256(c+1)).
 //
-// Mapping: one warp per request; each half-warp owns one chunk per round (lane j of the half
-// folds leaf j = words 32k+2j, 32k+2j+1 for k = 0..3, so each of the four 16-byte load
-// instructions reads 2 x 256 contiguous bytes -- fully coalesced), two rounds are loaded before any
-// is consumed (4 chunks = 4 KiB in flight per warp), the tree is 4 shuffle levels inside the
-// half-warp, and lane 0 folds both digests into the chain.  HBM-bound: 4 B/token + 8 B/chunk.
+// Mapping, two phases.  (1) k_chunk_digest: a persistent grid of warps walks the global chunk
+// index space kItem chunks at a time (balanced however request lengths vary); each half-warp owns
+// one chunk per round (lane j folds leaf j = words 32k+2j, 32k+2j+1 for k = 0..3, so each of the
+// four 16-byte load instructions reads 2 x 256 contiguous bytes -- fully coalesced), two rounds
+// are loaded before any is consumed (4 KiB in flight per warp), the tree is 4 shuffle levels
+// inside the half-warp, and the digest goes to out[c].  (2) k_chain: one thread per request
+// folds its digests into the chain in place (L2-resident).  HBM-bound: 4 B/token + 8 B/chunk.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -69,39 +71,77 @@ __device__ __forceinline__ uint64_t tree16(uint64_t v, int j) {
   return v;
 }
 
-__global__ void __launch_bounds__(kHashThreads, 4) k_hash_prefix(
+// Phase 1 -- chunk digests, balanced over the GLOBAL chunk index space (request lengths vary
+// 100x, so a warp-per-request mapping leaves a long tail): a persistent grid of warps takes
+// kItem consecutive chunks at a time, finds the owning request once with a 32-ary search over
+// chunk_offsets, and writes each chunk's digest to out[c].
+constexpr int kItem = 8;
+
+__device__ __forceinline__ int64_t warp_upper_bound(const int64_t* __restrict__ a, int64_t n,
+                                                    int64_t v) {
+  // first index i in [0, n) with a[i] > v (a non-decreasing), by 32-ary narrowing
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = n;
+  while (hi > lo) {
+    const int64_t span = hi - lo;
+    const int64_t step = span <= 32 ? 1 : (span + 31) / 32;
+    const int64_t i = lo + lane * step;
+    const bool le = i < hi && a[i] <= v;
+    const int k = __popc(__ballot_sync(0xffffffffu, le));
+    if (step == 1) return lo + k;
+    if (k == 0) return lo;
+    const int64_t nlo = lo + (k - 1) * step + 1;
+    if (k < 32 && lo + k * step < hi) hi = lo + k * step;
+    lo = nlo;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
     int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
     const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(kHashWarps) + (threadIdx.x >> 5);
-  if (r >= n_req) return;
   const int lane = threadIdx.x & 31;
   const int half = lane >> 4, j = lane & 15;
-  const int64_t t0 = offsets[r];
-  const int64_t nchunks = (offsets[r + 1] - t0) / 256;
-  uint64_t* dst = out + chunk_offsets[r];
-  const bool aligned = (t0 & 3) == 0;
-  const int32_t* base = tokens + t0 + half * 256 + j * 4;
-  uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
-  for (int64_t c = 0; c < nchunks; c += 2 * kRounds) {
-    Leaf f[kRounds];
+  const int64_t total = chunk_offsets[n_req];
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * kHashWarps;
+  for (int64_t item = blockIdx.x * static_cast<int64_t>(kHashWarps) + (threadIdx.x >> 5);
+       item * kItem < total; item += warps) {
+    const int64_t c0 = item * kItem;
+    const int64_t c1 = min(c0 + kItem, total);
+    int64_t r = warp_upper_bound(chunk_offsets, n_req + 1, c0) - 1;
+    for (int64_t c = c0; c < c1; c += 2 * kRounds) {
+      Leaf f[kRounds];
 #pragma unroll
-    for (int u = 0; u < kRounds; ++u)
-      if (c + 2 * u + half < nchunks) load_leaf(base + (c + 2 * u) * 256, aligned, f[u]);
-#pragma unroll
-    for (int u = 0; u < kRounds; ++u) {
-      const int64_t ca = c + 2 * u;
-      if (ca >= nchunks) break;
-      const uint64_t d = tree16(fold_leaf(f[u]), j);
-      const uint64_t db = __shfl_sync(0xffffffffu, d, 16);
-      if (lane == 0) {
-        h = fpair(h, d);
-        dst[ca] = h;
-        if (ca + 1 < nchunks) {
-          h = fpair(h, db);
-          dst[ca + 1] = h;
+      for (int u = 0; u < kRounds; ++u) {
+        const int64_t cc = c + 2 * u + half;
+        if (cc < c1) {
+          while (chunk_offsets[r + 1] <= cc) ++r;  // half-warp-uniform walk (items are short)
+          const int64_t t0 = offsets[r];
+          load_leaf(tokens + t0 + (cc - chunk_offsets[r]) * 256 + j * 4, (t0 & 3) == 0, f[u]);
         }
       }
+#pragma unroll
+      for (int u = 0; u < kRounds; ++u) {
+        const int64_t cc = c + 2 * u + half;
+        const uint64_t d = tree16(fold_leaf(f[u]), j);
+        if (j == 0 && cc < c1) out[cc] = d;
+      }
     }
+  }
+}
+
+// Phase 2 -- the per-request chain H_c = pair(H_{c-1}, digest_c), in place; one thread per
+// request, loads are independent of the chain so they pipeline; the digests are L2-resident.
+__global__ void k_chain(int64_t n_req, const int64_t* __restrict__ chunk_offsets,
+                        uint64_t* __restrict__ out) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n_req) return;
+  uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
+  const int64_t e = chunk_offsets[r + 1];
+#pragma unroll 4
+  for (int64_t c = chunk_offsets[r]; c < e; ++c) {
+    h = fpair(h, out[c]);
+    out[c] = h;
   }
 }
 
@@ -126,9 +166,10 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
-  const int64_t grid = (n_req + kHashWarps - 1) / kHashWarps;
-  k_hash_prefix<<<static_cast<unsigned>(grid), kHashThreads, 0, st>>>(n_req, offsets, tokens,
-                                                                     chunk_offsets, out);
+  // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
+  k_chunk_digest<<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  count_launch();
+  k_chain<<<ceil_div(n_req, 256), 256, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();
   return cudaGetLastError();
 }
