@@ -75,7 +75,16 @@ __device__ __forceinline__ uint64_t tree16(uint64_t v, int j) {
 // 100x, so a warp-per-request mapping leaves a long tail): a persistent grid of warps takes
 // kItem consecutive chunks at a time, finds the owning request once with a 32-ary search over
 // chunk_offsets, and writes each chunk's digest to out[c].
-constexpr int kItem = 8;
+constexpr int kItem = 16;
+
+__device__ __forceinline__ void st_evict_last(uint64_t* p, uint64_t v) {
+  asm volatile(
+      "{\n.reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+      "st.global.L2::cache_hint.b64 [%0], %1, pol;\n}" ::"l"(p),
+      "l"(v)
+      : "memory");
+}
 
 __device__ __forceinline__ int64_t warp_upper_bound(const int64_t* __restrict__ a, int64_t n,
                                                     int64_t v) {
@@ -108,23 +117,27 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
        item * kItem < total; item += warps) {
     const int64_t c0 = item * kItem;
     const int64_t c1 = min(c0 + kItem, total);
+    // lane k (< kItem) resolves chunk c0+k's token base once per item, so the token loads below
+    // do not wait on per-chunk table lookups
     int64_t r = warp_upper_bound(chunk_offsets, n_req + 1, c0) - 1;
+    int64_t tb = -1;
+    if (lane < kItem && c0 + lane < c1) {
+      while (chunk_offsets[r + 1] <= c0 + lane) ++r;
+      tb = offsets[r] + (c0 + lane - chunk_offsets[r]) * 256;
+    }
     for (int64_t c = c0; c < c1; c += 2 * kRounds) {
       Leaf f[kRounds];
 #pragma unroll
       for (int u = 0; u < kRounds; ++u) {
         const int64_t cc = c + 2 * u + half;
-        if (cc < c1) {
-          while (chunk_offsets[r + 1] <= cc) ++r;  // half-warp-uniform walk (items are short)
-          const int64_t t0 = offsets[r];
-          load_leaf(tokens + t0 + (cc - chunk_offsets[r]) * 256 + j * 4, (t0 & 3) == 0, f[u]);
-        }
+        const int64_t base = __shfl_sync(0xffffffffu, tb, static_cast<int>(cc - c0) & 31);
+        if (cc < c1) load_leaf(tokens + base + j * 4, (base & 3) == 0, f[u]);
       }
 #pragma unroll
       for (int u = 0; u < kRounds; ++u) {
         const int64_t cc = c + 2 * u + half;
         const uint64_t d = tree16(fold_leaf(f[u]), j);
-        if (j == 0 && cc < c1) out[cc] = d;
+        if (j == 0 && cc < c1) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
       }
     }
   }
@@ -138,8 +151,18 @@ __global__ void k_chain(int64_t n_req, const int64_t* __restrict__ chunk_offsets
   if (r >= n_req) return;
   uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
   const int64_t e = chunk_offsets[r + 1];
-#pragma unroll 4
-  for (int64_t c = chunk_offsets[r]; c < e; ++c) {
+  int64_t c = chunk_offsets[r];
+  for (; c + 8 <= e; c += 8) {  // 8 independent loads in flight, then the dependent chain
+    uint64_t d[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d[k] = out[c + k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      h = fpair(h, d[k]);
+      out[c + k] = h;
+    }
+  }
+  for (; c < e; ++c) {
     h = fpair(h, out[c]);
     out[c] = h;
   }
