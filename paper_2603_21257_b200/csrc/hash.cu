@@ -28,6 +28,19 @@ constexpr int kHashThreads = 256;
 constexpr int kHashWarps = kHashThreads / 32;
 constexpr int kRounds = 2;  // rounds of 2 chunks loaded ahead per warp
 
+// Token ids are read exactly once: stream them through L2 with evict_first so the 87 MB of chunk
+// digests written by phase 1 survive in L2 for phase 2.
+__device__ __forceinline__ int4 ld_evict_first(const void* p) {
+  int4 r;
+  asm volatile(
+      "{\n.reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], pol;\n}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+
 struct Leaf {
   int4 v[4];  // 16 int32 tokens
 };
@@ -37,7 +50,7 @@ struct Leaf {
 __device__ __forceinline__ void load_leaf(const int32_t* p, bool aligned, Leaf& f) {
   if (aligned) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) f.v[k] = ld_stream(p + 64 * k);
+    for (int k = 0; k < 4; ++k) f.v[k] = ld_evict_first(p + 64 * k);
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -152,12 +165,12 @@ __global__ void k_chain(int64_t n_req, const int64_t* __restrict__ chunk_offsets
   uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
   const int64_t e = chunk_offsets[r + 1];
   int64_t c = chunk_offsets[r];
-  for (; c + 8 <= e; c += 8) {  // 8 independent loads in flight, then the dependent chain
-    uint64_t d[8];
+  for (; c + 16 <= e; c += 16) {  // 16 independent loads in flight, then the dependent chain
+    uint64_t d[16];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) d[k] = out[c + k];
+    for (int k = 0; k < 16; ++k) d[k] = out[c + k];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 16; ++k) {
       h = fpair(h, d[k]);
       out[c + k] = h;
     }
