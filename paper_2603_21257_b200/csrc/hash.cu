@@ -158,27 +158,31 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
 
 // Phase 2 -- the per-request chain H_c = pair(H_{c-1}, digest_c), in place; one thread per
 // request, loads are independent of the chain so they pipeline; the digests are L2-resident.
-// One warp per request: 32 digests per coalesced load (the next 32 prefetched while the current
-// ones are chained); every lane runs the (cheap) chain redundantly and lane k keeps H_k, so the
-// results are stored coalesced too.
-__global__ void __launch_bounds__(256) k_chain(int64_t n_req, const int64_t* __restrict__ chunk_offsets,
+// One thread per request, software-pipelined: the next group of kG digests is loaded before the
+// current group is folded into the chain, so each iteration's latency overlaps the previous one.
+constexpr int kG = 32;
+
+__global__ void __launch_bounds__(128) k_chain(int64_t n_req, const int64_t* __restrict__ chunk_offsets,
                                                uint64_t* __restrict__ out) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(kHashWarps) + (threadIdx.x >> 5);
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r >= n_req) return;
-  const int lane = threadIdx.x & 31;
   const int64_t b = chunk_offsets[r], e = chunk_offsets[r + 1];
   uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
-  uint64_t next = b + lane < e ? out[b + lane] : 0;
-  for (int64_t c = b; c < e; c += 32) {
-    const uint64_t d = next;
-    if (c + 32 < e) next = c + 32 + lane < e ? out[c + 32 + lane] : 0;
-    const int n = static_cast<int>(e - c < 32 ? e - c : 32);
-    uint64_t mine = 0;
-    for (int k = 0; k < n; ++k) {
-      h = fpair(h, __shfl_sync(0xffffffffu, d, k));
-      if (lane == k) mine = h;
+  uint64_t cur[kG], nxt[kG];
+#pragma unroll
+  for (int k = 0; k < kG; ++k) cur[k] = b + k < e ? out[b + k] : 0;
+  for (int64_t c = b; c < e; c += kG) {
+#pragma unroll
+    for (int k = 0; k < kG; ++k) nxt[k] = c + kG + k < e ? out[c + kG + k] : 0;
+#pragma unroll
+    for (int k = 0; k < kG; ++k) {
+      if (c + k < e) {
+        h = fpair(h, cur[k]);
+        out[c + k] = h;
+      }
     }
-    if (lane < n) out[c + lane] = mine;
+#pragma unroll
+    for (int k = 0; k < kG; ++k) cur[k] = nxt[k];
   }
 }
 
@@ -206,7 +210,7 @@ cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int3
   // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
   k_chunk_digest<<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
-  k_chain<<<ceil_div(n_req, kHashWarps), kHashThreads, 0, st>>>(n_req, chunk_offsets, out);
+  k_chain<<<ceil_div(n_req, 128), 128, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();
   return cudaGetLastError();
 }
