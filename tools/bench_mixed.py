@@ -40,10 +40,18 @@ def mixed_batch(n, seed, block=256):
 
 
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--compute-per-token", type=float, default=4e-5,
+                    help="prefill seconds/token: 4e-5 = the reference calibration (types.hpp:91); "
+                         "~4e-6 approximates an 8B prefill on B200")
+    args = ap.parse_args()
     shape = ingest.LLAMA31_8B
     n = 48
     q = mixed_batch(n, 0)
-    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(32, 8, 128, 2))
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(32, 8, 128, 2),
+                          compute_per_token=args.compute_per_token)
     plans = [int(np.floor(q.context_tokens[i] * q.cache_hit_ratio[i] / 256)) for i in range(n)]
     n_slots = max(plans) + 64
     pool = ingest.ChunkPool(shape, n_slots)
