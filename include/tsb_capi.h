@@ -177,6 +177,36 @@ tsb_status tsb_gen_tokens_device(void* stream, uint64_t seed, int64_t n_req,
                                  const int64_t* shared_len, int32_t* out);
 
 /* ------------------------------------------------------------------------------------ */
+/* L2 chunk index (K7): chained prefix-chunk hash -> L2 pool slot, an open-addressing table   */
+/* in HBM.  Replaces the synthetic cache_hit_ratio input of cached_token_count               */
+/* (types.cpp:73-79) with a real prefix match: request r's matched prefix = the number of     */
+/* leading chunks whose hash is indexed (hash c names the prefix [0, 256(c+1)), so the match  */
+/* stops at the first absent chunk).  Hash values 2^64-1 and 2^64-2 are reserved.            */
+/* ------------------------------------------------------------------------------------ */
+typedef struct tsb_index tsb_index;
+/* capacity is rounded up to a power of two; keep the load factor below ~0.5. */
+tsb_status tsb_index_create(int device, int64_t capacity, tsb_index** out);
+void tsb_index_destroy(tsb_index* x);
+int64_t tsb_index_capacity(const tsb_index* x);
+/* Device pointers; async.  Re-inserting an indexed hash updates its slot. */
+tsb_status tsb_index_insert_device(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes,
+                                   const int64_t* slots);
+tsb_status tsb_index_erase_device(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes);
+/* chunk_offsets[n_req+1] as for the hasher; slots_out[c] = pool slot of chunk c for the matched
+ * prefix, -1 from the first miss on; matched_out[r] = matched chunks of request r. */
+tsb_status tsb_index_lookup_device(tsb_index* x, void* stream, int64_t n_req,
+                                   const int64_t* chunk_offsets, const uint64_t* hashes,
+                                   int64_t* slots_out, int64_t* matched_out);
+/* Live entries and failed inserts (table full); synchronises. */
+tsb_status tsb_index_stats(tsb_index* x, void* stream, int64_t* live, int64_t* full_failures);
+/* Host-pointer variants (synchronise); insert returns CAPACITY if the table is full.
+ * chunk_offsets[0] must be 0. */
+tsb_status tsb_index_insert(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes,
+                            const int64_t* slots);
+tsb_status tsb_index_lookup(tsb_index* x, void* stream, int64_t n_req, const int64_t* chunk_offsets,
+                            const uint64_t* hashes, int64_t* slots_out, int64_t* matched_out);
+
+/* ------------------------------------------------------------------------------------ */
 /* L2 chunk pool: pinned, portable, mapped host memory (replaces TierLedger(L2) as a byte   */
 /* store; engine.cpp:18-49 stays the accounting).  Slot s holds one full chunk             */
 /* [L][2][C][H][D] at host address base + s*chunk_bytes.                                   */

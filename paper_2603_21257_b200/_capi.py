@@ -139,6 +139,15 @@ _decl("tsb_score_queue", st, vp, vp, i64, P(Queue), C.c_int, P(f64), P(Cluster),
 _decl("tsb_hash_prefix_chunks_device", st, vp, i64, vp, vp, vp, vp)
 _decl("tsb_hash_prefix_chunks", st, vp, i64, vp, vp, vp, P(i64))
 _decl("tsb_gen_tokens_device", st, vp, u64, i64, vp, vp, vp, vp)
+_decl("tsb_index_create", st, C.c_int, i64, P(vp))
+_decl("tsb_index_destroy", None, vp)
+_decl("tsb_index_capacity", i64, vp)
+_decl("tsb_index_insert_device", st, vp, vp, i64, vp, vp)
+_decl("tsb_index_erase_device", st, vp, vp, i64, vp)
+_decl("tsb_index_lookup_device", st, vp, vp, i64, vp, vp, vp, vp)
+_decl("tsb_index_stats", st, vp, vp, P(i64), P(i64))
+_decl("tsb_index_insert", st, vp, vp, i64, vp, vp)
+_decl("tsb_index_lookup", st, vp, vp, i64, vp, vp, vp, vp)
 _decl("tsb_pool_create", st, P(KvShape), i64, P(vp))
 _decl("tsb_pool_wrap", st, P(KvShape), vp, i64, P(vp))
 _decl("tsb_pool_register", st, P(KvShape), vp, i64, P(vp))

@@ -1,0 +1,136 @@
+// index.cu — K7 device-side L2 chunk index: chained prefix-chunk hash -> L2 pool slot.
+//
+// SURVEY.md 8 f3.  The reference has no lookup: a request's cached prefix is the synthetic
+// `cache_hit_ratio` fed to cached_token_count (types.cpp:73-79).  Here the hashes K3 computes for
+// a request's full chunks are looked up in an open-addressing table (linear probing, 64-bit keys,
+// atomicCAS insert) that indexes the L2 pool; the matched prefix length (leading chunks present)
+// replaces the hit ratio and the matched slots are the ingest plan's sources.  Because hash c
+// names the whole prefix [0, 256(c+1)), the match stops at the first absent chunk.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tsb {
+namespace {
+
+constexpr uint64_t kEmpty = ~0ull;
+constexpr uint64_t kTomb = ~0ull - 1;
+
+__device__ __forceinline__ uint64_t slot_of(uint64_t h, uint64_t mask) {
+  return mix64(h) & mask;  // FNV low bits are weak; remix before masking
+}
+
+__global__ void k_index_insert(uint64_t* __restrict__ keys, int64_t* __restrict__ vals,
+                               uint64_t mask, int64_t n, const uint64_t* __restrict__ hashes,
+                               const int64_t* __restrict__ slots,
+                               unsigned long long* __restrict__ stats /* [0]=new, [1]=full */) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t h = hashes[i];
+  uint64_t p = slot_of(h, mask);
+  for (uint64_t probe = 0; probe <= mask; ++probe, p = (p + 1) & mask) {
+    const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(keys + p),
+                                    static_cast<unsigned long long>(kEmpty),
+                                    static_cast<unsigned long long>(h));
+    if (prev == kEmpty) {
+      vals[p] = slots[i];
+      atomicAdd(stats, 1ull);
+      return;
+    }
+    if (prev == h) {  // already indexed: the newest slot wins
+      vals[p] = slots[i];
+      return;
+    }
+  }
+  atomicAdd(stats + 1, 1ull);  // table full
+}
+
+__global__ void k_index_erase(uint64_t* __restrict__ keys, uint64_t mask, int64_t n,
+                              const uint64_t* __restrict__ hashes,
+                              unsigned long long* __restrict__ stats /* [2]=erased */) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t h = hashes[i];
+  uint64_t p = slot_of(h, mask);
+  for (uint64_t probe = 0; probe <= mask; ++probe, p = (p + 1) & mask) {
+    const uint64_t k = keys[p];
+    if (k == kEmpty) return;
+    if (k == h) {
+      if (atomicCAS(reinterpret_cast<unsigned long long*>(keys + p),
+                    static_cast<unsigned long long>(h), static_cast<unsigned long long>(kTomb)) == h)
+        atomicAdd(stats + 2, 1ull);
+      return;
+    }
+  }
+}
+
+__device__ __forceinline__ int64_t probe_find(const uint64_t* __restrict__ keys,
+                                              const int64_t* __restrict__ vals, uint64_t mask,
+                                              uint64_t h) {
+  uint64_t p = slot_of(h, mask);
+  for (uint64_t probe = 0; probe <= mask; ++probe, p = (p + 1) & mask) {
+    const uint64_t k = keys[p];
+    if (k == h) return vals[p];
+    if (k == kEmpty) return -1;
+  }
+  return -1;
+}
+
+// One warp per request: 32 chunks probed in parallel per step, ballot finds the first miss.
+__global__ void __launch_bounds__(256) k_index_lookup(const uint64_t* __restrict__ keys,
+                                                      const int64_t* __restrict__ vals,
+                                                      uint64_t mask, int64_t n_req,
+                                                      const int64_t* __restrict__ chunk_offsets,
+                                                      const uint64_t* __restrict__ hashes,
+                                                      int64_t* __restrict__ slots_out,
+                                                      int64_t* __restrict__ matched) {
+  const int64_t r = blockIdx.x * 8ll + (threadIdx.x >> 5);
+  if (r >= n_req) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = chunk_offsets[r], e = chunk_offsets[r + 1];
+  int64_t m = e - b;
+  bool missed = false;
+  for (int64_t c = b; c < e; c += 32) {
+    const int64_t cc = c + lane;
+    int64_t s = -1;
+    if (!missed && cc < e) s = probe_find(keys, vals, mask, hashes[cc]);
+    const unsigned miss = __ballot_sync(0xffffffffu, cc < e && s < 0);
+    if (!missed && miss) {
+      m = (c - b) + __ffs(miss) - 1;
+      missed = true;
+    }
+    if (cc < e) slots_out[cc] = (missed && cc - b >= m) ? -1 : s;
+  }
+  if (lane == 0) matched[r] = m;
+}
+
+}  // namespace
+
+cudaError_t launch_index_insert(uint64_t* keys, int64_t* vals, uint64_t mask, int64_t n,
+                                const uint64_t* hashes, const int64_t* slots,
+                                unsigned long long* stats, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_index_insert<<<ceil_div(n, 256), 256, 0, st>>>(keys, vals, mask, n, hashes, slots, stats);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_index_erase(uint64_t* keys, uint64_t mask, int64_t n, const uint64_t* hashes,
+                               unsigned long long* stats, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_index_erase<<<ceil_div(n, 256), 256, 0, st>>>(keys, mask, n, hashes, stats);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_index_lookup(const uint64_t* keys, const int64_t* vals, uint64_t mask,
+                                int64_t n_req, const int64_t* chunk_offsets,
+                                const uint64_t* hashes, int64_t* slots_out, int64_t* matched,
+                                cudaStream_t st) {
+  if (n_req == 0) return cudaSuccess;
+  k_index_lookup<<<ceil_div(n_req, 8), 256, 0, st>>>(keys, vals, mask, n_req, chunk_offsets,
+                                                     hashes, slots_out, matched);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace tsb

@@ -69,6 +69,17 @@ cudaError_t launch_gen_tokens(uint64_t seed, int64_t n_req, const int64_t* offse
                               const int64_t* doc, const int64_t* shared_len, int32_t* out,
                               cudaStream_t st);
 
+// L2 chunk index (K7).
+cudaError_t launch_index_insert(uint64_t* keys, int64_t* vals, uint64_t mask, int64_t n,
+                                const uint64_t* hashes, const int64_t* slots,
+                                unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_index_erase(uint64_t* keys, uint64_t mask, int64_t n, const uint64_t* hashes,
+                               unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_index_lookup(const uint64_t* keys, const int64_t* vals, uint64_t mask,
+                                int64_t n_req, const int64_t* chunk_offsets,
+                                const uint64_t* hashes, int64_t* slots_out, int64_t* matched,
+                                cudaStream_t st);
+
 // Synthetic prefill burner (K6, harness).
 cudaError_t launch_prefill_burn(uint64_t ns, int ctas, unsigned long long* sink, cudaStream_t st);
 

@@ -44,6 +44,63 @@ def hash_prefix_chunks_device(offsets: torch.Tensor, tokens: torch.Tensor, coffs
     return out
 
 
+class PrefixIndex:
+    """L2 chunk index on the GPU (K7): chained chunk hash -> L2 pool slot (tsb_index_*).
+
+    lookup() returns, per request, the matched prefix in chunks and the pool slots of those
+    chunks -- the real-prefix replacement for the reference's synthetic cache_hit_ratio."""
+
+    def __init__(self, capacity: int, device: int = 0):
+        h = C.c_void_p()
+        check(lib.tsb_index_create(device, int(capacity), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.tsb_index_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @property
+    def capacity(self) -> int:
+        return lib.tsb_index_capacity(self._h)
+
+    def insert(self, hashes: np.ndarray, slots: np.ndarray, stream=None):
+        hashes = np.ascontiguousarray(hashes, np.uint64)
+        slots = np.ascontiguousarray(slots, np.int64)
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        check(lib.tsb_index_insert(self._h, s, len(hashes), hashes.ctypes.data, slots.ctypes.data))
+
+    def erase_device(self, hashes: torch.Tensor, stream=None):
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        check(lib.tsb_index_erase_device(self._h, s, hashes.numel(), hashes.data_ptr()))
+
+    def lookup(self, chunk_offs: np.ndarray, hashes: np.ndarray, stream=None):
+        chunk_offs = np.ascontiguousarray(chunk_offs, np.int64)
+        hashes = np.ascontiguousarray(hashes, np.uint64)
+        n_req = len(chunk_offs) - 1
+        slots = np.empty(max(len(hashes), 1), np.int64)
+        matched = np.empty(max(n_req, 1), np.int64)
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        check(lib.tsb_index_lookup(self._h, s, n_req, chunk_offs.ctypes.data, hashes.ctypes.data,
+                                   slots.ctypes.data, matched.ctypes.data))
+        return matched[:n_req], slots[: len(hashes)]
+
+    def stats(self, stream=None):
+        live, full = C.c_int64(), C.c_int64()
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        check(lib.tsb_index_stats(self._h, s, C.byref(live), C.byref(full)))
+        return live.value, full.value
+
+
+def hit_ratio_for_match(context_tokens: int, matched_chunks: int, block: int = 256) -> float:
+    """A cache_hit_ratio whose floor rule (types.cpp:73-79) yields exactly matched_chunks."""
+    if matched_chunks * block >= context_tokens:
+        return 1.0
+    return (matched_chunks * block + block / 2) / context_tokens
+
+
 def gen_tokens_device(seed: int, offsets: torch.Tensor, doc: torch.Tensor, shared_len: torch.Tensor,
                       out: torch.Tensor, stream=None) -> torch.Tensor:
     s = (stream or torch.cuda.current_stream()).cuda_stream
