@@ -119,4 +119,13 @@ __device__ __forceinline__ void bulk_wait0() {
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
+// True the first time it is called for the current device with this flag: per-device one-time
+// kernel attribute setup (cudaFuncSetAttribute is per device).
+inline bool first_on_device(std::atomic<uint64_t>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  const uint64_t bit = 1ull << (dev & 63);
+  return (done.fetch_or(bit) & bit) == 0;
+}
+
 }  // namespace tsb

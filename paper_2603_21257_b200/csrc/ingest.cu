@@ -202,12 +202,11 @@ cudaError_t launch_ingest_bulk(const IngestGeom& g, const uint8_t* src, uint8_t*
   if (nseg == 0) return cudaSuccess;
   constexpr int kStages = 6;
   const size_t smem = static_cast<size_t>(kStages) * g.seg_bytes;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};
+  if (first_on_device(attr_set)) {
     cudaError_t e = cudaFuncSetAttribute(k_ingest_bulk<kStages>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   k_ingest_bulk<kStages><<<grid, 32, smem, st>>>(g, src, arena, items, bt, nseg);
   count_launch();

@@ -298,15 +298,14 @@ cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, in
   if (n == 0) return cudaSuccess;
   constexpr size_t kSmem = smem_bytes(kTileN);       // 68 KiB
   constexpr size_t kMergeSmem = smem_bytes(kMergeN);  // 34 KiB
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kSmem));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_merge_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(kMergeSmem));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int tiles = ceil_div(n, kTileN);
   if (tiles == 1) {

@@ -72,6 +72,16 @@ class PrefixIndex:
         s = (stream or torch.cuda.current_stream()).cuda_stream
         check(lib.tsb_index_insert(self._h, s, len(hashes), hashes.ctypes.data, slots.ctypes.data))
 
+    def insert_device(self, hashes: torch.Tensor, slots: torch.Tensor, stream=None):
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        check(lib.tsb_index_insert_device(self._h, s, hashes.numel(), hashes.data_ptr(), slots.data_ptr()))
+
+    def lookup_device(self, chunk_offs: torch.Tensor, hashes: torch.Tensor, slots_out: torch.Tensor,
+                      matched_out: torch.Tensor, stream=None):
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        check(lib.tsb_index_lookup_device(self._h, s, chunk_offs.numel() - 1, chunk_offs.data_ptr(),
+                                          hashes.data_ptr(), slots_out.data_ptr(), matched_out.data_ptr()))
+
     def erase_device(self, hashes: torch.Tensor, stream=None):
         s = (stream or torch.cuda.current_stream()).cuda_stream
         check(lib.tsb_index_erase_device(self._h, s, hashes.numel(), hashes.data_ptr()))

@@ -103,6 +103,17 @@ def main():
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     res["hash"] = {"tokens": int(offs[-1]), "chunks": int(coff[-1]), "ms": secs * 1e3, "GBps": nbytes / secs / 1e9,
                    "hbm_frac": nbytes / secs / 1e9 / peak, "algorithmic_bytes": int(nbytes)}
+    # K7: index every chunk hash of the queue (the L2 pool index), then look the queue up
+    idx = hasher.PrefixIndex(capacity=4 * hout.numel())
+    slots_t = torch.arange(hout.numel(), dtype=torch.int64, device=dev)
+    ins_s = timed(lambda: idx.insert_device(hout, slots_t), reps=1, warm=0)
+    m_out = torch.empty(n, dtype=torch.int64, device=dev)
+    s_out = torch.empty_like(hout)
+    look_s = timed(lambda: idx.lookup_device(coff, hout, s_out, m_out), reps=10)
+    live, full = idx.stats()
+    res["index"] = {"entries": live, "capacity": idx.capacity, "insert_ms": ins_s * 1e3, "lookup_ms": look_s * 1e3,
+                    "lookups_per_s": hout.numel() / look_s, "all_matched": bool((m_out.cpu().numpy() ==
+                                                                                np.diff(hasher.chunk_offsets(offs))).all())}
     # CPU hash_ref on a sample of 2000 requests, all host threads
     k = 2000
     sample_tok = tok[: int(offs[k])].cpu().numpy()
