@@ -106,9 +106,23 @@ class LoadStage {
     tsb_stage_stats stats{};
   };
   /// slots[i][c] = pool slot of request i's planned chunk c.
+  /// Real-time replay of arrivals with SimEngine's decoupled control loop (tsb_stage_run_online).
+  Result run_online(std::span<const RequestSpec> batch, const std::vector<std::vector<int64_t>>& slots,
+                    const ClusterConfig& config, const CostModelPair& models, tsb_stage_options opt,
+                    void* stream = nullptr) {
+    return run_impl(tsb_stage_run_online, batch, slots, config, models, opt, stream);
+  }
   Result run(std::span<const RequestSpec> batch, const std::vector<std::vector<int64_t>>& slots,
              const ClusterConfig& config, const CostModelPair& models, tsb_stage_options opt,
              void* stream = nullptr) {
+    return run_impl(tsb_stage_run, batch, slots, config, models, opt, stream);
+  }
+
+ private:
+  template <typename Fn>
+  Result run_impl(Fn fn, std::span<const RequestSpec> batch,
+                  const std::vector<std::vector<int64_t>>& slots, const ClusterConfig& config,
+                  const CostModelPair& models, tsb_stage_options opt, void* stream) {
     QueueSoA q(batch, nullptr);
     std::vector<int64_t> off(1, 0), flat;
     for (const auto& s : slots) {
@@ -120,12 +134,11 @@ class LoadStage {
     const tsb_cluster c = config.c_abi();
     Result r;
     r.requests.resize(batch.size());
-    check(tsb_stage_run(s_.get(), q.size(), q.get(), &c, m, off.data(), flat.data(), &opt, stream,
-                        r.requests.data(), &r.stats));
+    check(fn(s_.get(), q.size(), q.get(), &c, m, off.data(), flat.data(), &opt, stream,
+             r.requests.data(), &r.stats));
     return r;
   }
 
- private:
   struct Del {
     void operator()(tsb_stage* s) const { tsb_stage_destroy(s); }
   };

@@ -373,7 +373,9 @@ typedef struct {
   int64_t bytes;           /* bytes moved L2 -> L1 for this request on this GPU */
   double first_layer_ms;   /* run start -> layer lo of every chunk resident (CUDA events) */
   double resident_ms;      /* run start -> all layers resident (Timestamps::l1_resident) */
-  double done_ms;          /* run start -> prefill done / pages released */
+  double done_ms;          /* run start -> prefill done / pages released (first token) */
+  double admit_ms;         /* run start -> admitted (Timestamps::scheduled; host clock) */
+  double arrival_ms;       /* run start -> arrival (online mode: replayed arrival time) */
 } tsb_stage_request;
 
 typedef struct {
@@ -410,6 +412,21 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
                          const double models[4], const int64_t* slot_offsets,
                          const int64_t* slots, const tsb_stage_options* opt, void* stream,
                          tsb_stage_request* results, tsb_stage_stats* stats);
+/* Online replay: requests arrive at their arrival_time (seconds after the first arrival, on the
+ * host clock) and the stage runs SimEngine's decoupled control loop in real time
+ * (engine.cpp:290-302): the best pending request (PriorityKey order, keys from the GPU scorer)
+ * is admitted only when the ingest stage is idle and has no backlog (try_admit, :318-339);
+ * admission reserves L1 for its whole plan (proactive, :419); granted chunks are ingested in
+ * admission order (pcie_dispatch, :427-446); the compute stage prefills the best-key resident
+ * request whenever it is idle (try_start_compute, :448-473) with the K6 synthetic prefill
+ * (compute_base + compute_per_token*n + compute_quadratic*n^2); pages are released at
+ * ComputeDone (:280-282).  done_ms - arrival_ms is the request's TTFT.  opt->prefill is
+ * ignored (always on).  Synchronises; results may be NULL. */
+tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
+                                const tsb_cluster* c, const double models[4],
+                                const int64_t* slot_offsets, const int64_t* slots,
+                                const tsb_stage_options* opt, void* stream,
+                                tsb_stage_request* results, tsb_stage_stats* stats);
 /* Trace of the last run (when record_trace was set): copies min(n, cap) rows. */
 tsb_status tsb_stage_trace(tsb_stage* s, tsb_trace_row* out, int64_t cap, int64_t* n);
 

@@ -92,7 +92,8 @@ class StageOptions(C.Structure):
 
 class StageRequest(C.Structure):
     _fields_ = [("request_id", i64), ("pick_position", i32), ("deferred_chunks", i32), ("chunks", i64),
-                ("bytes", i64), ("first_layer_ms", f64), ("resident_ms", f64), ("done_ms", f64)]
+                ("bytes", i64), ("first_layer_ms", f64), ("resident_ms", f64), ("done_ms", f64),
+                ("admit_ms", f64), ("arrival_ms", f64)]
 
 
 class StageStats(C.Structure):
@@ -186,6 +187,8 @@ _decl("tsb_stage_destroy", None, vp)
 _decl("tsb_stage_run", st, vp, i64, P(Queue), P(Cluster), P(f64), vp, vp, P(StageOptions), vp, P(StageRequest),
       P(StageStats))
 _decl("tsb_stage_trace", st, vp, P(TraceRow), i64, P(i64))
+_decl("tsb_stage_run_online", st, vp, i64, P(Queue), P(Cluster), P(f64), vp, vp, P(StageOptions), vp,
+      P(StageRequest), P(StageStats))
 _decl("tsb_l1_verify_synthetic", st, vp, P(IngestItem), i64, i64, i64, u64, i64, vp, P(u64))
 
 EXPORTED = sorted(

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <ctime>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -320,7 +321,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     last_ms = std::max(last_ms, b);
     if (results)
       results[i] = tsb_stage_request{r.id, static_cast<int32_t>(pos_of[i]), r.deferred, r.n_chunks,
-                                     r.n_chunks * chunk_bytes, a, b, d};
+                                     r.n_chunks * chunk_bytes, a, b, d, 0.0, 0.0};
   }
   if (opt->record_trace) {
     for (auto& tr : s->trace) {
@@ -342,6 +343,286 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     stats->releases = releases;
     stats->kernel_launches = static_cast<int64_t>(tsb_kernel_launch_count() - launches0);
     stats->verify_mismatches = verify_mismatches;
+  }
+  return TSB_OK;
+}
+
+tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
+                                const tsb_cluster* c, const double models[4],
+                                const int64_t* slot_offsets, const int64_t* slots,
+                                const tsb_stage_options* opt, void* stream,
+                                tsb_stage_request* results, tsb_stage_stats* stats) {
+  const double wall0 = now_s();
+  const uint64_t launches0 = tsb_kernel_launch_count();
+  auto st = static_cast<cudaStream_t>(stream);
+  const int64_t L = s->shape.layers;
+  int64_t chunk_bytes_full = 0, page_bytes = 0, chunk_bytes = 0;
+  TSB_TRY(tsb_kv_shape_info(&s->shape, &chunk_bytes_full, &page_bytes, &chunk_bytes));
+  TSB_TRY(tsb_cluster_validate(c));
+  if (c->block_size_tokens != s->shape.chunk_tokens)
+    return fail(TSB_VALIDATION, "stage: cluster block_size_tokens must equal the KV chunk_tokens");
+  if (n == 0) return TSB_OK;
+  struct Rt {
+    int64_t id = 0, n_chunks = 0, compute_tokens = 0;
+    const int64_t* slots = nullptr;
+    int32_t row = -1, deferred = 0;
+    std::vector<int32_t> ready;
+    int64_t issued = 0, granted = 0;
+    bool arrived = false, admitted = false, dispatched_all = false, resident = false,
+         started = false, finished = false;
+    double arrival = 0.0, admit_t = 0.0;
+    cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr;
+  };
+  std::vector<Rt> R(static_cast<size_t>(n));
+  std::unordered_map<int64_t, size_t> by_id;
+  const int64_t l1_capacity = tsb_l1_capacity(s->l1);
+  double first_arrival = q->arrival[0];
+  for (int64_t i = 0; i < n; ++i) first_arrival = std::min(first_arrival, q->arrival[i]);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t cached = 0, compute = 0, nb = 0, bt = 0, bb = 0;
+    TSB_TRY(tsb_derive_block_plan(q, i, c, &cached, &compute, &nb, &bt, &bb));
+    Rt& r = R[i];
+    r.id = q->id[i];
+    r.n_chunks = nb;
+    r.compute_tokens = compute;
+    r.slots = slots + slot_offsets[i];
+    r.arrival = q->arrival[i] - first_arrival;
+    if (slot_offsets[i + 1] - slot_offsets[i] != nb)
+      return fail(TSB_VALIDATION, "stage: request " + std::to_string(r.id) + " lists " +
+                                      std::to_string(slot_offsets[i + 1] - slot_offsets[i]) +
+                                      " pool slots for a plan of " + std::to_string(nb) + " chunks");
+    if (nb * chunk_bytes > l1_capacity)
+      return fail(TSB_CAPACITY, "request " + std::to_string(r.id) + ": " +
+                                    std::to_string(nb * chunk_bytes) +
+                                    " resident bytes can never fit");
+    if (!by_id.emplace(r.id, static_cast<size_t>(i)).second)
+      return fail(TSB_VALIDATION, "run_simulation: duplicate request id " + std::to_string(r.id));
+  }
+  while (s->timing_pool.size() < static_cast<size_t>(3 * n)) {
+    cudaEvent_t e;
+    TSB_CUDA_TRY(cudaEventCreate(&e));
+    s->timing_pool.push_back(e);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    R[i].ev_first = s->timing_pool[3 * i];
+    R[i].ev_resident = s->timing_pool[3 * i + 1];
+    R[i].ev_done = s->timing_pool[3 * i + 2];
+  }
+  // Priority keys from the GPU scorer (K4), compared with PriorityKey::operator< on the host.
+  std::vector<double> primary(static_cast<size_t>(n));
+  std::vector<int64_t> order(static_cast<size_t>(n));
+  TSB_TRY(tsb_score_queue(s->scorer, stream, n, q, opt->policy, models, c, nullptr, nullptr,
+                          primary.data(), order.data()));
+  auto key_less = [&](size_t a, size_t b) {
+    if (primary[a] != primary[b]) return primary[a] < primary[b];
+    if (q->arrival[a] != q->arrival[b]) return q->arrival[a] < q->arrival[b];
+    return q->id[a] < q->id[b];
+  };
+  std::vector<size_t> by_arrival(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) by_arrival[i] = static_cast<size_t>(i);
+  std::stable_sort(by_arrival.begin(), by_arrival.end(),
+                   [&](size_t a, size_t b) { return R[a].arrival < R[b].arrival; });
+
+  cudaEvent_t ev_ingest = nullptr, ev_compute = nullptr;
+  TSB_CUDA_TRY(cudaEventCreateWithFlags(&ev_ingest, cudaEventDisableTiming));
+  TSB_CUDA_TRY(cudaEventCreateWithFlags(&ev_compute, cudaEventDisableTiming));
+  bool ingest_issued = false, compute_issued = false;
+  const int ctas = opt->prefill_ctas > 0 ? opt->prefill_ctas : 148;
+  std::vector<tsb_grant> grants(4096);
+  int64_t ingest_calls = 0, deferred_total = 0, releases = 0, bytes_total = 0;
+  std::vector<size_t> pending, admitted;
+  size_t next_arrival = 0, finished = 0;
+  int64_t pick = 0;
+  std::vector<int32_t> pick_pos(static_cast<size_t>(n), -1);
+
+  TSB_CUDA_TRY(cudaEventRecord(s->ev_start, st));
+  const double host0 = now_s();
+  auto done = [](cudaEvent_t e) { return cudaEventQuery(e) == cudaSuccess; };
+  tsb_status status = TSB_OK;
+  auto fail_out = [&](tsb_status st_) {
+    status = st_;
+    return st_;
+  };
+
+  while (finished < static_cast<size_t>(n)) {
+    const double now = now_s() - host0;
+    while (next_arrival < by_arrival.size() && R[by_arrival[next_arrival]].arrival <= now) {
+      R[by_arrival[next_arrival]].arrived = true;
+      pending.push_back(by_arrival[next_arrival++]);
+    }
+    bool progress = true;
+    while (progress) {
+      progress = false;
+      // ComputeDone -> release this request's L1 pages; FIFO grants to waiting reservations.
+      for (size_t i : admitted) {
+        Rt& r = R[i];
+        if (!r.started || r.finished || !done(r.ev_done)) continue;
+        r.finished = true;
+        ++finished;
+        progress = true;
+        if (r.row >= 0) {
+          int64_t ng = 0;
+          if (grants.size() < static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1)
+            grants.resize(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
+          if (tsb_l1_release_request(s->l1, r.id, grants.data(),
+                                     static_cast<int64_t>(grants.size()), &ng) != TSB_OK)
+            return fail_out(TSB_VALIDATION);
+          ++releases;
+          for (int64_t g = 0; g < ng; ++g) {
+            Rt& w = R[by_id.at(grants[g].request_id)];
+            w.ready.push_back(grants[g].block_index);
+            ++w.granted;
+          }
+        }
+      }
+      // PcieDone of a request's last chunk -> L1 resident -> compute ready.
+      for (size_t i : admitted) {
+        Rt& r = R[i];
+        if (r.dispatched_all && !r.resident && done(r.ev_resident)) {
+          r.resident = true;
+          progress = true;
+        }
+      }
+      // try_admit, decoupled (engine.cpp:318-339): the first stage must be idle with no backlog.
+      if (!pending.empty()) {
+        size_t bi = 0;
+        for (size_t k = 1; k < pending.size(); ++k)
+          if (key_less(pending[k], pending[bi])) bi = k;
+        Rt& r = R[pending[bi]];
+        bool backlog = false;
+        for (size_t i : admitted)
+          if (!R[i].dispatched_all) backlog = true;
+        bool can = false;
+        if (r.n_chunks > 0) {
+          can = !backlog && (!ingest_issued || done(ev_ingest));
+        } else {
+          bool ready_waiting = false;
+          for (size_t i : admitted)
+            if (R[i].resident && !R[i].started) ready_waiting = true;
+          can = (!compute_issued || done(ev_compute)) && !ready_waiting;
+        }
+        if (can) {
+          const size_t idx = pending[bi];
+          pending.erase(pending.begin() + static_cast<std::ptrdiff_t>(bi));
+          r.admitted = true;
+          r.admit_t = now_s() - host0;
+          pick_pos[idx] = static_cast<int32_t>(pick++);
+          admitted.push_back(idx);
+          for (int64_t ch = 0; ch < r.n_chunks; ++ch) {
+            int granted = 0;
+            const tsb_status rs = tsb_l1_request(s->l1, r.id, static_cast<int32_t>(ch), chunk_bytes,
+                                                 &granted, &r.row);
+            if (rs != TSB_OK) return fail_out(rs);
+            if (granted) {
+              r.ready.push_back(static_cast<int32_t>(ch));
+              ++r.granted;
+            } else {
+              ++r.deferred;
+              ++deferred_total;
+            }
+          }
+          if (r.n_chunks == 0) {
+            r.dispatched_all = true;
+            cudaEventRecord(r.ev_first, st);
+            cudaEventRecord(r.ev_resident, st);
+          }
+          progress = true;
+        }
+      }
+      // pcie_dispatch: granted chunks of admitted requests, in admission order.
+      for (size_t i : admitted) {
+        Rt& r = R[i];
+        if (r.ready.empty()) continue;
+        if (tsb_l1_sync_block_table(s->l1, stream) != TSB_OK) return fail_out(TSB_CUDA);
+        std::vector<tsb_ingest_item> items;
+        for (int32_t ch : r.ready) items.push_back(tsb_ingest_item{r.slots[ch], r.row, ch});
+        r.ready.clear();
+        r.issued += static_cast<int64_t>(items.size());
+        const bool last = r.issued == r.n_chunks;
+        std::vector<void*> evs;
+        if (last) {
+          evs.assign(static_cast<size_t>(L), nullptr);
+          evs[0] = r.ev_first;
+          evs[L - 1] = r.ev_resident;
+        }
+        const tsb_status is = tsb_ingest(s->l1, s->pool, items.data(),
+                                         static_cast<int64_t>(items.size()), 0, L, opt->mode,
+                                         stream, last ? evs.data() : nullptr);
+        if (is != TSB_OK) return fail_out(is);
+        if (last && L == 1) cudaEventRecord(r.ev_first, st);
+        cudaEventRecord(ev_ingest, st);
+        ingest_issued = true;
+        ++ingest_calls;
+        bytes_total += static_cast<int64_t>(items.size()) * chunk_bytes;
+        if (last) r.dispatched_all = true;
+        progress = true;
+      }
+      // try_start_compute (engine.cpp:448-473): best key among resident, not started.
+      if (!compute_issued || done(ev_compute)) {
+        size_t best = SIZE_MAX;
+        for (size_t i : admitted) {
+          const Rt& r = R[i];
+          if (!r.resident || r.started) continue;
+          if (best == SIZE_MAX || key_less(i, best)) best = i;
+        }
+        if (best != SIZE_MAX) {
+          Rt& r = R[best];
+          r.started = true;
+          const double ct = static_cast<double>(r.compute_tokens);
+          const double secs =
+              c->compute_base + c->compute_per_token * ct + c->compute_quadratic * ct * ct;
+          const auto ns = static_cast<uint64_t>(secs * 1e9);
+          cudaStreamWaitEvent(s->compute, r.ev_resident, 0);
+          for (uint64_t t = 0; t < ns; t += 250000)
+            if (tsb::launch_prefill_burn(std::min<uint64_t>(250000, ns - t), ctas, nullptr,
+                                         s->compute) != cudaSuccess)
+              return fail_out(TSB_CUDA);
+          cudaEventRecord(r.ev_done, s->compute);
+          cudaEventRecord(ev_compute, s->compute);
+          compute_issued = true;
+          progress = true;
+        }
+      }
+    }
+    if (finished < static_cast<size_t>(n)) {
+      // Nothing to do until the next completion or arrival: back off briefly.
+      const double wait = next_arrival < by_arrival.size()
+                              ? R[by_arrival[next_arrival]].arrival - (now_s() - host0)
+                              : 1.0;
+      if (wait > 50e-6) {
+        timespec ts{0, 20000};
+        nanosleep(&ts, nullptr);
+      }
+    }
+  }
+  TSB_CUDA_TRY(cudaStreamSynchronize(st));
+  TSB_CUDA_TRY(cudaStreamSynchronize(s->compute));
+  cudaEventDestroy(ev_ingest);
+  cudaEventDestroy(ev_compute);
+  if (status != TSB_OK) return status;
+
+  float last_ms = 0.f;
+  for (int64_t i = 0; i < n; ++i) {
+    Rt& r = R[i];
+    float a = 0.f, b = 0.f, d = 0.f;
+    TSB_CUDA_TRY(cudaEventElapsedTime(&a, s->ev_start, r.ev_first));
+    TSB_CUDA_TRY(cudaEventElapsedTime(&b, s->ev_start, r.ev_resident));
+    TSB_CUDA_TRY(cudaEventElapsedTime(&d, s->ev_start, r.ev_done));
+    last_ms = std::max(last_ms, b);
+    if (results)
+      results[i] = tsb_stage_request{r.id, pick_pos[i], r.deferred, r.n_chunks,
+                                     r.n_chunks * chunk_bytes, a, b, d, r.admit_t * 1e3,
+                                     r.arrival * 1e3};
+  }
+  if (stats) {
+    stats->bytes = bytes_total;
+    stats->device_ms = last_ms;
+    stats->wall_ms = (now_s() - wall0) * 1e3;
+    stats->ingest_calls = ingest_calls;
+    stats->deferred_chunks = deferred_total;
+    stats->releases = releases;
+    stats->kernel_launches = static_cast<int64_t>(tsb_kernel_launch_count() - launches0);
+    stats->verify_mismatches = 0;
   }
   return TSB_OK;
 }

@@ -38,10 +38,19 @@ class LoadStage:
 
     __del__ = close
 
+    def run_online(self, queue: QueueArrays, slot_lists: Sequence[Sequence[int]], config: ClusterConfig,
+                   models: Optional[CostModelPair] = None, policy: int = PolicyKind.Fifo, mode: int = AUTO,
+                   prefill_ctas: int = 0, stream=None) -> StageResult:
+        """Real-time replay: arrivals at their arrival_time, SimEngine's decoupled control loop
+        (tsb_stage_run_online).  requests['done_ms'] - requests['arrival_ms'] is each TTFT."""
+        return self.run(queue, slot_lists, config, models, policy, mode, prefill=True, prefill_ctas=prefill_ctas,
+                        stream=stream, _fn=lib.tsb_stage_run_online)
+
     def run(self, queue: QueueArrays, slot_lists: Sequence[Sequence[int]], config: ClusterConfig,
             models: Optional[CostModelPair] = None, policy: int = PolicyKind.Fifo, mode: int = AUTO,
             layer_events: bool = False, prefill: bool = False, prefill_ctas: int = 0, record_trace: bool = False,
-            verify_seed: int = 0, stream=None) -> StageResult:
+            verify_seed: int = 0, stream=None, _fn=None) -> StageResult:
+        fn = _fn or lib.tsb_stage_run
         models = models or cost_models_from_config(config)
         offs = np.zeros(len(slot_lists) + 1, np.int64)
         np.cumsum([len(s) for s in slot_lists], out=offs[1:])
@@ -53,8 +62,8 @@ class LoadStage:
         stats = capi.StageStats()
         qs = queue.struct()
         s = (stream or torch.cuda.current_stream()).cuda_stream
-        check(lib.tsb_stage_run(self._h, queue.n, C.byref(qs), C.byref(config.struct()), models.array(),
-                                offs.ctypes.data, slots.ctypes.data, C.byref(opt), s, res, C.byref(stats)))
+        check(fn(self._h, queue.n, C.byref(qs), C.byref(config.struct()), models.array(),
+                 offs.ctypes.data, slots.ctypes.data, C.byref(opt), s, res, C.byref(stats)))
         dt = np.dtype([(n, np.int64 if t in (capi.i64,) else np.int32 if t is capi.i32 else np.float64)
                        for n, t in capi.StageRequest._fields_])
         arr = np.frombuffer(bytes(res), dtype=dt, count=queue.n) if queue.n else np.zeros(0, dt)

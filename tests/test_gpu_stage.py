@@ -126,6 +126,31 @@ def test_stage_no_pressure_and_errors():
         stage.run(q2, slots, cfg, policy=t.PolicyKind.Edf)
 
 
+def test_stage_online_replay_decoupled_semantics():
+    """tsb_stage_run_online: arrivals replayed in real time; admission only when the ingest stage
+    is idle with no backlog; the best-key pending request wins (engine.cpp:318-339)."""
+    pool = ingest.ChunkPool(SHAPE, 24)
+    pool.fill_synthetic(3)
+    l1 = ingest.PagedKVCache(SHAPE, 64 * 16, max_rows=16, max_chunks=16)
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(4, 8, 128, 2), compute_base=1e-3,
+                          compute_per_token=1e-6)
+    # request 1 arrives first and occupies the stage; 2..4 arrive together while it runs, so the
+    # policy decides among them: SJF-cost must pick the cheapest (fewest chunks) first.
+    ctx = np.array([256 * 12, 256 * 9, 256 * 3, 256 * 6])
+    q = t.QueueArrays(4, id=np.arange(1, 5), arrival=np.array([0.0, 0.002, 0.002, 0.002]), context_tokens=ctx,
+                      query_tokens=np.full(4, 10), cache_hit_ratio=np.ones(4), flags=np.zeros(4, np.uint8))
+    slots = [list(range(c // 256)) for c in ctx]
+    stage = LoadStage(l1, pool)
+    res = stage.run_online(q, slots, cfg, policy=t.PolicyKind.SjfCost)
+    r = res.requests
+    assert list(np.argsort(r["pick_position"])) == [0, 2, 3, 1]
+    assert np.all(r["admit_ms"] >= r["arrival_ms"] - 0.05)
+    assert np.all(r["done_ms"] >= r["resident_ms"]) and np.all(r["resident_ms"] > 0)
+    assert l1.reserved() == 0
+    fifo = stage.run_online(q, slots, cfg, policy=t.PolicyKind.Fifo).requests
+    assert list(np.argsort(fifo["pick_position"])) == [0, 1, 2, 3]
+
+
 def test_stage_synthetic_prefill_overlap():
     """With K6 prefill on a lower-priority stream, ingest of later requests overlaps earlier
     prefills: the batch finishes well before sum(ingest) + sum(prefill)."""
