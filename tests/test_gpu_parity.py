@@ -261,6 +261,65 @@ def alloc_ref_block_table(shape, num_pages):
     return rows
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_allocator_random_script_matches_ledger_and_alloc_ref(seed):
+    """Random request/release scripts: grant/defer decisions, FIFO grant lists, reserved bytes
+    and page ids of the L1 allocator equal TierLedger (restated, pinned to the reference) driving
+    the FIFO page free list (alloc_ref)."""
+    lib = po.restate()
+    rng = np.random.default_rng(seed)
+    shape = SMALL
+    num_pages = 16 * 20
+    pb = shape.page_bytes * shape.pages_per_chunk  # one chunk reservation
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=64, max_chunks=8)
+    led = lib.orc_ledger_new(num_pages * shape.page_bytes)
+    pages = lib.orc_pages_new(num_pages)
+    held = {}   # request -> list of its pages in grant order (alloc_ref)
+    waiting = {}
+    live = []
+    buf = (C.c_int32 * 16)()
+    for step in range(300):
+        if live and (rng.random() < 0.35 or len(live) >= 48):  # 64 block-table rows
+            rid = live.pop(int(rng.integers(len(live))))
+            if waiting.get(rid):
+                live.append(rid)
+                continue
+            got = l1.release_request(rid)
+            freed = held.pop(rid)
+            arr = (C.c_int32 * len(freed))(*freed)
+            lib.orc_pages_give(pages, len(freed), arr)
+            rid_o, blk_o, by_o, n = (C.c_int64 * 64)(), (C.c_int32 * 64)(), (C.c_int64 * 64)(), C.c_int64()
+            assert lib.orc_ledger_release(led, len(freed) * shape.page_bytes, rid_o, blk_o, by_o, 64, C.byref(n)) == 0
+            want = [(rid_o[i], blk_o[i]) for i in range(n.value)]
+            assert [(g[0], g[1]) for g in got] == want
+            for r_, b_ in want:
+                assert lib.orc_pages_take(pages, 16, buf) == 16
+                held.setdefault(r_, []).extend(list(buf))
+                waiting[r_] -= 1
+                bt = l1.block_table()[[g[2] for g in got if g[0] == r_][0], b_ * 16:(b_ + 1) * 16]
+                assert list(bt) == list(buf)
+        else:
+            rid = 1000 + step
+            nch = int(rng.integers(1, 5))
+            for c in range(nch):
+                g, row = l1.request(rid, c, pb)
+                gr = C.c_int()
+                assert lib.orc_ledger_request(led, rid, c, pb, C.byref(gr)) == 0
+                assert bool(gr.value) == g
+                if g:
+                    assert lib.orc_pages_take(pages, 16, buf) == 16
+                    held.setdefault(rid, []).extend(list(buf))
+                    assert list(l1.block_table()[row, c * 16:(c + 1) * 16]) == list(buf)
+                else:
+                    waiting[rid] = waiting.get(rid, 0) + 1
+                    held.setdefault(rid, [])
+            live.append(rid)
+        assert l1.reserved() == lib.orc_ledger_reserved(led)
+        assert l1.deferred_count() == lib.orc_ledger_deferred(led)
+    lib.orc_ledger_free(led)
+    lib.orc_pages_free(pages)
+
+
 def test_page_ids_match_alloc_ref():
     pool, l1, items = build_scenario(SMALL)
     bt = l1.block_table()
