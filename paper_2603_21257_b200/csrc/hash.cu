@@ -6,15 +6,13 @@
 // 64-bit words (two int32 token ids each): 16 leaves of 8 words per 256-token chunk, a 4-level
 // pairwise tree, and a per-request chain so hash c names the whole prefix [0, 256(c+1)).
 //
-// Mapping (one kernel, k_chunk_digest): a persistent grid of warps walks the global chunk index
-// space kItem chunks at a time (balanced however request lengths vary); each half-warp owns one
-// chunk per round (lane j folds leaf j = words 32k+2j, 32k+2j+1 for k = 0..3, so each of the four
-// 16-byte load instructions reads 2 x 256 contiguous bytes -- fully coalesced), two rounds are
-// loaded before any is consumed (4 KiB in flight per warp), the tree is 4 shuffle levels inside
-// the half-warp, and the digest goes to out[c].  Each item then adds its per-request chunk
-// counts to a completion counter; the warp that completes a request folds the request's digests
-// into the chain in place right away, while they are hot in L2 -- no second pass, no waiting on
-// other warps.  HBM-bound: 4 B/token + 8 B/chunk.
+// Mapping, two phases.  (1) k_chunk_digest: a persistent grid of warps walks the global chunk
+// index space kItem chunks at a time (balanced however request lengths vary); each half-warp owns
+// one chunk per round (lane j folds leaf j = words 32k+2j, 32k+2j+1 for k = 0..3, so each of the
+// four 16-byte load instructions reads 2 x 256 contiguous bytes -- fully coalesced), two rounds
+// are loaded before any is consumed (4 KiB in flight per warp), the tree is 4 shuffle levels
+// inside the half-warp, and the digest goes to out[c].  (2) k_chain: one thread per request
+// folds its digests into the chain in place (L2-resident).  HBM-bound: 4 B/token + 8 B/chunk.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -86,11 +84,20 @@ __device__ __forceinline__ uint64_t tree16(uint64_t v, int j) {
   return v;
 }
 
-// Chunk digests are balanced over the GLOBAL chunk index space (request lengths vary 100x, so a
-// warp-per-request mapping leaves a long tail): a persistent grid of warps takes kItem
-// consecutive chunks at a time and finds the owning request once with a 32-ary search over
-// chunk_offsets.
+// Phase 1 -- chunk digests, balanced over the GLOBAL chunk index space (request lengths vary
+// 100x, so a warp-per-request mapping leaves a long tail): a persistent grid of warps takes
+// kItem consecutive chunks at a time, finds the owning request once with a 32-ary search over
+// chunk_offsets, and writes each chunk's digest to out[c].
 constexpr int kItem = 16;
+
+__device__ __forceinline__ void st_evict_last(uint64_t* p, uint64_t v) {
+  asm volatile(
+      "{\n.reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+      "st.global.L2::cache_hint.b64 [%0], %1, pol;\n}" ::"l"(p),
+      "l"(v)
+      : "memory");
+}
 
 __device__ __forceinline__ int64_t warp_upper_bound(const int64_t* __restrict__ a, int64_t n,
                                                     int64_t v) {
@@ -112,30 +119,9 @@ __device__ __forceinline__ int64_t warp_upper_bound(const int64_t* __restrict__ 
   return lo;
 }
 
-// Warp-cooperative chain of one request over digests already in out[] (read through L2, they
-// were written by other warps of this kernel): 32 digests per coalesced load, every lane runs the
-// chain redundantly and lane k keeps H_k, so the stores are coalesced too.
-__device__ void warp_chain(int64_t rr, const int64_t* __restrict__ chunk_offsets,
-                           uint64_t* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t b = chunk_offsets[rr], e = chunk_offsets[rr + 1];
-  uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
-  for (int64_t c = b; c < e; c += 32) {
-    const uint64_t d = c + lane < e ? __ldcg(reinterpret_cast<const unsigned long long*>(out + c + lane)) : 0;
-    const int n = static_cast<int>(e - c < 32 ? e - c : 32);
-    uint64_t mine = 0;
-    for (int k = 0; k < n; ++k) {
-      h = fpair(h, __shfl_sync(0xffffffffu, d, k));
-      if (lane == k) mine = h;
-    }
-    if (lane < n) out[c + lane] = mine;
-  }
-}
-
 __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
     int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
-    const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out,
-    unsigned int* __restrict__ done) {
+    const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int half = lane >> 4, j = lane & 15;
   const int64_t total = chunk_offsets[n_req];
@@ -144,12 +130,11 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
        item * kItem < total; item += warps) {
     const int64_t c0 = item * kItem;
     const int64_t c1 = min(c0 + kItem, total);
-    // lane k (< kItem) resolves chunk c0+k's request and token base once per item, so the token
-    // loads below do not wait on per-chunk table lookups
+    // lane k (< kItem) resolves chunk c0+k's token base once per item, so the token loads below
+    // do not wait on per-chunk table lookups
     int64_t r = warp_upper_bound(chunk_offsets, n_req + 1, c0) - 1;
     int64_t tb = -1;
-    const bool valid = lane < kItem && c0 + lane < c1;
-    if (valid) {
+    if (lane < kItem && c0 + lane < c1) {
       while (chunk_offsets[r + 1] <= c0 + lane) ++r;
       tb = offsets[r] + (c0 + lane - chunk_offsets[r]) * 256;
     }
@@ -165,32 +150,39 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
       for (int u = 0; u < kRounds; ++u) {
         const int64_t cc = c + 2 * u + half;
         const uint64_t d = tree16(fold_leaf(f[u]), j);
-        if (j == 0 && cc < c1) out[cc] = d;
+        if (j == 0 && cc < c1) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
       }
     }
-    // Completion counting: every request segment in this item adds its chunk count to done[r];
-    // the warp that completes a request chains it right away (its digests are hot in L2).
-    __threadfence();
-    __syncwarp();
-    const int64_t rprev = __shfl_up_sync(0xffffffffu, r, 1);
-    const bool head = valid && (lane == 0 || rprev != r);
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-    bool complete = false;
-    if (head) {
-      const unsigned above = heads & ~((2u << lane) - 1u);
-      const int end = above ? __ffs(above) - 1 : 32 - __clz(vmask);
-      const unsigned seg = static_cast<unsigned>(end - lane);
-      const unsigned old = atomicAdd(done + r, seg);
-      complete = old + seg == static_cast<unsigned>(chunk_offsets[r + 1] - chunk_offsets[r]);
+  }
+}
+
+// Phase 2 -- the per-request chain H_c = pair(H_{c-1}, digest_c), in place; one thread per
+// request, loads are independent of the chain so they pipeline; the digests are L2-resident.
+// One thread per request, software-pipelined: the next group of kG digests is loaded before the
+// current group is folded into the chain, so each iteration's latency overlaps the previous one.
+constexpr int kG = 32;
+
+__global__ void __launch_bounds__(128) k_chain(int64_t n_req, const int64_t* __restrict__ chunk_offsets,
+                                               uint64_t* __restrict__ out) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n_req) return;
+  const int64_t b = chunk_offsets[r], e = chunk_offsets[r + 1];
+  uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
+  uint64_t cur[kG], nxt[kG];
+#pragma unroll
+  for (int k = 0; k < kG; ++k) cur[k] = b + k < e ? out[b + k] : 0;
+  for (int64_t c = b; c < e; c += kG) {
+#pragma unroll
+    for (int k = 0; k < kG; ++k) nxt[k] = c + kG + k < e ? out[c + kG + k] : 0;
+#pragma unroll
+    for (int k = 0; k < kG; ++k) {
+      if (c + k < e) {
+        h = fpair(h, cur[k]);
+        out[c + k] = h;
+      }
     }
-    unsigned todo = __ballot_sync(0xffffffffu, complete);
-    if (todo) __threadfence();
-    while (todo) {
-      const int l = __ffs(todo) - 1;
-      todo &= todo - 1;
-      warp_chain(__shfl_sync(0xffffffffu, r, l), chunk_offsets, out);
-    }
+#pragma unroll
+    for (int k = 0; k < kG; ++k) cur[k] = nxt[k];
   }
 }
 
@@ -215,21 +207,10 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
-  // per-request completion counters (grow-only scratch, zeroed on the stream)
-  static thread_local unsigned int* done = nullptr;
-  static thread_local int64_t done_cap = 0;
-  if (n_req > done_cap) {
-    cudaFree(done);
-    done = nullptr;
-    done_cap = 0;
-    cudaError_t e = cudaMalloc(&done, sizeof(unsigned int) * static_cast<size_t>(n_req));
-    if (e != cudaSuccess) return e;
-    done_cap = n_req;
-  }
-  cudaError_t e = cudaMemsetAsync(done, 0, sizeof(unsigned int) * static_cast<size_t>(n_req), st);
-  if (e != cudaSuccess) return e;
-  // persistent grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
-  k_chunk_digest<<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, done);
+  // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
+  k_chunk_digest<<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  count_launch();
+  k_chain<<<ceil_div(n_req, 128), 128, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();
   return cudaGetLastError();
 }
