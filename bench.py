@@ -93,10 +93,11 @@ class ClockSampler:
 # shared pool across per-GPU processes
 # ------------------------------------------------------------------------------------------------
 def make_pool(shape_full, n_slots, world, rank, dist, seed):
-    """One pinned L2 pool per box: a /dev/shm segment page-locked by every rank when it fits,
-    else a private pinned pool per process (same bytes; documented in DESIGN.md)."""
+    """One pinned L2 pool per box: a /dev/shm segment page-locked by every rank when it fits;
+    otherwise each rank pins a shard-local pool holding only its KV heads (chunks laid out
+    [L][2][C][H/world][D]), so host memory stays at one pool's worth across the box.
+    Returns (pool, description, shape the rank ingests with)."""
     from paper_2603_21257_b200 import ingest
-
     from paper_2603_21257_b200.multirank import SharedSegment
 
     nbytes = n_slots * shape_full.chunk_bytes
@@ -108,10 +109,15 @@ def make_pool(shape_full, n_slots, world, rank, dist, seed):
             if rank == 0:
                 pool.fill_synthetic(seed)
             dist.barrier()
-            return pool, "shared /dev/shm segment, cudaHostRegister'ed by every rank"
+            return pool, "shared /dev/shm segment, cudaHostRegister'ed by every rank", shape_full.with_rank(world, rank)
+        local = ingest.KVShape(shape_full.layers, shape_full.kv_heads // world, shape_full.head_dim,
+                               shape_full.dtype_bytes, shape_full.chunk_tokens, shape_full.page_tokens)
+        pool = ingest.ChunkPool(local, n_slots)
+        pool.fill_synthetic(seed + rank)
+        return pool, "shard-local pinned pool per rank (/dev/shm too small for one shared pool)", local
     pool = ingest.ChunkPool(shape_full, n_slots)
     pool.fill_synthetic(seed)
-    return pool, "cudaHostAlloc portable|mapped" + (" (private per rank: /dev/shm too small)" if world > 1 else "")
+    return pool, "cudaHostAlloc portable|mapped", shape_full
 
 
 def torch_tensor_flag(flag: bool, dist) -> bool:
@@ -274,10 +280,11 @@ def run_ours(args):
     from paper_2603_21257_b200.workloads import WORKLOADS
 
     wl = WORKLOADS[args.workload]()
-    shape = wl.for_rank(world, rank)
+    wl.for_rank(world, rank)  # validates the head split
     seed = 20261017
     ce_peak = measure_ce_peak(torch)
-    pool, pool_kind = make_pool(wl.shape, wl.pool_slots, world, rank, dist, seed)
+    pool, pool_kind, shape = make_pool(wl.shape, wl.pool_slots, world, rank, dist, seed)
+    pool_seed = seed + rank if shape.tp_size == 1 and world > 1 else seed
 
     # L1 arena: most of HBM, fewer pages than the batch needs so FIFO deferral is exercised.
     free, total = torch.cuda.mem_get_info()
@@ -294,7 +301,7 @@ def run_ours(args):
 
     # warm-up (the first one also checks every page against the synthetic source pattern)
     for i in range(args.warmup):
-        r = run(seed if i == 0 else 0)
+        r = run(pool_seed if i == 0 else 0)
         if i == 0 and r.stats["verify_mismatches"]:
             raise SystemExit(f"ingest parity failure: {r.stats['verify_mismatches']} mismatching words")
     if dist:
