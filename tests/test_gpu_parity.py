@@ -451,3 +451,79 @@ def test_config1_full_size_llama8b_32k(mode):
         want = poolv[items["src_slot"][i], layer, kv, j * 16:(j + 1) * 16]
         assert np.array_equal(got, want)
     assert l1.release_request(1) == [] and l1.free_pages() == 2048
+
+
+# ---------------------------------------------------------------------------------------------
+# Geometry generality and edge cases
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("geom", [
+    dict(layers=3, kv_heads=4, head_dim=64, dtype_bytes=2, chunk_tokens=128, page_tokens=16),
+    dict(layers=2, kv_heads=8, head_dim=256, dtype_bytes=1, chunk_tokens=256, page_tokens=32),   # fp8 KV
+    dict(layers=2, kv_heads=2, head_dim=128, dtype_bytes=2, chunk_tokens=64, page_tokens=8),
+    dict(layers=1, kv_heads=16, head_dim=128, dtype_bytes=2, chunk_tokens=256, page_tokens=16),
+])
+@pytest.mark.parametrize("mode", ["zerocopy", "bulk", "ce"])
+def test_ingest_geometries_bit_exact(oracle, geom, mode):
+    shape = ingest.KVShape(**geom)
+    ppc = shape.pages_per_chunk
+    pool = ingest.ChunkPool(shape, 6)
+    pool.fill_synthetic(29)
+    num_pages = 8 * ppc + 3
+    arena = torch.zeros(shape.layers * 2 * num_pages * shape.page_tokens * shape.heads_local * shape.head_dim *
+                        shape.dtype_bytes, dtype=torch.uint8, device="cuda")
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=2, max_chunks=8, arena=arena)
+    cb = shape.page_bytes * ppc
+    items = []
+    for c in range(5):
+        g, row = l1.request(7, c, cb)
+        assert g
+        items.append(((c * 3) % 6, row, c))
+    l1.sync_block_table()
+    it = ingest.items_numpy(*zip(*items))
+    try:
+        ingest.ingest(l1, pool, it, mode=ingest.MODES[mode])
+    except t.Unsupported:
+        pytest.skip("segment too large for the bulk ring")
+    torch.cuda.synchronize()
+    want = oracle.scatter_ref(shape, pool.slot_view(0, 6), it, l1.block_table(), num_pages)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+
+
+def test_ingest_empty_and_bounds():
+    pool, l1, items = build_scenario(SMALL)
+    ingest.ingest(l1, pool, items[:0])  # no items: no work, no error
+    evs = [torch.cuda.Event() for _ in range(SMALL.layers)]
+    ingest.ingest(l1, pool, items[:0], layer_events=evs)
+    for e in evs:
+        e.synchronize()  # fences still recorded
+    with pytest.raises(t.ValidationError):
+        ingest.ingest(l1, pool, items, 0, SMALL.layers + 1)
+    with pytest.raises(t.ValidationError):
+        l1.request(55, 12, SMALL.page_bytes * 16)  # chunk index beyond the block-table row
+
+
+def test_hash_edge_lengths(oracle):
+    offs = np.array([0, 0, 1, 255, 511, 767, 768 + 1_000_000], np.int64)  # lengths 0,1,254,256,256,1_000_001
+    doc = np.zeros(len(offs) - 1, np.int64)
+    toks = oracle.gen_tokens(5, offs, doc, np.diff(offs))
+    got = hasher.hash_prefix_chunks(offs, toks)
+    assert np.array_equal(got, oracle.hash_prefix_chunks(offs, toks))
+    assert len(got) == sum(int(x) // 256 for x in np.diff(offs))
+
+
+@pytest.mark.parametrize("policy", [t.PolicyKind.SjfCost, t.PolicyKind.Edf])
+def test_scorer_one_million_requests(scorer, oracle, policy):
+    q = random_queue(1_000_000, 11)
+    cfg = CFGS["quad"]
+    m = t.cost_models_from_config(cfg)
+    tl, tc, pr, order = scorer.score(q, policy, m, cfg)
+    st, err, otl, otc, opr = oracle.score_queue(q, int(policy), [m.load.slope, m.load.intercept, m.comp.slope,
+                                                                 m.comp.intercept], cfg)
+    assert np.array_equal(pr.view(np.uint64), opr.view(np.uint64))
+    assert np.array_equal(order, oracle.sort_order(opr, q.arrival, q.id))
+
+
+def test_scorer_empty_queue(scorer):
+    q = t.QueueArrays(0)
+    tl, tc, pr, order = scorer.score(q, t.PolicyKind.Fifo, t.CostModelPair(), t.ClusterConfig())
+    assert len(order) == 0
