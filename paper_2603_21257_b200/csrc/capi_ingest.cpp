@@ -457,7 +457,7 @@ namespace {
 cudaError_t launch_scatter(const tsb::IngestGeom& g, const uint8_t* src, uint8_t* arena,
                            const tsb_ingest_item* items, const int32_t* bt, int64_t n,
                            cudaStream_t st) {
-  if (g_knobs.scatter_impl == 1 && g.seg_bytes * 6 <= 200 * 1024)
+  if (g_knobs.scatter_impl == 1 && g.seg_bytes * 2 <= tsb::kBulkSmem)
     return tsb::launch_ingest_bulk(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st);
   return tsb::launch_ingest_ldg(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st);
 }
@@ -607,7 +607,7 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
       TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
                                           g_knobs.zerocopy_ctas, st));
     } else {
-      if (g.seg_bytes * 6 > 200 * 1024)
+      if (g.seg_bytes * 2 > tsb::kBulkSmem)
         return fail(TSB_UNSUPPORTED, "ingest bulk: page segment too large for the smem ring");
       TSB_CUDA_TRY(tsb::launch_ingest_bulk(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
                                            g_knobs.bulk_ctas, st));

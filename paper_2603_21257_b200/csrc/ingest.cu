@@ -200,15 +200,22 @@ cudaError_t launch_ingest_bulk(const IngestGeom& g, const uint8_t* src, uint8_t*
                                int grid, cudaStream_t st) {
   const int64_t nseg = n_items * g.n_layers * 2 * g.ppc;
   if (nseg == 0) return cudaSuccess;
-  constexpr int kStages = 6;
-  const size_t smem = static_cast<size_t>(kStages) * g.seg_bytes;
+  // ring depth: as many stages of one segment as fit in kBulkSmem (6 for 32 KiB segments)
   static std::atomic<uint64_t> attr_set{0};
   if (first_on_device(attr_set)) {
-    cudaError_t e = cudaFuncSetAttribute(k_ingest_bulk<kStages>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_ingest_bulk<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_ingest_bulk<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_ingest_bulk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
     if (e != cudaSuccess) return e;
   }
-  k_ingest_bulk<kStages><<<grid, 32, smem, st>>>(g, src, arena, items, bt, nseg);
+  if (g.seg_bytes * 6 <= kBulkSmem)
+    k_ingest_bulk<6><<<grid, 32, 6 * g.seg_bytes, st>>>(g, src, arena, items, bt, nseg);
+  else if (g.seg_bytes * 3 <= kBulkSmem)
+    k_ingest_bulk<3><<<grid, 32, 3 * g.seg_bytes, st>>>(g, src, arena, items, bt, nseg);
+  else
+    k_ingest_bulk<2><<<grid, 32, 2 * g.seg_bytes, st>>>(g, src, arena, items, bt, nseg);
   count_launch();
   return cudaGetLastError();
 }
