@@ -191,10 +191,5 @@ _decl("tsb_stage_run_online", st, vp, i64, P(Queue), P(Cluster), P(f64), vp, vp,
       P(StageRequest), P(StageStats))
 _decl("tsb_l1_verify_synthetic", st, vp, P(IngestItem), i64, i64, i64, u64, i64, vp, P(u64))
 
-EXPORTED = sorted(
-    n for n in dir(lib) if n.startswith("tsb_")
-)  # populated lazily by ctypes; tests read the header instead
-
-
 def last_error() -> str:
     return lib.tsb_last_error().decode()

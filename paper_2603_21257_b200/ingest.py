@@ -209,14 +209,6 @@ class PagedKVCache:
         return t.view(dtype).view(2, self.num_pages, s.page_tokens, s.heads_local, s.head_dim)
 
 
-def items_array(rows: Sequence) -> "C.Array":
-    """[(src_slot, bt_row, chunk_index), ...] -> tsb_ingest_item[]"""
-    arr = (capi.IngestItem * len(rows))()
-    for i, (slot, row, chunk) in enumerate(rows):
-        arr[i].src_slot, arr[i].bt_row, arr[i].chunk_index = int(slot), int(row), int(chunk)
-    return arr
-
-
 def items_numpy(src_slot, bt_row, chunk_index) -> np.ndarray:
     dt = np.dtype([("src_slot", np.int64), ("bt_row", np.int32), ("chunk_index", np.int32)])
     a = np.empty(len(src_slot), dtype=dt)
