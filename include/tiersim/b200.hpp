@@ -32,12 +32,30 @@ class ChunkPool {
     check(tsb_pool_create(&s, slots, &p));
     p_.reset(p);
   }
+  /// Peer-HBM tier: the same slot layout in `device`'s memory (read locally or over NVLink).
+  static ChunkPool on_device(int device, const KvShape& shape, std::int64_t slots) {
+    const tsb_kv_shape s = shape.c_abi();
+    tsb_pool* p = nullptr;
+    check(tsb_pool_create_device(device, &s, slots, &p));
+    return ChunkPool(p);
+  }
+  /// Maps a pool another process exported with ipc_handle() (64 bytes).
+  static ChunkPool open_ipc(const KvShape& shape, const void* handle, int owner_device,
+                            std::int64_t slots) {
+    const tsb_kv_shape s = shape.c_abi();
+    tsb_pool* p = nullptr;
+    check(tsb_pool_open_ipc(&s, handle, owner_device, slots, &p));
+    return ChunkPool(p);
+  }
+  void ipc_handle(void* out64) const { check(tsb_pool_ipc_handle(p_.get(), out64)); }
+  bool on_device() const { return tsb_pool_location_of(p_.get()) == TSB_POOL_DEVICE; }
   void* slot(std::int64_t s) { return tsb_pool_slot_ptr(p_.get(), s); }
   std::int64_t slots() const { return tsb_pool_slots(p_.get()); }
   std::int64_t chunk_bytes() const { return tsb_pool_chunk_bytes(p_.get()); }
   tsb_pool* handle() { return p_.get(); }
 
  private:
+  explicit ChunkPool(tsb_pool* p) { p_.reset(p); }
   struct Del {
     void operator()(tsb_pool* p) const { tsb_pool_destroy(p); }
   };

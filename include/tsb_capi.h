@@ -229,6 +229,32 @@ int64_t tsb_pool_chunk_bytes(const tsb_pool* p);
 tsb_status tsb_pool_fill_synthetic(tsb_pool* p, uint64_t seed, int64_t first, int64_t n,
                                    void* stream);
 
+/* Peer-HBM tier: a chunk pool resident in GPU memory -- this GPU's or
+ * a peer's over NVLink / NVSwitch -- with the same slot layout.  It stands where the reference
+ * runs the L3->L2 network stage (engine.cpp:405-425): chunks another GPU already holds are
+ * read peer-to-peer by the ingest kernels instead of crossing the host link.  Ingest from a
+ * device pool runs K1 (SM loads; AUTO resolves to it) with the K2 grid, or K1b; CE is
+ * UNSUPPORTED.  tsb_pool_slot_ptr returns the device address for these pools. */
+typedef enum { TSB_POOL_HOST = 0, TSB_POOL_DEVICE = 1 } tsb_pool_location;
+/* cudaMalloc n_slots chunks on `device` (owned; freed on destroy). */
+tsb_status tsb_pool_create_device(int device, const tsb_kv_shape* shape, int64_t n_slots,
+                                  tsb_pool** out);
+/* Adopt caller-owned device memory of `device` (not freed on destroy). */
+tsb_status tsb_pool_wrap_device(int device, const tsb_kv_shape* shape, void* dev_base,
+                                int64_t n_slots, tsb_pool** out);
+/* Export a tsb_pool_create_device pool to other processes: writes a 64-byte
+ * cudaIpcMemHandle_t to handle_out. */
+tsb_status tsb_pool_ipc_handle(const tsb_pool* p, void* handle_out);
+/* Map a peer process's exported pool into this process (cudaIpcOpenMemHandle with lazy peer
+ * access); `owner_device` is the pool's device ordinal as this process numbers it (for the
+ * peer-access check; -1 = unknown).  Closed on destroy. */
+tsb_status tsb_pool_open_ipc(const tsb_kv_shape* shape, const void* handle, int owner_device,
+                             int64_t n_slots, tsb_pool** out);
+/* Enable peer access from `device` to `peer` (idempotent); UNSUPPORTED when the pair cannot. */
+tsb_status tsb_enable_peer_access(int device, int peer);
+int tsb_pool_location_of(const tsb_pool* p);
+int tsb_pool_device(const tsb_pool* p);
+
 /* ------------------------------------------------------------------------------------ */
 /* L1 paged allocator + block_table.                                                        */
 /* Byte accounting is exactly TierLedger (engine.cpp:18-49): a chunk reservation is        */

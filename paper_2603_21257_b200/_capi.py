@@ -108,6 +108,7 @@ class TraceRow(C.Structure):
 
 HAS_DEADLINE, HAS_MEASURED = 1, 2
 INGEST_AUTO, INGEST_ZEROCOPY, INGEST_BULK, INGEST_CE = range(4)
+POOL_HOST, POOL_DEVICE = 0, 1
 
 
 def _decl(name, restype, *argtypes):
@@ -157,6 +158,13 @@ _decl("tsb_pool_slot_ptr", vp, vp, i64)
 _decl("tsb_pool_slots", i64, vp)
 _decl("tsb_pool_chunk_bytes", i64, vp)
 _decl("tsb_pool_fill_synthetic", st, vp, u64, i64, i64, vp)
+_decl("tsb_pool_create_device", st, C.c_int, P(KvShape), i64, P(vp))
+_decl("tsb_pool_wrap_device", st, C.c_int, P(KvShape), vp, i64, P(vp))
+_decl("tsb_pool_ipc_handle", st, vp, C.c_char_p)
+_decl("tsb_pool_open_ipc", st, P(KvShape), C.c_char_p, C.c_int, i64, P(vp))
+_decl("tsb_enable_peer_access", st, C.c_int, C.c_int)
+_decl("tsb_pool_location_of", C.c_int, vp)
+_decl("tsb_pool_device", C.c_int, vp)
 _decl("tsb_ledger_create", st, C.c_int, i64, P(vp))
 _decl("tsb_ledger_destroy", None, vp)
 _decl("tsb_ledger_request", st, vp, i64, i32, i64, P(C.c_int))

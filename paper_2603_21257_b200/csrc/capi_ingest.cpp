@@ -88,15 +88,122 @@ struct UploadRing {
 // ---------------------------------------------------------------------------------------
 struct tsb_pool {
   tsb_kv_shape shape{};
-  uint8_t* host = nullptr;  // host address
-  uint8_t* dev = nullptr;   // device (UVA) alias of the same memory
+  uint8_t* host = nullptr;  // host address (NULL for device pools)
+  uint8_t* dev = nullptr;   // device (UVA) address: mapped host alias, local or peer HBM
   int64_t slots = 0;
   int64_t chunk_bytes = 0;
-  bool owned = false;
-  bool registered = false;
+  int location = TSB_POOL_HOST;
+  int device = -1;          // owning GPU of a device pool (-1: host pool / unknown)
+  bool owned = false;       // cudaFreeHost (host) or cudaFree (device) on destroy
+  bool registered = false;  // cudaHostUnregister on destroy
+  bool ipc = false;         // cudaIpcCloseMemHandle on destroy
 };
 
+namespace {
+
+tsb_status new_device_pool(const tsb_kv_shape* shape, int device, int64_t n_slots,
+                           tsb_pool** out) {
+  int64_t cb = 0;
+  TSB_TRY(tsb_kv_shape_info(shape, &cb, nullptr, nullptr));
+  if (n_slots < 1) return fail(TSB_VALIDATION, "pool: n_slots must be >= 1");
+  auto* p = new tsb_pool();
+  p->shape = *shape;
+  p->slots = n_slots;
+  p->chunk_bytes = cb;
+  p->location = TSB_POOL_DEVICE;
+  p->device = device;
+  *out = p;
+  return TSB_OK;
+}
+
+}  // namespace
+
 extern "C" {
+
+tsb_status tsb_enable_peer_access(int device, int peer) {
+  if (device == peer) return TSB_OK;
+  int can = 0;
+  TSB_CUDA_TRY(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can)
+    return fail(TSB_UNSUPPORTED, "peer access " + std::to_string(device) + " -> " +
+                                     std::to_string(peer) + " is not supported");
+  int prev = 0;
+  TSB_CUDA_TRY(cudaGetDevice(&prev));
+  TSB_CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(prev);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // not an error here; do not leave it for the next launch check
+    return TSB_OK;
+  }
+  if (e != cudaSuccess) return tsb::cuda_fail(e, "tsb_enable_peer_access");
+  return TSB_OK;
+}
+
+tsb_status tsb_pool_create_device(int device, const tsb_kv_shape* shape, int64_t n_slots,
+                                  tsb_pool** out) {
+  tsb_pool* p = nullptr;
+  TSB_TRY(new_device_pool(shape, device, n_slots, &p));
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->dev),
+                                       static_cast<size_t>(p->chunk_bytes) * n_slots);
+  if (e != cudaSuccess) {
+    delete p;
+    return tsb::cuda_fail(e, "tsb_pool_create_device (cudaMalloc)");
+  }
+  p->owned = true;
+  *out = p;
+  return TSB_OK;
+}
+
+tsb_status tsb_pool_wrap_device(int device, const tsb_kv_shape* shape, void* dev_base,
+                                int64_t n_slots, tsb_pool** out) {
+  cudaPointerAttributes a{};
+  TSB_CUDA_TRY(cudaPointerGetAttributes(&a, dev_base));
+  if (a.type != cudaMemoryTypeDevice)
+    return fail(TSB_VALIDATION, "tsb_pool_wrap_device: dev_base is not device memory");
+  if (a.device != device)
+    return fail(TSB_VALIDATION, "tsb_pool_wrap_device: dev_base lives on device " +
+                                    std::to_string(a.device));
+  tsb_pool* p = nullptr;
+  TSB_TRY(new_device_pool(shape, device, n_slots, &p));
+  p->dev = static_cast<uint8_t*>(dev_base);
+  *out = p;
+  return TSB_OK;
+}
+
+tsb_status tsb_pool_ipc_handle(const tsb_pool* p, void* handle_out) {
+  if (p->location != TSB_POOL_DEVICE || !p->owned)
+    return fail(TSB_VALIDATION, "tsb_pool_ipc_handle: only tsb_pool_create_device pools export");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handle");
+  cudaIpcMemHandle_t h;
+  TSB_CUDA_TRY(cudaIpcGetMemHandle(&h, p->dev));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return TSB_OK;
+}
+
+tsb_status tsb_pool_open_ipc(const tsb_kv_shape* shape, const void* handle, int owner_device,
+                             int64_t n_slots, tsb_pool** out) {
+  int cur = 0;
+  TSB_CUDA_TRY(cudaGetDevice(&cur));
+  if (owner_device >= 0) TSB_TRY(tsb_enable_peer_access(cur, owner_device));
+  tsb_pool* p = nullptr;
+  TSB_TRY(new_device_pool(shape, owner_device, n_slots, &p));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(reinterpret_cast<void**>(&p->dev), h,
+                                       cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    delete p;
+    return tsb::cuda_fail(e, "tsb_pool_open_ipc (cudaIpcOpenMemHandle)");
+  }
+  p->ipc = true;
+  *out = p;
+  return TSB_OK;
+}
+
+int tsb_pool_location_of(const tsb_pool* p) { return p->location; }
+int tsb_pool_device(const tsb_pool* p) { return p->device; }
 
 tsb_status tsb_pool_create(const tsb_kv_shape* shape, int64_t n_slots, tsb_pool** out) {
   int64_t cb = 0;
@@ -156,12 +263,19 @@ tsb_status tsb_pool_register(const tsb_kv_shape* shape, void* host_base, int64_t
 
 void tsb_pool_destroy(tsb_pool* p) {
   if (!p) return;
-  if (p->owned) cudaFreeHost(p->host);
-  if (p->registered) cudaHostUnregister(p->host);
+  if (p->location == TSB_POOL_DEVICE) {
+    if (p->owned) cudaFree(p->dev);
+    if (p->ipc) cudaIpcCloseMemHandle(p->dev);
+  } else {
+    if (p->owned) cudaFreeHost(p->host);
+    if (p->registered) cudaHostUnregister(p->host);
+  }
   delete p;
 }
 
-void* tsb_pool_slot_ptr(tsb_pool* p, int64_t slot) { return p->host + slot * p->chunk_bytes; }
+void* tsb_pool_slot_ptr(tsb_pool* p, int64_t slot) {
+  return (p->location == TSB_POOL_DEVICE ? p->dev : p->host) + slot * p->chunk_bytes;
+}
 int64_t tsb_pool_slots(const tsb_pool* p) { return p->slots; }
 int64_t tsb_pool_chunk_bytes(const tsb_pool* p) { return p->chunk_bytes; }
 
@@ -490,8 +604,10 @@ tsb::IngestGeom make_geom(const tsb_l1* l, int64_t layer_lo, int64_t layer_hi) {
   return g;
 }
 
-int resolve_mode(const tsb_l1* l, int mode, bool host_items) {
+int resolve_mode(const tsb_l1* l, const tsb_pool* pool, int mode, bool host_items) {
   if (mode != TSB_INGEST_AUTO) return mode;
+  // A device pool (local or peer HBM) is read by SM loads: no host link to saturate.
+  if (pool->location == TSB_POOL_DEVICE) return TSB_INGEST_ZEROCOPY;
   // Measured on B200 (profiles/r01_*): SM-initiated host reads plateau at ~92.6% of the copy
   // engines' H2D rate, so full-head chunks go through CE + K2; head-sharded chunks have
   // 256 B - 1 KiB runs that only the SM path reads without moving other ranks' heads.
@@ -560,6 +676,8 @@ tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, i
 tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
                      const tsb_ingest_item* items_host, int64_t n_items, int64_t lo, int64_t hi,
                      cudaStream_t st, void* const* layer_events) {
+  if (pool->location != TSB_POOL_HOST)
+    return fail(TSB_UNSUPPORTED, "ingest CE mode reads host pools; use zerocopy/bulk for device pools");
   if (l->shape.tp_size != 1)
     return fail(TSB_UNSUPPORTED,
                 "ingest CE mode copies whole token rows; use zerocopy/bulk when tp_size > 1");
@@ -601,16 +719,23 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
                      int64_t lo, int64_t hi, int mode, cudaStream_t st, void* const* layer_events) {
   // One launch per layer when the caller wants per-layer fences, else one launch in total.
   const int64_t step = layer_events ? 1 : hi - lo;
+  // Host pools are link-bound and saturate with a small grid; HBM / NVLink sources need the
+  // K2 grid to keep enough loads in flight.
+  const bool on_device = pool->location == TSB_POOL_DEVICE;
   for (int64_t l0 = lo; l0 < hi; l0 += step) {
     const tsb::IngestGeom g = make_geom(l, l0, l0 + step);
     if (mode == TSB_INGEST_ZEROCOPY) {
       TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
-                                          g_knobs.zerocopy_ctas, st));
+                                          on_device ? g_knobs.scatter_ctas : g_knobs.zerocopy_ctas,
+                                          st));
     } else {
       if (g.seg_bytes * 2 > tsb::kBulkSmem)
         return fail(TSB_UNSUPPORTED, "ingest bulk: page segment too large for the smem ring");
+      // The K1b ring fills an SM's shared memory: one resident CTA per SM.
+      int sms = 148;
+      if (on_device) TSB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, l->device));
       TSB_CUDA_TRY(tsb::launch_ingest_bulk(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
-                                           g_knobs.bulk_ctas, st));
+                                           on_device ? sms : g_knobs.bulk_ctas, st));
     }
     if (layer_events && layer_events[l0 - lo])
       TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[l0 - lo]), st));
@@ -625,7 +750,7 @@ tsb_status ingest_impl(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_d
     return fail(TSB_VALIDATION, "ingest: layer range must satisfy 0 <= lo < hi <= layers");
   if (pool->chunk_bytes != make_geom(l, 0, 1).chunk_bytes)
     return fail(TSB_VALIDATION, "ingest: pool chunk geometry differs from the L1 shape");
-  mode = resolve_mode(l, mode, items_host != nullptr);
+  mode = resolve_mode(l, pool, mode, items_host != nullptr);
   if (n_items == 0) {
     for (int64_t k = 0; layer_events && k < hi - lo; ++k)
       if (layer_events[k]) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[k]), st));

@@ -104,6 +104,53 @@ class ChunkPool:
         self._keepalive = keepalive
         return self
 
+    # ---- peer-HBM tier: the same slot layout resident in GPU memory ----
+    @classmethod
+    def _adopt(cls, shape: KVShape, h, n_slots: int, keepalive=None) -> "ChunkPool":
+        self = cls.__new__(cls)
+        self.shape, self._h, self.n_slots = shape, h, n_slots
+        self.chunk_bytes = lib.tsb_pool_chunk_bytes(h)
+        self._keepalive = keepalive
+        return self
+
+    @classmethod
+    def create_device(cls, shape: KVShape, n_slots: int, device: int = 0) -> "ChunkPool":
+        """HBM chunk pool on `device` (tsb_pool_create_device); export it with ipc_handle()."""
+        h = C.c_void_p()
+        check(lib.tsb_pool_create_device(int(device), C.byref(shape.struct()), int(n_slots), C.byref(h)))
+        return cls._adopt(shape, h, n_slots)
+
+    @classmethod
+    def wrap_device(cls, shape: KVShape, tensor: torch.Tensor, n_slots: Optional[int] = None) -> "ChunkPool":
+        """A CUDA tensor (kept alive by the pool) as the chunk pool (tsb_pool_wrap_device)."""
+        n_slots = tensor.numel() * tensor.element_size() // shape.chunk_bytes if n_slots is None else n_slots
+        h = C.c_void_p()
+        check(lib.tsb_pool_wrap_device(tensor.device.index, C.byref(shape.struct()), tensor.data_ptr(),
+                                       int(n_slots), C.byref(h)))
+        return cls._adopt(shape, h, n_slots, keepalive=tensor)
+
+    @classmethod
+    def open_ipc(cls, shape: KVShape, handle: bytes, n_slots: int, owner_device: int = -1) -> "ChunkPool":
+        """Map another process's create_device pool (cudaIpcOpenMemHandle, lazy peer access)."""
+        if len(handle) != 64:
+            raise ValueError("an IPC pool handle is 64 bytes")
+        h = C.c_void_p()
+        check(lib.tsb_pool_open_ipc(C.byref(shape.struct()), handle, int(owner_device), int(n_slots), C.byref(h)))
+        return cls._adopt(shape, h, n_slots)
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        check(lib.tsb_pool_ipc_handle(self._h, buf))
+        return buf.raw
+
+    @property
+    def on_device(self) -> bool:
+        return lib.tsb_pool_location_of(self._h) == capi.POOL_DEVICE
+
+    @property
+    def device(self) -> int:
+        return lib.tsb_pool_device(self._h)
+
     @property
     def handle(self):
         return self._h
@@ -116,10 +163,13 @@ class ChunkPool:
     __del__ = close
 
     def slot_ptr(self, slot: int) -> int:
+        """Host address of a slot (device address for a device pool)."""
         return lib.tsb_pool_slot_ptr(self._h, int(slot))
 
     def slot_view(self, slot: int, count: int = 1) -> np.ndarray:
-        """Writable uint8 numpy view of `count` slots (host memory)."""
+        """Writable uint8 numpy view of `count` slots (host pools only)."""
+        if self.on_device:
+            raise TypeError("slot_view: the pool is in device memory")
         buf = (C.c_uint8 * (self.chunk_bytes * count)).from_address(self.slot_ptr(slot))
         return np.frombuffer(buf, dtype=np.uint8)
 
@@ -265,6 +315,10 @@ def set_grid(zerocopy_ctas: int = 0, bulk_ctas: int = 0, scatter_ctas: int = 0):
     check(lib.tsb_ingest_set_grid(zerocopy_ctas, bulk_ctas, scatter_ctas))
 
 
-def set_ce(variant: int = 1, staging_bytes: int = 0):
-    """CE copy strategy: 0 per-item memcpy, 1 2D per consecutive-slot run (default), 2 batch API."""
+def enable_peer_access(device: int, peer: int):
+    check(lib.tsb_enable_peer_access(int(device), int(peer)))
+
+
+def set_ce(variant: int = 2, staging_bytes: int = 0):
+    """CE copy strategy: 0 per-item memcpy, 1 2D per consecutive-slot run, 2 batch API (default)."""
     check(lib.tsb_ingest_set_ce(variant, staging_bytes))

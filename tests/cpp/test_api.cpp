@@ -188,6 +188,26 @@ static void gpu_cases() {
     EXPECT(r.stats.verify_mismatches == 0 && r.stats.deferred_chunks > 0 && l1.reserved() == 0);
     EXPECT(r.stats.bytes == 14 * 256 * cfg.bytes_per_token);
   });
+  run("gpu: load stage from a device-resident (peer-HBM tier) pool", [] {
+    KvShape shape;
+    shape.layers = 4;
+    ChunkPool pool = ChunkPool::on_device(0, shape, 8);
+    EXPECT(pool.on_device());
+    check(tsb_pool_fill_synthetic(pool.handle(), 41, 0, 8, nullptr));
+    PagedAllocator l1(0, shape, 6 * 16, 8, 8);
+    LoadStage stage(l1, pool);
+    ClusterConfig cfg;
+    cfg.bytes_per_token = kv_bytes_per_token(4, 8, 128, 2);
+    std::vector<RequestSpec> batch = {spec(1, 0.0, 256 * 5), spec(2, 0.1, 256 * 4)};
+    std::vector<std::vector<int64_t>> slots = {{0, 1, 2, 3, 4}, {4, 5, 6, 7}};
+    tsb_stage_options opt{};
+    opt.mode = TSB_INGEST_AUTO;
+    opt.verify_seed = 41;
+    const auto r = stage.run(batch, slots, cfg, cost_models_from_config(cfg), opt);
+    EXPECT(r.stats.verify_mismatches == 0 && r.stats.deferred_chunks > 0 && l1.reserved() == 0);
+    unsigned char h[64];
+    pool.ipc_handle(h);  // exportable to the other per-GPU processes
+  });
   run("gpu: prefix hasher", [] {
     std::vector<std::int64_t> off = {0, 600, 1112};
     std::vector<std::int32_t> tok(1112);

@@ -197,11 +197,14 @@ def test_hash_device_path_and_token_generator(oracle):
 SMALL = ingest.KVShape(layers=4, kv_heads=8, head_dim=128, chunk_tokens=256, page_tokens=16)
 
 
-def build_scenario(shape, n_slots=8, num_pages=200, seed=17):
+def build_scenario(shape, n_slots=8, num_pages=200, seed=17, pool=None):
     """Pool of synthetic chunks; three requests through the L1 ledger (one deferred, then granted
-    after a release) so the block table is a non-trivial permutation of pages."""
-    pool = ingest.ChunkPool(shape, n_slots)
-    pool.fill_synthetic(seed)
+    after a release) so the block table is a non-trivial permutation of pages.  `pool`: use this
+    (already filled) pool instead of a fresh host pool."""
+    if pool is None:
+        pool = ingest.ChunkPool(shape, n_slots)
+        pool.fill_synthetic(seed)
+    n_slots = pool.n_slots
     arena = torch.zeros(shape.layers * 2 * num_pages * shape.page_tokens * shape.heads_local * shape.head_dim * 2,
                         dtype=torch.uint8, device="cuda")
     l1 = ingest.PagedKVCache(shape, num_pages, max_rows=4, max_chunks=12, arena=arena)
@@ -366,7 +369,7 @@ def test_ingest_ce_copy_variants_bit_exact(oracle, variant):
         ingest.ingest(l1, pool, items[::-1].copy(), 1, 3, mode=ingest.CE)
         torch.cuda.synchronize()
     finally:
-        ingest.set_ce(1)
+        ingest.set_ce()
     want = oracle.scatter_ref(SMALL, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
     assert np.array_equal(l1.arena.cpu().numpy(), want)
 

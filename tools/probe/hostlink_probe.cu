@@ -17,6 +17,36 @@ __device__ __forceinline__ int4 ld_nc(const int4* p) {
   return r;
 }
 
+__device__ __forceinline__ int4 ld_nc256(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_nc128(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+// warp-contiguous variant: each warp copies a contiguous 32 KiB span (like an ingest segment)
+template <int U, int HINT>
+__global__ void zc_seg(const int4* __restrict__ src, int4* __restrict__ dst, size_t nseg) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t s = warp; s < nseg; s += nw) {
+    const int4* sp = src + s * 2048; int4* dp = dst + s * 2048;
+    for (int v0 = lane; v0 < 2048; v0 += 32 * U) {
+      int4 b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) b[u] = HINT == 256 ? ld_nc256(sp + v0 + u * 32) : HINT == 128 ? ld_nc128(sp + v0 + u * 32) : ld_nc(sp + v0 + u * 32);
+#pragma unroll
+      for (int u = 0; u < U; ++u) dp[v0 + u * 32] = b[u];
+    }
+  }
+}
+
 template <int U>
 __global__ void zc_copy(const int4* __restrict__ src, int4* __restrict__ dst, size_t n16) {
   size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
@@ -114,7 +144,12 @@ int main(int argc, char** argv) {
   printf("{\"bytes\": %zu}\n", bytes);
   printf("CE_H2D GB/s %.2f\n", best([&] { CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice)); }, 5));
   printf("CE_D2H GB/s %.2f\n", best([&] { CK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost)); }, 3));
-  int grids[] = {8, 16, 32, 64, 148, 296, 592};
+  for (int g : {32, 64, 148}) {
+    printf("ZCSEG nohint grid %d GB/s %.2f\n", g, best([&] { zc_seg<8, 0><<<g, 256>>>((const int4*)hd, (int4*)d, bytes / 32768); }, 3));
+    printf("ZCSEG L2::128B grid %d GB/s %.2f\n", g, best([&] { zc_seg<8, 128><<<g, 256>>>((const int4*)hd, (int4*)d, bytes / 32768); }, 3));
+    printf("ZCSEG L2::256B grid %d GB/s %.2f\n", g, best([&] { zc_seg<8, 256><<<g, 256>>>((const int4*)hd, (int4*)d, bytes / 32768); }, 3));
+  }
+  int grids[] = {64};
   for (int g : grids) {
     for (int t : {256, 512}) {
       double gbs = best([&] { zc_copy<8><<<g, t>>>((const int4*)hd, (int4*)d, bytes / 16); }, 3);
