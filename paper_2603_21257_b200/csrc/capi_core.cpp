@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "hostcopy.h"
 #include "kernels.h"
 
 namespace tsb {
@@ -263,8 +264,9 @@ struct tsb_scorer {
   // host-variant staging
   void* qdev = nullptr;
   double* outdev = nullptr;
-  int64_t* orderdev = nullptr;
-  int64_t host_cap = 0;  // capacity of qdev/outdev/orderdev in requests
+  void* qhost = nullptr;    // pinned pack of the caller's queue arrays
+  void* outhost = nullptr;  // pinned results before they are unpacked to the caller
+  int64_t host_cap = 0;     // capacity of the four blocks above, in requests
 };
 
 namespace {
@@ -283,7 +285,8 @@ void scorer_free(tsb_scorer* s) {
   cudaFreeHost(s->err_host);
   cudaFree(s->qdev);
   cudaFree(s->outdev);
-  cudaFree(s->orderdev);
+  cudaFreeHost(s->qhost);
+  cudaFreeHost(s->outhost);
 }
 
 tsb_status scorer_reserve(tsb_scorer* s, int64_t n) {
@@ -389,22 +392,37 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
   if (n == 0) return TSB_OK;
   // Pack the SoA queue into one device block: 7 x 8-byte arrays + flags.
   const size_t w = sizeof(int64_t) * static_cast<size_t>(n);
-  if (n > s->host_cap) {  // grow-only device buffers: no allocation (and no implicit sync) per call
+  if (n > s->host_cap) {  // grow-only buffers: no allocation (and no implicit sync) per call
     const int64_t cap = std::max<int64_t>(n, 4096);
     const size_t wc = sizeof(int64_t) * static_cast<size_t>(cap);
     cudaFree(s->qdev);
     cudaFree(s->outdev);
-    cudaFree(s->orderdev);
+    cudaFreeHost(s->qhost);
+    cudaFreeHost(s->outhost);
     s->qdev = nullptr;
     s->outdev = nullptr;
-    s->orderdev = nullptr;
+    s->qhost = s->outhost = nullptr;
     s->host_cap = 0;
     TSB_CUDA_TRY(cudaMalloc(&s->qdev, 8 * wc + static_cast<size_t>(cap)));
-    TSB_CUDA_TRY(cudaMalloc(&s->outdev, 3 * wc));
-    TSB_CUDA_TRY(cudaMalloc(&s->orderdev, wc));
+    TSB_CUDA_TRY(cudaMalloc(&s->outdev, 4 * wc));  // t_load | t_comp | primary | order
+    TSB_CUDA_TRY(cudaMallocHost(&s->qhost, 8 * wc + static_cast<size_t>(cap)));
+    TSB_CUDA_TRY(cudaMallocHost(&s->outhost, 4 * wc));
     s->host_cap = cap;
   }
+  // The queue block is packed at the CURRENT n's stride so one H2D moves exactly 8*w+n bytes.
   auto* b = static_cast<uint8_t*>(s->qdev);
+  auto* hb = static_cast<uint8_t*>(s->qhost);
+  tsb::HostCopyTeam::get().run({{hb + 0 * w, q->id, w},
+                                {hb + 1 * w, q->arrival, w},
+                                {hb + 2 * w, q->context_tokens, w},
+                                {hb + 3 * w, q->query_tokens, w},
+                                {hb + 4 * w, q->cache_hit_ratio, w},
+                                {hb + 5 * w, q->deadline, w},
+                                {hb + 6 * w, q->measured_t_load, w},
+                                {hb + 7 * w, q->measured_t_comp, w},
+                                {hb + 8 * w, q->flags, static_cast<size_t>(n)}},
+                               tsb::HostCopyTeam::PACK_NT);
+  TSB_CUDA_TRY(cudaMemcpyAsync(b, hb, 8 * w + static_cast<size_t>(n), cudaMemcpyHostToDevice, st));
   tsb_queue dq;
   dq.id = reinterpret_cast<const int64_t*>(b + 0 * w);
   dq.arrival = reinterpret_cast<const double*>(b + 1 * w);
@@ -415,28 +433,24 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
   dq.measured_t_load = reinterpret_cast<const double*>(b + 6 * w);
   dq.measured_t_comp = reinterpret_cast<const double*>(b + 7 * w);
   dq.flags = b + 8 * w;
-  auto h2d = [&](const void* dst, const void* src, size_t bytes) -> cudaError_t {
-    if (!src) return cudaMemsetAsync(const_cast<void*>(dst), 0, bytes, st);
-    return cudaMemcpyAsync(const_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice, st);
-  };
-  TSB_CUDA_TRY(h2d(dq.id, q->id, w));
-  TSB_CUDA_TRY(h2d(dq.arrival, q->arrival, w));
-  TSB_CUDA_TRY(h2d(dq.context_tokens, q->context_tokens, w));
-  TSB_CUDA_TRY(h2d(dq.query_tokens, q->query_tokens, w));
-  TSB_CUDA_TRY(h2d(dq.cache_hit_ratio, q->cache_hit_ratio, w));
-  TSB_CUDA_TRY(h2d(dq.deadline, q->deadline, w));
-  TSB_CUDA_TRY(h2d(dq.measured_t_load, q->measured_t_load, w));
-  TSB_CUDA_TRY(h2d(dq.measured_t_comp, q->measured_t_comp, w));
-  TSB_CUDA_TRY(h2d(dq.flags, q->flags, static_cast<size_t>(n)));
   double* o = s->outdev;
+  auto* ord = reinterpret_cast<int64_t*>(o + 3 * n);
   int64_t err = -1;
-  TSB_TRY(tsb_score_queue_device(s, stream, n, &dq, policy, models, c, o, o + n, o + 2 * n,
-                                 s->orderdev, &err));
-  if (t_load) TSB_CUDA_TRY(cudaMemcpyAsync(t_load, o, w, cudaMemcpyDeviceToHost, st));
-  if (t_comp) TSB_CUDA_TRY(cudaMemcpyAsync(t_comp, o + n, w, cudaMemcpyDeviceToHost, st));
-  if (primary) TSB_CUDA_TRY(cudaMemcpyAsync(primary, o + 2 * n, w, cudaMemcpyDeviceToHost, st));
-  if (order) TSB_CUDA_TRY(cudaMemcpyAsync(order, s->orderdev, w, cudaMemcpyDeviceToHost, st));
+  TSB_TRY(tsb_score_queue_device(s, stream, n, &dq, policy, models, c, o, o + n, o + 2 * n, ord,
+                                 &err));
+  // Read back only the requested outputs: the three cost/key arrays are contiguous.
+  auto* ho = static_cast<uint8_t*>(s->outhost);
+  const int first = t_load ? 0 : t_comp ? 1 : primary ? 2 : 3;
+  const int last = order ? 3 : primary ? 2 : t_comp ? 1 : t_load ? 0 : -1;
+  if (last >= 0)
+    TSB_CUDA_TRY(cudaMemcpyAsync(ho + first * w, o + first * n, (last - first + 1) * w,
+                                 cudaMemcpyDeviceToHost, st));
   TSB_CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<tsb::CopySpan> outs;
+  void* dsts[4] = {t_load, t_comp, primary, order};
+  for (int k = 0; k < 4; ++k)
+    if (dsts[k]) outs.push_back({dsts[k], ho + k * w, w});
+  tsb::HostCopyTeam::get().run(outs, tsb::HostCopyTeam::UNPACK_FLUSH);
   return TSB_OK;
 }
 
