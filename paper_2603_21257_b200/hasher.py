@@ -56,7 +56,7 @@ class PrefixIndex:
         self._h = h
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # lib is None during interpreter exit
             lib.tsb_index_destroy(self._h)
             self._h = None
 

@@ -156,7 +156,7 @@ class ChunkPool:
         return self._h
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # lib is None during interpreter exit
             lib.tsb_pool_destroy(self._h)
             self._h = None
 
@@ -210,7 +210,7 @@ class PagedKVCache:
         return self._h
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # lib is None during interpreter exit
             lib.tsb_l1_destroy(self._h)
             self._h = None
 

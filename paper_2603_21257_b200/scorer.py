@@ -47,7 +47,7 @@ class BatchScorer:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # lib is None during interpreter exit
             lib.tsb_scorer_destroy(self._h)
             self._h = None
 

@@ -32,7 +32,7 @@ class LoadStage:
         self.l1, self.pool = l1, pool
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # lib is None during interpreter exit
             lib.tsb_stage_destroy(self._h)
             self._h = None
 

@@ -394,7 +394,7 @@ class TierLedger:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:
             lib.tsb_ledger_destroy(h)
             self._h = None
 
