@@ -156,33 +156,78 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
   }
 }
 
-// Phase 2 -- the per-request chain H_c = pair(H_{c-1}, digest_c), in place; one thread per
-// request, loads are independent of the chain so they pipeline; the digests are L2-resident.
-// One thread per request, software-pipelined: the next group of kG digests is loaded before the
-// current group is folded into the chain, so each iteration's latency overlaps the previous one.
-constexpr int kG = 32;
+// Phase 2 -- the per-request chain H_c = pair(H_{c-1}, digest_c), in place.  The chain is
+// serial per request, so lane i of a warp owns request r0+i; but its digests move through shared
+// memory transposed, so every global access is coalesced: a round covers kSpan digests of each
+// request, and one load instruction reads two requests' kSpan-digest rows (half-warp each, 128 B)
+// instead of 32 scattered 8-byte words.  Round t+1's rows are loaded into registers while round t
+// is folded (software pipeline).  kSpan = 16 keeps the kernel under 96 registers, so the 100K-
+// request grid is a single wave and the warp holding the longest request starts at once.
+constexpr int kChainWarps = 4;
+constexpr int kSpan = 16;
 
-__global__ void __launch_bounds__(128) k_chain(int64_t n_req, const int64_t* __restrict__ chunk_offsets,
-                                               uint64_t* __restrict__ out) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (r >= n_req) return;
-  const int64_t b = chunk_offsets[r], e = chunk_offsets[r + 1];
+__global__ void __launch_bounds__(32 * kChainWarps) k_chain(
+    int64_t n_req, const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
+  // [request][digest]; rows padded to 18 words: 16-byte aligned for the lane-row reads, and 8
+  // consecutive rows start on distinct bank quads
+  __shared__ __align__(16) uint64_t buf[kChainWarps][32][kSpan + 2];
+  __shared__ int64_t sb[kChainWarps][32], sn[kChainWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int half = lane >> 4, j = lane & 15;
+  const int64_t r0 = (blockIdx.x * static_cast<int64_t>(kChainWarps) + w) * 32;
+  if (r0 >= n_req) return;
+  const int64_t r = r0 + lane;
+  const int64_t b = r < n_req ? chunk_offsets[r] : 0;
+  const int64_t n = r < n_req ? chunk_offsets[r + 1] - b : 0;
+  sb[w][lane] = b;
+  sn[w][lane] = n;
+  const int rounds = __reduce_max_sync(0xffffffffu, static_cast<unsigned>((n + kSpan - 1) / kSpan));
+  __syncwarp();
+  uint64_t (*bw)[kSpan + 2] = buf[w];
+  uint64_t nx[16];  // nx[p]: digest j of request 2p+half in the next round
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    const int q = 2 * p + half;
+    nx[p] = j < sn[w][q] ? out[sb[w][q] + j] : 0;
+  }
   uint64_t h = (kFnvOffset << 32) | (kFnvOffset >> 32);
-  uint64_t cur[kG], nxt[kG];
+  for (int t = 0; t < rounds; ++t) {
+    const int64_t o = static_cast<int64_t>(t) * kSpan + j;
 #pragma unroll
-  for (int k = 0; k < kG; ++k) cur[k] = b + k < e ? out[b + k] : 0;
-  for (int64_t c = b; c < e; c += kG) {
+    for (int p = 0; p < 16; ++p) bw[2 * p + half][j] = nx[p];
+    __syncwarp();
+    if (t + 1 < rounds) {
 #pragma unroll
-    for (int k = 0; k < kG; ++k) nxt[k] = c + kG + k < e ? out[c + kG + k] : 0;
-#pragma unroll
-    for (int k = 0; k < kG; ++k) {
-      if (c + k < e) {
-        h = fpair(h, cur[k]);
-        out[c + k] = h;
+      for (int p = 0; p < 16; ++p) {
+        const int q = 2 * p + half;
+        nx[p] = o + kSpan < sn[w][q] ? out[sb[w][q] + o + kSpan] : 0;
       }
     }
+    // This lane's digests left in the round.  All shared-memory reads (128-bit) issue before the
+    // serial fold, and the fold is branch-free (select), so each step costs only the two
+    // dependent 64-bit FNV multiplies.
+    const int m = static_cast<int>(min(n - static_cast<int64_t>(t) * kSpan, int64_t{kSpan}));
+    ulonglong2 v[kSpan / 2];
 #pragma unroll
-    for (int k = 0; k < kG; ++k) cur[k] = nxt[k];
+    for (int k = 0; k < kSpan / 2; ++k) v[k] = reinterpret_cast<const ulonglong2*>(bw[lane])[k];
+#pragma unroll
+    for (int k = 0; k < kSpan / 2; ++k) {
+      const uint64_t g0 = fpair(h, v[k].x);
+      h = 2 * k < m ? g0 : h;
+      v[k].x = h;
+      const uint64_t g1 = fpair(h, v[k].y);
+      h = 2 * k + 1 < m ? g1 : h;
+      v[k].y = h;
+    }
+#pragma unroll
+    for (int k = 0; k < kSpan / 2; ++k) reinterpret_cast<ulonglong2*>(bw[lane])[k] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const int q = 2 * p + half;
+      if (o < sn[w][q]) out[sb[w][q] + o] = bw[q][j];
+    }
+    __syncwarp();
   }
 }
 
@@ -210,7 +255,7 @@ cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int3
   // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
   k_chunk_digest<<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
-  k_chain<<<ceil_div(n_req, 128), 128, 0, st>>>(n_req, chunk_offsets, out);
+  k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();
   return cudaGetLastError();
 }
