@@ -9,10 +9,14 @@ page release (tsb_stage_run, the public C-ABI call).  Default workload = BASELIN
 (Qwen2.5-32B KV, 16 x 128K @ 0.9 hit).  With N GPUs the KV heads are sharded TP-style: every rank
 ingests its head slice of the same batch from the pool (strong scaling, no data-path collective).
 
-  value : payload bytes of all ranks / max over ranks of the CUDA-event time of the K timed steps
-  e2e   : the same bytes / max over ranks of the host wall time of the K public-API calls
-  roofline     : the dominant kernel (K2 paged scatter, HBM-bound) timed live with CUDA events
-  host_link    : ingest GB/s per GPU vs the live-measured copy-engine H2D peak of this box
+  value : inputs resident in HBM -- the same L2 pool (slots, bytes) held in device memory; payload
+          bytes of all ranks / max over ranks of the CUDA-event time of the K timed stage passes
+  e2e   : the L2 pool in pinned host memory, so every payload byte crosses the host link inside
+          the timed region; the same bytes / max over ranks of the host wall time of the K
+          public-API calls (the headline against the reference arm)
+  roofline     : the value arm's dominant kernel (K1 over the HBM pool, HBM-bound), live CUDA events
+  roofline_k2  : the e2e arm's kernel (K2 paged scatter from the CE staging ring)
+  host_link    : the e2e arm's device-timed GB/s per GPU vs the live copy-engine H2D peak
   cpu_baseline : the oracle's scatter_ref (port) on the host cores, bounded sample (rank 0, N=1)
 """
 from __future__ import annotations
@@ -148,19 +152,20 @@ def measure_ce_peak(torch, reps=5):
 
 def measure_k2(torch, l1, shape, n_items=128, reps=20):
     """K2 (k_ingest_ldg over an HBM staging buffer) timed alone with CUDA events on its stream:
-    one layer of n_items chunks per launch; algorithmic bytes = read + write of the payload."""
+    one layer of n_items chunks per launch; algorithmic bytes = read + write of this rank's
+    payload (the staging holds full-head layer slices; K2 reads this rank's heads of each row)."""
     from paper_2603_21257_b200 import _capi, ingest
     from paper_2603_21257_b200.tiersim import check
 
     cb = shape.page_bytes * shape.pages_per_chunk
     rid = 1 << 40
-    rows = []
     for c in range(n_items):
         g, row = l1.request(rid, c, cb)
         assert g
     l1.sync_block_table()
-    layer_bytes = 2 * shape.chunk_tokens * shape.kv_heads * shape.head_dim * shape.dtype_bytes
-    staging = torch.empty(n_items * layer_bytes, dtype=torch.uint8, device="cuda")
+    full_layer = 2 * shape.chunk_tokens * shape.kv_heads * shape.head_dim * shape.dtype_bytes
+    local_layer = full_layer // shape.tp_size
+    staging = torch.empty(n_items * full_layer, dtype=torch.uint8, device="cuda")
     items = ingest.items_numpy(np.arange(n_items), [row] * n_items, np.arange(n_items))
     dev_items = torch.from_numpy(items.view(np.uint8).copy()).cuda()
     s = torch.cuda.current_stream()
@@ -177,7 +182,7 @@ def measure_k2(torch, l1, shape, n_items=128, reps=20):
     avg_s = a.elapsed_time(b) * 1e-3 / reps
     l1.release_request(rid)
     del staging
-    return 2 * n_items * layer_bytes, avg_s
+    return 2 * n_items * local_layer, avg_s
 
 
 def measured_peaks():
@@ -188,12 +193,15 @@ def measured_peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def k2_traffic_from_profile():
-    p = ROOT / "profiles" / "k2_ncu_summary.json"
-    if p.exists():
-        d = json.loads(p.read_text())
-        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
-    return None, None
+def scaled_traffic(summary_name, alg_bytes):
+    """dram read+write bytes of one launch from a committed `ncu --set full` summary, scaled from
+    the profiled launch's algorithmic bytes to this launch's (null when not captured)."""
+    p = ROOT / "profiles" / summary_name
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    dram, alg = d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+    return dram * alg_bytes / alg if dram and alg else None
 
 
 # ------------------------------------------------------------------------------------------------
@@ -260,6 +268,64 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def timed_steps(torch, run, steps, dist, capi):
+    """W warm-up steps are run by the caller; this times exactly `steps` calls of `run()`,
+    bracketed by a barrier + synchronize on both sides.  Returns (device s, wall s, last result,
+    kernel launches, clocks)."""
+    dev = torch.cuda.current_device()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = capi.lib.tsb_kernel_launch_count()
+    walls, results = [], None
+    with ClockSampler(dev) as clk:
+        ev0.record(s)
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            results = run()
+            walls.append(time.perf_counter() - t0)
+        ev1.record(s)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = capi.lib.tsb_kernel_launch_count() - launches0
+    return ev0.elapsed_time(ev1) * 1e-3, sum(walls), results, launches, clk.summary()
+
+
+def measure_k1_hbm(torch, l1, pool, shape, n_items, reps=10):
+    """K1 (k_ingest_ldg, K2 grid) reading the HBM-resident pool, timed alone with CUDA events:
+    the stage's dominant launch -- layers [1, L) of a request's n_items chunks (layer 0 goes
+    first, alone, to fence the first layer); algorithmic bytes = read + write of the payload."""
+    from paper_2603_21257_b200 import ingest
+
+    cb = shape.page_bytes * shape.pages_per_chunk
+    rid = (1 << 40) + 1
+    for c in range(n_items):
+        g, row = l1.request(rid, c, cb)
+        assert g
+    l1.sync_block_table()
+    items = ingest.items_numpy(np.arange(n_items) % pool.n_slots, [row] * n_items, np.arange(n_items))
+    dev_items = torch.from_numpy(items.view(np.uint8).copy()).cuda()
+    s = torch.cuda.current_stream()
+    lo = 1 if shape.layers > 1 else 0
+    launch = lambda: ingest.ingest_device(l1, pool, dev_items, n_items, lo, shape.layers, mode=ingest.ZEROCOPY,
+                                          stream=s)
+    for _ in range(3):
+        launch()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(reps):
+        launch()
+    b.record(s)
+    b.synchronize()
+    avg_s = a.elapsed_time(b) * 1e-3 / reps
+    l1.release_request(rid)
+    layer_bytes = 2 * shape.chunk_tokens * shape.heads_local * shape.head_dim * shape.dtype_bytes
+    return 2 * n_items * (shape.layers - lo) * layer_bytes, avg_s
+
+
 def run_ours(args):
     import torch
 
@@ -275,6 +341,7 @@ def run_ours(args):
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     from paper_2603_21257_b200 import _capi, ingest
+    from paper_2603_21257_b200.multirank import reduce_timing
     from paper_2603_21257_b200.stage import LoadStage
     from paper_2603_21257_b200.tiersim import PolicyKind
     from paper_2603_21257_b200.workloads import WORKLOADS
@@ -285,8 +352,22 @@ def run_ours(args):
     ce_peak = measure_ce_peak(torch)
     pool, pool_kind, shape = make_pool(wl.shape, wl.pool_slots, world, rank, dist, seed)
     pool_seed = seed + rank if shape.tp_size == 1 and world > 1 else seed
+    pool_shape = pool.shape
+    if args.emulate_tp > 1:  # one GPU standing in for rank 0 of a TP-sharded box (configs[2])
+        if world > 1:
+            raise SystemExit("--emulate-tp is for single-GPU runs")
+        shape = wl.shape.with_rank(args.emulate_tp, 0)
 
-    # L1 arena: most of HBM, fewer pages than the batch needs so FIFO deferral is exercised.
+    # The same L2 pool resident in this GPU's HBM (same slot layout and contents): the `value` arm.
+    dpool = None
+    if not args.no_hbm_arm:
+        free, _ = torch.cuda.mem_get_info()
+        if wl.pool_slots * pool_shape.chunk_bytes + (40 << 30) < free:
+            dpool = ingest.ChunkPool.create_device(pool_shape, wl.pool_slots, device=dev)
+            dpool.fill_synthetic(pool_seed)
+
+    # L1 arena: most of the remaining HBM, fewer pages than the batch needs so FIFO deferral is
+    # exercised.  Both arms share it.
     free, total = torch.cuda.mem_get_info()
     page = shape.page_bytes
     need_pages = wl.chunks * shape.pages_per_chunk
@@ -294,54 +375,54 @@ def run_ours(args):
     num_pages = min(arena_bytes // page, need_pages)
     max_chunks = max(len(s) for s in wl.slots)
     l1 = ingest.PagedKVCache(shape, num_pages, max_rows=wl.queue.n + 1, max_chunks=max(max_chunks, 128))
-    stage = LoadStage(l1, pool)
     mode = ingest.MODES[args.mode]
-    run = lambda verify=0: stage.run(wl.queue, wl.slots, wl.config, policy=PolicyKind.Fifo, mode=mode,
-                                     verify_seed=verify)
+    stage_host = LoadStage(l1, pool)
+    run_host = lambda verify=0: stage_host.run(wl.queue, wl.slots, wl.config, policy=PolicyKind.Fifo, mode=mode,
+                                               verify_seed=verify)
 
-    # warm-up (the first one also checks every page against the synthetic source pattern)
+    # ---- value: L2 pool resident in HBM, CUDA events around K stage passes ----------------------
+    hbm = None
+    if dpool is not None:
+        stage_dev = LoadStage(l1, dpool)
+        run_dev = lambda verify=0: stage_dev.run(wl.queue, wl.slots, wl.config, policy=PolicyKind.Fifo,
+                                                 verify_seed=verify)
+        for i in range(args.warmup):
+            r = run_dev(pool_seed if i == 0 else 0)
+            if i == 0 and r.stats["verify_mismatches"]:
+                raise SystemExit(f"ingest parity failure (HBM pool): {r.stats['verify_mismatches']} words")
+        d_s, d_wall, d_res, d_launch, d_clk = timed_steps(torch, run_dev, args.steps, dist, _capi)
+        d_s, d_wall, d_bytes = reduce_timing(dist, d_s, d_wall, float(d_res.stats["bytes"]), device="cuda")
+        k1_items = max_chunks
+        k1_alg, k1_s = measure_k1_hbm(torch, l1, dpool, shape, k1_items)
+        hbm = dict(dev_s=d_s, bytes=d_bytes, launches=d_launch, clocks=d_clk, stats=d_res.stats,
+                   k1_alg=k1_alg, k1_s=k1_s, k1_items=k1_items)
+        stage_dev.close()
+        dpool.close()
+        torch.cuda.synchronize()
+
+    # ---- e2e: pinned host pool, every byte crosses the host link inside the timed region -------
     for i in range(args.warmup):
-        r = run(pool_seed if i == 0 else 0)
+        r = run_host(pool_seed if i == 0 else 0)  # the first one checks every page
         if i == 0 and r.stats["verify_mismatches"]:
             raise SystemExit(f"ingest parity failure: {r.stats['verify_mismatches']} mismatching words")
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    s = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = _capi.lib.tsb_kernel_launch_count()
-    walls, results = [], None
-    with ClockSampler(dev) as clk:
-        ev0.record(s)
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            results = run()
-            walls.append(time.perf_counter() - t0)
-        ev1.record(s)
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    gpu_launches = _capi.lib.tsb_kernel_launch_count() - launches0
-    dev_s = ev0.elapsed_time(ev1) * 1e-3
-    wall_s = sum(walls)
+    h_s, wall_s, results, h_launch, h_clk = timed_steps(torch, run_host, args.steps, dist, _capi)
     local_bytes = results.stats["bytes"]
-    from paper_2603_21257_b200.multirank import reduce_timing
-
-    dev_s, wall_s, total_bytes = reduce_timing(dist, dev_s, wall_s, float(local_bytes), device="cuda")
-    value = args.steps * total_bytes / dev_s / 1e9
+    h_s, wall_s, total_bytes = reduce_timing(dist, h_s, wall_s, float(local_bytes), device="cuda")
+    host_dev_rate = args.steps * total_bytes / h_s / 1e9
     e2e = args.steps * total_bytes / wall_s / 1e9
 
     # The hand-written SM ingest kernels on the same stage, first 2 requests of the batch: K1
     # (16-byte zero-copy loads) and K1b (cp.async.bulk / TMA engine).  AUTO picks CE+K2 for
     # full-head chunks because SM-initiated host reads cap at ~92.6% of the copy-engine rate.
+    s = torch.cuda.current_stream()
     modes = {}
     if not args.no_alt_modes:
         sub = type(wl.queue)(2, **{k: getattr(wl.queue, k)[:2] for k, _ in type(wl.queue).FIELDS})
         for name in ("bulk", "zerocopy", "ce"):
-            stage.run(sub, wl.slots[:2], wl.config, mode=ingest.MODES[name])  # warm
+            stage_host.run(sub, wl.slots[:2], wl.config, mode=ingest.MODES[name])  # warm
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(s)
-            r = stage.run(sub, wl.slots[:2], wl.config, mode=ingest.MODES[name])
+            r = stage_host.run(sub, wl.slots[:2], wl.config, mode=ingest.MODES[name])
             b.record(s)
             b.synchronize()
             modes[name] = {"GBps": r.stats["bytes"] / (a.elapsed_time(b) * 1e-3) / 1e9,
@@ -349,14 +430,16 @@ def run_ours(args):
         if dist:
             dist.barrier()
 
-    # dominant kernel roofline (K2), measured live; host-link fraction vs live CE peak
-    layer_bytes = 2 * shape.chunk_tokens * shape.kv_heads * shape.head_dim * shape.dtype_bytes
+    # K2 (the CE path's paged scatter, HBM-bound), measured live on the stage's group size
+    layer_bytes = 2 * shape.chunk_tokens * shape.heads_local * shape.head_dim * shape.dtype_bytes
     k2_items = min((512 << 20) // layer_bytes, max_chunks)  # the stage's K2 group: one staging half
-    alg_bytes, k2_s = measure_k2(torch, l1, shape, n_items=k2_items)
+    k2_alg, k2_s = measure_k2(torch, l1, shape, n_items=k2_items)
     hbm_peak, hbm_src = measured_peaks()
-    traffic, traffic_alg = k2_traffic_from_profile()
-    if traffic and traffic_alg:
-        traffic = traffic * alg_bytes / traffic_alg  # scale the per-launch ncu bytes to this launch
+    k2_traffic = scaled_traffic("k2_ncu_summary.json", k2_alg)
+    k2_roof = {"bound": "hbm", "kernel": "k_ingest_ldg (K2 paged scatter from the CE staging ring)",
+               "achieved": k2_alg / k2_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+               "frac": k2_alg / k2_s / 1e9 / hbm_peak, "traffic": k2_traffic, "peak_source": hbm_src,
+               "algorithmic_bytes_per_launch": int(k2_alg), "launch_us": k2_s * 1e6}
     req = results.requests
     order = np.argsort(req["pick_position"])
     ttft = {"first_layer_ms_p50": float(np.median(req["first_layer_ms"])),
@@ -365,28 +448,49 @@ def run_ours(args):
             "resident_ms_first_request": float(req["resident_ms"][order[0]]),
             "reference_model_ms_per_request": float(len(wl.slots[0]) * (10e-6 + shape.local_chunk_bytes / 64e9) * 1e3)}
     bt_bytes = wl.queue.n * l1.stride * 4
+    host_link = {"achieved": host_dev_rate / world, "peak": ce_peak, "unit": "GB/s",
+                 "frac": host_dev_rate / world / ce_peak, "ms_per_step": h_s / args.steps * 1e3,
+                 "peak_source": "live pinned 1 GiB cudaMemcpy H2D, best of 5, this box",
+                 "kernel_launches": int(h_launch)}
+    e2e_obj = {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(local_bytes + bt_bytes + wl.queue.n * 66),
+               "d2h_bytes_per_step": int(wl.queue.n * (8 + 16)),
+               "source": "L2 pool in pinned host memory (" + pool_kind + "); host wall time of the public-API "
+                         "calls (tsb_stage_run); the KV payload is the H2D traffic"}
+    cfg = {"workload": wl.name, "description": wl.description,
+           "parallelism": (f"kv-head shards tp{world}" if world > 1 else
+                           f"single GPU as rank 0 of a tp{args.emulate_tp} head split" if args.emulate_tp > 1
+                           else "single GPU"),
+           "ingest_mode": args.mode, "policy": "fifo", "l1_pages": int(num_pages),
+           "l1_page_bytes": int(page), "l1_gib": round(num_pages * page / 2**30, 1),
+           "bytes_per_step": int(total_bytes), "pool": pool_kind,
+           "l2_flush": "inputs larger than L2 (each step streams the whole batch: 100s of GB)"}
+    if hbm is not None:
+        value = args.steps * hbm["bytes"] / hbm["dev_s"] / 1e9
+        ms_per_step = hbm["dev_s"] / args.steps * 1e3
+        launches = hbm["launches"]
+        clocks = hbm["clocks"]
+        k1_traffic = scaled_traffic("k1hbm_ncu_summary.json", hbm["k1_alg"])
+        roofline = {"bound": "hbm", "kernel": "k_ingest_ldg (K1 over the HBM-resident pool, 1184 CTAs)",
+                    "achieved": hbm["k1_alg"] / hbm["k1_s"] / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hbm["k1_alg"] / hbm["k1_s"] / 1e9 / hbm_peak, "traffic": k1_traffic,
+                    "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(hbm["k1_alg"]),
+                    "launch_us": hbm["k1_s"] * 1e6, "items_per_launch": hbm["k1_items"],
+                    "algorithmic_bytes": "read + write of the payload (2 x chunks x layers [1, L) x layer slice)"}
+        cfg["value_source"] = ("L2 pool resident in HBM (tsb_pool_create_device, same slots and bytes); "
+                               "CUDA events on the stage stream around the K passes")
+        cfg["hbm_arm_stage"] = {k: hbm["stats"][k] for k in ("ingest_calls", "deferred_chunks", "releases",
+                                                             "kernel_launches")}
+    else:  # HBM cannot hold pool + L1: value falls back to the host-pool device time
+        value, ms_per_step, launches, clocks, roofline = host_dev_rate, h_s / args.steps * 1e3, h_launch, h_clk, k2_roof
+        cfg["value_source"] = "L2 pool in pinned host memory (HBM too small for the pool); CUDA events"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": wl.name, "description": wl.description,
-                   "parallelism": f"kv-head shards tp{world}" if world > 1 else "single GPU",
-                   "ingest_mode": args.mode, "policy": "fifo", "l1_pages": int(num_pages),
-                   "l1_page_bytes": int(page), "l1_gib": round(num_pages * page / 2**30, 1),
-                   "bytes_per_step": int(total_bytes), "pool": pool_kind,
-                   "l2_flush": "inputs larger than L2 (each step streams the whole batch from host memory)"},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(local_bytes + bt_bytes + wl.queue.n * 66),
-                "d2h_bytes_per_step": int(wl.queue.n * (8 + 16))},
-        "gpu_launches": int(gpu_launches),
-        "roofline": {"bound": "hbm", "kernel": "k_ingest_ldg (K2 paged scatter from the CE staging ring)",
-                     "achieved": alg_bytes / k2_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": alg_bytes / k2_s / 1e9 / hbm_peak, "traffic": traffic, "peak_source": hbm_src,
-                     "algorithmic_bytes_per_launch": int(alg_bytes), "launch_us": k2_s * 1e6},
-        "host_link": {"achieved": value / world, "peak": ce_peak, "unit": "GB/s", "frac": value / world / ce_peak,
-                      "peak_source": "live pinned 1 GiB cudaMemcpy H2D, best of 5, this box"},
-        "ttft_load_ms": ttft,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": cfg,
+        "e2e": e2e_obj, "gpu_launches": int(launches), "roofline": roofline,
+        "roofline_k2": k2_roof, "host_link": host_link, "ttft_load_ms": ttft,
         "stage": {k: results.stats[k] for k in ("ingest_calls", "deferred_chunks", "releases", "kernel_launches")},
-        "clocks": clk.summary(),
+        "clocks": clocks, "clocks_e2e": h_clk,
         "ingest_modes_2req": modes,
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -412,7 +516,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="qwen16x128k")
     ap.add_argument("--mode", default="auto", choices=["auto", "ce", "bulk", "zerocopy"])
-    ap.add_argument("--l1-gib", type=int, default=144)
+    ap.add_argument("--l1-gib", type=int, default=100)
+    ap.add_argument("--emulate-tp", type=int, default=1, help="one GPU ingests rank 0's head slice of a tpN split")
+    ap.add_argument("--no-hbm-arm", action="store_true", help="skip the HBM-resident-pool arm (value)")
     ap.add_argument("--cpu-sample-chunks", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt-modes", action="store_true", help="skip the K1/K1b/CE side measurements")

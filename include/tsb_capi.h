@@ -333,12 +333,16 @@ typedef struct {
 } tsb_ingest_item;
 
 typedef enum {
-  TSB_INGEST_AUTO = 0,     /* CE for full-head shapes, ZEROCOPY for head-sharded shapes */
+  TSB_INGEST_AUTO = 0,     /* host pool: CE for full-head shapes and for head-sharded item
+                              lists whose consecutive-slot runs carry >= 3.1 MB per copy,
+                              else ZEROCOPY; device pool or device items: ZEROCOPY */
   TSB_INGEST_ZEROCOPY = 1, /* K1: SM 16B loads from mapped host memory, scatter to pages */
   TSB_INGEST_BULK = 2,     /* K1b: cp.async.bulk host->smem->pages, one issuing lane/CTA */
   TSB_INGEST_CE = 3        /* copy engine H2D into an HBM staging ring, then K2 scatter;
                               host reads run on an internal copy stream ordered after the
-                              work queued on `stream` before the call (tp_size == 1 only) */
+                              work queued on `stream` before the call.  Head-sharded shapes
+                              copy only this rank's heads: one strided cudaMemcpy3DAsync per
+                              run of consecutive slots per layer */
 } tsb_ingest_mode;
 
 /* items: host array (copied into a pinned ring internally, so it may be reused on return).
@@ -362,7 +366,8 @@ tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_cta
 tsb_status tsb_ingest_set_scatter(int impl, int ctas);
 /* CE copy strategy: 0 = one cudaMemcpyAsync per (item, layer), 1 = one cudaMemcpy2DAsync per
  * run of consecutive pool slots, 2 = one cudaMemcpyBatchAsync per staging group (default:
- * 99.6% of the CE peak for any slot order, measured on B200).
+ * 99.6% of the CE peak for any slot order, measured on B200).  Full-head shapes only;
+ * head-sharded shapes always use one 3D copy per consecutive-slot run.
  * staging_bytes: HBM staging ring size (0 = default 512 MiB). */
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes);
 

@@ -604,14 +604,49 @@ tsb::IngestGeom make_geom(const tsb_l1* l, int64_t layer_lo, int64_t layer_hi) {
   return g;
 }
 
-int resolve_mode(const tsb_l1* l, const tsb_pool* pool, int mode, bool host_items) {
+// Copy-engine cost model for head-sharded slices, measured on B200
+// (repo:profiles/r01_ce_strided_probe.jsonl): a strided cudaMemcpy3DAsync moves a rank's slice
+// at the contiguous H2D rate (55.3-55.6 GB/s for 256 B - 1 KiB runs) but costs ~4.6 us per
+// call, while SM zero-copy loads cap at ~51.4 GB/s with no per-call cost.  The copy engines
+// win once a call carries more than 4.6 us / (1/51.4 - 1/55.6 GB/s) ~ 3.1 MB.
+constexpr double kCeBytesPerCallBreakEven = 3.1e6;
+
+// Consecutive-slot runs in an item list: the number of 3D copies one layer needs.
+int64_t slot_runs(const tsb_ingest_item* it, int64_t n) {
+  int64_t runs = n > 0 ? 1 : 0;
+  for (int64_t k = 1; k < n; ++k) runs += it[k].src_slot != it[k - 1].src_slot + 1;
+  return runs;
+}
+
+// Geometry of one layer of items staged packed in HBM: each item's slice of this rank's heads,
+// [K|V][C][run] contiguous, item k at k * layer_src.  K2 reads it as contiguous segments.
+tsb::IngestGeom make_staged_geom(const tsb_l1* l, int64_t layer) {
+  tsb::IngestGeom g = make_geom(l, layer, layer + 1);
+  g.row = g.run;
+  g.head_off = 0;
+  g.kv_src = l->shape.chunk_tokens * g.run;
+  g.layer_src = 2 * g.kv_src;
+  g.staged = 1;
+  g.item_stride = g.layer_src;
+  return g;
+}
+
+int resolve_mode(const tsb_l1* l, const tsb_pool* pool, int mode, const tsb_ingest_item* items_host,
+                 int64_t n_items) {
   if (mode != TSB_INGEST_AUTO) return mode;
   // A device pool (local or peer HBM) is read by SM loads: no host link to saturate.
   if (pool->location == TSB_POOL_DEVICE) return TSB_INGEST_ZEROCOPY;
+  // Device-side item lists cannot drive host-issued copies.
+  if (!items_host) return TSB_INGEST_ZEROCOPY;
   // Measured on B200 (profiles/r01_*): SM-initiated host reads plateau at ~92.6% of the copy
-  // engines' H2D rate, so full-head chunks go through CE + K2; head-sharded chunks have
-  // 256 B - 1 KiB runs that only the SM path reads without moving other ranks' heads.
-  return (l->shape.tp_size == 1 && host_items) ? TSB_INGEST_CE : TSB_INGEST_ZEROCOPY;
+  // engines' H2D rate, so full-head chunks go through CE + K2.
+  if (l->shape.tp_size == 1) return TSB_INGEST_CE;
+  // Head-sharded chunks: the copy engines pull only this rank's heads with one strided 3D copy
+  // per run of consecutive slots; worth it when the runs are long enough.
+  const tsb_kv_shape& s = l->shape;
+  const double slice = 2.0 * s.chunk_tokens * (s.kv_heads / s.tp_size) * s.head_dim * s.dtype_bytes;
+  const double per_call = slice * n_items / static_cast<double>(slot_runs(items_host, n_items));
+  return per_call >= kCeBytesPerCallBreakEven ? TSB_INGEST_CE : TSB_INGEST_ZEROCOPY;
 }
 
 tsb_status ensure_staging(tsb_l1* l) {
@@ -627,24 +662,48 @@ tsb_status ensure_staging(tsb_l1* l) {
   return TSB_OK;
 }
 
-// Copies layer `layer` of items [0, n) into stage (item k at stage + k*layer_bytes) on the
-// copy-engine stream.
+// Copies layer `layer` of items [0, n) into stage (item k at stage + k * g.layer_src, where g is
+// the packed staged geometry) on the copy-engine stream.
 tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, int64_t n,
                          int64_t layer, const tsb::IngestGeom& g, uint8_t* stage) {
-  const int64_t lb = g.layer_src;
-  const uint8_t* base = pool->host + layer * lb;
+  const tsb::IngestGeom src = make_geom(l, layer, layer + 1);  // pool (slot) geometry
+  const int64_t lb = g.layer_src;                               // packed slice of one item
+  const uint8_t* base = pool->host + layer * src.layer_src + src.head_off;
+  if (src.run != src.row) {
+    // Head-sharded: one 3D copy per run of consecutive slots.  x = this rank's run of each token
+    // row, y = the 2*C rows of the layer (pitch = the full row), z = slots (slice pitch = one
+    // chunk = L*2*C rows).  The destination is packed: [item][K|V][C][run].
+    const size_t rows_per_chunk = static_cast<size_t>(src.chunk_bytes / src.row);
+    const size_t rows = static_cast<size_t>(2 * l->shape.chunk_tokens);
+    int64_t k = 0;
+    while (k < n) {
+      int64_t e = k + 1;
+      while (e < n && it[e].src_slot == it[e - 1].src_slot + 1) ++e;
+      cudaMemcpy3DParms p{};
+      p.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(base + it[k].src_slot * src.chunk_bytes),
+                                     static_cast<size_t>(src.row), static_cast<size_t>(src.run),
+                                     rows_per_chunk);
+      p.dstPtr = make_cudaPitchedPtr(stage + k * lb, static_cast<size_t>(src.run),
+                                     static_cast<size_t>(src.run), rows);
+      p.extent = make_cudaExtent(static_cast<size_t>(src.run), rows, static_cast<size_t>(e - k));
+      p.kind = cudaMemcpyHostToDevice;
+      TSB_CUDA_TRY(cudaMemcpy3DAsync(&p, l->ce_stream));
+      k = e;
+    }
+    return TSB_OK;
+  }
   switch (g_knobs.ce_variant) {
     case 0:
       for (int64_t k = 0; k < n; ++k)
-        TSB_CUDA_TRY(cudaMemcpyAsync(stage + k * lb, base + it[k].src_slot * g.chunk_bytes, lb,
+        TSB_CUDA_TRY(cudaMemcpyAsync(stage + k * lb, base + it[k].src_slot * src.chunk_bytes, lb,
                                      cudaMemcpyHostToDevice, l->ce_stream));
       return TSB_OK;
     case 2: {
-      std::vector<void*> dst(n), src(n);
+      std::vector<void*> dst(n), srcp(n);
       std::vector<size_t> sz(n, static_cast<size_t>(lb));
       for (int64_t k = 0; k < n; ++k) {
         dst[k] = stage + k * lb;
-        src[k] = const_cast<uint8_t*>(base + it[k].src_slot * g.chunk_bytes);
+        srcp[k] = const_cast<uint8_t*>(base + it[k].src_slot * src.chunk_bytes);
       }
       cudaMemcpyAttributes attr{};
       attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
@@ -652,7 +711,7 @@ tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, i
       attr.dstLocHint.type = cudaMemLocationTypeDevice;
       attr.dstLocHint.id = l->device;
       size_t idx = 0, fail_idx = 0;
-      TSB_CUDA_TRY(cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), static_cast<size_t>(n),
+      TSB_CUDA_TRY(cudaMemcpyBatchAsync(dst.data(), srcp.data(), sz.data(), static_cast<size_t>(n),
                                         &attr, &idx, 1, &fail_idx, l->ce_stream));
       return TSB_OK;
     }
@@ -661,8 +720,8 @@ tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, i
       while (k < n) {
         int64_t e = k + 1;
         while (e < n && it[e].src_slot == it[e - 1].src_slot + 1) ++e;
-        TSB_CUDA_TRY(cudaMemcpy2DAsync(stage + k * lb, lb, base + it[k].src_slot * g.chunk_bytes,
-                                       g.chunk_bytes, lb, e - k, cudaMemcpyHostToDevice,
+        TSB_CUDA_TRY(cudaMemcpy2DAsync(stage + k * lb, lb, base + it[k].src_slot * src.chunk_bytes,
+                                       src.chunk_bytes, lb, e - k, cudaMemcpyHostToDevice,
                                        l->ce_stream));
         k = e;
       }
@@ -678,13 +737,10 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
                      cudaStream_t st, void* const* layer_events) {
   if (pool->location != TSB_POOL_HOST)
     return fail(TSB_UNSUPPORTED, "ingest CE mode reads host pools; use zerocopy/bulk for device pools");
-  if (l->shape.tp_size != 1)
-    return fail(TSB_UNSUPPORTED,
-                "ingest CE mode copies whole token rows; use zerocopy/bulk when tp_size > 1");
   if (!items_host)
     return fail(TSB_UNSUPPORTED, "ingest CE mode needs host-visible items (use tsb_ingest)");
   TSB_TRY(ensure_staging(l));
-  tsb::IngestGeom g = make_geom(l, lo, lo + 1);
+  tsb::IngestGeom g = make_staged_geom(l, lo);
   const int64_t lb = g.layer_src;
   const int64_t half = l->staging_bytes / 2;
   if (lb > half) return fail(TSB_UNSUPPORTED, "ingest CE: one chunk layer exceeds the staging ring");
@@ -693,9 +749,7 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
   TSB_CUDA_TRY(cudaEventRecord(l->ev_fence, st));
   TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_fence, 0));
   for (int64_t layer = lo; layer < hi; ++layer) {
-    g = make_geom(l, layer, layer + 1);
-    g.staged = 1;
-    g.item_stride = lb;
+    g = make_staged_geom(l, layer);
     for (int64_t i0 = 0; i0 < n_items; i0 += per_group) {
       const int64_t n = std::min(per_group, n_items - i0);
       const int b = l->next_buf;
@@ -717,13 +771,19 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
 
 tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev, int64_t n_items,
                      int64_t lo, int64_t hi, int mode, cudaStream_t st, void* const* layer_events) {
-  // One launch per layer when the caller wants per-layer fences, else one launch in total.
-  const int64_t step = layer_events ? 1 : hi - lo;
+  // One launch per span of layers ending at a requested fence (or at hi): per-layer fences give
+  // per-layer launches, a fence only on the first and last layer gives two launches.
   // Host pools are link-bound and saturate with a small grid; HBM / NVLink sources need the
   // K2 grid to keep enough loads in flight.
   const bool on_device = pool->location == TSB_POOL_DEVICE;
-  for (int64_t l0 = lo; l0 < hi; l0 += step) {
-    const tsb::IngestGeom g = make_geom(l, l0, l0 + step);
+  int64_t l0 = lo;
+  while (l0 < hi) {
+    int64_t l1 = l0 + 1;  // exclusive end of this launch
+    if (layer_events)
+      while (l1 < hi && !layer_events[l1 - 1 - lo]) ++l1;
+    else
+      l1 = hi;
+    const tsb::IngestGeom g = make_geom(l, l0, l1);
     if (mode == TSB_INGEST_ZEROCOPY) {
       TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
                                           on_device ? g_knobs.scatter_ctas : g_knobs.zerocopy_ctas,
@@ -737,8 +797,9 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
       TSB_CUDA_TRY(tsb::launch_ingest_bulk(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
                                            on_device ? sms : g_knobs.bulk_ctas, st));
     }
-    if (layer_events && layer_events[l0 - lo])
-      TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[l0 - lo]), st));
+    if (layer_events && layer_events[l1 - 1 - lo])
+      TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[l1 - 1 - lo]), st));
+    l0 = l1;
   }
   return TSB_OK;
 }
@@ -750,7 +811,7 @@ tsb_status ingest_impl(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_d
     return fail(TSB_VALIDATION, "ingest: layer range must satisfy 0 <= lo < hi <= layers");
   if (pool->chunk_bytes != make_geom(l, 0, 1).chunk_bytes)
     return fail(TSB_VALIDATION, "ingest: pool chunk geometry differs from the L1 shape");
-  mode = resolve_mode(l, pool, mode, items_host != nullptr);
+  mode = resolve_mode(l, pool, mode, items_host, n_items);
   if (n_items == 0) {
     for (int64_t k = 0; layer_events && k < hi - lo; ++k)
       if (layer_events[k]) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[k]), st));

@@ -375,10 +375,15 @@ def test_ingest_ce_copy_variants_bit_exact(oracle, variant):
 
 
 @pytest.mark.parametrize("tp", [(2, 0), (2, 1), (4, 3), (8, 5)])
-@pytest.mark.parametrize("mode", ["zerocopy", "bulk"])
+@pytest.mark.parametrize("mode", ["zerocopy", "bulk", "ce", "ce_runs"])
 def test_ingest_head_sharded_bit_exact(oracle, tp, mode):
+    """Head-sharded slices; "ce" = strided 3D copies of random slots (runs of 1), "ce_runs" =
+    consecutive slots 2..7, 0..5 (multi-slot 3D copies), both then K2 over the packed staging."""
     shape = SMALL.with_rank(*tp)
     pool, l1, items = build_scenario(shape)
+    if mode == "ce_runs":
+        items["src_slot"] = (np.arange(len(items)) + 2) % pool.n_slots
+        mode = "ce"
     ingest.ingest(l1, pool, items, mode=ingest.MODES[mode])
     torch.cuda.synchronize()
     want = oracle.scatter_ref(shape, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
@@ -407,14 +412,36 @@ def test_ingest_per_layer_with_events_equals_whole(oracle):
     assert tuple(l1.layer(0).shape) == (2, 200, 16, 8, 128)
 
 
+@pytest.mark.parametrize("mode", ["zerocopy", "bulk", "ce"])
+def test_ingest_sparse_layer_events(oracle, mode):
+    """Fences on some layers only: the SM kernels launch once per span of layers ending at a
+    fence (here [0,1) and [1,4)); each fence still means "layers up to here are resident"."""
+    pool, l1, items = build_scenario(SMALL)
+    s = torch.cuda.Stream()
+    e0, e3 = torch.cuda.Event(), torch.cuda.Event()
+    launches = _capi.lib.tsb_kernel_launch_count()
+    with torch.cuda.stream(s):
+        ingest.ingest(l1, pool, items, 0, SMALL.layers, mode=ingest.MODES[mode], stream=s,
+                      layer_events=[e0, None, None, e3])
+    e0.synchronize()
+    page0 = l1.block_table()[items["bt_row"][0], items["chunk_index"][0] * 16]
+    assert l1.layer(0, torch.int16)[0, page0].abs().sum().item() > 0
+    e3.synchronize()
+    if mode != "ce":
+        assert _capi.lib.tsb_kernel_launch_count() - launches == 2
+    want = oracle.scatter_ref(SMALL, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+
+
 def test_ingest_errors_fail_loudly():
     pool, l1, items = build_scenario(SMALL)
     with pytest.raises(t.ValidationError):
         ingest.ingest(l1, pool, items, 3, 3)
-    with pytest.raises(t.Unsupported):
-        shp = SMALL.with_rank(2, 0)
-        p2, l2, it2 = build_scenario(shp)
-        ingest.ingest(l2, p2, it2, mode=ingest.CE)
+    with pytest.raises(t.Unsupported):  # the copy engines read host pools only
+        dpool = ingest.ChunkPool.create_device(SMALL, 2)
+        it0 = items[:1].copy()
+        it0["src_slot"] = 0
+        ingest.ingest(l1, dpool, it0, mode=ingest.CE)
     with pytest.raises(t.CapacityError):
         l1.request(99, 0, 10**15)
     with pytest.raises(t.ValidationError):

@@ -15,7 +15,11 @@ for s in $steps; do
       timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
       timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> /dev/null; echo "bench ref rc=$?"
       timeout 600 python bench.py --workload llama8b32k > gpurun_out/bench_llama8b.json 2> /dev/null; echo "bench 8b rc=$?"
-      timeout 900 python bench.py --workload llama70b32k --mode zerocopy > gpurun_out/bench_70b.json 2> /dev/null; echo "bench 70b rc=$?" ;;
+      timeout 900 python bench.py --workload llama70b32k > gpurun_out/bench_70b.json 2> /dev/null; echo "bench 70b rc=$?"
+      for tp in 2 4 8; do
+        timeout 900 python bench.py --workload llama70b32k --emulate-tp $tp --no-cpu-baseline > gpurun_out/bench_70b_tp$tp.json 2> /dev/null; echo "bench 70b tp$tp rc=$?"
+        timeout 900 python bench.py --workload llama70b32k --emulate-tp $tp --mode zerocopy --no-cpu-baseline --no-hbm-arm --no-alt-modes > gpurun_out/bench_70b_tp${tp}_k1.json 2> /dev/null; echo "bench 70b tp$tp k1 rc=$?"
+      done ;;
     tools)
       timeout 600 python tools/bench_queue.py > gpurun_out/bench_queue.json 2> /dev/null; echo "queue rc=$?"
       timeout 900 python tools/bench_mixed.py > gpurun_out/bench_mixed_ref.json 2> /dev/null; echo "mixed rc=$?"
