@@ -1,6 +1,6 @@
 """Small, single-purpose workloads for ncu (one GPU, short):  python tools/prof_targets.py <what>
 
-what: scorer | hash | ingest-ce | ingest-bulk | ingest-zerocopy | ingest-tp8
+what: scorer | hash | ingest-ce | ingest-bulk | ingest-zerocopy | ingest-tp8 | ingest-hbm | ingest-hbm-tp8
 """
 from __future__ import annotations
 
@@ -33,6 +33,23 @@ def ingest_once(shape, n_chunks, mode, reps=2):
     assert ingest.verify_synthetic(l1, pool, items, 3) == 0
 
 
+def ingest_hbm(shape, n_chunks, reps=2):
+    """K1 over an HBM-resident pool as the stage issues it: layer 0 alone, then layers [1, L)."""
+    pool = ingest.ChunkPool.create_device(shape, n_chunks)
+    pool.fill_synthetic(3)
+    l1 = ingest.PagedKVCache(shape, n_chunks * shape.pages_per_chunk, 1, n_chunks)
+    cb = shape.page_bytes * shape.pages_per_chunk
+    for c in range(n_chunks):
+        g, row = l1.request(1, c, cb)
+    l1.sync_block_table()
+    items = ingest.items_numpy(np.random.default_rng(0).permutation(n_chunks), [row] * n_chunks, np.arange(n_chunks))
+    evs = [torch.cuda.Event() if k in (0, shape.layers - 1) else None for k in range(shape.layers)]
+    for _ in range(reps):
+        ingest.ingest(l1, pool, items, layer_events=evs)
+    torch.cuda.synchronize()
+    assert ingest.verify_synthetic(l1, pool, items, 3) == 0
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     if what == "scorer":
@@ -47,5 +64,9 @@ if __name__ == "__main__":
         ingest_once(ingest.LLAMA31_8B, 128, ingest.ZEROCOPY)
     elif what == "ingest-tp8":
         ingest_once(ingest.LLAMA3_70B.with_rank(8, 7), 128, ingest.ZEROCOPY)
+    elif what == "ingest-hbm":
+        ingest_hbm(ingest.LLAMA31_8B, 128)
+    elif what == "ingest-hbm-tp8":
+        ingest_hbm(ingest.LLAMA3_70B.with_rank(8, 7), 128)
     else:
         raise SystemExit(__doc__)
