@@ -65,6 +65,9 @@ class ClockSampler:
                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             threading.Thread(target=self._read, daemon=True).start()
+            t0 = time.time()  # a timed region shorter than the sampling period still gets the first sample
+            while not self.lines and time.time() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
