@@ -6,9 +6,9 @@
 // 64-bit words (two int32 token ids each): 16 leaves of 8 words per 256-token chunk, a 4-level
 // pairwise tree, and a per-request chain so hash c names the whole prefix [0, 256(c+1)).
 //
-// Mapping, two phases.  (1) k_chunk_digest: a persistent grid of warps walks the global chunk
-// index space kItem chunks at a time (balanced however request lengths vary); each half-warp owns
-// one chunk per round (lane j folds leaf j = words 32k+2j, 32k+2j+1 for k = 0..3, so each of the
+// Mapping, two phases.  (1) k_chunk_digest: each warp of a persistent grid walks one contiguous,
+// equal share of the global chunk index space (balanced however request lengths vary); each
+// half-warp owns one chunk per round (lane j folds leaf j = words 32k+2j, 32k+2j+1 for k = 0..3, so each of the
 // four 16-byte load instructions reads 2 x 256 contiguous bytes -- fully coalesced), two rounds
 // are loaded before any is consumed (4 KiB in flight per warp), the tree is 4 shuffle levels
 // inside the half-warp, and the digest goes to out[c].  (2) k_chain: one thread per request
@@ -26,7 +26,6 @@ __device__ __forceinline__ uint64_t fpair(uint64_t a, uint64_t b) {
 
 constexpr int kHashThreads = 256;
 constexpr int kHashWarps = kHashThreads / 32;
-constexpr int kRounds = 2;  // rounds of 2 chunks loaded ahead per warp
 
 // Token ids are read exactly once: stream them through L2 with evict_first so the 87 MB of chunk
 // digests written by phase 1 survive in L2 for phase 2.
@@ -85,11 +84,19 @@ __device__ __forceinline__ uint64_t tree16(uint64_t v, int j) {
 }
 
 // Phase 1 -- chunk digests, balanced over the GLOBAL chunk index space (request lengths vary
-// 100x, so a warp-per-request mapping leaves a long tail): a persistent grid of warps takes
-// kItem consecutive chunks at a time, finds the owning request once with a 32-ary search over
-// chunk_offsets, and writes each chunk's digest to out[c].
-constexpr int kItem = 16;
-
+// 100x, so a warp-per-request mapping leaves a long tail).  Each warp of the persistent grid
+// owns one contiguous, equal share of the chunk index space: it finds its first chunk's
+// request once (32-ary search over chunk_offsets) and then walks forward, each half-warp
+// carrying its own (request, chunk base, token base) and stepping to the next request only at a
+// boundary (~once per 100 chunks).  No per-chunk lookups sit between the token loads, and each
+// warp streams one contiguous stretch of tokens.
+//
+// Measured (profiles/r01_k3_variants.md): this kernel is bound by instruction issue, not by
+// HBM: ~270 warp instructions per 2 chunks (8 FNV steps per lane of 6 instructions each, plus
+// the 4-level shuffle tree executed by every lane) against 1.8 ms of issue time at 51% issue
+// efficiency.  Moving the token loads to TMA / cp.async staging with a lane-per-chunk fold
+// (5x fewer instructions) lost to instruction-cache misses, bank conflicts of 1 KiB-strided
+// chunks, and per-copy TMA cost (2.3-5.1 ms); see the profile notes.
 __device__ __forceinline__ void st_evict_last(uint64_t* p, uint64_t v) {
   asm volatile(
       "{\n.reg .b64 pol;\n"
@@ -119,38 +126,59 @@ __device__ __forceinline__ int64_t warp_upper_bound(const int64_t* __restrict__ 
   return lo;
 }
 
-__global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
+// Running position of one half-warp: the request owning chunk `c` and its bases.
+struct ReqCursor {
+  int64_t r, cb, nb, tb;  // request, its first chunk, next request's first chunk, token base
+  __device__ __forceinline__ int64_t base_of(int64_t c, const int64_t* __restrict__ co,
+                                             const int64_t* __restrict__ offs) {
+    while (c >= nb) {  // rare: crossing into the next non-empty request
+      ++r;
+      cb = nb;
+      nb = co[r + 1];
+      tb = offs[r];
+    }
+    return tb + (c - cb) * 256;
+  }
+};
+
+// Rotating software pipeline of R rounds: the loads of round u + R are issued as soon as round u
+// has been folded, so a warp always has R - 1 to R rounds (2 KiB each) in flight, including
+// while it computes.
+template <int R, int kMinBlocks>
+__global__ void __launch_bounds__(kHashThreads, kMinBlocks) k_chunk_digest(
     int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
     const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int half = lane >> 4, j = lane & 15;
   const int64_t total = chunk_offsets[n_req];
   const int64_t warps = static_cast<int64_t>(gridDim.x) * kHashWarps;
-  for (int64_t item = blockIdx.x * static_cast<int64_t>(kHashWarps) + (threadIdx.x >> 5);
-       item * kItem < total; item += warps) {
-    const int64_t c0 = item * kItem;
-    const int64_t c1 = min(c0 + kItem, total);
-    // lane k (< kItem) resolves chunk c0+k's token base once per item, so the token loads below
-    // do not wait on per-chunk table lookups
-    int64_t r = warp_upper_bound(chunk_offsets, n_req + 1, c0) - 1;
-    int64_t tb = -1;
-    if (lane < kItem && c0 + lane < c1) {
-      while (chunk_offsets[r + 1] <= c0 + lane) ++r;
-      tb = offsets[r] + (c0 + lane - chunk_offsets[r]) * 256;
+  const int64_t w = blockIdx.x * static_cast<int64_t>(kHashWarps) + (threadIdx.x >> 5);
+  const int64_t c_begin = total * w / warps, c_end = total * (w + 1) / warps;
+  if (c_begin >= c_end) return;
+  ReqCursor cur;
+  cur.r = warp_upper_bound(chunk_offsets, n_req + 1, c_begin) - 1;
+  cur.cb = chunk_offsets[cur.r];
+  cur.nb = chunk_offsets[cur.r + 1];
+  cur.tb = offsets[cur.r];
+  Leaf f[R];
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const int64_t cc = c_begin + 2 * u + half;
+    if (cc < c_end) {
+      const int64_t base = cur.base_of(cc, chunk_offsets, offsets);
+      load_leaf(tokens + base + j * 4, (base & 3) == 0, f[u]);
     }
-    for (int64_t c = c0; c < c1; c += 2 * kRounds) {
-      Leaf f[kRounds];
+  }
+  for (int64_t c = c_begin; c < c_end; c += 2 * R) {
 #pragma unroll
-      for (int u = 0; u < kRounds; ++u) {
-        const int64_t cc = c + 2 * u + half;
-        const int64_t base = __shfl_sync(0xffffffffu, tb, static_cast<int>(cc - c0) & 31);
-        if (cc < c1) load_leaf(tokens + base + j * 4, (base & 3) == 0, f[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < kRounds; ++u) {
-        const int64_t cc = c + 2 * u + half;
-        const uint64_t d = tree16(fold_leaf(f[u]), j);
-        if (j == 0 && cc < c1) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
+    for (int u = 0; u < R; ++u) {
+      const int64_t cc = c + 2 * u + half;
+      const uint64_t d = tree16(fold_leaf(f[u]), j);
+      if (j == 0 && cc < c_end) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
+      const int64_t nc = cc + 2 * R;
+      if (nc < c_end) {
+        const int64_t base = cur.base_of(nc, chunk_offsets, offsets);
+        load_leaf(tokens + base + j * 4, (base & 3) == 0, f[u]);
       }
     }
   }
@@ -253,7 +281,7 @@ cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int3
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
   // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
-  k_chunk_digest<<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  k_chunk_digest<2, 4><<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
   k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();
