@@ -473,7 +473,7 @@ def run_ours(args):
         launches = hbm["launches"]
         clocks = hbm["clocks"]
         k1_traffic = scaled_traffic("k1hbm_ncu_summary.json", hbm["k1_alg"])
-        roofline = {"bound": "hbm", "kernel": "k_ingest_ldg (K1 over the HBM-resident pool, 1184 CTAs)",
+        roofline = {"bound": "hbm", "kernel": "k_ingest_ldg (K1 over the HBM-resident pool, 4736 CTAs, 4 loads in flight per lane)",
                     "achieved": hbm["k1_alg"] / hbm["k1_s"] / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": hbm["k1_alg"] / hbm["k1_s"] / 1e9 / hbm_peak, "traffic": k1_traffic,
                     "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(hbm["k1_alg"]),

@@ -32,7 +32,7 @@ namespace {
 struct Knobs {
   int zerocopy_ctas = 64;
   int bulk_ctas = 64;
-  int scatter_ctas = 148 * 8;  // K2 sweep (r01): 5.6-5.9 TB/s from 592 CTAs up, 8 warps each
+  int scatter_ctas = 148 * 32;  // HBM-source grid (K2, K1 over device pools): r01 K1 sweep
   int scatter_impl = 0;  // K2: 0 = SM load/store warps, 1 = bulk-copy (TMA engine)
   int ce_variant = 2;
   int64_t staging_bytes = 1ll << 30;  // 2 x 512 MiB: one K2 launch per layer of a 460-chunk request
@@ -552,14 +552,14 @@ tsb_status tsb_l1_sync_block_table(tsb_l1* l, void* stream) {
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas) {
   g_knobs.zerocopy_ctas = zerocopy_ctas > 0 ? zerocopy_ctas : 64;
   g_knobs.bulk_ctas = bulk_ctas > 0 ? bulk_ctas : 64;
-  g_knobs.scatter_ctas = scatter_ctas > 0 ? scatter_ctas : 148 * 8;
+  g_knobs.scatter_ctas = scatter_ctas > 0 ? scatter_ctas : 148 * 32;
   return TSB_OK;
 }
 
 tsb_status tsb_ingest_set_scatter(int impl, int ctas) {
   if (impl < 0 || impl > 1) return fail(TSB_VALIDATION, "ingest_set_scatter: impl must be 0 or 1");
   g_knobs.scatter_impl = impl;
-  g_knobs.scatter_ctas = ctas > 0 ? ctas : (impl == 0 ? 148 * 8 : 148);
+  g_knobs.scatter_ctas = ctas > 0 ? ctas : (impl == 0 ? 148 * 32 : 148);
   return TSB_OK;
 }
 
@@ -573,7 +573,7 @@ cudaError_t launch_scatter(const tsb::IngestGeom& g, const uint8_t* src, uint8_t
                            cudaStream_t st) {
   if (g_knobs.scatter_impl == 1 && g.seg_bytes * 2 <= tsb::kBulkSmem)
     return tsb::launch_ingest_bulk(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st);
-  return tsb::launch_ingest_ldg(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st);
+  return tsb::launch_ingest_ldg(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st, true);
 }
 
 }  // namespace
@@ -787,7 +787,7 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
     if (mode == TSB_INGEST_ZEROCOPY) {
       TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
                                           on_device ? g_knobs.scatter_ctas : g_knobs.zerocopy_ctas,
-                                          st));
+                                          st, on_device));
     } else {
       if (g.seg_bytes * 2 > tsb::kBulkSmem)
         return fail(TSB_UNSUPPORTED, "ingest bulk: page segment too large for the smem ring");

@@ -184,13 +184,24 @@ __global__ void k_verify_synth(IngestGeom g, const uint8_t* __restrict__ arena,
 
 cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
                               const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
-                              int grid, cudaStream_t st) {
+                              int grid, cudaStream_t st, bool hbm_source) {
   const int64_t nseg = n_items * g.n_layers * 2 * g.ppc;
   if (nseg == 0) return cudaSuccess;
-  if (g.run == g.row)
-    k_ingest_ldg<true, 8><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
-  else
-    k_ingest_ldg<false, 8><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+  // Loads in flight per lane: 8 over the host link (microsecond latency, 64 CTAs); 4 from HBM,
+  // where the sweep (profiles/r01_k1_sweep.jsonl) peaks with 4 loads per lane and a 32-CTA-per-
+  // SM grid: 6.54-6.63 TB/s for full-head segments (U=8: 6.06-6.10 at 1184 CTAs).
+  const bool contig = g.run == g.row;
+  if (hbm_source) {
+    if (contig)
+      k_ingest_ldg<true, 4><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+    else
+      k_ingest_ldg<false, 4><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+  } else {
+    if (contig)
+      k_ingest_ldg<true, 8><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+    else
+      k_ingest_ldg<false, 8><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+  }
   count_launch();
   return cudaGetLastError();
 }

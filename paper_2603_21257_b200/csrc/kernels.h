@@ -33,9 +33,11 @@ struct IngestGeom {
   int64_t item_stride;
 };
 
+// hbm_source: the source is device memory (HBM staging ring, local or peer HBM pool) rather
+// than mapped host memory; picks the loads-in-flight depth.
 cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
                               const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
-                              int grid, cudaStream_t st);
+                              int grid, cudaStream_t st, bool hbm_source);
 // Shared memory of the K1b ring (bytes); a segment must fit twice (<= 100 KiB).
 constexpr int kBulkSmem = 200 * 1024;
 cudaError_t launch_ingest_bulk(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
