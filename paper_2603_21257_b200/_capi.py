@@ -185,6 +185,7 @@ _decl("tsb_l1_sync_block_table", st, vp, vp)
 _decl("tsb_ingest", st, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_device", st, vp, vp, vp, i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_set_ce", st, C.c_int, i64)
+_decl("tsb_ingest_resolve_mode", st, vp, vp, P(IngestItem), i64, C.c_int, P(C.c_int))
 _decl("tsb_ingest_set_scatter", st, C.c_int, C.c_int)
 _decl("tsb_scatter_device", st, vp, vp, vp, i64, i64, i64, vp)
 _decl("tsb_ingest_set_grid", st, C.c_int, C.c_int, C.c_int)

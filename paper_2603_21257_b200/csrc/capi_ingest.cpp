@@ -856,6 +856,15 @@ tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* i
                      static_cast<cudaStream_t>(stream), layer_events);
 }
 
+tsb_status tsb_ingest_resolve_mode(const tsb_l1* l, const tsb_pool* pool,
+                                   const tsb_ingest_item* items, int64_t n_items, int mode,
+                                   int* resolved) {
+  if (mode < TSB_INGEST_AUTO || mode > TSB_INGEST_CE)
+    return fail(TSB_VALIDATION, "ingest: unknown mode " + std::to_string(mode));
+  *resolved = resolve_mode(l, pool, mode, items, n_items);
+  return TSB_OK;
+}
+
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes) {
   if (variant < 0 || variant > 2) return fail(TSB_VALIDATION, "ingest_set_ce: variant must be 0, 1 or 2");
   g_knobs.ce_variant = variant;

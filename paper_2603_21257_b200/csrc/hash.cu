@@ -13,6 +13,8 @@
 // are loaded before any is consumed (4 KiB in flight per warp), the tree is 4 shuffle levels
 // inside the half-warp, and the digest goes to out[c].  (2) k_chain: one thread per request
 // folds its digests into the chain in place (L2-resident).  HBM-bound: 4 B/token + 8 B/chunk.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -73,16 +75,6 @@ __device__ __forceinline__ uint64_t fold_leaf(const Leaf& f) {
   return h;
 }
 
-// 4-level pairwise tree over the 16 leaves of each half-warp; result in lanes 0 and 16.
-__device__ __forceinline__ uint64_t tree16(uint64_t v, int j) {
-#pragma unroll
-  for (int d = 1; d < 16; d <<= 1) {
-    const uint64_t o = __shfl_down_sync(0xffffffffu, v, d, 16);
-    if ((j & (2 * d - 1)) == 0) v = fpair(v, o);
-  }
-  return v;
-}
-
 // Phase 1 -- chunk digests, balanced over the GLOBAL chunk index space (request lengths vary
 // 100x, so a warp-per-request mapping leaves a long tail).  Each warp of the persistent grid
 // owns one contiguous, equal share of the chunk index space: it finds its first chunk's
@@ -141,10 +133,24 @@ struct ReqCursor {
   }
 };
 
-// Rotating software pipeline of R rounds: the loads of round u + R are issued as soon as round u
-// has been folded, so a warp always has R - 1 to R rounds (2 KiB each) in flight, including
-// while it computes.
-template <int R, int kMinBlocks>
+// The 4-level pairwise tree of two rounds at once (leaf j of round 0 in v0, of round 1 in v1, on
+// lane j of each half-warp).  Level 1 pairs round 0 on even lanes and round 1 on odd lanes, so
+// levels 2-4 carry both rounds in one shuffle + FNV pair per lane instead of two.  Round 0's
+// digest ends in lane 0, round 1's in lane 1.
+__device__ __forceinline__ uint64_t tree16x2(uint64_t v0, uint64_t v1, int j) {
+  const uint64_t r = __shfl_xor_sync(0xffffffffu, (j & 1) ? v0 : v1, 1, 16);
+  uint64_t v = (j & 1) ? fpair(r, v1) : fpair(v0, r);
+#pragma unroll
+  for (int d = 2; d < 16; d <<= 1) {
+    const uint64_t o = __shfl_down_sync(0xffffffffu, v, d, 16);
+    if ((j & (2 * d - 1)) < 2) v = fpair(v, o);
+  }
+  return v;
+}
+
+// Rotating software pipeline of two rounds: the loads of round u + 2 are issued as soon as round
+// u has been folded, so a warp keeps 1-2 rounds (2 KiB each) in flight while it computes.
+template <int kMinBlocks>
 __global__ void __launch_bounds__(kHashThreads, kMinBlocks) k_chunk_digest(
     int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
     const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
@@ -160,27 +166,29 @@ __global__ void __launch_bounds__(kHashThreads, kMinBlocks) k_chunk_digest(
   cur.cb = chunk_offsets[cur.r];
   cur.nb = chunk_offsets[cur.r + 1];
   cur.tb = offsets[cur.r];
-  Leaf f[R];
+  Leaf f[2];
 #pragma unroll
-  for (int u = 0; u < R; ++u) {
+  for (int u = 0; u < 2; ++u) {
     const int64_t cc = c_begin + 2 * u + half;
     if (cc < c_end) {
       const int64_t base = cur.base_of(cc, chunk_offsets, offsets);
       load_leaf(tokens + base + j * 4, (base & 3) == 0, f[u]);
     }
   }
-  for (int64_t c = c_begin; c < c_end; c += 2 * R) {
+  for (int64_t c = c_begin; c < c_end; c += 4) {
+    uint64_t v[2];
 #pragma unroll
-    for (int u = 0; u < R; ++u) {
-      const int64_t cc = c + 2 * u + half;
-      const uint64_t d = tree16(fold_leaf(f[u]), j);
-      if (j == 0 && cc < c_end) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
-      const int64_t nc = cc + 2 * R;
+    for (int u = 0; u < 2; ++u) {
+      v[u] = fold_leaf(f[u]);
+      const int64_t nc = c + 2 * u + half + 4;
       if (nc < c_end) {
         const int64_t base = cur.base_of(nc, chunk_offsets, offsets);
         load_leaf(tokens + base + j * 4, (base & 3) == 0, f[u]);
       }
     }
+    const uint64_t d = tree16x2(v[0], v[1], j);
+    const int64_t cc = c + 2 * j + half;  // lane 0: round 0's chunk, lane 1: round 1's
+    if (j < 2 && cc < c_end) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
   }
 }
 
@@ -281,7 +289,11 @@ cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int3
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
   // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
-  k_chunk_digest<2, 4><<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  static const int cps = getenv("TSB_K3_CPS") ? atoi(getenv("TSB_K3_CPS")) : 3;
+  if (cps == 4)
+    k_chunk_digest<4><<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  else
+    k_chunk_digest<3><<<148 * 3, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
   k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();

@@ -319,6 +319,14 @@ def enable_peer_access(device: int, peer: int):
     check(lib.tsb_enable_peer_access(int(device), int(peer)))
 
 
+def resolve_mode(l1: PagedKVCache, pool: ChunkPool, items=None, mode: int = AUTO) -> int:
+    """The kernel path tsb_ingest takes for these items (AUTO resolved; items=None: device items)."""
+    ptr, n = _items_ptr(items) if items is not None else (None, 0)
+    out = C.c_int()
+    check(lib.tsb_ingest_resolve_mode(l1.handle, pool.handle, ptr, n, int(mode), C.byref(out)))
+    return out.value
+
+
 def set_ce(variant: int = 2, staging_bytes: int = 0):
     """CE copy strategy: 0 per-item memcpy, 1 2D per consecutive-slot run, 2 batch API (default)."""
     check(lib.tsb_ingest_set_ce(variant, staging_bytes))

@@ -433,6 +433,29 @@ def test_ingest_sparse_layer_events(oracle, mode):
     assert np.array_equal(l1.arena.cpu().numpy(), want)
 
 
+def test_auto_mode_resolution():
+    """AUTO: host pool + full heads -> CE; head-sharded -> CE when consecutive-slot runs carry
+    >= 3.1 MB per strided copy, else K1; device pool or device items -> K1 (zero-copy kernel)."""
+    shape = ingest.LLAMA3_70B.with_rank(8, 3)  # 256 B runs; one chunk's layer slice = 128 KiB
+    pool = ingest.ChunkPool(ingest.LLAMA3_70B, 40)
+    l1 = ingest.PagedKVCache(shape, 64, max_rows=1, max_chunks=40)
+    run = ingest.items_numpy(np.arange(40), np.zeros(40, np.int32), np.arange(40))   # 40 x 128 KiB = 5.2 MB
+    short = ingest.items_numpy(np.arange(20), np.zeros(20, np.int32), np.arange(20))  # 2.6 MB per copy
+    scattered = run.copy()
+    scattered["src_slot"] = np.random.default_rng(0).permutation(40)
+    assert ingest.resolve_mode(l1, pool, run) == ingest.CE
+    assert ingest.resolve_mode(l1, pool, short) == ingest.ZEROCOPY
+    assert ingest.resolve_mode(l1, pool, scattered) == ingest.ZEROCOPY
+    assert ingest.resolve_mode(l1, pool, None) == ingest.ZEROCOPY
+    assert ingest.resolve_mode(l1, pool, scattered, ingest.BULK) == ingest.BULK
+    full = ingest.PagedKVCache(ingest.LLAMA3_70B, 64, max_rows=1, max_chunks=40)
+    assert ingest.resolve_mode(full, pool, scattered) == ingest.CE
+    dpool = ingest.ChunkPool.create_device(ingest.LLAMA3_70B, 2)
+    assert ingest.resolve_mode(full, dpool, run[:1]) == ingest.ZEROCOPY
+    with pytest.raises(t.ValidationError):
+        ingest.resolve_mode(full, pool, run, 7)
+
+
 def test_ingest_errors_fail_loudly():
     pool, l1, items = build_scenario(SMALL)
     with pytest.raises(t.ValidationError):

@@ -1,5 +1,5 @@
-"""K1 over an HBM-resident pool: sweep loads-in-flight (TSB_K1_U, set per process) and grid for
-the stage's dominant launch shape (layers [1, L) of one request).  One JSON line per grid."""
+"""K1 over an HBM-resident pool: sweep the grid for the stage's dominant launch shape (layers
+[1, L) of one request); SHAPE=qwen|8b|70b|70b_tp2|70b_tp8.  One JSON line per grid."""
 import json
 import os
 import sys
@@ -40,7 +40,7 @@ def main():
             b.record(s)
             b.synchronize()
             best = min(best, a.elapsed_time(b) * 1e-3)
-        print(json.dumps(dict(shape=which, U=os.environ.get("TSB_K1_U", "8"), grid=grid, ms=best * 1e3,
+        print(json.dumps(dict(shape=which, grid=grid, ms=best * 1e3,
                               TBps=alg / best / 1e12)), flush=True)
     ingest.set_grid()
     assert ingest.verify_synthetic(l1, pool, items, 3, 1, shape.layers) == 0
