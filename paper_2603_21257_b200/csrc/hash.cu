@@ -13,8 +13,6 @@
 // are loaded before any is consumed (4 KiB in flight per warp), the tree is 4 shuffle levels
 // inside the half-warp, and the digest goes to out[c].  (2) k_chain: one thread per request
 // folds its digests into the chain in place (L2-resident).  HBM-bound: 4 B/token + 8 B/chunk.
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.h"
 
@@ -48,10 +46,30 @@ struct Leaf {
 
 // Lane j of a half-warp loads tokens [64k + 4j, 64k + 4j + 4) for k = 0..3: every 16-byte load
 // instruction of the warp reads two contiguous 256-byte runs (one per chunk).
-__device__ __forceinline__ void load_leaf(const int32_t* p, bool aligned, Leaf& f) {
-  if (aligned) {
+__device__ __forceinline__ int2 ld_evict_first2(const void* p) {
+  int2 r;
+  asm volatile(
+      "{\n.reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], pol;\n}"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p));
+  return r;
+}
+
+// Token bases are 4-byte aligned only (requests have arbitrary lengths): 16-byte loads when the
+// leaf's address allows, else 8-byte, else 4-byte (the class is uniform over a half-warp).
+__device__ __forceinline__ void load_leaf(const int32_t* p, Leaf& f) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 15) == 0) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) f.v[k] = ld_evict_first(p + 64 * k);
+  } else if ((a & 7) == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int2 lo = ld_evict_first2(p + 64 * k), hi = ld_evict_first2(p + 64 * k + 2);
+      f.v[k] = make_int4(lo.x, lo.y, hi.x, hi.y);
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -76,19 +94,16 @@ __device__ __forceinline__ uint64_t fold_leaf(const Leaf& f) {
 }
 
 // Phase 1 -- chunk digests, balanced over the GLOBAL chunk index space (request lengths vary
-// 100x, so a warp-per-request mapping leaves a long tail).  Each warp of the persistent grid
-// owns one contiguous, equal share of the chunk index space: it finds its first chunk's
-// request once (32-ary search over chunk_offsets) and then walks forward, each half-warp
-// carrying its own (request, chunk base, token base) and stepping to the next request only at a
-// boundary (~once per 100 chunks).  No per-chunk lookups sit between the token loads, and each
-// warp streams one contiguous stretch of tokens.
+// 100x, so a warp-per-request mapping leaves a long tail).  Each CTA of the persistent grid owns
+// one contiguous, equal share of the chunk index space, which its warps walk interleaved: a warp
+// finds its first chunk's request once (32-ary search over chunk_offsets) and then walks
+// forward, each half-warp carrying its own (request, chunk base, token base) and stepping to the
+// next request only at a boundary (~once per 100 chunks).  No per-chunk lookups sit between the
+// token loads.
 //
-// Measured (profiles/r01_k3_variants.md): this kernel is bound by instruction issue, not by
-// HBM: ~270 warp instructions per 2 chunks (8 FNV steps per lane of 6 instructions each, plus
-// the 4-level shuffle tree executed by every lane) against 1.8 ms of issue time at 51% issue
-// efficiency.  Moving the token loads to TMA / cp.async staging with a lane-per-chunk fold
-// (5x fewer instructions) lost to instruction-cache misses, bank conflicts of 1 KiB-strided
-// chunks, and per-copy TMA cost (2.3-5.1 ms); see the profile notes.
+// Measured variants are in profiles/r01_k3_variants.md: TMA / cp.async staging with a
+// lane-per-chunk fold (5x fewer instructions) lost to instruction-cache misses, bank conflicts
+// of 1 KiB-strided chunks, and per-copy TMA cost (2.3-5.1 ms).
 __device__ __forceinline__ void st_evict_last(uint64_t* p, uint64_t v) {
   asm volatile(
       "{\n.reg .b64 pol;\n"
@@ -150,40 +165,44 @@ __device__ __forceinline__ uint64_t tree16x2(uint64_t v0, uint64_t v1, int j) {
 
 // Rotating software pipeline of two rounds: the loads of round u + 2 are issued as soon as round
 // u has been folded, so a warp keeps 1-2 rounds (2 KiB each) in flight while it computes.
-template <int kMinBlocks>
-__global__ void __launch_bounds__(kHashThreads, kMinBlocks) k_chunk_digest(
+__global__ void __launch_bounds__(kHashThreads, 3) k_chunk_digest(
     int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
     const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int half = lane >> 4, j = lane & 15;
   const int64_t total = chunk_offsets[n_req];
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * kHashWarps;
-  const int64_t w = blockIdx.x * static_cast<int64_t>(kHashWarps) + (threadIdx.x >> 5);
-  const int64_t c_begin = total * w / warps, c_end = total * (w + 1) / warps;
-  if (c_begin >= c_end) return;
+  // The CTA owns a contiguous, equal share of the chunk space; its 8 warps interleave over it in
+  // groups of 4 chunks (2 rounds x 2 half-warps), so each CTA streams one region with all its
+  // warps on adjacent addresses.
+  const int w = threadIdx.x >> 5;
+  const int64_t c_begin = total * blockIdx.x / gridDim.x;
+  const int64_t c_end = total * (blockIdx.x + 1) / gridDim.x;
+  const int64_t first = c_begin + 4 * w;
+  if (first >= c_end) return;
+  constexpr int64_t kStride = 4 * kHashWarps;  // chunks between a warp's consecutive groups
   ReqCursor cur;
-  cur.r = warp_upper_bound(chunk_offsets, n_req + 1, c_begin) - 1;
+  cur.r = warp_upper_bound(chunk_offsets, n_req + 1, first) - 1;
   cur.cb = chunk_offsets[cur.r];
   cur.nb = chunk_offsets[cur.r + 1];
   cur.tb = offsets[cur.r];
   Leaf f[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const int64_t cc = c_begin + 2 * u + half;
+    const int64_t cc = first + 2 * u + half;
     if (cc < c_end) {
       const int64_t base = cur.base_of(cc, chunk_offsets, offsets);
-      load_leaf(tokens + base + j * 4, (base & 3) == 0, f[u]);
+      load_leaf(tokens + base + j * 4, f[u]);
     }
   }
-  for (int64_t c = c_begin; c < c_end; c += 4) {
+  for (int64_t c = first; c < c_end; c += kStride) {
     uint64_t v[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       v[u] = fold_leaf(f[u]);
-      const int64_t nc = c + 2 * u + half + 4;
+      const int64_t nc = c + 2 * u + half + kStride;
       if (nc < c_end) {
         const int64_t base = cur.base_of(nc, chunk_offsets, offsets);
-        load_leaf(tokens + base + j * 4, (base & 3) == 0, f[u]);
+        load_leaf(tokens + base + j * 4, f[u]);
       }
     }
     const uint64_t d = tree16x2(v[0], v[1], j);
@@ -289,11 +308,8 @@ cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int3
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
   // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
-  static const int cps = getenv("TSB_K3_CPS") ? atoi(getenv("TSB_K3_CPS")) : 3;
-  if (cps == 4)
-    k_chunk_digest<4><<<148 * 4, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
-  else
-    k_chunk_digest<3><<<148 * 3, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  // 3 CTAs of 8 warps per SM: the two-round pipeline needs 80 registers (64 would spill)
+  k_chunk_digest<<<148 * 3, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
   k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();
