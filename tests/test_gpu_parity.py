@@ -506,6 +506,28 @@ def test_config1_full_size_llama8b_32k(mode):
     assert l1.release_request(1) == [] and l1.free_pages() == 2048
 
 
+@pytest.mark.parametrize("tp", [2, 8])
+def test_config2_full_size_llama70b_head_shards(tp):
+    """configs[2]: Llama-3-70B KV, one 32K prefix (128 chunks of 80 MiB), rank tp-1 of a tp-way
+    head split, AUTO (strided copy-engine 3D copies + K2), per-layer fences.  Every word of every
+    page is checked against the synthetic source (verify kernel)."""
+    full = ingest.LLAMA3_70B
+    shape = full.with_rank(tp, tp - 1)
+    pool = ingest.ChunkPool(full, 128)
+    pool.fill_synthetic(11)
+    l1 = ingest.PagedKVCache(shape, 2048, max_rows=1, max_chunks=128)
+    for c in range(128):
+        g, row = l1.request(1, c, shape.page_bytes * 16)
+        assert g
+    l1.sync_block_table()
+    items = ingest.items_numpy(np.arange(128), [row] * 128, np.arange(128))
+    assert ingest.resolve_mode(l1, pool, items) == ingest.CE
+    evs = [torch.cuda.Event() for _ in range(shape.layers)]
+    ingest.ingest(l1, pool, items, layer_events=evs)
+    evs[-1].synchronize()
+    assert ingest.verify_synthetic(l1, pool, items, seed=11) == 0
+
+
 # ---------------------------------------------------------------------------------------------
 # Geometry generality and edge cases
 # ---------------------------------------------------------------------------------------------
