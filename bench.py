@@ -377,7 +377,8 @@ def run_ours(args):
     arena_bytes = min(free - (10 << 30), args.l1_gib << 30)
     num_pages = min(arena_bytes // page, need_pages)
     max_chunks = max(len(s) for s in wl.slots)
-    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=wl.queue.n + 1, max_chunks=max(max_chunks, 128))
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=wl.queue.n + 1, max_chunks=max(max_chunks, 128),
+                             layout=ingest.LAYOUTS[args.layout])
     mode = ingest.MODES[args.mode]
     stage_host = LoadStage(l1, pool)
     run_host = lambda verify=0: stage_host.run(wl.queue, wl.slots, wl.config, policy=PolicyKind.Fifo, mode=mode,
@@ -421,7 +422,7 @@ def run_ours(args):
     modes = {}
     if not args.no_alt_modes:
         sub = type(wl.queue)(2, **{k: getattr(wl.queue, k)[:2] for k, _ in type(wl.queue).FIELDS})
-        for name in ("bulk", "zerocopy", "ce"):
+        for name in (("zerocopy", "ce") if args.layout == "flashinfer_hnd" else ("bulk", "zerocopy", "ce")):
             stage_host.run(sub, wl.slots[:2], wl.config, mode=ingest.MODES[name])  # warm
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(s)
@@ -463,7 +464,7 @@ def run_ours(args):
            "parallelism": (f"kv-head shards tp{world}" if world > 1 else
                            f"single GPU as rank 0 of a tp{args.emulate_tp} head split" if args.emulate_tp > 1
                            else "single GPU"),
-           "ingest_mode": args.mode, "policy": "fifo", "l1_pages": int(num_pages),
+           "ingest_mode": args.mode, "policy": "fifo", "l1_layout": args.layout, "l1_pages": int(num_pages),
            "l1_page_bytes": int(page), "l1_gib": round(num_pages * page / 2**30, 1),
            "bytes_per_step": int(total_bytes), "pool": pool_kind,
            "l2_flush": "inputs larger than L2 (each step streams the whole batch: 100s of GB)"}
@@ -520,6 +521,8 @@ def main():
     ap.add_argument("--workload", default="qwen16x128k")
     ap.add_argument("--mode", default="auto", choices=["auto", "ce", "bulk", "zerocopy"])
     ap.add_argument("--l1-gib", type=int, default=100)
+    ap.add_argument("--layout", default="flash_attn", choices=["flash_attn", "flashinfer_nhd", "flashinfer_hnd"],
+                    help="the consumer's L1 page layout")
     ap.add_argument("--emulate-tp", type=int, default=1, help="one GPU ingests rank 0's head slice of a tpN split")
     ap.add_argument("--no-hbm-arm", action="store_true", help="skip the HBM-resident-pool arm (value)")
     ap.add_argument("--cpu-sample-chunks", type=int, default=128)

@@ -65,13 +65,16 @@ class ChunkPool {
 /// L1 tier: paged HBM with TierLedger semantics (capacity = pages x page bytes).
 class PagedAllocator {
  public:
+  /// layout: the consumer's page layout (tsb_kv_layout: flash-attn, FlashInfer NHD or HND).
   PagedAllocator(int device, const KvShape& shape, std::int64_t num_pages, std::int64_t max_rows,
-                 std::int64_t max_chunks, void* arena = nullptr) {
+                 std::int64_t max_chunks, void* arena = nullptr, int layout = TSB_LAYOUT_FLASH_ATTN) {
     const tsb_kv_shape s = shape.c_abi();
     tsb_l1* l = nullptr;
     check(tsb_l1_create(device, &s, num_pages, max_rows, max_chunks, arena, &l));
     l_.reset(l);
+    if (layout != TSB_LAYOUT_FLASH_ATTN) check(tsb_l1_set_layout(l, layout));
   }
+  int layout() const { return tsb_l1_layout(l_.get()); }
   /// TierLedger::request semantics; returns Granted/Deferred and the request's block_table row.
   std::pair<bool, std::int32_t> request(std::int64_t request_id, std::int32_t block_index,
                                         std::int64_t bytes) {

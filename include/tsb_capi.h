@@ -290,6 +290,17 @@ int64_t tsb_ledger_deferred(const tsb_ledger* l);
 tsb_status tsb_l1_create(int device, const tsb_kv_shape* shape, int64_t num_pages,
                          int64_t max_rows, int64_t max_chunks, void* arena, tsb_l1** out);
 void tsb_l1_destroy(tsb_l1* l1);
+/* Physical layout of each layer's pages, the consumer's KV-cache layout (installed vLLM 0.22:
+ * v1/attention/backends/flash_attn.py:140-149 and flashinfer.py:357-389).  Same bytes per page;
+ * only the addresses differ.  Default FLASH_ATTN. */
+typedef enum {
+  TSB_LAYOUT_FLASH_ATTN = 0,    /* layer = [2][pages][P][H_local][D]  (K and V planes)      */
+  TSB_LAYOUT_FLASHINFER_NHD = 1, /* layer = [pages][2][P][H_local][D]  (page-major, NHD)     */
+  TSB_LAYOUT_FLASHINFER_HND = 2  /* layer = [pages][2][H_local][P][D]  (page-major, HND)     */
+} tsb_kv_layout;
+/* Sets the page layout; VALIDATION unless nothing is reserved yet. */
+tsb_status tsb_l1_set_layout(tsb_l1* l1, int layout);
+int tsb_l1_layout(const tsb_l1* l1);
 /* TierLedger::request (engine.cpp:22-36).  bytes must be a whole number of local pages
  * (a chunk: chunk_tokens * local bytes/token).  *granted = 1 when granted now; *bt_row gets
  * the request's block_table row (assigned at its first reservation). */
@@ -337,7 +348,8 @@ typedef enum {
                               lists whose consecutive-slot runs carry >= 3.1 MB per copy,
                               else ZEROCOPY; device pool or device items: ZEROCOPY */
   TSB_INGEST_ZEROCOPY = 1, /* K1: SM 16B loads from mapped host memory, scatter to pages */
-  TSB_INGEST_BULK = 2,     /* K1b: cp.async.bulk host->smem->pages, one issuing lane/CTA */
+  TSB_INGEST_BULK = 2,     /* K1b: cp.async.bulk host->smem->pages, one issuing lane/CTA
+                              (not for TSB_LAYOUT_FLASHINFER_HND: UNSUPPORTED) */
   TSB_INGEST_CE = 3        /* copy engine H2D into an HBM staging ring, then K2 scatter;
                               host reads run on an internal copy stream ordered after the
                               work queued on `stream` before the call.  Head-sharded shapes

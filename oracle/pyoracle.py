@@ -100,6 +100,8 @@ def restate():
         d(lib, "orc_pages_give", None, vp, i64, vp)
         d(lib, "orc_pages_available", i64, vp)
         d(lib, "orc_scatter_ref", None, C.POINTER(OrcShape), vp, i64, vp, vp, i64, i64, vp, i64, i64, C.c_int)
+        d(lib, "orc_scatter_ref_layout", None, C.POINTER(OrcShape), vp, i64, vp, vp, i64, i64, vp, i64, i64, C.c_int,
+          C.c_int)
         d(lib, "orc_mix64", u64, u64)
         d(lib, "orc_synth_word", u64, u64, u64)
         d(lib, "orc_synth_fill", None, u64, u64, u64, vp, C.c_int)
@@ -199,8 +201,10 @@ def ref_drain_order(q, policy, models, cfg) -> np.ndarray:
 
 
 def scatter_ref(shape, pool: np.ndarray, items: np.ndarray, block_table: np.ndarray, num_pages: int,
-                layer_lo: int = 0, layer_hi=None, threads: int = 1, arena: np.ndarray = None) -> np.ndarray:
-    """items: structured array (src_slot i64, bt_row i32, chunk_index i32)."""
+                layer_lo: int = 0, layer_hi=None, threads: int = 1, arena: np.ndarray = None,
+                layout: int = 0) -> np.ndarray:
+    """items: structured array (src_slot i64, bt_row i32, chunk_index i32).  layout: 0 flash-attn,
+    1 FlashInfer NHD, 2 FlashInfer HND (orc_scatter_ref_layout)."""
     layer_hi = shape.layers if layer_hi is None else layer_hi
     hl = shape.kv_heads // shape.tp_size
     layer_bytes = 2 * num_pages * shape.page_tokens * hl * shape.head_dim * shape.dtype_bytes
@@ -209,8 +213,8 @@ def scatter_ref(shape, pool: np.ndarray, items: np.ndarray, block_table: np.ndar
     s = OrcShape(shape.layers, shape.kv_heads, shape.head_dim, shape.dtype_bytes, shape.chunk_tokens,
                  shape.page_tokens, shape.tp_size, shape.tp_rank)
     bt = np.ascontiguousarray(block_table, np.int32)
-    restate().orc_scatter_ref(C.byref(s), pool.ctypes.data, len(items), items.ctypes.data, bt.ctypes.data,
-                              bt.shape[1], num_pages, arena.ctypes.data, layer_lo, layer_hi, threads)
+    restate().orc_scatter_ref_layout(C.byref(s), pool.ctypes.data, len(items), items.ctypes.data, bt.ctypes.data,
+                                     bt.shape[1], num_pages, arena.ctypes.data, layer_lo, layer_hi, threads, layout)
     return arena
 
 

@@ -327,10 +327,14 @@ int64_t orc_pages_available(const orc_pages* p) { return p->len; }
 /* the chunk layout [L][2][C][H][D] into the paged layout [L][2][pages][P][Hl][D] */
 /* through block_table.  TP rank r keeps heads [r*Hl, (r+1)*Hl).               */
 /* ------------------------------------------------------------------------ */
-void orc_scatter_ref(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,
-                     const orc_ingest_item* items, const int32_t* block_table,
-                     int64_t bt_stride, int64_t num_pages, uint8_t* arena, int64_t layer_lo,
-                     int64_t layer_hi, int threads) {
+/* layout (the consumer's KV-cache layout, installed vLLM 0.22):                 */
+/*   0 flash-attn   layer = [2][pages][P][Hl][D]  (v1/attention/backends/flash_attn.py:140-149) */
+/*   1 FlashInfer   layer = [pages][2][P][Hl][D]  (flashinfer.py:357-368, NHD order :380-381)  */
+/*   2 FlashInfer   layer = [pages][2][Hl][P][D]  (HND stride order, flashinfer.py:385-386)    */
+void orc_scatter_ref_layout(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,
+                            const orc_ingest_item* items, const int32_t* block_table,
+                            int64_t bt_stride, int64_t num_pages, uint8_t* arena, int64_t layer_lo,
+                            int64_t layer_hi, int threads, int layout) {
   const int64_t L = s->layers, H = s->kv_heads, D = s->head_dim, E = s->dtype_bytes;
   const int64_t C = s->chunk_tokens, P = s->page_tokens;
   const int64_t Hl = H / s->tp_size, h0 = s->tp_rank * Hl;
@@ -347,9 +351,15 @@ void orc_scatter_ref(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items
     for (int64_t kv = 0; kv < 2; ++kv) {
       for (int64_t j = 0; j < ppc; ++j) {
         const int64_t page = block_table[it.bt_row * bt_stride + it.chunk_index * ppc + j];
-        uint8_t* dst = arena + (((l * 2 + kv) * num_pages + page) * P) * run;
+        const int64_t seg = P * run; /* one (layer, K|V, page) unit */
+        uint8_t* dst = arena + l * 2 * num_pages * seg +
+                       (layout == 0 ? (kv * num_pages + page) * seg : (page * 2 + kv) * seg);
         const uint8_t* src = chunk + ((l * 2 + kv) * C + j * P) * row + h0 * D * E;
-        if (run == row) {
+        if (layout == 2) { /* [Hl][P][D]: head h's row of token t */
+          for (int64_t h = 0; h < Hl; ++h)
+            for (int64_t t = 0; t < P; ++t)
+              memcpy(dst + (h * P + t) * D * E, src + t * row + h * D * E, (size_t)(D * E));
+        } else if (run == row) {
           memcpy(dst, src, (size_t)(P * row));
         } else {
           for (int64_t t = 0; t < P; ++t) memcpy(dst + t * run, src + t * row, (size_t)run);
@@ -357,6 +367,14 @@ void orc_scatter_ref(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items
       }
     }
   }
+}
+
+void orc_scatter_ref(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,
+                     const orc_ingest_item* items, const int32_t* block_table,
+                     int64_t bt_stride, int64_t num_pages, uint8_t* arena, int64_t layer_lo,
+                     int64_t layer_hi, int threads) {
+  orc_scatter_ref_layout(s, pool, n_items, items, block_table, bt_stride, num_pages, arena, layer_lo,
+                         layer_hi, threads, 0);
 }
 
 /* ------------------------------------------------------------------------ */

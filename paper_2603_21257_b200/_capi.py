@@ -178,6 +178,8 @@ _decl("tsb_l1_release_request", st, vp, i64, P(Grant), i64, P(i64))
 for _n in ("reserved", "capacity", "deferred", "free_pages", "num_pages", "page_bytes", "block_table_stride"):
     _decl(f"tsb_l1_{_n}", i64, vp)
 _decl("tsb_l1_arena", vp, vp)
+_decl("tsb_l1_set_layout", st, vp, C.c_int)
+_decl("tsb_l1_layout", C.c_int, vp)
 _decl("tsb_l1_layer_ptr", vp, vp, i64)
 _decl("tsb_l1_block_table_host", vp, vp)
 _decl("tsb_l1_block_table_device", vp, vp)

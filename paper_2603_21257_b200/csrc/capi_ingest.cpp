@@ -303,6 +303,7 @@ struct tsb_l1 {
   int64_t num_pages = 0;
   int64_t page_bytes = 0;  // local bytes of one page across all layers (K and V)
   int64_t ppc = 0;         // pages per chunk
+  int layout = TSB_LAYOUT_FLASH_ATTN;
   tsb::Ledger ledger{2, 1};  // TierLedger(L1) byte accounting; capacity = pages * page_bytes
   // FIFO free list of page ids
   std::vector<int32_t> ring;
@@ -514,6 +515,16 @@ tsb_status tsb_l1_release_request(tsb_l1* l, int64_t request_id, tsb_grant* out,
   return TSB_OK;
 }
 
+tsb_status tsb_l1_set_layout(tsb_l1* l, int layout) {
+  if (layout < TSB_LAYOUT_FLASH_ATTN || layout > TSB_LAYOUT_FLASHINFER_HND)
+    return fail(TSB_VALIDATION, "l1: unknown layout " + std::to_string(layout));
+  if (l->ledger.reserved() != 0 || l->ledger.deferred() != 0)
+    return fail(TSB_VALIDATION, "l1: the page layout can only change while nothing is reserved");
+  l->layout = layout;
+  return TSB_OK;
+}
+int tsb_l1_layout(const tsb_l1* l) { return l->layout; }
+
 int64_t tsb_l1_reserved(const tsb_l1* l) { return l->ledger.reserved(); }
 int64_t tsb_l1_capacity(const tsb_l1* l) { return l->ledger.capacity(); }
 int64_t tsb_l1_deferred(const tsb_l1* l) { return l->ledger.deferred(); }
@@ -571,7 +582,7 @@ namespace {
 cudaError_t launch_scatter(const tsb::IngestGeom& g, const uint8_t* src, uint8_t* arena,
                            const tsb_ingest_item* items, const int32_t* bt, int64_t n,
                            cudaStream_t st) {
-  if (g_knobs.scatter_impl == 1 && g.seg_bytes * 2 <= tsb::kBulkSmem)
+  if (g_knobs.scatter_impl == 1 && g.seg_bytes * 2 <= tsb::kBulkSmem && !g.hnd)
     return tsb::launch_ingest_bulk(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st);
   return tsb::launch_ingest_ldg(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st, true);
 }
@@ -594,8 +605,16 @@ tsb::IngestGeom make_geom(const tsb_l1* l, int64_t layer_lo, int64_t layer_hi) {
   g.ppc = l->ppc;
   g.seg_bytes = g.P * g.run;
   g.num_pages = l->num_pages;
-  g.kv_dst = l->num_pages * g.seg_bytes;
-  g.layer_dst = 2 * g.kv_dst;
+  g.layer_dst = 2 * l->num_pages * g.seg_bytes;
+  if (l->layout == TSB_LAYOUT_FLASH_ATTN) {  // [2][pages][P][H][D]
+    g.kv_dst = l->num_pages * g.seg_bytes;
+    g.page_dst = g.seg_bytes;
+  } else {                                   // [pages][2][P][H][D] or [pages][2][H][P][D]
+    g.kv_dst = g.seg_bytes;
+    g.page_dst = 2 * g.seg_bytes;
+  }
+  g.head_bytes = s.head_dim * s.dtype_bytes;
+  g.hnd = l->layout == TSB_LAYOUT_FLASHINFER_HND ? 1 : 0;
   g.bt_stride = l->stride;
   g.layer_lo = static_cast<int32_t>(layer_lo);
   g.n_layers = static_cast<int32_t>(layer_hi - layer_lo);
@@ -791,6 +810,8 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
     } else {
       if (g.seg_bytes * 2 > tsb::kBulkSmem)
         return fail(TSB_UNSUPPORTED, "ingest bulk: page segment too large for the smem ring");
+      if (g.hnd)
+        return fail(TSB_UNSUPPORTED, "ingest bulk: HND pages need a per-head transpose; use zerocopy or ce");
       // The K1b ring fills an SM's shared memory: one resident CTA per SM.
       int sms = 148;
       if (on_device) TSB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, l->device));

@@ -37,15 +37,25 @@ __device__ __forceinline__ SegAddr seg_addr(const IngestGeom& g, const uint8_t* 
                                 : it.src_slot * g.chunk_bytes + g.layer_lo * g.layer_src;
   a.src = src + base + l * g.layer_src + kv * g.kv_src + j * g.P * g.row + g.head_off;
   a.dst = arena + (g.layer_lo + l) * g.layer_dst + kv * g.kv_dst +
-          static_cast<int64_t>(page) * g.seg_bytes;
+          static_cast<int64_t>(page) * g.page_dst;
   a.ok = page >= 0 && page < g.num_pages;
   return a;
+}
+
+// Destination byte offset of 16-byte vector v of a segment (P token rows of vpr vectors): NHD
+// pages keep the source order; HND pages ([H_local][P][D]) move each head's row of token t to
+// head * P * D*E + t * D*E.
+template <bool kHnd>
+__device__ __forceinline__ int64_t seg_dst_off(const IngestGeom& g, int v, int vpr) {
+  if (!kHnd) return static_cast<int64_t>(v) * 16;
+  const int64_t t = v / vpr, b = static_cast<int64_t>(v % vpr) * 16;
+  return (b / g.head_bytes) * g.P * g.head_bytes + t * g.head_bytes + b % g.head_bytes;
 }
 
 // K1 / K2: one warp per segment, 16-byte streaming loads, U loads in flight per lane before
 // the stores.  Source may be mapped host memory (K1, zero-copy over PCIe) or an HBM staging
 // buffer (K2).
-template <bool kContig, int U>
+template <bool kContig, int U, bool kHnd>
 __global__ void __launch_bounds__(256) k_ingest_ldg(IngestGeom g, const uint8_t* __restrict__ src,
                                                     uint8_t* __restrict__ arena,
                                                     const tsb_ingest_item* __restrict__ items,
@@ -73,7 +83,7 @@ __global__ void __launch_bounds__(256) k_ingest_ldg(IngestGeom g, const uint8_t*
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32;
-        if (v < nvec) st_stream(a.dst + static_cast<int64_t>(v) * 16, buf[u]);
+        if (v < nvec) st_stream(a.dst + seg_dst_off<kHnd>(g, v, vpr), buf[u]);
       }
     }
   }
@@ -169,8 +179,18 @@ __global__ void k_verify_synth(IngestGeom g, const uint8_t* __restrict__ arena,
       continue;
     }
     const int64_t src_off = reinterpret_cast<int64_t>(a.src);  // src base was nullptr
+    const int64_t words_per_head = g.head_bytes / 8;
     for (int64_t w = threadIdx.x; w < words; w += blockDim.x) {
-      const int64_t t = w / words_per_run, c = w % words_per_run;
+      // destination word w -> (token t, word c of this rank's run)
+      int64_t t, c;
+      if (g.hnd) {
+        const int64_t h = w / (g.P * words_per_head), r = w % (g.P * words_per_head);
+        t = r / words_per_head;
+        c = h * words_per_head + r % words_per_head;
+      } else {
+        t = w / words_per_run;
+        c = w % words_per_run;
+      }
       const uint64_t expect =
           synth_word(seed, static_cast<uint64_t>(src_off + t * g.row + c * 8) / 8);
       bad += reinterpret_cast<const uint64_t*>(a.dst)[w] != expect;
@@ -178,6 +198,24 @@ __global__ void k_verify_synth(IngestGeom g, const uint8_t* __restrict__ arena,
   }
   for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
+}
+
+template <bool kHnd>
+void launch_ldg_variant(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
+                        const tsb_ingest_item* items, const int32_t* bt, int64_t nseg, int grid,
+                        cudaStream_t st, bool hbm_source) {
+  const bool contig = g.run == g.row;
+  if (hbm_source) {
+    if (contig)
+      k_ingest_ldg<true, 4, kHnd><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+    else
+      k_ingest_ldg<false, 4, kHnd><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+  } else {
+    if (contig)
+      k_ingest_ldg<true, 8, kHnd><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+    else
+      k_ingest_ldg<false, 8, kHnd><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
+  }
 }
 
 }  // namespace
@@ -190,18 +228,10 @@ cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* 
   // Loads in flight per lane: 8 over the host link (microsecond latency, 64 CTAs); 4 from HBM,
   // where the sweep (profiles/r01_k1_sweep.jsonl) peaks with 4 loads per lane and a 32-CTA-per-
   // SM grid: 6.54-6.63 TB/s for full-head segments (U=8: 6.06-6.10 at 1184 CTAs).
-  const bool contig = g.run == g.row;
-  if (hbm_source) {
-    if (contig)
-      k_ingest_ldg<true, 4><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
-    else
-      k_ingest_ldg<false, 4><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
-  } else {
-    if (contig)
-      k_ingest_ldg<true, 8><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
-    else
-      k_ingest_ldg<false, 8><<<grid, 256, 0, st>>>(g, src, arena, items, bt, nseg);
-  }
+  if (g.hnd)
+    launch_ldg_variant<true>(g, src, arena, items, bt, nseg, grid, st, hbm_source);
+  else
+    launch_ldg_variant<false>(g, src, arena, items, bt, nseg, grid, st, hbm_source);
   count_launch();
   return cudaGetLastError();
 }

@@ -21,8 +21,11 @@ struct IngestGeom {
   int64_t ppc;          // pages per chunk (C/P)
   int64_t seg_bytes;    // P*run
   int64_t num_pages;
-  int64_t kv_dst;       // num_pages*seg_bytes
-  int64_t layer_dst;    // 2*kv_dst
+  int64_t kv_dst;       // K -> V plane stride of the destination (layout-dependent)
+  int64_t page_dst;     // page stride of the destination (layout-dependent)
+  int64_t layer_dst;    // 2*num_pages*seg_bytes
+  int64_t head_bytes;   // D*E: one head's row inside a page
+  int32_t hnd;          // 1: pages are [H_local][P][D] (TSB_LAYOUT_FLASHINFER_HND), else [P][H_local][D]
   int64_t bt_stride;    // block_table row stride (int32 entries)
   int32_t layer_lo;     // first layer of the launch
   int32_t n_layers;     // layers in the launch

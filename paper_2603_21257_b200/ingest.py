@@ -21,6 +21,10 @@ from .tiersim import Tier, check
 
 ZEROCOPY, BULK, CE, AUTO = capi.INGEST_ZEROCOPY, capi.INGEST_BULK, capi.INGEST_CE, capi.INGEST_AUTO
 MODES = {"auto": AUTO, "zerocopy": ZEROCOPY, "bulk": BULK, "ce": CE}
+# Page layouts of the L1 arena (tsb_kv_layout): the consumer's KV-cache layout.
+LAYOUT_FLASH_ATTN, LAYOUT_FLASHINFER_NHD, LAYOUT_FLASHINFER_HND = 0, 1, 2
+LAYOUTS = {"flash_attn": LAYOUT_FLASH_ATTN, "flashinfer_nhd": LAYOUT_FLASHINFER_NHD,
+           "flashinfer_hnd": LAYOUT_FLASHINFER_HND}
 
 
 @dataclass(frozen=True)
@@ -186,7 +190,7 @@ class PagedKVCache:
     free list, written into the request's block_table row."""
 
     def __init__(self, shape: KVShape, num_pages: int, max_rows: int, max_chunks: int, device: int = 0,
-                 arena: Optional[torch.Tensor] = None):
+                 arena: Optional[torch.Tensor] = None, layout: int = 0):
         self.shape = shape
         self.device = device
         self.num_pages = num_pages
@@ -204,6 +208,9 @@ class PagedKVCache:
         self.max_rows, self.max_chunks = max_rows, max_chunks
         self.stride = lib.tsb_l1_block_table_stride(h)
         self.page_bytes = lib.tsb_l1_page_bytes(h)
+        if layout != LAYOUT_FLASH_ATTN:
+            check(lib.tsb_l1_set_layout(h, int(layout)))
+        self.layout = layout
 
     @property
     def handle(self):
@@ -253,10 +260,15 @@ class PagedKVCache:
         check(lib.tsb_l1_sync_block_table(self._h, _stream(stream)))
 
     def layer(self, layer: int, dtype=torch.bfloat16) -> torch.Tensor:
-        """vLLM flash-attn view of one layer: [2, num_pages, page_tokens, heads_local, head_dim]."""
+        """One layer in the consumer's layout: flash-attn [2, pages, P, H_local, D]; FlashInfer NHD
+        [pages, 2, P, H_local, D]; FlashInfer HND [pages, 2, H_local, P, D]."""
         s = self.shape
-        t = self.arena[layer * self.layer_bytes:(layer + 1) * self.layer_bytes]
-        return t.view(dtype).view(2, self.num_pages, s.page_tokens, s.heads_local, s.head_dim)
+        t = self.arena[layer * self.layer_bytes:(layer + 1) * self.layer_bytes].view(dtype)
+        if self.layout == LAYOUT_FLASHINFER_NHD:
+            return t.view(self.num_pages, 2, s.page_tokens, s.heads_local, s.head_dim)
+        if self.layout == LAYOUT_FLASHINFER_HND:
+            return t.view(self.num_pages, 2, s.heads_local, s.page_tokens, s.head_dim)
+        return t.view(2, self.num_pages, s.page_tokens, s.heads_local, s.head_dim)
 
 
 def items_numpy(src_slot, bt_row, chunk_index) -> np.ndarray:

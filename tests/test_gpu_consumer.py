@@ -23,13 +23,17 @@ def _reference_attention(q, k, v):
     return torch.einsum("ht,thd->hd", torch.softmax(s, dim=-1), v)
 
 
-@pytest.mark.parametrize("mode", ["ce", "bulk"])
-def test_flashinfer_paged_decode_reads_ingested_pages(mode):
+@pytest.mark.parametrize("mode,layout", [("ce", "flash_attn"), ("bulk", "flash_attn"), ("ce", "flashinfer_nhd"),
+                                         ("zerocopy", "flashinfer_nhd"), ("ce", "flashinfer_hnd"),
+                                         ("zerocopy", "flashinfer_hnd")])
+def test_flashinfer_paged_decode_reads_ingested_pages(mode, layout):
+    """flash_attn: K and V planes passed as a (k, v) tuple; FlashInfer NHD / HND: the layer tensor
+    [pages, 2, P, H, D] / [pages, 2, H, P, D] passed as is with kv_layout NHD / HND."""
     flashinfer = pytest.importorskip("flashinfer")
     shape = ingest.KVShape(layers=2, kv_heads=8, head_dim=128)
     pool = ingest.ChunkPool(shape, 12)
     pool.fill_synthetic(31)
-    l1 = ingest.PagedKVCache(shape, num_pages=400, max_rows=4, max_chunks=8)
+    l1 = ingest.PagedKVCache(shape, num_pages=400, max_rows=4, max_chunks=8, layout=ingest.LAYOUTS[layout])
     cb = shape.page_bytes * shape.pages_per_chunk
     rng = np.random.default_rng(0)
     plans = {1: [5, 2, 9], 2: [0, 1], 3: [7, 8, 3, 11]}  # request -> pool slots of its chunks
@@ -59,12 +63,13 @@ def test_flashinfer_paged_decode_reads_ingested_pages(mode):
     chunks = chunks.view(pool.n_slots, shape.layers, 2, 256, 8, 128)
     workspace = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
     for layer in range(shape.layers):
-        kv = l1.layer(layer)  # [2, pages, 16, 8, 128] bf16 (vLLM flash-attn layout)
-        wrapper = flashinfer.BatchDecodeWithPagedKVCacheWrapper(workspace, "NHD")
+        kv = l1.layer(layer)
+        kv_layout = "HND" if layout == "flashinfer_hnd" else "NHD"
+        wrapper = flashinfer.BatchDecodeWithPagedKVCacheWrapper(workspace, kv_layout)
         wrapper.plan(indptr_t, indices_t, last_t, hq, 8, 128, 16, pos_encoding_mode="NONE",
                      q_data_type=torch.bfloat16, kv_data_type=torch.bfloat16)
         q = (torch.randn(len(plans), hq, 128, generator=torch.Generator().manual_seed(layer)) * 0.05).to(dev, torch.bfloat16)
-        out = wrapper.run(q, (kv[0], kv[1]))
+        out = wrapper.run(q, (kv[0], kv[1]) if layout == "flash_attn" else kv)
         for b, (rid, slots) in enumerate(plans.items()):
             src = chunks[slots, layer]  # [n_chunks, 2, 256, 8, 128]
             k = src[:, 0].reshape(-1, 8, 128).to(dev)

@@ -433,6 +433,44 @@ def test_ingest_sparse_layer_events(oracle, mode):
     assert np.array_equal(l1.arena.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("layout", ["flashinfer_nhd", "flashinfer_hnd"])
+@pytest.mark.parametrize("mode", ["zerocopy", "bulk", "ce", "auto"])
+@pytest.mark.parametrize("tp", [(1, 0), (2, 1), (8, 6)])
+def test_ingest_layouts_bit_exact(oracle, layout, mode, tp):
+    """The consumer's page layout (vLLM FlashInfer NHD / HND): same pages, permuted addresses."""
+    lay = ingest.LAYOUTS[layout]
+    shape = SMALL.with_rank(*tp)
+    pool = ingest.ChunkPool(SMALL, 8)
+    pool.fill_synthetic(17)
+    num_pages = 200
+    arena = torch.zeros(shape.layers * 2 * num_pages * 16 * shape.heads_local * 128 * 2, dtype=torch.uint8,
+                        device="cuda")
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=2, max_chunks=12, arena=arena, layout=lay)
+    rows = [l1.request(5, c, shape.page_bytes * 16)[1] for c in range(7)]
+    l1.sync_block_table()
+    items = ingest.items_numpy([3, 4, 5, 6, 0, 1, 7], rows, range(7))
+    if mode == "bulk" and lay == ingest.LAYOUT_FLASHINFER_HND:
+        with pytest.raises(t.Unsupported):
+            ingest.ingest(l1, pool, items, mode=ingest.BULK)
+        return
+    ingest.ingest(l1, pool, items, mode=ingest.MODES[mode])
+    torch.cuda.synchronize()
+    want = oracle.scatter_ref(shape, pool.slot_view(0, 8), items, l1.block_table(), num_pages, layout=lay)
+    assert np.array_equal(arena.cpu().numpy(), want)
+    assert ingest.verify_synthetic(l1, pool, items, seed=17) == 0
+    assert tuple(l1.layer(0).shape)[:2] == (num_pages, 2)
+
+
+def test_layout_fixed_once_reserved():
+    l1 = ingest.PagedKVCache(SMALL, 64, max_rows=1, max_chunks=2)
+    l1.request(1, 0, SMALL.page_bytes * 16)
+    with pytest.raises(t.ValidationError):
+        t.check(_capi.lib.tsb_l1_set_layout(l1.handle, ingest.LAYOUT_FLASHINFER_NHD))
+    l1.release_request(1)
+    t.check(_capi.lib.tsb_l1_set_layout(l1.handle, ingest.LAYOUT_FLASHINFER_HND))
+    assert _capi.lib.tsb_l1_layout(l1.handle) == ingest.LAYOUT_FLASHINFER_HND
+
+
 def test_auto_mode_resolution():
     """AUTO: host pool + full heads -> CE; head-sharded -> CE when consecutive-slot runs carry
     >= 3.1 MB per strided copy, else K1; device pool or device items -> K1 (zero-copy kernel)."""

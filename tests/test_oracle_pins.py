@@ -234,8 +234,9 @@ def test_prefix_hash_properties():
     assert lib.orc_chain(1, 2) != lib.orc_chain(2, 1)
 
 
-def _numpy_scatter(shape, pool_chunks, items, bt, num_pages, layer_lo, layer_hi):
-    """Independent numpy statement of the layouts: chunk [L][2][C][H][D] -> pages [L][2][N][P][Hl][D]."""
+def _numpy_scatter(shape, pool_chunks, items, bt, num_pages, layer_lo, layer_hi, layout=0):
+    """Independent numpy statement of the layouts: chunk [L][2][C][H][D] -> pages [L][2][N][P][Hl][D]
+    (flash-attn), then permuted per layer to FlashInfer NHD [N][2][P][Hl][D] or HND [N][2][Hl][P][D]."""
     L, H, D, C_, P = shape.layers, shape.kv_heads, shape.head_dim, shape.chunk_tokens, shape.page_tokens
     hl = H // shape.tp_size
     h0 = shape.tp_rank * hl
@@ -246,11 +247,16 @@ def _numpy_scatter(shape, pool_chunks, items, bt, num_pages, layer_lo, layer_hi)
         for j in range(C_ // P):
             page = bt[row, chunk * (C_ // P) + j]
             arena[layer_lo:layer_hi, :, page] = src[layer_lo:layer_hi, :, j]
+    if layout == 1:
+        arena = np.ascontiguousarray(arena.transpose(0, 2, 1, 3, 4, 5))
+    elif layout == 2:
+        arena = np.ascontiguousarray(arena.transpose(0, 2, 1, 4, 3, 5))
     return arena.view(np.uint8).reshape(-1)
 
 
+@pytest.mark.parametrize("layout", [0, 1, 2])
 @pytest.mark.parametrize("tp", [(1, 0), (2, 1), (4, 2), (8, 7)])
-def test_scatter_ref_matches_numpy_layout_statement(tp):
+def test_scatter_ref_matches_numpy_layout_statement(tp, layout):
     class S:
         layers, kv_heads, head_dim, dtype_bytes, chunk_tokens, page_tokens = 3, 8, 16, 2, 64, 16
         tp_size, tp_rank = tp
@@ -267,6 +273,6 @@ def test_scatter_ref_matches_numpy_layout_statement(tp):
     items = np.array([(4, 0, 0), (1, 0, 1), (0, 2, 1), (2, 2, 2), (2, 2, 3)],
                      dtype=[("src_slot", np.int64), ("bt_row", np.int32), ("chunk_index", np.int32)])
     for lo, hi in ((0, 3), (1, 2)):
-        got = po.scatter_ref(s, pool, items, bt, num_pages, lo, hi)
-        want = _numpy_scatter(s, pool, [tuple(x) for x in items], bt, num_pages, lo, hi)
+        got = po.scatter_ref(s, pool, items, bt, num_pages, lo, hi, layout=layout)
+        want = _numpy_scatter(s, pool, [tuple(x) for x in items], bt, num_pages, lo, hi, layout)
         assert np.array_equal(got, want)
