@@ -116,6 +116,7 @@ def make_pool(shape_full, n_slots, world, rank, dist, seed):
             if rank == 0:
                 pool.fill_synthetic(seed)
             dist.barrier()
+            seg.unlink()  # every rank has mapped and registered it: nothing outlives the run
             return pool, "shared /dev/shm segment, cudaHostRegister'ed by every rank", shape_full.with_rank(world, rank)
         local = ingest.KVShape(shape_full.layers, shape_full.kv_heads // world, shape_full.head_dim,
                                shape_full.dtype_bytes, shape_full.chunk_tokens, shape_full.page_tokens)
@@ -127,11 +128,16 @@ def make_pool(shape_full, n_slots, world, rank, dist, seed):
     return pool, "cudaHostAlloc portable|mapped", shape_full
 
 
+def coll_device(dist) -> str:
+    """Device of the tensors the timing/agreement collectives use: CUDA under NCCL, host under gloo."""
+    return "cpu" if dist is not None and dist.get_backend() == "gloo" else "cuda"
+
+
 def torch_tensor_flag(flag: bool, dist) -> bool:
     """All ranks agree on a boolean (logical AND over ranks)."""
     import torch
 
-    t = torch.tensor([1 if flag else 0], device="cuda")
+    t = torch.tensor([1 if flag else 0], device=coll_device(dist))
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     return bool(t.item())
 
@@ -337,8 +343,15 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as tdist
 
+        # TSB_BENCH_ONE_DEVICE=1 (a validation mode, not a measurement): every rank on cuda:0 over
+        # gloo, to exercise the multi-rank path (shared pool, head shards, reductions) on one GPU.
+        one_dev = os.environ.get("TSB_BENCH_ONE_DEVICE") == "1"
+        local = 0 if one_dev else local
         torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
     else:
         torch.cuda.set_device(0)
@@ -395,7 +408,8 @@ def run_ours(args):
             if i == 0 and r.stats["verify_mismatches"]:
                 raise SystemExit(f"ingest parity failure (HBM pool): {r.stats['verify_mismatches']} words")
         d_s, d_wall, d_res, d_launch, d_clk = timed_steps(torch, run_dev, args.steps, dist, _capi)
-        d_s, d_wall, d_bytes = reduce_timing(dist, d_s, d_wall, float(d_res.stats["bytes"]), device="cuda")
+        d_s, d_wall, d_bytes = reduce_timing(dist, d_s, d_wall, float(d_res.stats["bytes"]),
+                                             device=coll_device(dist))
         k1_items = max_chunks
         k1_alg, k1_s = measure_k1_hbm(torch, l1, dpool, shape, k1_items)
         hbm = dict(dev_s=d_s, bytes=d_bytes, launches=d_launch, clocks=d_clk, stats=d_res.stats,
@@ -411,7 +425,7 @@ def run_ours(args):
             raise SystemExit(f"ingest parity failure: {r.stats['verify_mismatches']} mismatching words")
     h_s, wall_s, results, h_launch, h_clk = timed_steps(torch, run_host, args.steps, dist, _capi)
     local_bytes = results.stats["bytes"]
-    h_s, wall_s, total_bytes = reduce_timing(dist, h_s, wall_s, float(local_bytes), device="cuda")
+    h_s, wall_s, total_bytes = reduce_timing(dist, h_s, wall_s, float(local_bytes), device=coll_device(dist))
     host_dev_rate = args.steps * total_bytes / h_s / 1e9
     e2e = args.steps * total_bytes / wall_s / 1e9
 

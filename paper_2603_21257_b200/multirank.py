@@ -67,6 +67,12 @@ class SharedSegment:
 
         return ctypes.addressof(ctypes.c_char.from_buffer(self.mm))
 
+    def unlink(self):
+        """Rank 0 removes the /dev/shm name once every rank has mapped it: the mappings stay valid
+        and the memory is returned when the last process exits, so no segment outlives the run."""
+        if self.rank == 0 and os.path.exists(self.path):
+            os.unlink(self.path)
+
     def close(self, unlink: bool = False):
         try:
             self.mm.close()

@@ -36,6 +36,9 @@ def _worker(rank, world, port, q):
         if rank == 0:
             view[:] = po.synth_fill(3, 0, nbytes // 8).view(np.uint8)
         dist.barrier()
+        seg.unlink()  # every rank has mapped it: the name goes, the mappings stay
+        dist.barrier()
+        assert not os.path.exists(seg.path)
         assert np.array_equal(view[:64], po.synth_fill(3, 0, 8).view(np.uint8))
 
         # each rank scatters its head slice; identical block tables on every rank
