@@ -282,14 +282,16 @@ def timed_steps(torch, run, steps, dist, capi):
     bracketed by a barrier + synchronize on both sides.  Returns (device s, wall s, last result,
     kernel launches, clocks)."""
     dev = torch.cuda.current_device()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = capi.lib.tsb_kernel_launch_count()
     walls, results = [], None
+    # The sampler starts (and delivers its first sample) before the barrier, so every rank leaves
+    # the barrier straight into its timed region: no start skew between ranks.
     with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        launches0 = capi.lib.tsb_kernel_launch_count()
         ev0.record(s)
         for _ in range(steps):
             t0 = time.perf_counter()
