@@ -257,7 +257,7 @@ struct tsb_scorer {
   uint64_t *kp = nullptr, *ka = nullptr, *ki = nullptr, *kp2 = nullptr, *ka2 = nullptr,
            *ki2 = nullptr;
   int64_t *idx = nullptr, *idx2 = nullptr;
-  unsigned long long* err = nullptr;       // [0] missing deadline, [1] NaN key (device)
+  unsigned long long* err = nullptr;       // [0] missing deadline, [1] NaN key, [2] keys sorted (device)
   unsigned long long* err_host = nullptr;  // pinned readback
   int policy = 0;
   const int64_t* last_ids = nullptr;  // device ids of the last scored queue (messages)
@@ -335,7 +335,7 @@ tsb_status tsb_scorer_create(int device, int64_t capacity, tsb_scorer** out) {
   TSB_CUDA_TRY(cudaSetDevice(device));
   auto* s = new tsb_scorer();
   s->device = device;
-  cudaError_t e = cudaMalloc(&s->err, 2 * sizeof(unsigned long long));
+  cudaError_t e = cudaMalloc(&s->err, 3 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMallocHost(&s->err_host, 2 * sizeof(unsigned long long));
   if (e != cudaSuccess) {
     scorer_free(s);
@@ -369,14 +369,14 @@ tsb_status tsb_score_queue_device(tsb_scorer* s, void* stream, int64_t n, const 
   auto st = static_cast<cudaStream_t>(stream);
   s->policy = policy;
   s->last_ids = q->id;
-  TSB_CUDA_TRY(cudaMemsetAsync(s->err, 0xff, 2 * sizeof(unsigned long long), st));
+  TSB_CUDA_TRY(cudaMemsetAsync(s->err, 0xff, 3 * sizeof(unsigned long long), st));
   tsb::ScoreParams p{policy, models[0], models[1], models[2], models[3], c->compute_quadratic,
                      c->block_size_tokens};
   TSB_CUDA_TRY(tsb::launch_score(n, *q, p, t_load, t_comp, primary, s->kp, s->ka, s->ki, s->err,
                                  s->err + 1, st));
   if (order)
     TSB_CUDA_TRY(tsb::launch_order(n, s->kp, s->ka, s->ki, s->idx, s->kp2, s->ka2, s->ki2,
-                                   s->idx2, order, st));
+                                   s->idx2, order, s->err + 2, st));
   if (err_index) return scorer_check_errors(s, st, err_index);
   return TSB_OK;
 }

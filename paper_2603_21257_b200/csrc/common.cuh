@@ -119,6 +119,34 @@ __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Programmatic dependent launch: a kernel launched with TSB_PDL may start (launch processing,
+// CTA rasterisation) while the previous kernel on the stream is finishing; pdl_wait() at its top
+// blocks until that kernel has completed and its writes are visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+#define TSB_PDL(kernel, grid, block, smem, st, ...)                                        \
+  do {                                                                                    \
+    const cudaError_t _e = ::tsb::launch_pdl(kernel, grid, block, smem, st, __VA_ARGS__); \
+    if (_e != cudaSuccess) return _e;                                                     \
+    count_launch();                                                                       \
+  } while (0)
+
 #endif  // __CUDACC__
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }

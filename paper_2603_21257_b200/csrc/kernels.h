@@ -64,10 +64,11 @@ cudaError_t launch_score(int64_t n, tsb_queue q, ScoreParams p, double* t_load, 
                          unsigned long long* err_missing, unsigned long long* err_nan,
                          cudaStream_t st);
 // Sorts (kp, ka, ki) ascending, producing the permutation in order_out.  Scratch must hold
-// 2 * n of each key array plus 2 * n int64 indices.
+// 2 * n of each key array plus 2 * n int64 indices.  *sorted (device) must be nonzero on entry;
+// it is cleared when the keys are not already in order (then the merge sort runs).
 cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, int64_t* idx,
                          uint64_t* kp2, uint64_t* ka2, uint64_t* ki2, int64_t* idx2,
-                         int64_t* order_out, cudaStream_t st);
+                         int64_t* order_out, unsigned long long* sorted, cudaStream_t st);
 
 // Prefix hasher (K3) and token generator.
 cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int32_t* tokens,

@@ -16,6 +16,8 @@
 // end of the CTA's output window with a 32-ary search over global memory, the window's inputs
 // are staged in shared memory, and each thread merges 4 outputs.  Latency-bound at 100K
 // requests (~3 MB of keys).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -155,7 +157,10 @@ __device__ __forceinline__ void merge_items(uint8_t* sb, int a, int alen, int b,
 __global__ void __launch_bounds__(kThreads, 1) k_tile_sort(
     int64_t n, const uint64_t* __restrict__ kp, const uint64_t* __restrict__ ka,
     const uint64_t* __restrict__ ki, uint64_t* __restrict__ okp, uint64_t* __restrict__ oka,
-    uint64_t* __restrict__ oki, int64_t* __restrict__ oidx, int64_t* __restrict__ order_out) {
+    uint64_t* __restrict__ oki, int64_t* __restrict__ oidx, int64_t* __restrict__ order_out,
+    const unsigned long long* __restrict__ sorted) {
+  pdl_wait();
+  if (*sorted) return;  // the queue is already in key order: k_iota_if_sorted writes the order
   extern __shared__ __align__(16) uint8_t sbuf[];
   const int t = threadIdx.x;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTileN;
@@ -233,7 +238,9 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_pass(
     int64_t n, int64_t width, const uint64_t* __restrict__ kp, const uint64_t* __restrict__ ka,
     const uint64_t* __restrict__ ki, const int64_t* __restrict__ idx, uint64_t* __restrict__ okp,
     uint64_t* __restrict__ oka, uint64_t* __restrict__ oki, int64_t* __restrict__ oidx,
-    int64_t* __restrict__ order_out) {
+    int64_t* __restrict__ order_out, const unsigned long long* __restrict__ sorted) {
+  pdl_wait();
+  if (*sorted) return;
   extern __shared__ __align__(16) uint8_t sbuf[];
   __shared__ int split[2];
   const int t = threadIdx.x, warp = t >> 5;
@@ -279,6 +286,30 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_pass(
   }
 }
 
+// Adaptive fast path: a queue whose records are already in key order (FIFO over an arrival-
+// ordered queue, the common case) needs no sort.  One pass clears *sorted on the first
+// out-of-order neighbour pair; the sort kernels then run only if it was cleared, and
+// k_iota_if_sorted writes the identity permutation otherwise.
+__global__ void k_check_sorted(int64_t n, const uint64_t* __restrict__ kp,
+                               const uint64_t* __restrict__ ka, const uint64_t* __restrict__ ki,
+                               unsigned long long* __restrict__ sorted) {
+  pdl_wait();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  bool ok = true;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i + 1 < n; i += stride)
+    ok &= rec_less(load_rec(kp, ka, ki, nullptr, i), load_rec(kp, ka, ki, nullptr, i + 1));
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *sorted = 0;
+}
+
+__global__ void k_iota_if_sorted(int64_t n, const unsigned long long* __restrict__ sorted,
+                                 int64_t* __restrict__ order_out) {
+  pdl_wait();
+  if (!*sorted) return;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    order_out[i] = i;
+}
+
 }  // namespace
 
 cudaError_t launch_score(int64_t n, tsb_queue q, ScoreParams p, double* t_load, double* t_comp,
@@ -294,8 +325,10 @@ cudaError_t launch_score(int64_t n, tsb_queue q, ScoreParams p, double* t_load, 
 
 cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, int64_t* idx,
                          uint64_t* kp2, uint64_t* ka2, uint64_t* ki2, int64_t* idx2,
-                         int64_t* order_out, cudaStream_t st) {
+                         int64_t* order_out, unsigned long long* sorted, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
+  const int check_grid = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), 148 * 4));
+  TSB_PDL(k_check_sorted, check_grid, 256, 0, st, n, kp, ka, ki, sorted);
   constexpr size_t kSmem = smem_bytes(kTileN);       // 68 KiB
   constexpr size_t kMergeSmem = smem_bytes(kMergeN);  // 34 KiB
   static std::atomic<uint64_t> attr{0};
@@ -309,25 +342,26 @@ cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, in
   }
   const int tiles = ceil_div(n, kTileN);
   if (tiles == 1) {
-    k_tile_sort<<<1, kThreads, kSmem, st>>>(n, kp, ka, ki, nullptr, nullptr, nullptr, nullptr,
-                                            order_out);
-    count_launch();
-    return cudaGetLastError();
-  }
-  k_tile_sort<<<tiles, kThreads, kSmem, st>>>(n, kp, ka, ki, kp2, ka2, ki2, idx2, nullptr);
-  count_launch();
+    TSB_PDL(k_tile_sort, 1, kThreads, kSmem, st, n, kp, ka, ki, nullptr, nullptr, nullptr, nullptr,
+            order_out, sorted);
+  } else {
+  TSB_PDL(k_tile_sort, tiles, kThreads, kSmem, st, n, kp, ka, ki, kp2, ka2, ki2, idx2, nullptr, sorted);
   uint64_t *sp = kp2, *sa = ka2, *si = ki2, *dp = kp, *da = ka, *di = ki;
   int64_t *sx = idx2, *dx = idx;
   for (int64_t width = kTileN; width < n; width *= 2) {
     const bool last = width * 2 >= n;
-    k_merge_pass<<<ceil_div(n, kMergeN), kMergeThreads, kMergeSmem, st>>>(
-        n, width, sp, sa, si, sx, dp, da, di, dx, last ? order_out : nullptr);
-    count_launch();
+    TSB_PDL(k_merge_pass, ceil_div(n, kMergeN), kMergeThreads, kMergeSmem, st, n, width,
+            static_cast<const uint64_t*>(sp), static_cast<const uint64_t*>(sa),
+            static_cast<const uint64_t*>(si), static_cast<const int64_t*>(sx), dp, da, di, dx,
+            last ? order_out : nullptr, static_cast<const unsigned long long*>(sorted));
     std::swap(sp, dp);
     std::swap(sa, da);
     std::swap(si, di);
     std::swap(sx, dx);
   }
+  }
+  TSB_PDL(k_iota_if_sorted, check_grid, 256, 0, st, n, static_cast<const unsigned long long*>(sorted),
+          order_out);
   return cudaGetLastError();
 }
 

@@ -140,6 +140,33 @@ def test_large_queue_matches_oracle(scorer, oracle, n, policy):
     assert np.array_equal(order, oracle.sort_order(opr, q.arrival, q.id))
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 2049, 100_000])
+@pytest.mark.parametrize("perturb", [None, "swap_last", "swap_first", "tie_ids"])
+def test_presorted_queue_fast_path(scorer, oracle, n, perturb):
+    """FIFO over an arrival-ordered queue is already in key order: K5 skips the merge sort
+    (k_check_sorted / k_iota_if_sorted).  One displaced pair must fall back to the full sort."""
+    q = random_queue(n, 7)
+    order_in = np.lexsort((q.id, q.arrival))
+    for name, _ in t.QueueArrays.FIELDS:
+        setattr(q, name, getattr(q, name)[order_in].copy())
+    if perturb == "swap_last" and n > 1:
+        q.arrival[[-1, -2]] = q.arrival[[-2, -1]]
+        q.id[[-1, -2]] = q.id[[-2, -1]]
+    elif perturb == "swap_first" and n > 1:
+        q.arrival[[0, 1]] = q.arrival[[1, 0]]
+        q.id[[0, 1]] = q.id[[1, 0]]
+    elif perturb == "tie_ids" and n > 2:
+        q.arrival[:3] = q.arrival[0]  # equal arrival: ids decide
+        q.id[:3] = q.id[:3][::-1].copy()
+    cfg = CFGS["default"]
+    m = t.cost_models_from_config(cfg)
+    _, _, pr, order = scorer.score(q, t.PolicyKind.Fifo, m, cfg)
+    want = oracle.sort_order(pr, q.arrival, q.id)
+    assert np.array_equal(order, want)
+    if perturb is None:
+        assert np.array_equal(order, np.arange(n))
+
+
 def test_signed_zero_and_infinite_keys_order(scorer, oracle):
     q = t.QueueArrays(4, id=np.array([4, 3, 2, 1]), arrival=np.array([0.0, -0.0, 0.0, 1.0]),
                       context_tokens=np.zeros(4, np.int64), query_tokens=np.ones(4, np.int64),
