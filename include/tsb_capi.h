@@ -358,7 +358,8 @@ typedef enum {
 } tsb_ingest_mode;
 
 /* items: host array (copied into a pinned ring internally, so it may be reused on return).
- * All grants for the items must already be in the block table (tsb_l1_sync_block_table). */
+ * All grants for the items must already be in the block table (tsb_l1_sync_block_table).
+ * VALIDATION if an item's slot, row or chunk index is outside the pool / block table. */
 tsb_status tsb_ingest(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
                       int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
                       void* const* layer_events);
@@ -368,7 +369,7 @@ tsb_status tsb_ingest_resolve_mode(const tsb_l1* l1, const tsb_pool* pool,
                                    const tsb_ingest_item* items, int64_t n_items, int mode,
                                    int* resolved);
 /* Device-items variant (items already in device memory; CE mode needs host items and returns
- * UNSUPPORTED here). */
+ * UNSUPPORTED here).  The items are not range-checked: the caller guarantees them. */
 tsb_status tsb_ingest_device(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items_dev,
                              int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
                              void* stream, void* const* layer_events);

@@ -860,6 +860,17 @@ tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, i
   const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb_ingest_item));
   if (n_items > per)
     return fail(TSB_VALIDATION, "ingest: at most " + std::to_string(per) + " items per call");
+  // Host items are checked before any device work: an out-of-range slot or row would make the
+  // kernels read outside the pool (a sticky fault for the context) instead of failing the call.
+  for (int64_t k = 0; k < n_items; ++k) {
+    const tsb_ingest_item& it = items[k];
+    if (it.src_slot < 0 || it.src_slot >= pool->slots || it.bt_row < 0 || it.bt_row >= l->rows ||
+        it.chunk_index < 0 || it.chunk_index >= l->max_chunks)
+      return fail(TSB_VALIDATION, "ingest: item " + std::to_string(k) + " (slot " +
+                                      std::to_string(it.src_slot) + ", row " + std::to_string(it.bt_row) +
+                                      ", chunk " + std::to_string(it.chunk_index) +
+                                      ") is outside the pool / block table");
+  }
   void* dptr = nullptr;
   int slot = 0;
   if (n_items > 0)

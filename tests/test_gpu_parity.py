@@ -640,6 +640,13 @@ def test_ingest_empty_and_bounds():
         ingest.ingest(l1, pool, items, 0, SMALL.layers + 1)
     with pytest.raises(t.ValidationError):
         l1.request(55, 12, SMALL.page_bytes * 16)  # chunk index beyond the block-table row
+    for field, bad in (("src_slot", pool.n_slots), ("src_slot", -1), ("bt_row", 4), ("chunk_index", 12)):
+        it = items[:2].copy()
+        it[field][1] = bad
+        with pytest.raises(t.ValidationError, match="outside the pool"):
+            ingest.ingest(l1, pool, it)
+    ingest.ingest(l1, pool, items)  # the context is still healthy
+    torch.cuda.synchronize()
 
 
 def test_hash_edge_lengths(oracle):
