@@ -363,6 +363,13 @@ typedef enum {
 tsb_status tsb_ingest(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
                       int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
                       void* const* layer_events);
+/* Two-tier ingest: an item with src_slot < 0 names slot ~src_slot of hbm_pool (a chunk already
+ * resident in this GPU's or a peer's HBM -- the peer-HBM tier that stands in for the L3->L2
+ * network stage, engine.cpp:405-425); the others name slots of pool.  The HBM-tier items are
+ * moved first (K1 at HBM / NVLink speed), then the rest with `mode`; layer_events cover both. */
+tsb_status tsb_ingest_tiered(tsb_l1* l1, tsb_pool* pool, tsb_pool* hbm_pool,
+                             const tsb_ingest_item* items, int64_t n_items, int64_t layer_lo,
+                             int64_t layer_hi, int mode, void* stream, void* const* layer_events);
 /* The kernel path tsb_ingest takes for these items and mode (AUTO resolved; other modes returned
  * as given).  items: host array or NULL (device items). */
 tsb_status tsb_ingest_resolve_mode(const tsb_l1* l1, const tsb_pool* pool,
@@ -454,6 +461,9 @@ typedef struct {
 
 tsb_status tsb_stage_create(tsb_l1* l1, tsb_pool* pool, tsb_stage** out);
 void tsb_stage_destroy(tsb_stage* s);
+/* HBM tier of the stage (NULL clears it): in tsb_stage_run / _online, a slot < 0 names slot ~slot
+ * of hbm_pool (same chunk geometry as the L2 pool); those chunks bypass the host link. */
+tsb_status tsb_stage_set_hbm_tier(tsb_stage* s, tsb_pool* hbm_pool);
 /* Runs one batch to completion (synchronises).  Request i's planned chunk c is stored in pool
  * slot slots[slot_offsets[i] + c]; slot_offsets has n+1 entries and each request must list
  * exactly derive_block_plan(spec_i).size() slots.  results may be NULL. */

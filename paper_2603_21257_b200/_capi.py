@@ -187,6 +187,7 @@ _decl("tsb_l1_sync_block_table", st, vp, vp)
 _decl("tsb_ingest", st, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_device", st, vp, vp, vp, i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_set_ce", st, C.c_int, i64)
+_decl("tsb_ingest_tiered", st, vp, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_resolve_mode", st, vp, vp, P(IngestItem), i64, C.c_int, P(C.c_int))
 _decl("tsb_ingest_set_scatter", st, C.c_int, C.c_int)
 _decl("tsb_scatter_device", st, vp, vp, vp, i64, i64, i64, vp)
@@ -195,6 +196,7 @@ _decl("tsb_l1_device", C.c_int, vp)
 _decl("tsb_l1_shape", st, vp, P(KvShape))
 _decl("tsb_stage_create", st, vp, vp, P(vp))
 _decl("tsb_stage_destroy", None, vp)
+_decl("tsb_stage_set_hbm_tier", st, vp, vp)
 _decl("tsb_stage_run", st, vp, i64, P(Queue), P(Cluster), P(f64), vp, vp, P(StageOptions), vp, P(StageRequest),
       P(StageStats))
 _decl("tsb_stage_trace", st, vp, P(TraceRow), i64, P(i64))

@@ -881,6 +881,32 @@ tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, i
   return TSB_OK;
 }
 
+tsb_status tsb_ingest_tiered(tsb_l1* l, tsb_pool* pool, tsb_pool* hbm_pool,
+                             const tsb_ingest_item* items, int64_t n_items, int64_t layer_lo,
+                             int64_t layer_hi, int mode, void* stream, void* const* layer_events) {
+  std::vector<tsb_ingest_item> host, tier;
+  for (int64_t k = 0; k < n_items; ++k) {
+    if (items[k].src_slot >= 0) {
+      host.push_back(items[k]);
+    } else {
+      if (!hbm_pool)
+        return fail(TSB_VALIDATION, "ingest: item " + std::to_string(k) +
+                                        " names the HBM tier (negative slot) but none is set");
+      tier.push_back(tsb_ingest_item{~items[k].src_slot, items[k].bt_row, items[k].chunk_index});
+    }
+  }
+  if (tier.empty())
+    return tsb_ingest(l, pool, host.data(), static_cast<int64_t>(host.size()), layer_lo, layer_hi,
+                      mode, stream, layer_events);
+  // The HBM tier goes first at HBM / NVLink speed, so the fences recorded by the host-tier call
+  // (same stream) cover both.
+  TSB_TRY(tsb_ingest(l, hbm_pool, tier.data(), static_cast<int64_t>(tier.size()), layer_lo,
+                     layer_hi, TSB_INGEST_AUTO, stream, host.empty() ? layer_events : nullptr));
+  if (host.empty()) return TSB_OK;
+  return tsb_ingest(l, pool, host.data(), static_cast<int64_t>(host.size()), layer_lo, layer_hi,
+                    mode, stream, layer_events);
+}
+
 tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
                              int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
                              void* stream, void* const* layer_events) {

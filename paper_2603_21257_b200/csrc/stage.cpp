@@ -56,6 +56,7 @@ double now_s() {
 struct tsb_stage {
   tsb_l1* l1 = nullptr;
   tsb_pool* pool = nullptr;
+  tsb_pool* hbm_pool = nullptr;  // HBM tier: slots < 0 name slot ~slot of this pool
   tsb_kv_shape shape{};
   int device = 0;
   tsb_scorer* scorer = nullptr;
@@ -86,6 +87,13 @@ tsb_status tsb_stage_create(tsb_l1* l1, tsb_pool* pool, tsb_stage** out) {
   for (auto& e : s->layer_ev) TSB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   TSB_TRY(tsb_scorer_create(s->device, 1024, &s->scorer));
   *out = s;
+  return TSB_OK;
+}
+
+tsb_status tsb_stage_set_hbm_tier(tsb_stage* s, tsb_pool* hbm_pool) {
+  if (hbm_pool && tsb_pool_chunk_bytes(hbm_pool) != tsb_pool_chunk_bytes(s->pool))
+    return fail(TSB_VALIDATION, "stage: the HBM tier's chunk geometry differs from the L2 pool's");
+  s->hbm_pool = hbm_pool;
   return TSB_OK;
 }
 
@@ -142,9 +150,12 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       return fail(TSB_VALIDATION, "stage: request " + std::to_string(r.id) + " lists " +
                                       std::to_string(slot_offsets[i + 1] - slot_offsets[i]) +
                                       " pool slots for a plan of " + std::to_string(nb) + " chunks");
-    for (int64_t k = 0; k < nb; ++k)
-      if (r.slots[k] < 0 || r.slots[k] >= tsb_pool_slots(s->pool))
-        return fail(TSB_VALIDATION, "stage: pool slot out of range");
+    for (int64_t k = 0; k < nb; ++k) {
+      const int64_t sl = r.slots[k];
+      const bool ok = sl >= 0 ? sl < tsb_pool_slots(s->pool)
+                              : (s->hbm_pool && ~sl < tsb_pool_slots(s->hbm_pool));
+      if (!ok) return fail(TSB_VALIDATION, "stage: pool slot out of range");
+    }
     if (nb * chunk_bytes > l1_capacity)
       return fail(TSB_CAPACITY, "request " + std::to_string(r.id) + ": " +
                                     std::to_string(nb * chunk_bytes) +
@@ -235,8 +246,8 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
         evs[L - 1] = r.ev_resident;
         evp = evs.data();
       }
-      TSB_TRY(tsb_ingest(s->l1, s->pool, items.data(), static_cast<int64_t>(items.size()), 0, L,
-                         opt->mode, stream, evp));
+      TSB_TRY(tsb_ingest_tiered(s->l1, s->pool, s->hbm_pool, items.data(),
+                                static_cast<int64_t>(items.size()), 0, L, opt->mode, stream, evp));
       if (last && L == 1) TSB_CUDA_TRY(cudaEventRecord(r.ev_first, st));
       if (opt->record_trace) {
         cudaEvent_t ce;
@@ -284,8 +295,10 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     TSB_CUDA_TRY(cudaEventSynchronize(r.ev_done));
     if (opt->verify_seed && r.n_chunks > 0) {
       std::vector<tsb_ingest_item> items;
+      // both tiers hold the synthetic pattern of the seed at their own slot index
       for (int64_t ch = 0; ch < r.n_chunks; ++ch)
-        items.push_back(tsb_ingest_item{r.slots[ch], r.row, static_cast<int32_t>(ch)});
+        items.push_back(tsb_ingest_item{r.slots[ch] < 0 ? ~r.slots[ch] : r.slots[ch], r.row,
+                                        static_cast<int32_t>(ch)});
       uint64_t mm = 0;
       TSB_TRY(tsb_l1_verify_synthetic(s->l1, items.data(), r.n_chunks, 0, L, opt->verify_seed,
                                       tsb_pool_chunk_bytes(s->pool), stream, &mm));
@@ -545,9 +558,9 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
           evs[0] = r.ev_first;
           evs[L - 1] = r.ev_resident;
         }
-        const tsb_status is = tsb_ingest(s->l1, s->pool, items.data(),
-                                         static_cast<int64_t>(items.size()), 0, L, opt->mode,
-                                         stream, last ? evs.data() : nullptr);
+        const tsb_status is = tsb_ingest_tiered(s->l1, s->pool, s->hbm_pool, items.data(),
+                                                static_cast<int64_t>(items.size()), 0, L,
+                                                opt->mode, stream, last ? evs.data() : nullptr);
         if (is != TSB_OK) return fail_out(is);
         if (last && L == 1) cudaEventRecord(r.ev_first, st);
         cudaEventRecord(ev_ingest, st);

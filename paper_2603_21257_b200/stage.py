@@ -31,6 +31,12 @@ class LoadStage:
         self._h = h
         self.l1, self.pool = l1, pool
 
+    def set_hbm_tier(self, hbm_pool: Optional[ChunkPool]):
+        """Chunks whose slot is < 0 in run()/run_online() come from slot ~slot of hbm_pool (this GPU's
+        or a peer's HBM) instead of crossing the host link; None clears the tier."""
+        check(lib.tsb_stage_set_hbm_tier(self._h, hbm_pool.handle if hbm_pool is not None else None))
+        self.hbm_pool = hbm_pool
+
     def close(self):
         if getattr(self, "_h", None) and lib is not None:  # lib is None during interpreter exit
             lib.tsb_stage_destroy(self._h)

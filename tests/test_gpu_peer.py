@@ -137,3 +137,60 @@ def test_ipc_pool_across_processes():
     for p in procs:
         p.join(timeout=60)
     assert results == {0: "ok", 1: "ok"}, results
+
+
+def test_tiered_ingest_mixes_hbm_tier_and_host_pool(oracle):
+    """tsb_ingest_tiered: negative slots come from the HBM tier, the rest over the host link; both
+    pools hold the same synthetic pattern per slot index, so the pages equal scatter_ref over the
+    host pool at |slot|.  Every mode of the host part, full heads and a TP shard."""
+    from test_gpu_parity import SMALL
+
+    for tp in ((1, 0), (4, 1)):
+        shape = SMALL.with_rank(*tp)
+        host = ingest.ChunkPool(SMALL, 8)
+        host.fill_synthetic(21)
+        tier = ingest.ChunkPool.create_device(SMALL, 8)
+        tier.fill_synthetic(21)
+        for mode in ("auto", "ce", "zerocopy", "bulk"):
+            num_pages = 160
+            arena = torch.zeros(shape.layers * 2 * num_pages * 16 * shape.heads_local * 128 * 2, dtype=torch.uint8,
+                                device="cuda")
+            l1 = ingest.PagedKVCache(shape, num_pages, max_rows=2, max_chunks=10, arena=arena)
+            rows = [l1.request(3, c, shape.page_bytes * 16)[1] for c in range(9)]
+            l1.sync_block_table()
+            content = [5, 0, 7, 7, 1, 2, 3, 6, 4]
+            slots = [s if c % 3 else ~s for c, s in enumerate(content)]  # every third chunk from the tier
+            items = ingest.items_numpy(slots, rows, range(9))
+            evs = [torch.cuda.Event() for _ in range(shape.layers)]
+            ingest.ingest_tiered(l1, host, tier, items, mode=ingest.MODES[mode], layer_events=evs)
+            evs[-1].synchronize()
+            want = oracle.scatter_ref(shape, host.slot_view(0, 8), ingest.items_numpy(content, rows, range(9)),
+                                      l1.block_table(), num_pages)
+            assert np.array_equal(arena.cpu().numpy(), want), (tp, mode)
+            l1.close()
+    with pytest.raises(t.ValidationError, match="HBM tier"):
+        ingest.ingest_tiered(l1, host, None, items)
+
+
+def test_stage_with_hbm_tier_verifies_every_page():
+    from paper_2603_21257_b200.stage import LoadStage
+
+    shape = ingest.KVShape(layers=4, kv_heads=8, head_dim=128)
+    host = ingest.ChunkPool(shape, 12)
+    host.fill_synthetic(8)
+    tier = ingest.ChunkPool.create_device(shape, 6)
+    tier.fill_synthetic(8)
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(4, 8, 128, 2), block_size_tokens=256)
+    q = t.QueueArrays(3, id=np.array([1, 2, 3]), arrival=np.array([0.0, 0.1, 0.2]),
+                      context_tokens=np.array([256 * 5, 256 * 6, 256 * 4]), query_tokens=np.full(3, 10),
+                      cache_hit_ratio=np.ones(3), flags=np.zeros(3, np.uint8))
+    slots = [[~0, ~1, 2, 3, 4], [5, ~2, 6, ~3, 7, 8], [~4, ~5, 9, 10]]  # negative: chunk resident in the HBM tier
+    l1 = ingest.PagedKVCache(shape, 10 * 16, max_rows=4, max_chunks=8)  # 10 chunks of pages: deferral
+    stage = LoadStage(l1, host)
+    with pytest.raises(t.ValidationError):
+        stage.run(q, slots, cfg, verify_seed=8)  # no tier set: negative slots are out of range
+    stage.set_hbm_tier(tier)
+    res = stage.run(q, slots, cfg, verify_seed=8)
+    assert res.stats["verify_mismatches"] == 0
+    assert res.stats["bytes"] == 15 * shape.local_chunk_bytes
+    assert res.stats["deferred_chunks"] > 0
