@@ -114,6 +114,16 @@ inline void ingest(PagedAllocator& l1, ChunkPool& pool, std::span<const tsb_inge
                    layer_lo, layer_hi, mode, stream, layer_events));
 }
 
+/// Two-tier pcie_dispatch: items with src_slot < 0 come from slot ~src_slot of `tier` (HBM).
+inline void ingest_tiered(PagedAllocator& l1, ChunkPool& pool, ChunkPool* tier,
+                          std::span<const tsb_ingest_item> items, std::int64_t layer_lo,
+                          std::int64_t layer_hi, void* stream, void* const* layer_events = nullptr,
+                          int mode = TSB_INGEST_AUTO) {
+  check(tsb_ingest_tiered(l1.handle(), pool.handle(), tier ? tier->handle() : nullptr, items.data(),
+                          static_cast<int64_t>(items.size()), layer_lo, layer_hi, mode, stream,
+                          layer_events));
+}
+
 /// The real-time load stage (SimEngine's dispatch semantics with real bytes).
 class LoadStage {
  public:
@@ -126,7 +136,9 @@ class LoadStage {
     std::vector<tsb_stage_request> requests;
     tsb_stage_stats stats{};
   };
-  /// slots[i][c] = pool slot of request i's planned chunk c.
+  /// HBM tier (this GPU's or a peer's device pool): a slot s < 0 names slot ~s of it.
+  void set_hbm_tier(ChunkPool* tier) { check(tsb_stage_set_hbm_tier(s_.get(), tier ? tier->handle() : nullptr)); }
+  /// slots[i][c] = pool slot of request i's planned chunk c (< 0: slot ~s of the HBM tier).
   /// Real-time replay of arrivals with SimEngine's decoupled control loop (tsb_stage_run_online).
   Result run_online(std::span<const RequestSpec> batch, const std::vector<std::vector<int64_t>>& slots,
                     const ClusterConfig& config, const CostModelPair& models, tsb_stage_options opt,
