@@ -192,8 +192,10 @@ int64_t tsb_index_capacity(const tsb_index* x);
 tsb_status tsb_index_insert_device(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes,
                                    const int64_t* slots);
 tsb_status tsb_index_erase_device(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes);
-/* chunk_offsets[n_req+1] as for the hasher; slots_out[c] = pool slot of chunk c for the matched
- * prefix, -1 from the first miss on; matched_out[r] = matched chunks of request r. */
+/* chunk_offsets[n_req+1] as for the hasher; slots_out[c] = the value inserted for chunk c (a pool
+ * slot, or ~slot for a chunk held in the HBM tier: tsb_ingest_tiered / tsb_stage_set_hbm_tier
+ * take it as is) for the matched prefix, -1 from the first miss on; matched_out[r] = matched
+ * chunks of request r (authoritative: a stored value may itself be negative). */
 tsb_status tsb_index_lookup_device(tsb_index* x, void* stream, int64_t n_req,
                                    const int64_t* chunk_offsets, const uint64_t* hashes,
                                    int64_t* slots_out, int64_t* matched_out);

@@ -63,16 +63,21 @@ __global__ void k_index_erase(uint64_t* __restrict__ keys, uint64_t mask, int64_
   }
 }
 
-__device__ __forceinline__ int64_t probe_find(const uint64_t* __restrict__ keys,
-                                              const int64_t* __restrict__ vals, uint64_t mask,
-                                              uint64_t h) {
+// Any int64 value may be stored (a negative one names the HBM tier: slot ~v), so a miss is a
+// flag, not a value.
+__device__ __forceinline__ bool probe_find(const uint64_t* __restrict__ keys,
+                                           const int64_t* __restrict__ vals, uint64_t mask,
+                                           uint64_t h, int64_t* v) {
   uint64_t p = slot_of(h, mask);
   for (uint64_t probe = 0; probe <= mask; ++probe, p = (p + 1) & mask) {
     const uint64_t k = keys[p];
-    if (k == h) return vals[p];
-    if (k == kEmpty) return -1;
+    if (k == h) {
+      *v = vals[p];
+      return true;
+    }
+    if (k == kEmpty) return false;
   }
-  return -1;
+  return false;
 }
 
 // One warp per request: 32 chunks probed in parallel per step, ballot finds the first miss.
@@ -92,8 +97,9 @@ __global__ void __launch_bounds__(256) k_index_lookup(const uint64_t* __restrict
   for (int64_t c = b; c < e; c += 32) {
     const int64_t cc = c + lane;
     int64_t s = -1;
-    if (!missed && cc < e) s = probe_find(keys, vals, mask, hashes[cc]);
-    const unsigned miss = __ballot_sync(0xffffffffu, cc < e && s < 0);
+    bool found = false;
+    if (!missed && cc < e) found = probe_find(keys, vals, mask, hashes[cc], &s);
+    const unsigned miss = __ballot_sync(0xffffffffu, cc < e && !missed && !found);
     if (!missed && miss) {
       m = (c - b) + __ffs(miss) - 1;
       missed = true;

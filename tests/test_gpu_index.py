@@ -112,3 +112,45 @@ def test_request_path_tokens_to_pages():
     res = LoadStage(l1, pool).run(q, slot_lists, cfg, verify_seed=13)
     assert res.stats["verify_mismatches"] == 0
     assert list(res.requests["chunks"]) == list(matched)
+
+
+def test_request_path_with_hbm_tier_hits():
+    """The index stores ~slot for chunks resident in the HBM tier: lookups hand the stage negative
+    slots, which tsb_stage_set_hbm_tier routes to the tier; every page still verifies."""
+    shape = ingest.KVShape(layers=2, kv_heads=8, head_dim=128)
+    n_docs, doc_chunks = 2, 16
+    pool = ingest.ChunkPool(shape, n_docs * doc_chunks)
+    pool.fill_synthetic(19)
+    tier = ingest.ChunkPool.create_device(shape, n_docs * doc_chunks)
+    tier.fill_synthetic(19)  # same content per slot index
+    doff = np.arange(n_docs + 1, dtype=np.int64) * doc_chunks * 256
+    dtok = po.gen_tokens(4, doff, np.arange(n_docs), np.full(n_docs, doc_chunks * 256))
+    dh = hasher.hash_prefix_chunks(doff, dtok)
+    vals = np.arange(len(dh), dtype=np.int64)
+    hot = (vals % doc_chunks) < 6  # the first 6 chunks of every document are in the HBM tier
+    vals[hot] = ~vals[hot]
+    idx = hasher.PrefixIndex(capacity=256)
+    idx.insert(dh, vals)
+    n = 4
+    doc = np.array([0, 1, 0, 1])
+    shared = np.array([16 * 256, 9 * 256 + 7, 4 * 256, 0])
+    lens = shared + 300
+    offs = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=offs[1:])
+    toks = po.gen_tokens(4, offs, doc, shared)
+    coffs = hasher.chunk_offsets(offs)
+    matched, slots = idx.lookup(coffs, hasher.hash_prefix_chunks(offs, toks))
+    assert list(matched) == [16, 9, 4, 0]
+    slot_lists = [list(slots[coffs[i]:coffs[i] + matched[i]]) for i in range(n)]
+    assert slot_lists[0][:6] == [~c for c in range(6)] and slot_lists[0][6] == 6
+    q = t.QueueArrays(n, id=np.arange(1, n + 1), arrival=np.arange(n) * 0.1, context_tokens=lens,
+                      query_tokens=np.full(n, 20),
+                      cache_hit_ratio=[hasher.hit_ratio_for_match(int(lens[i]), int(matched[i])) for i in range(n)],
+                      flags=np.zeros(n, np.uint8))
+    l1 = ingest.PagedKVCache(shape, 20 * 16, max_rows=8, max_chunks=32)
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(2, 8, 128, 2))
+    stage = LoadStage(l1, pool)
+    stage.set_hbm_tier(tier)
+    res = stage.run(q, slot_lists, cfg, verify_seed=19)
+    assert res.stats["verify_mismatches"] == 0
+    assert list(res.requests["chunks"]) == list(matched)
