@@ -16,12 +16,17 @@ for s in $steps; do
       timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> /dev/null; echo "bench ref rc=$?"
       timeout 600 python bench.py --workload llama8b32k > gpurun_out/bench_llama8b.json 2> /dev/null; echo "bench 8b rc=$?"
       timeout 900 python bench.py --workload llama70b32k > gpurun_out/bench_70b.json 2> /dev/null; echo "bench 70b rc=$?"
+      timeout 900 python bench.py --hbm-tier-chunks 46 --no-cpu-baseline --no-alt-modes > gpurun_out/bench_qwen_tier46.json 2> /dev/null; echo "bench tier rc=$?"
+      for lay in flashinfer_nhd flashinfer_hnd; do
+        timeout 900 python bench.py --layout $lay --no-cpu-baseline --no-alt-modes > gpurun_out/bench_qwen_$lay.json 2> /dev/null; echo "bench $lay rc=$?"
+      done
       for tp in 2 4 8; do
         timeout 900 python bench.py --workload llama70b32k --emulate-tp $tp --no-cpu-baseline > gpurun_out/bench_70b_tp$tp.json 2> /dev/null; echo "bench 70b tp$tp rc=$?"
         timeout 900 python bench.py --workload llama70b32k --emulate-tp $tp --mode zerocopy --no-cpu-baseline --no-hbm-arm --no-alt-modes > gpurun_out/bench_70b_tp${tp}_k1.json 2> /dev/null; echo "bench 70b tp$tp k1 rc=$?"
       done ;;
     tools)
       timeout 600 python tools/bench_queue.py > gpurun_out/bench_queue.json 2> /dev/null; echo "queue rc=$?"
+      timeout 600 python tools/bench_peer.py > gpurun_out/peer_tier.jsonl 2> /dev/null; echo "peer rc=$?"
       timeout 900 python tools/bench_mixed.py > gpurun_out/bench_mixed_ref.json 2> /dev/null; echo "mixed rc=$?"
       timeout 900 python tools/bench_mixed.py --compute-per-token 4e-6 > gpurun_out/bench_mixed_b200.json 2> /dev/null; echo "mixed b200 rc=$?" ;;
     ncu)
