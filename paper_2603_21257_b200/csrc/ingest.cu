@@ -46,10 +46,12 @@ __device__ __forceinline__ SegAddr seg_addr(const IngestGeom& g, const uint8_t* 
 // pages keep the source order; HND pages ([H_local][P][D]) move each head's row of token t to
 // head * P * D*E + t * D*E.
 template <bool kHnd>
-__device__ __forceinline__ int64_t seg_dst_off(const IngestGeom& g, int v, int vpr) {
+__device__ __forceinline__ int64_t seg_dst_off(const IngestGeom& g, int v, int vpr, int vph) {
   if (!kHnd) return static_cast<int64_t>(v) * 16;
-  const int64_t t = v / vpr, b = static_cast<int64_t>(v % vpr) * 16;
-  return (b / g.head_bytes) * g.P * g.head_bytes + t * g.head_bytes + b % g.head_bytes;
+  // 32-bit index math (64-bit division would dominate the store path): vph = vectors per head row
+  const int t = v / vpr, c = v - t * vpr;
+  const int h = c / vph, w = c - h * vph;
+  return (static_cast<int64_t>(h) * g.P + t) * g.head_bytes + w * 16;
 }
 
 // K1 / K2: one warp per segment, 16-byte streaming loads, U loads in flight per lane before
@@ -65,6 +67,7 @@ __global__ void __launch_bounds__(256) k_ingest_ldg(IngestGeom g, const uint8_t*
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int vpr = static_cast<int>(g.run >> 4);
+  const int vph = static_cast<int>(g.head_bytes >> 4);
   const int nvec = static_cast<int>(g.P) * vpr;
   for (int64_t s = warp; s < nseg; s += nwarps) {
     const SegAddr a = seg_addr(g, src, arena, items, bt, s);
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(256) k_ingest_ldg(IngestGeom g, const uint8_t*
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32;
-        if (v < nvec) st_stream(a.dst + seg_dst_off<kHnd>(g, v, vpr), buf[u]);
+        if (v < nvec) st_stream(a.dst + seg_dst_off<kHnd>(g, v, vpr, vph), buf[u]);
       }
     }
   }
