@@ -639,14 +639,14 @@ int64_t slot_runs(const tsb_ingest_item* it, int64_t n) {
 
 // Geometry of one layer of items staged packed in HBM: each item's slice of this rank's heads,
 // [K|V][C][run] contiguous, item k at k * layer_src.  K2 reads it as contiguous segments.
-tsb::IngestGeom make_staged_geom(const tsb_l1* l, int64_t layer) {
-  tsb::IngestGeom g = make_geom(l, layer, layer + 1);
+tsb::IngestGeom make_staged_geom(const tsb_l1* l, int64_t layer, int64_t n_layers = 1) {
+  tsb::IngestGeom g = make_geom(l, layer, layer + n_layers);
   g.row = g.run;
   g.head_off = 0;
   g.kv_src = l->shape.chunk_tokens * g.run;
   g.layer_src = 2 * g.kv_src;
   g.staged = 1;
-  g.item_stride = g.layer_src;
+  g.item_stride = n_layers * g.layer_src;  // item k's layers at k * n_layers * layer slice
   return g;
 }
 
@@ -681,19 +681,22 @@ tsb_status ensure_staging(tsb_l1* l) {
   return TSB_OK;
 }
 
-// Copies layer `layer` of items [0, n) into stage (item k at stage + k * g.layer_src, where g is
-// the packed staged geometry) on the copy-engine stream.
-tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, int64_t n,
-                         int64_t layer, const tsb::IngestGeom& g, uint8_t* stage) {
+// Copies layers [layer, layer + nl) of items [0, n) into stage, packed: item k's layers at
+// k * nl * (packed layer slice), each layer [K|V][C][this rank's run] -- on the copy-engine
+// stream.  A chunk's layers are adjacent in the pool slot, so nl layers are one contiguous
+// span (full heads) or one strided run of nl * 2 * C rows (head shards).
+tsb_status ce_copy_layers(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, int64_t n,
+                          int64_t layer, int64_t nl, uint8_t* stage) {
   const tsb::IngestGeom src = make_geom(l, layer, layer + 1);  // pool (slot) geometry
-  const int64_t lb = g.layer_src;                               // packed slice of one item
+  const int64_t lb = make_staged_geom(l, layer).layer_src;      // packed slice of one item-layer
+  const int64_t span = nl * lb;                                 // one item's bytes in the stage
   const uint8_t* base = pool->host + layer * src.layer_src + src.head_off;
   if (src.run != src.row) {
     // Head-sharded: one 3D copy per run of consecutive slots.  x = this rank's run of each token
-    // row, y = the 2*C rows of the layer (pitch = the full row), z = slots (slice pitch = one
-    // chunk = L*2*C rows).  The destination is packed: [item][K|V][C][run].
+    // row, y = the nl*2*C rows of the layers (pitch = the full row), z = slots (slice pitch = one
+    // chunk = L*2*C rows).  The destination is packed.
     const size_t rows_per_chunk = static_cast<size_t>(src.chunk_bytes / src.row);
-    const size_t rows = static_cast<size_t>(2 * l->shape.chunk_tokens);
+    const size_t rows = static_cast<size_t>(nl * 2 * l->shape.chunk_tokens);
     int64_t k = 0;
     while (k < n) {
       int64_t e = k + 1;
@@ -702,7 +705,7 @@ tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, i
       p.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(base + it[k].src_slot * src.chunk_bytes),
                                      static_cast<size_t>(src.row), static_cast<size_t>(src.run),
                                      rows_per_chunk);
-      p.dstPtr = make_cudaPitchedPtr(stage + k * lb, static_cast<size_t>(src.run),
+      p.dstPtr = make_cudaPitchedPtr(stage + k * span, static_cast<size_t>(src.run),
                                      static_cast<size_t>(src.run), rows);
       p.extent = make_cudaExtent(static_cast<size_t>(src.run), rows, static_cast<size_t>(e - k));
       p.kind = cudaMemcpyHostToDevice;
@@ -714,14 +717,14 @@ tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, i
   switch (g_knobs.ce_variant) {
     case 0:
       for (int64_t k = 0; k < n; ++k)
-        TSB_CUDA_TRY(cudaMemcpyAsync(stage + k * lb, base + it[k].src_slot * src.chunk_bytes, lb,
+        TSB_CUDA_TRY(cudaMemcpyAsync(stage + k * span, base + it[k].src_slot * src.chunk_bytes, span,
                                      cudaMemcpyHostToDevice, l->ce_stream));
       return TSB_OK;
     case 2: {
       std::vector<void*> dst(n), srcp(n);
-      std::vector<size_t> sz(n, static_cast<size_t>(lb));
+      std::vector<size_t> sz(n, static_cast<size_t>(span));
       for (int64_t k = 0; k < n; ++k) {
-        dst[k] = stage + k * lb;
+        dst[k] = stage + k * span;
         srcp[k] = const_cast<uint8_t*>(base + it[k].src_slot * src.chunk_bytes);
       }
       cudaMemcpyAttributes attr{};
@@ -739,8 +742,8 @@ tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, i
       while (k < n) {
         int64_t e = k + 1;
         while (e < n && it[e].src_slot == it[e - 1].src_slot + 1) ++e;
-        TSB_CUDA_TRY(cudaMemcpy2DAsync(stage + k * lb, lb, base + it[k].src_slot * src.chunk_bytes,
-                                       src.chunk_bytes, lb, e - k, cudaMemcpyHostToDevice,
+        TSB_CUDA_TRY(cudaMemcpy2DAsync(stage + k * span, span, base + it[k].src_slot * src.chunk_bytes,
+                                       src.chunk_bytes, span, e - k, cudaMemcpyHostToDevice,
                                        l->ce_stream));
         k = e;
       }
@@ -749,8 +752,10 @@ tsb_status ce_copy_layer(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, i
   }
 }
 
-// CE + K2: per layer and per staging group, the copy engine lands the items' layer slices in
-// one half of the HBM staging ring while K2 scatters the other half into pages.
+// CE + K2: per staging group, the copy engines land the group's slices in one half of the HBM
+// staging ring while K2 scatters the other half into pages.  A group is a set of items and a span
+// of layers: when one layer of every item fits a half, consecutive layers up to the next requested
+// fence share a group (fewer, larger copies and K2 launches); else one layer, items split.
 tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
                      const tsb_ingest_item* items_host, int64_t n_items, int64_t lo, int64_t hi,
                      cudaStream_t st, void* const* layer_events) {
@@ -759,31 +764,41 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
   if (!items_host)
     return fail(TSB_UNSUPPORTED, "ingest CE mode needs host-visible items (use tsb_ingest)");
   TSB_TRY(ensure_staging(l));
-  tsb::IngestGeom g = make_staged_geom(l, lo);
-  const int64_t lb = g.layer_src;
+  const int64_t lb = make_staged_geom(l, lo).layer_src;
   const int64_t half = l->staging_bytes / 2;
   if (lb > half) return fail(TSB_UNSUPPORTED, "ingest CE: one chunk layer exceeds the staging ring");
-  const int64_t per_group = half / lb;
+  const int64_t items_per_half = half / lb;
   // Host reads are ordered after the work already queued on `st` (stream semantics).
   TSB_CUDA_TRY(cudaEventRecord(l->ev_fence, st));
   TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_fence, 0));
-  for (int64_t layer = lo; layer < hi; ++layer) {
-    g = make_staged_geom(l, layer);
+  int64_t layer = lo;
+  while (layer < hi) {
+    int64_t span_end = hi;  // exclusive end of the layers before (and including) the next fence
+    if (layer_events) {
+      span_end = layer + 1;
+      while (span_end < hi && !layer_events[span_end - 1 - lo]) ++span_end;
+    }
+    const int64_t nl = n_items <= items_per_half
+                           ? std::max<int64_t>(1, std::min(span_end - layer, half / (n_items * lb)))
+                           : 1;
+    const int64_t per_group = n_items <= items_per_half ? n_items : items_per_half;
+    const tsb::IngestGeom g = make_staged_geom(l, layer, nl);
     for (int64_t i0 = 0; i0 < n_items; i0 += per_group) {
       const int64_t n = std::min(per_group, n_items - i0);
       const int b = l->next_buf;
       l->next_buf ^= 1;
       uint8_t* stage = l->staging + b * half;
       if (l->k2_used[b]) TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_k2[b], 0));
-      TSB_TRY(ce_copy_layer(l, pool, items_host + i0, n, layer, g, stage));
+      TSB_TRY(ce_copy_layers(l, pool, items_host + i0, n, layer, nl, stage));
       TSB_CUDA_TRY(cudaEventRecord(l->ev_ce[b], l->ce_stream));
       TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_ce[b], 0));
       TSB_CUDA_TRY(launch_scatter(g, stage, l->arena, items_dev + i0, l->bt_dev, n, st));
       TSB_CUDA_TRY(cudaEventRecord(l->ev_k2[b], st));
       l->k2_used[b] = true;
     }
-    if (layer_events && layer_events[layer - lo])
-      TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[layer - lo]), st));
+    layer += nl;
+    if (layer_events && layer_events[layer - 1 - lo])
+      TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[layer - 1 - lo]), st));
   }
   return TSB_OK;
 }
