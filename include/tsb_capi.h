@@ -354,9 +354,11 @@ typedef enum {
                               (not for TSB_LAYOUT_FLASHINFER_HND: UNSUPPORTED) */
   TSB_INGEST_CE = 3        /* copy engine H2D into an HBM staging ring, then K2 scatter;
                               host reads run on an internal copy stream ordered after the
-                              work queued on `stream` before the call.  Head-sharded shapes
-                              copy only this rank's heads: one strided cudaMemcpy3DAsync per
-                              run of consecutive slots per layer */
+                              work queued on `stream` before the call.  Consecutive layers up
+                              to the next requested fence share a staging group when they
+                              fit.  Head-sharded shapes copy only this rank's heads: one
+                              strided cudaMemcpy3DAsync per run of consecutive slots per
+                              group */
 } tsb_ingest_mode;
 
 /* items: host array (copied into a pinned ring internally, so it may be reused on return).
