@@ -208,6 +208,28 @@ static void gpu_cases() {
     unsigned char h[64];
     pool.ipc_handle(h);  // exportable to the other per-GPU processes
   });
+  run("gpu: load stage with an HBM tier and FlashInfer HND pages", [] {
+    KvShape shape;
+    shape.layers = 4;
+    ChunkPool pool(shape, 8);
+    check(tsb_pool_fill_synthetic(pool.handle(), 77, 0, 8, nullptr));
+    ChunkPool tier = ChunkPool::on_device(0, shape, 8);
+    check(tsb_pool_fill_synthetic(tier.handle(), 77, 0, 8, nullptr));  // same content per slot
+    PagedAllocator l1(0, shape, 6 * 16, 8, 8, nullptr, TSB_LAYOUT_FLASHINFER_HND);
+    EXPECT(l1.layout() == TSB_LAYOUT_FLASHINFER_HND);
+    LoadStage stage(l1, pool);
+    stage.set_hbm_tier(&tier);
+    ClusterConfig cfg;
+    cfg.bytes_per_token = kv_bytes_per_token(4, 8, 128, 2);
+    std::vector<RequestSpec> batch = {spec(1, 0.0, 256 * 5), spec(2, 0.1, 256 * 4)};
+    std::vector<std::vector<int64_t>> slots = {{~0ll, ~1ll, 2, 3, 4}, {4, ~5ll, 6, ~7ll}};  // ~s: HBM tier
+    tsb_stage_options opt{};
+    opt.mode = TSB_INGEST_AUTO;
+    opt.verify_seed = 77;
+    const auto r = stage.run(batch, slots, cfg, cost_models_from_config(cfg), opt);
+    EXPECT(r.stats.verify_mismatches == 0 && r.stats.deferred_chunks > 0 && l1.reserved() == 0);
+    EXPECT(r.stats.bytes == 9 * 256 * cfg.bytes_per_token);
+  });
   run("gpu: prefix hasher", [] {
     std::vector<std::int64_t> off = {0, 600, 1112};
     std::vector<std::int32_t> tok(1112);
