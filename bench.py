@@ -216,7 +216,9 @@ def scaled_traffic(summary_name, alg_bytes):
 # ------------------------------------------------------------------------------------------------
 # CPU baseline (oracle port, test infrastructure) -- rank 0, N = 1 only
 # ------------------------------------------------------------------------------------------------
-def cpu_scatter_baseline(shape, sample_chunks, seed, threads, reps=2, pool_view=None):
+def cpu_scatter_baseline(shape, sample_chunks, seed, threads, reps=2, pool_view=None, min_seconds=0.0):
+    """scatter_ref over `sample_chunks` chunks, `reps` timed passes (more until min_seconds of
+    CPU work): returns (GB/s over all timed passes, bytes per pass, mean seconds per pass)."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import pyoracle as po
 
@@ -232,13 +234,14 @@ def cpu_scatter_baseline(shape, sample_chunks, seed, threads, reps=2, pool_view=
     arena = np.empty(shape.layers * 2 * num_pages * shape.page_tokens * shape.heads_local * shape.head_dim
                      * shape.dtype_bytes, np.uint8)
     po.scatter_ref(shape, pool_view, items, bt, num_pages, threads=threads, arena=arena)  # first touch
-    best = 1e9
-    for _ in range(reps):
+    times = []
+    while len(times) < reps or sum(times) < min_seconds:
         t0 = time.perf_counter()
         po.scatter_ref(shape, pool_view, items, bt, num_pages, threads=threads, arena=arena)
-        best = min(best, time.perf_counter() - t0)
+        times.append(time.perf_counter() - t0)
     nbytes = sample_chunks * shape.local_chunk_bytes
-    return nbytes / best / 1e9, nbytes, best
+    mean = sum(times) / len(times)
+    return nbytes / mean / 1e9, nbytes, mean
 
 
 # ------------------------------------------------------------------------------------------------
@@ -534,10 +537,12 @@ def run_ours(args):
         threads = os.cpu_count() or 1
         sample = args.cpu_sample_chunks
         view = pool.slot_view(0, sample)
-        gbs, nbytes, secs = cpu_scatter_baseline(wl.shape, sample, seed, threads, pool_view=view)
+        gbs, nbytes, secs = cpu_scatter_baseline(wl.shape, sample, seed, threads, pool_view=view, min_seconds=10.0)
+        passes = max(2, int(round(10.0 / secs)))
         line["cpu_baseline"] = {"value": gbs, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"{sample} chunks ({nbytes / 1e9:.2f} GB) of {wl.name} from the pinned "
-                                          f"pool, oracle scatter_ref, {threads} threads, best of 2"}
+                                          f"pool, oracle scatter_ref, {threads} threads, ~{passes} passes over "
+                                          f">= 10 s of CPU work (mean)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
