@@ -19,7 +19,24 @@
 namespace tsb {
 namespace {
 
-__device__ __forceinline__ uint64_t fstep(uint64_t h, uint64_t w) { return (h ^ w) * kFnvPrime; }
+// One FNV step (h ^ w) * P with P = 2^40 + 0x1b3 (engine.cpp:504): in 32-bit halves the product
+// is lo*0x1b3 (wide) with hi*0x1b3 + (lo << 8) added to the upper word -- three IMADs where the
+// generic 64-bit multiply takes four.
+__device__ __forceinline__ uint64_t fstep(uint64_t h, uint64_t w) {
+  static_assert(kFnvPrime == (1ull << 40) + 0x1b3, "FNV-64 prime");
+  const uint64_t x = h ^ w;
+  uint64_t r;
+  asm("{\n.reg .u32 xl, xh, rl, rh;\n"
+      "mov.b64 {xl, xh}, %1;\n"
+      "mul.wide.u32 %0, xl, 0x1b3;\n"
+      "mov.b64 {rl, rh}, %0;\n"
+      "mad.lo.u32 rh, xh, 0x1b3, rh;\n"
+      "mad.lo.u32 rh, xl, 256, rh;\n"
+      "mov.b64 %0, {rl, rh};\n}"
+      : "=l"(r)
+      : "l"(x));
+  return r;
+}
 __device__ __forceinline__ uint64_t fpair(uint64_t a, uint64_t b) {
   return fstep(fstep(kFnvOffset, a), b);
 }
@@ -308,7 +325,7 @@ cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int3
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
   // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
-  // 3 CTAs of 8 warps per SM: the two-round pipeline needs 80 registers (64 would spill)
+  // 3 CTAs of 8 warps per SM (4 measured no faster)
   k_chunk_digest<<<148 * 3, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
   k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
