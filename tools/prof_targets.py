@@ -1,6 +1,6 @@
 """Small, single-purpose workloads for ncu (one GPU, short):  python tools/prof_targets.py <what>
 
-what: scorer | hash | ingest-ce | ingest-bulk | ingest-zerocopy | ingest-tp8 | ingest-hbm | ingest-hbm-tp8
+what: scorer | hash | index | ingest-ce | ingest-bulk | ingest-zerocopy | ingest-tp8 | ingest-hbm | ingest-hbm-tp8
 """
 from __future__ import annotations
 
@@ -50,12 +50,30 @@ def ingest_hbm(shape, n_chunks, reps=2):
     assert ingest.verify_synthetic(l1, pool, items, 3) == 0
 
 
+def index_once(n=4_000_000, n_req=100_000):
+    """K7: insert n chunk hashes, then look up n_req requests' chunk lists (half of them hits)."""
+    from paper_2603_21257_b200 import hasher
+
+    rng = np.random.default_rng(0)
+    keys = rng.integers(1, 2**63, n, dtype=np.int64).astype(np.uint64)
+    idx = hasher.PrefixIndex(capacity=1 << 23)
+    idx.insert(keys, np.arange(n, dtype=np.int64))
+    per = n // n_req
+    coffs = np.arange(n_req + 1, dtype=np.int64) * per
+    probe = keys[: n_req * per].copy()
+    probe[1::2] ^= np.uint64(1)  # misses from the second chunk of every other position
+    idx.lookup(coffs, probe)
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     if what == "scorer":
         bench_scorer()
     elif what == "hash":
         bench_hash()
+    elif what == "index":
+        index_once()
     elif what == "ingest-ce":
         ingest_once(ingest.LLAMA31_8B, 128, ingest.CE)
     elif what == "ingest-bulk":
