@@ -375,7 +375,8 @@ tsb_status tsb_ingest_tiered(tsb_l1* l1, tsb_pool* pool, tsb_pool* hbm_pool,
                              const tsb_ingest_item* items, int64_t n_items, int64_t layer_lo,
                              int64_t layer_hi, int mode, void* stream, void* const* layer_events);
 /* The kernel path tsb_ingest takes for these items and mode (AUTO resolved; other modes returned
- * as given).  items: host array or NULL (device items). */
+ * as given) -- which mechanism carries the pcie_dispatch hop (engine.cpp:427-446).  items: host
+ * array or NULL (device items). */
 tsb_status tsb_ingest_resolve_mode(const tsb_l1* l1, const tsb_pool* pool,
                                    const tsb_ingest_item* items, int64_t n_items, int mode,
                                    int* resolved);
