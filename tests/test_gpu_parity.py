@@ -498,6 +498,30 @@ def test_layout_fixed_once_reserved():
     assert _capi.lib.tsb_l1_layout(l1.handle) == ingest.LAYOUT_FLASHINFER_HND
 
 
+@pytest.mark.parametrize("tp", [(1, 0), (4, 2)])
+def test_ce_layer_groups_with_subranges_and_fences(oracle, tp):
+    """CE groups consecutive layers up to the next fence: a layer sub-range [1, 4) with a fence only
+    on its last layer (one group), then layer 0 alone with its own fence; runs of consecutive
+    slots and scattered slots mixed.  Equals the whole scatter."""
+    shape = SMALL.with_rank(*tp)
+    pool = ingest.ChunkPool(SMALL, 8)
+    pool.fill_synthetic(23)
+    num_pages = 200
+    arena = torch.zeros(shape.layers * 2 * num_pages * 16 * shape.heads_local * 128 * 2, dtype=torch.uint8,
+                        device="cuda")
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=2, max_chunks=12, arena=arena)
+    rows = [l1.request(9, c, shape.page_bytes * 16)[1] for c in range(8)]
+    l1.sync_block_table()
+    items = ingest.items_numpy([2, 3, 4, 5, 7, 0, 1, 6], rows, range(8))
+    e_last, e0 = torch.cuda.Event(), torch.cuda.Event()
+    ingest.ingest(l1, pool, items, 1, 4, mode=ingest.CE, layer_events=[None, None, e_last])
+    ingest.ingest(l1, pool, items, 0, 1, mode=ingest.CE, layer_events=[e0])
+    e0.synchronize()
+    e_last.synchronize()
+    want = oracle.scatter_ref(shape, pool.slot_view(0, 8), items, l1.block_table(), num_pages)
+    assert np.array_equal(arena.cpu().numpy(), want)
+
+
 def test_auto_mode_resolution():
     """AUTO: host pool + full heads -> CE; head-sharded -> CE when consecutive-slot runs carry
     >= 3.1 MB per strided copy, else K1; device pool or device items -> K1 (zero-copy kernel)."""
