@@ -443,6 +443,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   const int ctas = opt->prefill_ctas > 0 ? opt->prefill_ctas : 148;
   std::vector<tsb_grant> grants(4096);
   int64_t ingest_calls = 0, deferred_total = 0, releases = 0, bytes_total = 0;
+  uint64_t verify_mismatches = 0;
   std::vector<size_t> pending, admitted;
   size_t next_arrival = 0, finished = 0;
   int64_t pick = 0;
@@ -473,6 +474,17 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
         r.finished = true;
         ++finished;
         progress = true;
+        if (opt->verify_seed && r.n_chunks > 0) {  // opt-in check (synchronises the stream)
+          std::vector<tsb_ingest_item> items;
+          for (int64_t ch = 0; ch < r.n_chunks; ++ch)
+            items.push_back(tsb_ingest_item{r.slots[ch] < 0 ? ~r.slots[ch] : r.slots[ch], r.row,
+                                            static_cast<int32_t>(ch)});
+          uint64_t mm = 0;
+          if (tsb_l1_verify_synthetic(s->l1, items.data(), r.n_chunks, 0, L, opt->verify_seed,
+                                      tsb_pool_chunk_bytes(s->pool), stream, &mm) != TSB_OK)
+            return fail_out(TSB_CUDA);
+          verify_mismatches += mm;
+        }
         if (r.row >= 0) {
           int64_t ng = 0;
           if (grants.size() < static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1)
@@ -635,7 +647,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     stats->deferred_chunks = deferred_total;
     stats->releases = releases;
     stats->kernel_launches = static_cast<int64_t>(tsb_kernel_launch_count() - launches0);
-    stats->verify_mismatches = 0;
+    stats->verify_mismatches = verify_mismatches;
   }
   return TSB_OK;
 }

@@ -46,11 +46,12 @@ class LoadStage:
 
     def run_online(self, queue: QueueArrays, slot_lists: Sequence[Sequence[int]], config: ClusterConfig,
                    models: Optional[CostModelPair] = None, policy: int = PolicyKind.Fifo, mode: int = AUTO,
-                   prefill_ctas: int = 0, stream=None) -> StageResult:
+                   prefill_ctas: int = 0, verify_seed: int = 0, stream=None) -> StageResult:
         """Real-time replay: arrivals at their arrival_time, SimEngine's decoupled control loop
-        (tsb_stage_run_online).  requests['done_ms'] - requests['arrival_ms'] is each TTFT."""
+        (tsb_stage_run_online).  requests['done_ms'] - requests['arrival_ms'] is each TTFT.
+        verify_seed (opt-in, perturbs timing): check every page of each request before release."""
         return self.run(queue, slot_lists, config, models, policy, mode, prefill=True, prefill_ctas=prefill_ctas,
-                        stream=stream, _fn=lib.tsb_stage_run_online)
+                        verify_seed=verify_seed, stream=stream, _fn=lib.tsb_stage_run_online)
 
     def run(self, queue: QueueArrays, slot_lists: Sequence[Sequence[int]], config: ClusterConfig,
             models: Optional[CostModelPair] = None, policy: int = PolicyKind.Fifo, mode: int = AUTO,

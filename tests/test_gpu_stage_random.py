@@ -81,3 +81,34 @@ def test_random_stage_runs_verify(seed):
     assert st == 0
     want = po.sort_order(pr, q.arrival, q.id)
     assert list(np.argsort(res.requests["pick_position"])) == list(want)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_online_runs_verify(seed):
+    """The real-time loop (tsb_stage_run_online) over random geometries, layouts and HBM-tier
+    chunks: arrivals within ~20 ms, prefill burner on; every page verified before release."""
+    rng, full, shape, layout, mode, policy = _case(100 + seed)
+    n_slots = int(rng.integers(4, 10))
+    pool = ingest.ChunkPool(full, n_slots)
+    pool.fill_synthetic(7 + seed)
+    tier = ingest.ChunkPool.create_device(full, n_slots)
+    tier.fill_synthetic(7 + seed)
+    n = int(rng.integers(2, 7))
+    ctx = rng.integers(1, 5, n) * full.chunk_tokens
+    q = t.QueueArrays(n, id=np.arange(n) + 1, arrival=np.sort(np.round(rng.random(n) * 0.02, 4)),
+                      context_tokens=ctx, query_tokens=np.full(n, 8), cache_hit_ratio=np.ones(n),
+                      flags=np.full(n, 1, np.uint8), deadline=0.5 + rng.random(n))
+    slot_lists = [[(~s if rng.random() < 0.3 else s) for s in rng.integers(0, n_slots, int(c // full.chunk_tokens))]
+                  for c in ctx]
+    ppc = shape.pages_per_chunk
+    l1 = ingest.PagedKVCache(shape, int(ppc * (4 + rng.integers(0, 4))), max_rows=n + 1, max_chunks=4,
+                             layout=layout)
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(full.layers, full.kv_heads, full.head_dim,
+                                                               full.dtype_bytes),
+                          block_size_tokens=full.chunk_tokens, compute_per_token=1e-7, compute_base=1e-4)
+    stage = LoadStage(l1, pool)
+    stage.set_hbm_tier(tier)
+    res = stage.run_online(q, slot_lists, cfg, policy=policy, mode=ingest.MODES[mode], verify_seed=7 + seed)
+    assert res.stats["verify_mismatches"] == 0, (seed, mode, layout)
+    assert res.stats["bytes"] == sum(len(s) for s in slot_lists) * shape.local_chunk_bytes
+    assert l1.reserved() == 0
