@@ -370,7 +370,8 @@ tsb_status tsb_ingest(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items, 
 /* Two-tier ingest: an item with src_slot < 0 names slot ~src_slot of hbm_pool (a chunk already
  * resident in this GPU's or a peer's HBM -- the peer-HBM tier that stands in for the L3->L2
  * network stage, engine.cpp:405-425); the others name slots of pool.  The HBM-tier items are
- * moved first (K1 at HBM / NVLink speed), then the rest with `mode`; layer_events cover both. */
+ * moved by K1 (HBM / NVLink speed) on an internal stream beside the host part (`mode`), so the
+ * link never waits for them; layer_events and later work on `stream` cover both. */
 tsb_status tsb_ingest_tiered(tsb_l1* l1, tsb_pool* pool, tsb_pool* hbm_pool,
                              const tsb_ingest_item* items, int64_t n_items, int64_t layer_lo,
                              int64_t layer_hi, int mode, void* stream, void* const* layer_events);

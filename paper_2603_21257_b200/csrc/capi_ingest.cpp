@@ -328,6 +328,11 @@ struct tsb_l1 {
   int64_t staging_bytes = 0;
   cudaStream_t ce_stream = nullptr;
   cudaEvent_t ev_fence = nullptr;
+  // two-tier ingest: the HBM-tier part runs on its own stream beside the host part; the host
+  // part's first layer fence waits for it (fence_dep, consumed once)
+  cudaStream_t tier_stream = nullptr;
+  cudaEvent_t ev_tier_start = nullptr, ev_tier_done = nullptr;
+  cudaEvent_t fence_dep = nullptr;
   cudaEvent_t ev_ce[2] = {};
   cudaEvent_t ev_k2[2] = {};
   bool k2_used[2] = {};
@@ -351,6 +356,9 @@ void l1_free(tsb_l1* l) {
   for (auto& e : l->ev_k2)
     if (e) cudaEventDestroy(e);
   if (l->ce_stream) cudaStreamDestroy(l->ce_stream);
+  if (l->ev_tier_start) cudaEventDestroy(l->ev_tier_start);
+  if (l->ev_tier_done) cudaEventDestroy(l->ev_tier_done);
+  if (l->tier_stream) cudaStreamDestroy(l->tier_stream);
 }
 
 // Grants one reservation: takes pages from the free-list front into the block table row.
@@ -752,6 +760,17 @@ tsb_status ce_copy_layers(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, 
   }
 }
 
+// Records a requested layer fence; the first one of a call waits for l->fence_dep (the HBM-tier
+// part of a two-tier ingest) so that every fence covers both tiers.
+tsb_status record_fence(tsb_l1* l, void* ev, cudaStream_t st) {
+  if (l->fence_dep) {
+    TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->fence_dep, 0));
+    l->fence_dep = nullptr;
+  }
+  TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev), st));
+  return TSB_OK;
+}
+
 // CE + K2: per staging group, the copy engines land the group's slices in one half of the HBM
 // staging ring while K2 scatters the other half into pages.  A group is a set of items and a span
 // of layers: when one layer of every item fits a half, consecutive layers up to the next requested
@@ -797,8 +816,7 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
       l->k2_used[b] = true;
     }
     layer += nl;
-    if (layer_events && layer_events[layer - 1 - lo])
-      TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[layer - 1 - lo]), st));
+    if (layer_events && layer_events[layer - 1 - lo]) TSB_TRY(record_fence(l, layer_events[layer - 1 - lo], st));
   }
   return TSB_OK;
 }
@@ -833,8 +851,7 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
       TSB_CUDA_TRY(tsb::launch_ingest_bulk(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
                                            on_device ? sms : g_knobs.bulk_ctas, st));
     }
-    if (layer_events && layer_events[l1 - 1 - lo])
-      TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[l1 - 1 - lo]), st));
+    if (layer_events && layer_events[l1 - 1 - lo]) TSB_TRY(record_fence(l, layer_events[l1 - 1 - lo], st));
     l0 = l1;
   }
   return TSB_OK;
@@ -850,7 +867,7 @@ tsb_status ingest_impl(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_d
   mode = resolve_mode(l, pool, mode, items_host, n_items);
   if (n_items == 0) {
     for (int64_t k = 0; layer_events && k < hi - lo; ++k)
-      if (layer_events[k]) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[k]), st));
+      if (layer_events[k]) TSB_TRY(record_fence(l, layer_events[k], st));
     return TSB_OK;
   }
   switch (mode) {
@@ -913,13 +930,26 @@ tsb_status tsb_ingest_tiered(tsb_l1* l, tsb_pool* pool, tsb_pool* hbm_pool,
   if (tier.empty())
     return tsb_ingest(l, pool, host.data(), static_cast<int64_t>(host.size()), layer_lo, layer_hi,
                       mode, stream, layer_events);
-  // The HBM tier goes first at HBM / NVLink speed, so the fences recorded by the host-tier call
-  // (same stream) cover both.
-  TSB_TRY(tsb_ingest(l, hbm_pool, tier.data(), static_cast<int64_t>(tier.size()), layer_lo,
-                     layer_hi, TSB_INGEST_AUTO, stream, host.empty() ? layer_events : nullptr));
-  if (host.empty()) return TSB_OK;
-  return tsb_ingest(l, pool, host.data(), static_cast<int64_t>(host.size()), layer_lo, layer_hi,
-                    mode, stream, layer_events);
+  // The HBM tier runs on an internal stream beside the host part (the link never waits for it);
+  // the host part's first fence, and everything queued on `stream` after the call, wait for it.
+  auto st = static_cast<cudaStream_t>(stream);
+  if (!l->tier_stream) {
+    TSB_CUDA_TRY(cudaStreamCreateWithFlags(&l->tier_stream, cudaStreamNonBlocking));
+    TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_tier_start, cudaEventDisableTiming));
+    TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_tier_done, cudaEventDisableTiming));
+  }
+  TSB_CUDA_TRY(cudaEventRecord(l->ev_tier_start, st));
+  TSB_CUDA_TRY(cudaStreamWaitEvent(l->tier_stream, l->ev_tier_start, 0));
+  TSB_TRY(tsb_ingest(l, hbm_pool, tier.data(), static_cast<int64_t>(tier.size()), layer_lo, layer_hi,
+                     TSB_INGEST_AUTO, l->tier_stream, nullptr));
+  TSB_CUDA_TRY(cudaEventRecord(l->ev_tier_done, l->tier_stream));
+  l->fence_dep = l->ev_tier_done;
+  const tsb_status hs = tsb_ingest(l, pool, host.data(), static_cast<int64_t>(host.size()), layer_lo,
+                                   layer_hi, mode, stream, layer_events);
+  l->fence_dep = nullptr;
+  TSB_TRY(hs);
+  TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_tier_done, 0));
+  return TSB_OK;
 }
 
 tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
