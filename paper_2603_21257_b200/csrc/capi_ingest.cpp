@@ -927,6 +927,13 @@ tsb_status tsb_ingest_tiered(tsb_l1* l, tsb_pool* pool, tsb_pool* hbm_pool,
       tier.push_back(tsb_ingest_item{~items[k].src_slot, items[k].bt_row, items[k].chunk_index});
     }
   }
+  if (!pool && !host.empty()) return fail(TSB_VALIDATION, "ingest: host-tier items but no L2 pool");
+  if (tier.empty() && host.empty()) {  // nothing to move: the fences are recorded as is
+    for (int64_t k = 0; layer_events && k < layer_hi - layer_lo; ++k)
+      if (layer_events[k])
+        TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[k]), static_cast<cudaStream_t>(stream)));
+    return TSB_OK;
+  }
   if (tier.empty())
     return tsb_ingest(l, pool, host.data(), static_cast<int64_t>(host.size()), layer_lo, layer_hi,
                       mode, stream, layer_events);
@@ -943,6 +950,12 @@ tsb_status tsb_ingest_tiered(tsb_l1* l, tsb_pool* pool, tsb_pool* hbm_pool,
   TSB_TRY(tsb_ingest(l, hbm_pool, tier.data(), static_cast<int64_t>(tier.size()), layer_lo, layer_hi,
                      TSB_INGEST_AUTO, l->tier_stream, nullptr));
   TSB_CUDA_TRY(cudaEventRecord(l->ev_tier_done, l->tier_stream));
+  if (host.empty()) {  // every chunk came from the tier: the fences only wait for it
+    TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_tier_done, 0));
+    for (int64_t k = 0; layer_events && k < layer_hi - layer_lo; ++k)
+      if (layer_events[k]) TSB_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[k]), st));
+    return TSB_OK;
+  }
   l->fence_dep = l->ev_tier_done;
   const tsb_status hs = tsb_ingest(l, pool, host.data(), static_cast<int64_t>(host.size()), layer_lo,
                                    layer_hi, mode, stream, layer_events);
