@@ -306,14 +306,15 @@ def ingest(l1: PagedKVCache, pool: ChunkPool, items, layer_lo: int = 0, layer_hi
                          _events(layer_events, layer_hi - layer_lo)))
 
 
-def ingest_tiered(l1: PagedKVCache, pool: ChunkPool, hbm_pool: Optional[ChunkPool], items, layer_lo: int = 0,
+def ingest_tiered(l1: PagedKVCache, pool: Optional[ChunkPool], hbm_pool: Optional[ChunkPool], items, layer_lo: int = 0,
                   layer_hi: Optional[int] = None, mode: int = AUTO, stream=None,
                   layer_events: Optional[Sequence] = None):
     """tsb_ingest_tiered: items with src_slot < 0 come from slot ~src_slot of hbm_pool (the HBM tier,
     K1 at HBM / NVLink speed), the rest from pool; the fences cover both."""
     layer_hi = l1.shape.layers if layer_hi is None else layer_hi
     ptr, n = _items_ptr(items)
-    check(lib.tsb_ingest_tiered(l1.handle, pool.handle, hbm_pool.handle if hbm_pool is not None else None, ptr, n,
+    check(lib.tsb_ingest_tiered(l1.handle, pool.handle if pool is not None else None,
+                                hbm_pool.handle if hbm_pool is not None else None, ptr, n,
                                 layer_lo, layer_hi, int(mode), _stream(stream),
                                 _events(layer_events, layer_hi - layer_lo)))
 

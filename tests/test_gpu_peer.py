@@ -194,3 +194,30 @@ def test_stage_with_hbm_tier_verifies_every_page():
     assert res.stats["verify_mismatches"] == 0
     assert res.stats["bytes"] == 15 * shape.local_chunk_bytes
     assert res.stats["deferred_chunks"] > 0
+
+
+def test_tiered_ingest_all_tier_and_empty(oracle):
+    """All chunks from the HBM tier (no L2 pool given) and an empty call: fences still fire."""
+    from test_gpu_parity import SMALL
+
+    host = ingest.ChunkPool(SMALL, 4)
+    host.fill_synthetic(5)
+    tier = ingest.ChunkPool.create_device(SMALL, 4)
+    tier.fill_synthetic(5)
+    arena = torch.zeros(SMALL.layers * 2 * 64 * 16 * 8 * 128 * 2, dtype=torch.uint8, device="cuda")
+    l1 = ingest.PagedKVCache(SMALL, 64, max_rows=1, max_chunks=4, arena=arena)
+    rows = [l1.request(1, c, SMALL.page_bytes * 16)[1] for c in range(3)]
+    l1.sync_block_table()
+    evs = [torch.cuda.Event() for _ in range(SMALL.layers)]
+    ingest.ingest_tiered(l1, None, tier, ingest.items_numpy([~3, ~1, ~2], rows, [0, 1, 2]), layer_events=evs)
+    for e in evs:
+        e.synchronize()
+    want = oracle.scatter_ref(SMALL, host.slot_view(0, 4), ingest.items_numpy([3, 1, 2], rows, [0, 1, 2]),
+                              l1.block_table(), 64)
+    assert np.array_equal(arena.cpu().numpy(), want)
+    evs2 = [torch.cuda.Event() for _ in range(SMALL.layers)]
+    ingest.ingest_tiered(l1, None, None, ingest.items_numpy([], [], []), layer_events=evs2)
+    for e in evs2:
+        e.synchronize()
+    with pytest.raises(t.ValidationError, match="no L2 pool"):
+        ingest.ingest_tiered(l1, None, tier, ingest.items_numpy([0], [rows[0]], [0]))
