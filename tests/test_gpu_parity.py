@@ -522,6 +522,23 @@ def test_ce_layer_groups_with_subranges_and_fences(oracle, tp):
     assert np.array_equal(arena.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("tp", [(1, 0), (4, 1)])
+def test_ce_small_staging_splits_items(oracle, tp):
+    """A staging half that holds 3 item-layers: CE splits the items of each layer into groups of 3
+    (no layer grouping), ping-ponging the two halves many times per call."""
+    shape = SMALL.with_rank(*tp)
+    lb = 2 * shape.chunk_tokens * shape.heads_local * shape.head_dim * shape.dtype_bytes
+    pool, l1, items = build_scenario(shape)
+    ingest.set_ce(2, 2 * 3 * lb)
+    try:
+        ingest.ingest(l1, pool, items, mode=ingest.CE)
+        torch.cuda.synchronize()
+    finally:
+        ingest.set_ce()
+    want = oracle.scatter_ref(shape, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+
+
 def test_auto_mode_resolution():
     """AUTO: host pool + full heads -> CE; head-sharded -> CE when consecutive-slot runs carry
     >= 3.1 MB per strided copy, else K1; device pool or device items -> K1 (zero-copy kernel)."""
