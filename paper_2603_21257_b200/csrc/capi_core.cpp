@@ -304,12 +304,9 @@ tsb_status scorer_reserve(tsb_scorer* s, int64_t n) {
   return TSB_OK;
 }
 
-// Checks the K4 error words (synchronising on stream) and maps them to the reference's
-// exceptions: MissingDeadline "<policy>: request <id> has no deadline" (scheduler.cpp:62-68).
-tsb_status scorer_check_errors(tsb_scorer* s, cudaStream_t st, int64_t* err_index) {
-  TSB_CUDA_TRY(cudaMemcpyAsync(s->err_host, s->err, 2 * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, st));
-  TSB_CUDA_TRY(cudaStreamSynchronize(st));
+// Maps the K4 error words (already in err_host) to the reference's exceptions:
+// MissingDeadline "<policy>: request <id> has no deadline" (scheduler.cpp:62-68).
+tsb_status scorer_errors_from_host(tsb_scorer* s, int64_t* err_index) {
   const unsigned long long miss = s->err_host[0], nan = s->err_host[1];
   if (err_index) *err_index = -1;
   if (miss == ~0ull && nan == ~0ull) return TSB_OK;
@@ -325,6 +322,14 @@ tsb_status scorer_check_errors(tsb_scorer* s, cudaStream_t st, int64_t* err_inde
   }
   return fail(TSB_VALIDATION,
               "request " + std::to_string(id) + ": priority key is NaN (non-finite cost inputs)");
+}
+
+// Reads the K4 error words back (synchronising on stream) and maps them.
+tsb_status scorer_check_errors(tsb_scorer* s, cudaStream_t st, int64_t* err_index) {
+  TSB_CUDA_TRY(cudaMemcpyAsync(s->err_host, s->err, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, st));
+  TSB_CUDA_TRY(cudaStreamSynchronize(st));
+  return scorer_errors_from_host(s, err_index);
 }
 
 }  // namespace
@@ -435,9 +440,11 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
   dq.flags = b + 8 * w;
   double* o = s->outdev;
   auto* ord = reinterpret_cast<int64_t*>(o + 3 * n);
-  int64_t err = -1;
+  // Scoring, the error words and the requested outputs in one stream pass: a single sync.
   TSB_TRY(tsb_score_queue_device(s, stream, n, &dq, policy, models, c, o, o + n, o + 2 * n, ord,
-                                 &err));
+                                 nullptr));
+  TSB_CUDA_TRY(cudaMemcpyAsync(s->err_host, s->err, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, st));
   // Read back only the requested outputs: the three cost/key arrays are contiguous.
   auto* ho = static_cast<uint8_t*>(s->outhost);
   const int first = t_load ? 0 : t_comp ? 1 : primary ? 2 : 3;
@@ -446,6 +453,7 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
     TSB_CUDA_TRY(cudaMemcpyAsync(ho + first * w, o + first * n, (last - first + 1) * w,
                                  cudaMemcpyDeviceToHost, st));
   TSB_CUDA_TRY(cudaStreamSynchronize(st));
+  TSB_TRY(scorer_errors_from_host(s, nullptr));
   std::vector<tsb::CopySpan> outs;
   void* dsts[4] = {t_load, t_comp, primary, order};
   for (int k = 0; k < 4; ++k)
