@@ -1,3 +1,5 @@
+"""Where a small `value` step goes (configs[0], HBM-resident pool): the stage call vs its K1
+launches vs the scorer round trip.  Probe only.   python tools/probe/stage_overhead_probe.py"""
 import sys, time, json
 sys.path.insert(0, '.')
 import numpy as np, torch
@@ -29,8 +31,6 @@ print('score n=1', timeit(lambda: sc.score(wl.queue, PolicyKind.Fifo, m, cfg)))
 for c in range(128): l1.request(99, c, shape.page_bytes * 16)
 l1.sync_block_table()
 items = ingest.items_numpy(np.arange(128), [0] * 128, np.arange(128))
-items['bt_row'] = l1.request(99, 0, 0)[1] if False else items['bt_row']
-row = [r for r in range(4)][0]
 bt = l1.block_table(); row = int(np.where((bt >= 0).any(axis=1))[0][0])
 items['bt_row'] = row
 dev_items = torch.from_numpy(items.view(np.uint8).copy()).cuda()
