@@ -235,7 +235,7 @@ tsb_status tsb_pool_fill_synthetic(tsb_pool* p, uint64_t seed, int64_t first, in
  * a peer's over NVLink / NVSwitch -- with the same slot layout.  It stands where the reference
  * runs the L3->L2 network stage (engine.cpp:405-425): chunks another GPU already holds are
  * read peer-to-peer by the ingest kernels instead of crossing the host link.  Ingest from a
- * device pool runs K1 (SM loads; AUTO resolves to it) with the K2 grid, or K1b; CE is
+ * device pool runs K1 (SM loads; AUTO resolves to it) with the HBM grid, or K1b; CE is
  * UNSUPPORTED.  tsb_pool_slot_ptr returns the device address for these pools. */
 typedef enum { TSB_POOL_HOST = 0, TSB_POOL_DEVICE = 1 } tsb_pool_location;
 /* cudaMalloc n_slots chunks on `device` (owned; freed on destroy). */

@@ -826,7 +826,7 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
   // One launch per span of layers ending at a requested fence (or at hi): per-layer fences give
   // per-layer launches, a fence only on the first and last layer gives two launches.
   // Host pools are link-bound and saturate with a small grid; HBM / NVLink sources need the
-  // K2 grid to keep enough loads in flight.
+  // HBM grid (4736 CTAs, 4 loads in flight per lane) to keep enough loads in flight.
   const bool on_device = pool->location == TSB_POOL_DEVICE;
   int64_t l0 = lo;
   while (l0 < hi) {
