@@ -569,6 +569,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt-modes", action="store_true", help="skip the K1/K1b/CE side measurements")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        raise SystemExit(f"--gpus {args.gpus}: launch one process per GPU with "
+                         f"`python -m torch.distributed.run --nproc-per-node {args.gpus} bench.py --gpus {args.gpus}`")
     if args.impl == "reference":
         run_reference(args)
     else:
