@@ -94,6 +94,36 @@ def test_reference_scheduler_cases_on_gpu():
         drain([_req(1, 0.0), _req(2, 0.0, 3.0)], t.PolicyKind.Edf, {})
 
 
+def test_reference_scheduler_properties_on_gpu():
+    """test_scheduler.cpp:104-183 properties through the GPU order (schedule_order = K4 + K5):
+    scale invariance of SJF-cost, FIFO = arrival order, SJF-cost optimal for mean completion over
+    every permutation (n <= 6), LSTF = EDF when every request costs the same."""
+    import itertools
+
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        n = int(rng.integers(2, 7))
+        q = [t.RequestSpec(id=int(i) + 1, arrival_time=float(rng.integers(0, 3)), context_tokens=1000,
+                           query_tokens=10, deadline=float(rng.random() * 5 + 1)) for i in range(n)]
+        costs = {r.id: t.ServiceCost(float(rng.random()), float(rng.random())) for r in q}
+        sjf = t.schedule_order(q, t.PolicyKind.SjfCost, costs)
+        scaled = {k: t.ServiceCost(v.t_load * 8.0, v.t_comp * 8.0) for k, v in costs.items()}
+        assert t.schedule_order(q, t.PolicyKind.SjfCost, scaled) == sjf  # scale invariance (x8 is exact)
+        fifo = t.schedule_order(q, t.PolicyKind.Fifo, costs)
+        assert fifo == [r.id for r in sorted(q, key=lambda r: (r.arrival_time, r.id))]
+        total = {k: v.t_load + v.t_comp for k, v in costs.items()}
+        def mean_completion(order):
+            done, acc = 0.0, 0.0
+            for i in order:
+                done += total[i]
+                acc += done
+            return acc / n
+        best = min(mean_completion(p) for p in itertools.permutations([r.id for r in q]))
+        assert mean_completion(sjf) == pytest.approx(best, rel=1e-12)
+        same = {r.id: t.ServiceCost(0.25, 0.125) for r in q}
+        assert t.schedule_order(q, t.PolicyKind.Lstf, same) == t.schedule_order(q, t.PolicyKind.Edf, same)
+
+
 def test_missing_deadline_reports_first_queue_index(golden, scorer):
     g = golden("ref_queue.npz")
     q = golden_queue(g)
