@@ -391,6 +391,11 @@ tsb_status tsb_ingest_device(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* 
  * (src_slot is ignored). */
 tsb_status tsb_scatter_device(tsb_l1* l1, const void* staging, const tsb_ingest_item* items_dev,
                               int64_t n_items, int64_t layer_lo, int64_t layer_hi, void* stream);
+/* K2 alone on the CE path's staging format: item i's layers [layer_lo, layer_hi) of this rank's
+ * heads only, packed [layer][K/V][C][H_local][D], at staging + i*(hi-lo)*2*C*H_local*D*E. */
+tsb_status tsb_scatter_device_packed(tsb_l1* l1, const void* staging,
+                                     const tsb_ingest_item* items_dev, int64_t n_items,
+                                     int64_t layer_lo, int64_t layer_hi, void* stream);
 /* Tuning knobs for measurement (0 = default). */
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas);
 /* K2 implementation: 0 = SM 16-byte load/store warps (default), 1 = cp.async.bulk ring. */

@@ -191,6 +191,7 @@ _decl("tsb_ingest_tiered", st, vp, vp, vp, P(IngestItem), i64, i64, i64, C.c_int
 _decl("tsb_ingest_resolve_mode", st, vp, vp, P(IngestItem), i64, C.c_int, P(C.c_int))
 _decl("tsb_ingest_set_scatter", st, C.c_int, C.c_int)
 _decl("tsb_scatter_device", st, vp, vp, vp, i64, i64, i64, vp)
+_decl("tsb_scatter_device_packed", st, vp, vp, vp, i64, i64, i64, vp)
 _decl("tsb_ingest_set_grid", st, C.c_int, C.c_int, C.c_int)
 _decl("tsb_l1_device", C.c_int, vp)
 _decl("tsb_l1_shape", st, vp, P(KvShape))

@@ -1001,6 +1001,17 @@ tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_i
   return TSB_OK;
 }
 
+tsb_status tsb_scatter_device_packed(tsb_l1* l, const void* staging,
+                                     const tsb_ingest_item* items_dev, int64_t n_items,
+                                     int64_t layer_lo, int64_t layer_hi, void* stream) {
+  if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
+    return fail(TSB_VALIDATION, "scatter: layer range must satisfy 0 <= lo < hi <= layers");
+  const tsb::IngestGeom g = make_staged_geom(l, layer_lo, layer_hi - layer_lo);
+  TSB_CUDA_TRY(launch_scatter(g, static_cast<const uint8_t*>(staging), l->arena, items_dev,
+                              l->bt_dev, n_items, static_cast<cudaStream_t>(stream)));
+  return TSB_OK;
+}
+
 tsb_status tsb_l1_verify_synthetic(tsb_l1* l, const tsb_ingest_item* items, int64_t n_items,
                                    int64_t layer_lo, int64_t layer_hi, uint64_t seed,
                                    int64_t pool_chunk_bytes, void* stream,

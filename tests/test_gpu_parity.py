@@ -415,6 +415,25 @@ def test_k2_scatter_alone_bit_exact(oracle):
     assert np.array_equal(l1.arena.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("tp", [(1, 0), (4, 1)])
+def test_k2_scatter_packed_bit_exact(oracle, tp):
+    """tsb_scatter_device_packed: K2 from the CE path's staging format (this rank's heads only,
+    layers [1, 3) of each item packed)."""
+    shape = SMALL.with_rank(*tp)
+    pool, l1, items = build_scenario(shape)
+    lo, hi = 1, 3
+    hl, h0 = shape.heads_local, shape.tp_rank * shape.heads_local
+    chunks = pool.slot_view(0, pool.n_slots).view(np.uint16).reshape(pool.n_slots, SMALL.layers, 2, 256, 8, 128)
+    packed = np.ascontiguousarray(chunks[items["src_slot"], lo:hi, :, :, h0:h0 + hl, :])
+    staging = torch.from_numpy(packed.view(np.uint8).reshape(-1)).cuda()
+    dev_items = torch.from_numpy(items.view(np.uint8).copy()).cuda()
+    t.check(_capi.lib.tsb_scatter_device_packed(l1.handle, staging.data_ptr(), dev_items.data_ptr(), len(items), lo,
+                                                hi, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = oracle.scatter_ref(shape, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages, lo, hi)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2])
 def test_ingest_ce_copy_variants_bit_exact(oracle, variant):
     """CE strategies: per-item memcpy, 2D copy per run of consecutive slots, batched memcpy."""
