@@ -361,7 +361,8 @@ typedef enum {
                               group */
 } tsb_ingest_mode;
 
-/* items: host array (copied into a pinned ring internally, so it may be reused on return).
+/* One pcie_dispatch with real bytes (engine.cpp:427-446; PcieDone engine.cpp:258-272).
+ * items: host array (copied into a pinned ring internally, so it may be reused on return).
  * All grants for the items must already be in the block table (tsb_l1_sync_block_table).
  * VALIDATION if an item's slot, row or chunk index is outside the pool / block table. */
 tsb_status tsb_ingest(tsb_l1* l1, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
@@ -396,7 +397,8 @@ tsb_status tsb_scatter_device(tsb_l1* l1, const void* staging, const tsb_ingest_
 tsb_status tsb_scatter_device_packed(tsb_l1* l1, const void* staging,
                                      const tsb_ingest_item* items_dev, int64_t n_items,
                                      int64_t layer_lo, int64_t layer_hi, void* stream);
-/* Tuning knobs for measurement (0 = default). */
+/* Tuning knobs for measurement (0 = default); no reference counterpart (the reference models
+ * the hop's cost only, engine.cpp:206-207). */
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas);
 /* K2 implementation: 0 = SM 16-byte load/store warps (default), 1 = cp.async.bulk ring. */
 tsb_status tsb_ingest_set_scatter(int impl, int ctas);
