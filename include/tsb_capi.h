@@ -34,7 +34,8 @@ typedef enum {
   TSB_MISSING_DEADLINE = 3, /* MissingDeadline */
   TSB_DEGENERATE_FIT = 4,   /* DegenerateFit */
   TSB_CUDA = 5,             /* CUDA runtime failure (tiersim::Error) */
-  TSB_UNSUPPORTED = 6       /* shape/option not supported by the kernels */
+  TSB_UNSUPPORTED = 6,      /* shape/option not supported by the kernels */
+  TSB_UNKNOWN_PROFILE = 7   /* UnknownProfile (builtin_profile, workload.cpp:35) */
 } tsb_status;
 
 const char* tsb_last_error(void);
@@ -109,6 +110,41 @@ tsb_status tsb_derive_block_plan(const tsb_queue* q, int64_t i, const tsb_cluste
                                  int64_t* cached_tokens, int64_t* compute_tokens,
                                  int64_t* n_blocks, int64_t* block_tokens,
                                  int64_t* block_bytes);
+
+/* ------------------------------------------------------------------------------------ */
+/* Synthetic request stream (workload.cpp:31-36, 70-135; rng.hpp:19-70): the product's own  */
+/* generate_workload / solo_baseline_ttft / assign_slos, bit-identical to the reference's.  */
+/* ------------------------------------------------------------------------------------ */
+typedef struct {
+  int64_t num_requests;       /* DatasetProfile (workload.hpp:19-28) */
+  double context_tokens_mean;
+  double context_tokens_cv;
+  double query_tokens_mean;
+  double query_tokens_cv;
+  double qps;                 /* WorkloadSpec (workload.hpp:55-68) */
+  int64_t count;              /* 0 = num_requests */
+  int32_t hit_kind;           /* HitRatioSource: 0 Fixed, 1 UniformChoice */
+  double hit_fixed;
+  const double* hit_choices;
+  int64_t n_hit_choices;
+  uint64_t seed;
+} tsb_workload_spec;
+/* builtin_profile("loogle" | "icl" | "code") into the profile fields (others defaulted:
+ * qps 1, count 0, fixed hit 1.0, seed 0); TSB_UNKNOWN_PROFILE otherwise. */
+tsb_status tsb_builtin_profile(const char* name, tsb_workload_spec* out);
+tsb_status tsb_workload_validate(const tsb_workload_spec* w);
+int64_t tsb_workload_count(const tsb_workload_spec* w);
+/* generate_workload (workload.cpp:70-99): ids 1..n, Poisson arrivals, lognormal lengths. */
+tsb_status tsb_generate_workload(const tsb_workload_spec* w, int64_t cap, int64_t* id,
+                                 double* arrival, int64_t* context_tokens,
+                                 int64_t* query_tokens, double* cache_hit_ratio, int64_t* n_out);
+/* solo_baseline_ttft (workload.cpp:101-115) of entry i: its TTFT alone in an empty system. */
+tsb_status tsb_solo_baseline_ttft(const tsb_queue* q, int64_t i, const tsb_cluster* c,
+                                  double* ttft);
+/* assign_slos (workload.cpp:117-135): deadline_out[i] = arrival + factor * solo baseline. */
+tsb_status tsb_assign_slos(int64_t n, const tsb_queue* q, const tsb_cluster* c,
+                           const double* factors, int64_t n_factors, uint64_t seed,
+                           double* deadline_out);
 
 /* ------------------------------------------------------------------------------------ */
 /* Cost model (cost_model.cpp:14-85)                                                      */
@@ -222,6 +258,17 @@ tsb_status tsb_pool_wrap(const tsb_kv_shape* shape, void* host_base, int64_t n_s
  * every per-GPU process maps, so all GPUs of a box read one L2 pool; unregistered on destroy. */
 tsb_status tsb_pool_register(const tsb_kv_shape* shape, void* host_base, int64_t n_slots,
                              tsb_pool** out);
+/* NUMA-placed pool: anonymous memory bound to `numa_node` (mbind MPOL_BIND; -1 = default
+ * policy), transparent huge pages advised, then page-locked portable|mapped.  One per GPU on the
+ * GPU's own socket (tsb_device_numa_node) keeps each host link reading local DIMMs; the
+ * reference's single L2 capacity (ClusterConfig::l2_capacity, types.hpp:88) becomes per-socket
+ * shard pools of one rank's KV heads each.  munmap'ed on destroy. */
+tsb_status tsb_pool_create_numa(const tsb_kv_shape* shape, int64_t n_slots, int numa_node,
+                                tsb_pool** out);
+/* NUMA node backing the pool's first page (get_mempolicy), -1 if unknown or a device pool. */
+int tsb_pool_numa_node(const tsb_pool* p);
+/* NUMA node of a GPU's PCIe root (sysfs numa_node of its bus id), -1 if unknown. */
+int tsb_device_numa_node(int device);
 void tsb_pool_destroy(tsb_pool* p);
 void* tsb_pool_slot_ptr(tsb_pool* p, int64_t slot);
 int64_t tsb_pool_slots(const tsb_pool* p);

@@ -11,6 +11,10 @@ CUDA path against the reference's own outputs.
   ref_ledger.npz    a random TierLedger request/release script and the reference's decisions
   ref_misc.json     kv_bytes_per_token, cost_models_from_config, config_fingerprint values
   hash_frozen.npz   frozen prefix-hash vectors of the restatement (definition regression)
+  ref_workload.npz  generate_workload streams (builtin + custom profiles, fixed and uniform hit
+                    sources) and assign_slos deadlines, for the product's own generator
+
+  python oracle/gen_golden.py --only workload   regenerates ref_workload.npz alone
 """
 from __future__ import annotations
 
@@ -176,5 +180,50 @@ def main():
     print("golden fixtures written to", GOLD)
 
 
+WORKLOAD_CASES = [
+    # (profile, ctx_mean, ctx_cv, q_mean, q_cv, count, qps, seed, hit_kind, hit_fixed, choices)
+    ("loogle", 0, 0, 0, 0, 0, 1.0, 0, 0, 1.0, []),
+    ("loogle", 0, 0, 0, 0, 2000, 18.0, 7, 1, 0.0, [0.25, 0.5, 0.75, 1.0]),
+    ("icl", 0, 0, 0, 0, 500, 3.5, 123456789, 0, 0.9, []),
+    ("code", 0, 0, 0, 0, 300, 0.25, 2**63 + 11, 1, 0.0, [0.0, 1.0]),
+    ("custom", 24000.0, 1.0, 28.0, 0.5, 1000, 8.0, 3, 1, 0.0, [0.25, 0.5, 0.75, 0.9, 1.0]),
+    ("custom", 5000.0, 0.0, 10.0, 0.0, 50, 1e9, 5, 0, 0.5, []),
+]
+
+
+def gen_workload():
+    r = po.ref()
+    out = {}
+    for k, (prof, cm, cc, qm, qc, count, qps, seed, hk, hf, ch) in enumerate(WORKLOAD_CASES):
+        n = count or 120
+        ids, arr, ctx, qry, hit = po.generate_workload(prof, n, seed, qps=qps, hit_fixed=hf,
+                                                       hit_choices=ch if hk else None, ctx_mean=cm, ctx_cv=cc,
+                                                       q_mean=qm, q_cv=qc)
+        q = Q(id=ids, arrival=arr, context_tokens=ctx, query_tokens=qry, cache_hit_ratio=hit,
+              flags=np.zeros(n, np.uint8), deadline=np.zeros(n), measured_t_load=np.zeros(n),
+              measured_t_comp=np.zeros(n))
+        if k == 1:  # some measured-cost rows for the solo-baseline replay path
+            q.flags[::7] = 2
+            q.measured_t_load[::7] = np.linspace(0.0, 0.3, len(q.flags[::7]))
+            q.measured_t_comp[::7] = 0.01
+        cfg = Cfg(bytes_per_token=262144, l1_capacity=10**13, l2_capacity=10**13) if k == 4 else Cfg()
+        dl = np.empty(n)
+        fac = np.array([2.0, 4.0, 8.0])
+        st = r.ref_assign_slos(n, C.byref(po.queue_struct(q)), C.byref(po.cluster_struct(cfg)),
+                               (C.c_double * 4)(*ref_models(cfg)), fac.ctypes.data, 3, seed, dl.ctypes.data)
+        assert st == 0, r.ref_last_error()
+        for name in ("id", "arrival", "context_tokens", "query_tokens", "cache_hit_ratio", "flags",
+                     "measured_t_load", "measured_t_comp"):
+            out[f"c{k}_{name}"] = getattr(q, name)
+        out[f"c{k}_deadline"] = dl
+        out[f"c{k}_cfg"] = np.array([cfg.bytes_per_token, cfg.l1_capacity, cfg.l2_capacity])
+    np.savez_compressed(GOLD / "ref_workload.npz", **out)
+    print("wrote", GOLD / "ref_workload.npz")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--only", "workload"]:
+        gen_workload()
+    else:
+        main()
+        gen_workload()

@@ -144,6 +144,8 @@ def ref():
         d(lib, "ref_config_fingerprint", u64, C.POINTER(OrcCluster), C.c_int, u64)
         d(lib, "ref_generate_workload", i64, C.c_char_p, f64, f64, f64, f64, i64, f64, u64, C.c_int, f64, vp, i64,
           i64, vp, vp, vp, vp, vp)
+        d(lib, "ref_assign_slos", C.c_int, i64, C.POINTER(OrcQueue), C.POINTER(OrcCluster), C.POINTER(f64), vp, i64,
+          u64, vp)
         d(lib, "ref_run_simulation", C.c_int, i64, C.POINTER(OrcQueue), C.POINTER(OrcCluster), C.c_int,
           C.POINTER(f64), u64, vp, C.POINTER(f64))
         _ref = lib

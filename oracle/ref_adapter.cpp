@@ -300,6 +300,21 @@ int64_t ref_generate_workload(const char* profile, double ctx_mean, double ctx_c
   }
 }
 
+// assign_slos (workload.cpp:117-135): deadlines for a queue (input order).
+int ref_assign_slos(int64_t n, const orc_queue* q, const orc_cluster* c, const double m[4],
+                    const double* factors, int64_t n_factors, uint64_t seed, double* deadline) {
+  try {
+    std::vector<tiersim::RequestSpec> reqs;
+    for (int64_t i = 0; i < n; ++i) reqs.push_back(to_spec(q, i));
+    const auto out = tiersim::assign_slos(reqs, to_cfg(c), to_models(m),
+                                          std::span<const double>(factors, static_cast<size_t>(n_factors)), seed);
+    for (int64_t i = 0; i < n; ++i) deadline[i] = *out[static_cast<size_t>(i)].deadline;
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 // run_simulation (engine.cpp:536-552) for the sim-vs-real comparison: per-request
 // (scheduled, l1_resident, first_token, ttft) in input order; returns mean TTFT via out.
 int ref_run_simulation(int64_t n, const orc_queue* q, const orc_cluster* c, int policy,

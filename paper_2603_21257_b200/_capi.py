@@ -22,7 +22,8 @@ if not LIB_PATH.exists():
 lib = C.CDLL(str(LIB_PATH))
 
 # ---- status -------------------------------------------------------------------------------
-TSB_OK, TSB_VALIDATION, TSB_CAPACITY, TSB_MISSING_DEADLINE, TSB_DEGENERATE_FIT, TSB_CUDA, TSB_UNSUPPORTED = range(7)
+(TSB_OK, TSB_VALIDATION, TSB_CAPACITY, TSB_MISSING_DEADLINE, TSB_DEGENERATE_FIT, TSB_CUDA, TSB_UNSUPPORTED,
+ TSB_UNKNOWN_PROFILE) = range(8)
 
 i64, u64, f64, i32, u8 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint8
 P = C.POINTER
@@ -77,6 +78,15 @@ class Queue(C.Structure):
     ]
 
 
+class WorkloadSpec(C.Structure):
+    """tsb_workload_spec == DatasetProfile + WorkloadSpec (workload.hpp:19-68)."""
+
+    _fields_ = [("num_requests", i64), ("context_tokens_mean", f64), ("context_tokens_cv", f64),
+                ("query_tokens_mean", f64), ("query_tokens_cv", f64), ("qps", f64), ("count", i64),
+                ("hit_kind", i32), ("hit_fixed", f64), ("hit_choices", vp), ("n_hit_choices", i64),
+                ("seed", u64)]
+
+
 class Grant(C.Structure):
     _fields_ = [("request_id", i64), ("block_index", i32), ("bt_row", i32), ("bytes", i64)]
 
@@ -128,6 +138,12 @@ _decl("tsb_kv_bytes_per_token", st, i64, i64, i64, i64, P(i64))
 _decl("tsb_kv_shape_info", st, P(KvShape), P(i64), P(i64), P(i64))
 _decl("tsb_request_validate", st, P(Queue), i64)
 _decl("tsb_derive_block_plan", st, P(Queue), i64, P(Cluster), P(i64), P(i64), P(i64), P(i64), P(i64))
+_decl("tsb_builtin_profile", st, C.c_char_p, P(WorkloadSpec))
+_decl("tsb_workload_validate", st, P(WorkloadSpec))
+_decl("tsb_workload_count", i64, P(WorkloadSpec))
+_decl("tsb_generate_workload", st, P(WorkloadSpec), i64, vp, vp, vp, vp, vp, P(i64))
+_decl("tsb_solo_baseline_ttft", st, P(Queue), i64, P(Cluster), P(f64))
+_decl("tsb_assign_slos", st, i64, P(Queue), P(Cluster), vp, i64, u64, vp)
 _decl("tsb_cost_models_from_config", None, P(Cluster), P(f64))
 _decl("tsb_predict", f64, f64, f64, i64)
 _decl("tsb_fit_linear", st, i64, vp, vp, P(f64), P(f64), P(C.c_int), P(C.c_int))
@@ -153,6 +169,9 @@ _decl("tsb_index_lookup", st, vp, vp, i64, vp, vp, vp, vp)
 _decl("tsb_pool_create", st, P(KvShape), i64, P(vp))
 _decl("tsb_pool_wrap", st, P(KvShape), vp, i64, P(vp))
 _decl("tsb_pool_register", st, P(KvShape), vp, i64, P(vp))
+_decl("tsb_pool_create_numa", st, P(KvShape), i64, C.c_int, P(vp))
+_decl("tsb_pool_numa_node", C.c_int, vp)
+_decl("tsb_device_numa_node", C.c_int, C.c_int)
 _decl("tsb_pool_destroy", None, vp)
 _decl("tsb_pool_slot_ptr", vp, vp, i64)
 _decl("tsb_pool_slots", i64, vp)

@@ -13,8 +13,13 @@
 // has completed (the reference releases L1 at ComputeDone, engine.cpp:280-282).  Therefore an
 // in-flight async copy of a row can never hand a kernel a stale page id.
 #include <cuda_runtime.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
+#include <cstdio>
 #include <cstring>
 #include <deque>
 #include <string>
@@ -97,6 +102,8 @@ struct tsb_pool {
   bool owned = false;       // cudaFreeHost (host) or cudaFree (device) on destroy
   bool registered = false;  // cudaHostUnregister on destroy
   bool ipc = false;         // cudaIpcCloseMemHandle on destroy
+  size_t mmapped = 0;       // tsb_pool_create_numa: munmap length on destroy
+  int numa_node = -1;       // node the pages were bound to (-1: default policy)
 };
 
 namespace {
@@ -261,6 +268,61 @@ tsb_status tsb_pool_register(const tsb_kv_shape* shape, void* host_base, int64_t
   return TSB_OK;
 }
 
+// ---- NUMA placement: every GPU's host link should pull from the DIMMs of
+// its own socket, so an 8-GPU box does not funnel 8 links through one memory controller + UPI.
+int tsb_device_numa_node(int device) {
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) return -1;
+  for (char* c = bus; *c; ++c) *c = static_cast<char>(std::tolower(*c));
+  const std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+  FILE* f = std::fopen(path.c_str(), "r");
+  if (!f) return -1;
+  int node = -1;
+  if (std::fscanf(f, "%d", &node) != 1) node = -1;
+  std::fclose(f);
+  return node;
+}
+
+tsb_status tsb_pool_create_numa(const tsb_kv_shape* shape, int64_t n_slots, int numa_node,
+                                tsb_pool** out) {
+  int64_t cb = 0;
+  TSB_TRY(tsb_kv_shape_info(shape, &cb, nullptr, nullptr));
+  if (n_slots < 1) return fail(TSB_VALIDATION, "pool: n_slots must be >= 1");
+  if (numa_node > 1023) return fail(TSB_VALIDATION, "pool: numa_node out of range");
+  const size_t len = static_cast<size_t>(cb) * static_cast<size_t>(n_slots);
+  void* base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (base == MAP_FAILED) return fail(TSB_CAPACITY, "tsb_pool_create_numa: mmap of " + std::to_string(len) + " bytes failed");
+  madvise(base, len, MADV_HUGEPAGE);  // fewer pages to pin and fewer IOMMU/GMMU entries
+  int bound = -1;
+  if (numa_node >= 0) {
+    unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+    mask[numa_node / (8 * sizeof(unsigned long))] = 1ul << (numa_node % (8 * sizeof(unsigned long)));
+    constexpr int kMpolBind = 2;
+    if (syscall(SYS_mbind, base, len, kMpolBind, mask, 1024ul, 0u) != 0) {
+      munmap(base, len);
+      return fail(TSB_VALIDATION, "tsb_pool_create_numa: mbind to node " + std::to_string(numa_node) + " failed");
+    }
+    bound = numa_node;
+  }
+  // cudaHostRegister faults every page in -- on the bound node -- and pins it.
+  tsb_status st = tsb_pool_register(shape, base, n_slots, out);
+  if (st != TSB_OK) {
+    munmap(base, len);
+    return st;
+  }
+  (*out)->mmapped = len;
+  (*out)->numa_node = bound;
+  return TSB_OK;
+}
+
+int tsb_pool_numa_node(const tsb_pool* p) {
+  if (p->location != TSB_POOL_HOST || !p->host) return -1;
+  // get_mempolicy(MPOL_F_NODE | MPOL_F_ADDR): the node backing the first page.
+  int node = -1;
+  if (syscall(SYS_get_mempolicy, &node, nullptr, 0ul, p->host, 3ul) != 0) return p->numa_node;
+  return node;
+}
+
 void tsb_pool_destroy(tsb_pool* p) {
   if (!p) return;
   if (p->location == TSB_POOL_DEVICE) {
@@ -269,6 +331,7 @@ void tsb_pool_destroy(tsb_pool* p) {
   } else {
     if (p->owned) cudaFreeHost(p->host);
     if (p->registered) cudaHostUnregister(p->host);
+    if (p->mmapped) munmap(p->host, p->mmapped);
   }
   delete p;
 }

@@ -84,6 +84,11 @@ def _stream(stream) -> int:
     return s.cuda_stream
 
 
+def device_numa_node(device: int) -> int:
+    """NUMA node of a GPU's PCIe root (-1 if the platform does not say)."""
+    return lib.tsb_device_numa_node(int(device))
+
+
 class ChunkPool:
     """L2 tier: pinned + portable + mapped host memory, one full chunk per slot."""
 
@@ -107,6 +112,19 @@ class ChunkPool:
         self.chunk_bytes = lib.tsb_pool_chunk_bytes(h)
         self._keepalive = keepalive
         return self
+
+    @classmethod
+    def create_numa(cls, shape: KVShape, n_slots: int, numa_node: int) -> "ChunkPool":
+        """Pinned pool whose pages live on NUMA node `numa_node` (tsb_pool_create_numa; -1 = the
+        default policy).  Use device_numa_node(gpu) to put each GPU's pool on its own socket."""
+        h = C.c_void_p()
+        check(lib.tsb_pool_create_numa(C.byref(shape.struct()), int(n_slots), int(numa_node), C.byref(h)))
+        return cls._adopt(shape, h, n_slots)
+
+    @property
+    def numa_node(self) -> int:
+        """NUMA node backing the first page (-1: unknown / device pool)."""
+        return lib.tsb_pool_numa_node(self._h)
 
     # ---- peer-HBM tier (SURVEY.md section 8 f4): the same slot layout resident in GPU memory ----
     @classmethod

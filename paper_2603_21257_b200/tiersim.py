@@ -48,6 +48,10 @@ class Unsupported(Error):
     pass
 
 
+class UnknownProfile(Error):
+    """error.hpp:43-47"""
+
+
 _STATUS = {
     capi.TSB_VALIDATION: ValidationError,
     capi.TSB_CAPACITY: CapacityError,
@@ -55,6 +59,7 @@ _STATUS = {
     capi.TSB_DEGENERATE_FIT: DegenerateFit,
     capi.TSB_CUDA: CudaError,
     capi.TSB_UNSUPPORTED: Unsupported,
+    capi.TSB_UNKNOWN_PROFILE: UnknownProfile,
 }
 
 
@@ -373,6 +378,120 @@ def schedule_order(queue: Sequence[RequestSpec], policy: PolicyKind, costs: Opti
     """The full pick_next drain of a fixed queue as one GPU sort: returns request ids in pick order."""
     order = default_scorer().order_specs(queue, policy, costs=costs, models=models, config=config)
     return [queue[int(i)].id for i in order]
+
+
+# ---- workload.hpp ----------------------------------------------------------------------------
+@dataclass
+class DatasetProfile:
+    """workload.hpp:19-28"""
+
+    name: str = ""
+    num_requests: int = 0
+    context_tokens_mean: float = 0.0
+    context_tokens_cv: float = 0.5
+    query_tokens_mean: float = 0.0
+    query_tokens_cv: float = 0.5
+
+
+def builtin_profile(name: str) -> DatasetProfile:
+    """workload.cpp:31-36; raises UnknownProfile."""
+    w = capi.WorkloadSpec()
+    check(lib.tsb_builtin_profile(name.encode(), C.byref(w)))
+    return DatasetProfile(name, w.num_requests, w.context_tokens_mean, w.context_tokens_cv, w.query_tokens_mean,
+                          w.query_tokens_cv)
+
+
+@dataclass
+class HitRatioSource:
+    """workload.hpp:33-45: a fixed value, or a uniform pick from `choices`."""
+
+    fixed_value: Optional[float] = 1.0
+    choices: Optional[Sequence[float]] = None
+
+    @staticmethod
+    def fixed(v: float) -> "HitRatioSource":
+        return HitRatioSource(v, None)
+
+    @staticmethod
+    def uniform_choice(values: Sequence[float]) -> "HitRatioSource":
+        return HitRatioSource(None, list(values))
+
+
+@dataclass
+class WorkloadSpec:
+    """workload.hpp:55-68"""
+
+    profile: DatasetProfile = field(default_factory=DatasetProfile)
+    qps: float = 1.0
+    count: int = 0
+    hit_ratio_source: HitRatioSource = field(default_factory=HitRatioSource)
+    seed: int = 0
+
+    def _struct(self):
+        w = capi.WorkloadSpec()
+        p = self.profile
+        w.num_requests, w.context_tokens_mean, w.context_tokens_cv = p.num_requests, p.context_tokens_mean, p.context_tokens_cv
+        w.query_tokens_mean, w.query_tokens_cv = p.query_tokens_mean, p.query_tokens_cv
+        w.qps, w.count, w.seed = self.qps, self.count, self.seed
+        h = self.hit_ratio_source
+        keep = None
+        if h.choices is None:
+            w.hit_kind, w.hit_fixed = 0, h.fixed_value
+        else:
+            keep = np.ascontiguousarray(h.choices, np.float64)
+            w.hit_kind, w.hit_choices, w.n_hit_choices = 1, keep.ctypes.data, len(keep)
+        return w, keep
+
+    def effective_count(self) -> int:
+        w, _ = self._struct()
+        return lib.tsb_workload_count(C.byref(w))
+
+
+def generate_queue(spec: WorkloadSpec) -> QueueArrays:
+    """generate_workload (workload.cpp:70-99) as a struct-of-arrays queue (no deadlines)."""
+    w, keep = spec._struct()
+    check(lib.tsb_workload_validate(C.byref(w)))
+    n = lib.tsb_workload_count(C.byref(w))
+    q = QueueArrays(n)
+    got = C.c_int64()
+    check(lib.tsb_generate_workload(C.byref(w), n, q.id.ctypes.data, q.arrival.ctypes.data,
+                                    q.context_tokens.ctypes.data, q.query_tokens.ctypes.data,
+                                    q.cache_hit_ratio.ctypes.data, C.byref(got)))
+    del keep
+    return q
+
+
+def generate_workload(spec: WorkloadSpec) -> list[RequestSpec]:
+    """workload.cpp:70-99: the reference's RequestSpec stream, bit for bit."""
+    q = generate_queue(spec)
+    return [RequestSpec(int(q.id[i]), float(q.arrival[i]), int(q.context_tokens[i]), int(q.query_tokens[i]),
+                        float(q.cache_hit_ratio[i]), dataset_tag=spec.profile.name) for i in range(q.n)]
+
+
+def solo_baseline_ttft(spec: RequestSpec, config: ClusterConfig, models: Optional[CostModelPair] = None) -> float:
+    """workload.cpp:101-115 (the models do not enter the solo timing)."""
+    q, s = _q1(spec)
+    out = C.c_double()
+    check(lib.tsb_solo_baseline_ttft(C.byref(s), 0, C.byref(config.struct()), C.byref(out)))
+    return out.value
+
+
+def assign_slos_queue(q: QueueArrays, config: ClusterConfig, factors: Sequence[float], seed: int) -> QueueArrays:
+    """assign_slos (workload.cpp:117-135) in place on a queue: sets deadline + HAS_DEADLINE."""
+    f = np.ascontiguousarray(factors, np.float64)
+    out = np.empty(q.n, np.float64)
+    check(lib.tsb_assign_slos(q.n, C.byref(q.struct()), C.byref(config.struct()), f.ctypes.data, len(f), int(seed),
+                              out.ctypes.data))
+    q.deadline[:] = out
+    q.flags |= capi.HAS_DEADLINE
+    return q
+
+
+def assign_slos(requests: Sequence[RequestSpec], config: ClusterConfig, models: Optional[CostModelPair],
+                factors: Sequence[float], seed: int) -> list[RequestSpec]:
+    q = assign_slos_queue(QueueArrays.from_specs(requests), config, factors, seed)
+    return [RequestSpec(r.id, r.arrival_time, r.context_tokens, r.query_tokens, r.cache_hit_ratio,
+                        float(q.deadline[i]), r.measured_cost, r.dataset_tag) for i, r in enumerate(requests)]
 
 
 # ---- engine.hpp TierLedger --------------------------------------------------------------------
