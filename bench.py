@@ -7,16 +7,21 @@ A step is one pass of the load stage over the batch: GPU scoring + pick order, T
 semantics page grants with FIFO deferral, block-table upload, ingest of every planned chunk, and
 page release (tsb_stage_run, the public C-ABI call).  Default workload = BASELINE.json configs[1]
 (Qwen2.5-32B KV, 16 x 128K @ 0.9 hit).  With N GPUs the KV heads are sharded TP-style: every rank
-ingests its head slice of the same batch from the pool (strong scaling, no data-path collective).
+ingests its head slice of the same batch from its own NUMA-local pinned pool (strong scaling, no
+data-path collective).  Without torchrun, --gpus N > 1 launches the N ranks itself.
 
-  value : inputs resident in HBM -- the same L2 pool (slots, bytes) held in device memory; payload
-          bytes of all ranks / max over ranks of the CUDA-event time of the K timed stage passes
-  e2e   : the L2 pool in pinned host memory, so every payload byte crosses the host link inside
-          the timed region; the same bytes / max over ranks of the host wall time of the K
-          public-API calls (the headline against the reference arm)
-  roofline     : the value arm's dominant kernel (K1 over the HBM pool, HBM-bound), live CUDA events
-  roofline_k2  : the e2e arm's kernel (K2 paged scatter from the CE staging ring)
-  host_link    : the e2e arm's device-timed GB/s per GPU vs the live copy-engine H2D peak
+  value    : the north-star hop, L2 pinned host pool -> L1 pages; payload bytes of all ranks / max
+             over ranks of the CUDA-event time of the K timed stage passes (engine.cpp:206-207,
+             427-446 made real)
+  e2e      : the same K passes timed by the host wall clock around the public API calls
+             (tsb_stage_run: queue + block-table uploads, results read back)
+  roofline : the value arm's bound -- the host link, achieved per-GPU GB/s against the live
+             copy-engine H2D peak of this box; K2 (the paged scatter that follows the copy
+             engines, HBM-bound) is reported beside it with its ncu DRAM bytes (roofline_k2)
+  hbm_tier : the same step with the pool held in HBM (the peer-HBM tier's K1 path), not the
+             headline
+  workloads: driver-visible lines for configs[0] (Llama-8B 32K), configs[2] (70B, rank 0 of a
+             tp 1/2/4/8 head split on this GPU) and configs[4] (100K-request scorer + hasher)
   cpu_baseline : the oracle's scatter_ref (port) on the host cores, bounded sample (rank 0, N=1)
 """
 from __future__ import annotations
@@ -25,6 +30,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -39,10 +45,50 @@ sys.path.insert(0, str(ROOT))
 METRIC = "KV ingest GB/s per GPU and aggregate vs host-link/HBM roofline; TTFT load ms"
 UNIT = "GB/s"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+GEN5_X16_GBS = 63.0        # PCIe Gen5 x16 per direction, theory
+
+# BASELINE.json configs as plain numbers (the reference arm builds its sample from these without
+# importing the product package; tests/test_bench_cpu.py checks they equal workloads.WORKLOADS).
+SPECS = {
+    "qwen16x128k": dict(name="qwen2.5-32b_16x128k_hit0.9", layers=64, kv_heads=8, head_dim=128, n_req=16,
+                        ctx=131072, hit=0.9, query=28, n_docs=2),
+    "llama8b32k": dict(name="llama3.1-8b_1x32k", layers=32, kv_heads=8, head_dim=128, n_req=1, ctx=32768,
+                       hit=1.0, query=28, n_docs=1),
+    "llama70b32k": dict(name="llama3-70b_1x32k", layers=80, kv_heads=8, head_dim=128, n_req=1, ctx=32768,
+                        hit=1.0, query=28, n_docs=1),
+}
 
 
 def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def cpu_model() -> str:
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------------------------------------
+# self-launch: `python bench.py --gpus N` without torchrun starts N ranks itself
+# ------------------------------------------------------------------------------------------------
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    env = dict(os.environ)
+    if args.one_device:
+        env["TSB_BENCH_ONE_DEVICE"] = "1"
+    return subprocess.call(cmd, env=env)
 
 
 # ------------------------------------------------------------------------------------------------
@@ -97,35 +143,48 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
-# shared pool across per-GPU processes
+# pools
 # ------------------------------------------------------------------------------------------------
-def make_pool(shape_full, n_slots, world, rank, dist, seed):
-    """One pinned L2 pool per box: a /dev/shm segment page-locked by every rank when it fits;
-    otherwise each rank pins a shard-local pool holding only its KV heads (chunks laid out
-    [L][2][C][H/world][D]), so host memory stays at one pool's worth across the box.
-    Returns (pool, description, shape the rank ingests with)."""
+def make_pool(shape_full, n_slots, world, rank, dist, seed, kind, device):
+    """The L2 pool this rank reads.  kind:
+      numa   (default) pinned memory bound to the GPU's NUMA node (tsb_pool_create_numa).  With
+             N > 1 ranks each rank holds only its KV heads (chunks [L][2][C][H/N][D]), so the box
+             holds one pool's worth of host memory and every link reads its own socket's DIMMs.
+      shared one /dev/shm segment of full chunks page-locked by every rank (strided head reads)
+      hostalloc  cudaHostAlloc portable|mapped (round-1 default; N = 1 only)
+    Returns (pool, description, shape the rank ingests with, seed of the pool contents)."""
     from paper_2603_21257_b200 import ingest
-    from paper_2603_21257_b200.multirank import SharedSegment
 
-    nbytes = n_slots * shape_full.chunk_bytes
+    node = ingest.device_numa_node(device)
+    if kind == "shared" and world > 1:
+        from paper_2603_21257_b200.multirank import SharedSegment
+
+        nbytes = n_slots * shape_full.chunk_bytes
+        if not torch_tensor_flag(SharedSegment.fits(nbytes), dist):
+            raise SystemExit("--pool shared: /dev/shm cannot hold the pool")
+        seg = SharedSegment(f"tsb_pool_{os.environ.get('MASTER_PORT', '0')}_{nbytes}", nbytes, rank, dist.barrier)
+        pool = ingest.ChunkPool.register(shape_full, seg.address(), n_slots, keepalive=seg)
+        if rank == 0:
+            pool.fill_synthetic(seed)
+        dist.barrier()
+        seg.unlink()  # every rank has mapped and registered it: nothing outlives the run
+        return pool, "shared /dev/shm segment of full chunks, cudaHostRegister'ed by every rank", \
+            shape_full.with_rank(world, rank), seed
     if world > 1:
-        shared = torch_tensor_flag(SharedSegment.fits(nbytes), dist)
-        if shared:
-            seg = SharedSegment(f"tsb_pool_{os.environ.get('MASTER_PORT', '0')}_{nbytes}", nbytes, rank, dist.barrier)
-            pool = ingest.ChunkPool.register(shape_full, seg.address(), n_slots, keepalive=seg)
-            if rank == 0:
-                pool.fill_synthetic(seed)
-            dist.barrier()
-            seg.unlink()  # every rank has mapped and registered it: nothing outlives the run
-            return pool, "shared /dev/shm segment, cudaHostRegister'ed by every rank", shape_full.with_rank(world, rank)
         local = ingest.KVShape(shape_full.layers, shape_full.kv_heads // world, shape_full.head_dim,
                                shape_full.dtype_bytes, shape_full.chunk_tokens, shape_full.page_tokens)
-        pool = ingest.ChunkPool(local, n_slots)
+        pool = ingest.ChunkPool.create_numa(local, n_slots, node)
         pool.fill_synthetic(seed + rank)
-        return pool, "shard-local pinned pool per rank (/dev/shm too small for one shared pool)", local
-    pool = ingest.ChunkPool(shape_full, n_slots)
+        return pool, f"rank-local pinned pool of this rank's KV heads on NUMA node {pool.numa_node} " \
+                     f"(GPU's node {node}; tsb_pool_create_numa)", local, seed + rank
+    if kind == "hostalloc":
+        pool = ingest.ChunkPool(shape_full, n_slots)
+        desc = "cudaHostAlloc portable|mapped"
+    else:
+        pool = ingest.ChunkPool.create_numa(shape_full, n_slots, node)
+        desc = f"pinned pool on NUMA node {pool.numa_node} (GPU's node {node}; tsb_pool_create_numa)"
     pool.fill_synthetic(seed)
-    return pool, "cudaHostAlloc portable|mapped", shape_full
+    return pool, desc, shape_full, seed
 
 
 def coll_device(dist) -> str:
@@ -195,124 +254,9 @@ def measure_k2(torch, l1, shape, n_items=128, reps=20):
     return 2 * n_items * n_layers * local_layer, avg_s
 
 
-def measured_peaks():
-    p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
-        d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
-    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
-
-
-def scaled_traffic(summary_name, alg_bytes):
-    """dram read+write bytes of one launch from a committed `ncu --set full` summary, scaled from
-    the profiled launch's algorithmic bytes to this launch's (null when not captured)."""
-    p = ROOT / "profiles" / summary_name
-    if not p.exists():
-        return None
-    d = json.loads(p.read_text())
-    dram, alg = d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
-    return dram * alg_bytes / alg if dram and alg else None
-
-
-# ------------------------------------------------------------------------------------------------
-# CPU baseline (oracle port, test infrastructure) -- rank 0, N = 1 only
-# ------------------------------------------------------------------------------------------------
-def cpu_scatter_baseline(shape, sample_chunks, seed, threads, reps=2, pool_view=None, min_seconds=0.0):
-    """scatter_ref over `sample_chunks` chunks, `reps` timed passes (more until min_seconds of
-    CPU work): returns (GB/s over all timed passes, bytes per pass, mean seconds per pass)."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import pyoracle as po
-
-    cb = shape.chunk_bytes
-    if pool_view is None:
-        pool_view = po.synth_fill(seed, 0, sample_chunks * cb // 8, threads).view(np.uint8)
-    num_pages = sample_chunks * shape.pages_per_chunk
-    rng = np.random.default_rng(seed)
-    bt = rng.permutation(num_pages).astype(np.int32).reshape(1, -1)
-    items = np.zeros(sample_chunks, dtype=[("src_slot", np.int64), ("bt_row", np.int32), ("chunk_index", np.int32)])
-    items["src_slot"] = np.arange(sample_chunks)
-    items["chunk_index"] = np.arange(sample_chunks)
-    arena = np.empty(shape.layers * 2 * num_pages * shape.page_tokens * shape.heads_local * shape.head_dim
-                     * shape.dtype_bytes, np.uint8)
-    po.scatter_ref(shape, pool_view, items, bt, num_pages, threads=threads, arena=arena)  # first touch
-    times = []
-    while len(times) < reps or sum(times) < min_seconds:
-        t0 = time.perf_counter()
-        po.scatter_ref(shape, pool_view, items, bt, num_pages, threads=threads, arena=arena)
-        times.append(time.perf_counter() - t0)
-    nbytes = sample_chunks * shape.local_chunk_bytes
-    mean = sum(times) / len(times)
-    return nbytes / mean / 1e9, nbytes, mean
-
-
-# ------------------------------------------------------------------------------------------------
-def run_reference(args):
-    """The reference CPU implementation of the path on the host cores: the reference moves no
-    bytes (proj/ is a simulator), so this is the oracle port scatter_ref over the same chunk
-    layouts, all host threads, one bounded sample per step."""
-    rank, world, _ = env_rank()
-    if rank != 0:
-        return
-    from paper_2603_21257_b200.workloads import WORKLOADS
-
-    wl = WORKLOADS[args.workload]()
-    shape = wl.shape
-    threads = os.cpu_count() or 1
-    sample = args.cpu_sample_chunks
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import pyoracle as po
-
-    pool_view = po.synth_fill(7, 0, sample * shape.chunk_bytes // 8, threads).view(np.uint8)
-    times = []
-    for i in range(args.warmup + args.steps):
-        gbs, nbytes, secs = cpu_scatter_baseline(shape, sample, 7, threads, reps=1, pool_view=pool_view)
-        if i >= args.warmup:
-            times.append(secs)
-    tot = sum(times)
-    value = args.steps * nbytes / tot / 1e9
-    desc = f"{sample} chunks ({nbytes / 1e9:.2f} GB) of request 1 of {wl.name}, scatter_ref, {threads} threads"
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": wl.name, "sample": desc},
-            "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def timed_steps(torch, run, steps, dist, capi):
-    """W warm-up steps are run by the caller; this times exactly `steps` calls of `run()`,
-    bracketed by a barrier + synchronize on both sides.  Returns (device s, wall s, last result,
-    kernel launches, clocks)."""
-    dev = torch.cuda.current_device()
-    s = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    walls, results = [], None
-    # The sampler starts (and delivers its first sample) before the barrier, so every rank leaves
-    # the barrier straight into its timed region: no start skew between ranks.
-    with ClockSampler(dev) as clk:
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        launches0 = capi.lib.tsb_kernel_launch_count()
-        ev0.record(s)
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            results = run()
-            walls.append(time.perf_counter() - t0)
-        ev1.record(s)
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    launches = capi.lib.tsb_kernel_launch_count() - launches0
-    return ev0.elapsed_time(ev1) * 1e-3, sum(walls), results, launches, clk.summary()
-
-
 def measure_k1_hbm(torch, l1, pool, shape, n_items, reps=10):
-    """K1 (k_ingest_ldg, K2 grid) reading the HBM-resident pool, timed alone with CUDA events:
-    the stage's dominant launch -- layers [1, L) of a request's n_items chunks (layer 0 goes
-    first, alone, to fence the first layer); algorithmic bytes = read + write of the payload."""
+    """K1 (k_ingest_ldg, HBM grid) reading the HBM-resident pool, timed alone with CUDA events:
+    layers [1, L) of a request's n_items chunks; algorithmic bytes = read + write of the payload."""
     from paper_2603_21257_b200 import ingest
 
     cb = shape.page_bytes * shape.pages_per_chunk
@@ -341,6 +285,291 @@ def measure_k1_hbm(torch, l1, pool, shape, n_items, reps=10):
     return 2 * n_items * (shape.layers - lo) * layer_bytes, avg_s
 
 
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def scaled_traffic(summary_name, alg_bytes):
+    """dram read+write bytes of one launch from a committed `ncu --set full` summary, scaled from
+    the profiled launch's algorithmic bytes to this launch's (null when not captured)."""
+    p = ROOT / "profiles" / summary_name
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    dram, alg = d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+    return dram * alg_bytes / alg if dram and alg else None
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU arm (oracle port, test infrastructure): numpy + oracle/ only, never the product package
+# ------------------------------------------------------------------------------------------------
+class _Shape:
+    def __init__(self, layers, kv_heads, head_dim, dtype_bytes=2, chunk_tokens=256, page_tokens=16, tp_size=1,
+                 tp_rank=0):
+        self.__dict__.update(locals())
+        del self.__dict__["self"]
+        self.heads_local = kv_heads // tp_size
+        self.chunk_bytes = layers * 2 * chunk_tokens * kv_heads * head_dim * dtype_bytes
+        self.local_chunk_bytes = self.chunk_bytes // tp_size
+        self.pages_per_chunk = chunk_tokens // page_tokens
+
+
+def reference_sample(spec, per_request: int):
+    """The configs batch in the oracle's FIFO pick order, cut to its first `per_request` chunks
+    per request: (shape, items, block_table, num_pages, distinct pool slots used)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle as po
+
+    shape = _Shape(spec["layers"], spec["kv_heads"], spec["head_dim"])
+    n = spec["n_req"]
+    nb = int(np.floor(spec["ctx"] * spec["hit"] / 256.0))  # cached_token_count (types.cpp:73-79)
+    ids = np.arange(1, n + 1, dtype=np.int64)
+    arrival = np.arange(n) * 1e-3
+    order = po.sort_order(arrival, arrival, ids)  # FIFO: primary = arrival (scheduler.cpp:47-49)
+    k = min(per_request, nb)
+    # slot s of document d holds chunk s; request r reads document r % n_docs
+    slots_used = sorted({(r % spec["n_docs"]) * k + c for r in range(n) for c in range(k)})
+    remap = {s: i for i, s in enumerate(slots_used)}
+    items = np.zeros(n * k, dtype=[("src_slot", np.int64), ("bt_row", np.int32), ("chunk_index", np.int32)])
+    for j, r in enumerate(order):
+        for c in range(k):
+            items[j * k + c] = (remap[(int(r) % spec["n_docs"]) * k + c], j, c)
+    num_pages = n * k * shape.pages_per_chunk
+    bt = np.random.default_rng(5).permutation(num_pages).astype(np.int32).reshape(n, k * shape.pages_per_chunk)
+    return shape, items, bt, num_pages, len(slots_used)
+
+
+def cpu_scatter(shape, pool_view, items, bt, num_pages, threads, arena):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle as po
+
+    t0 = time.perf_counter()
+    po.scatter_ref(shape, pool_view, items, bt, num_pages, threads=threads, arena=arena)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    """The reference's CPU implementation of the path on the host cores: the reference moves no
+    bytes (proj/ is a simulator), so this is the oracle port scatter_ref over the same batch in
+    the same pick order, all host threads, one bounded sample per step."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle as po
+
+    spec = SPECS[args.workload]
+    threads = os.cpu_count() or 1
+    shape, items, bt, num_pages, n_slots = reference_sample(spec, args.cpu_chunks_per_request)
+    pool_view = po.synth_fill(7, 0, n_slots * shape.chunk_bytes // 8, threads).view(np.uint8)
+    arena = np.empty(shape.layers * 2 * num_pages * 16 * shape.heads_local * shape.head_dim * 2, np.uint8)
+    nbytes = len(items) * shape.local_chunk_bytes
+    times = []
+    for i in range(args.warmup + args.steps):
+        secs = cpu_scatter(shape, pool_view, items, bt, num_pages, threads, arena)
+        if i >= args.warmup:
+            times.append(secs)
+    tot = sum(times)
+    value = args.steps * nbytes / tot / 1e9
+    desc = (f"{spec['name']} batch in FIFO pick order, first {len(items) // spec['n_req']} chunks of each of the "
+            f"{spec['n_req']} requests per step ({len(items)} chunks, {nbytes / 1e9:.2f} GB; pool {n_slots} slots), "
+            f"oracle scatter_ref into paged L1 through a permuted block_table, {threads} threads")
+    cpu = {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc, "cpu_model": cpu_model()}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": spec["name"], "sample": desc, "same_batch_as_ours": True},
+            "impl": "reference", "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+def timed_steps(torch, run, steps, dist, capi):
+    """W warm-up steps are run by the caller; this times exactly `steps` calls of `run()`,
+    bracketed by a barrier + synchronize on both sides.  Returns (device s, wall s, last result,
+    kernel launches, clocks)."""
+    dev = torch.cuda.current_device()
+    s = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    walls, results = [], None
+    # The sampler starts (and delivers its first sample) before the barrier, so every rank leaves
+    # the barrier straight into its timed region: no start skew between ranks.
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        launches0 = capi.lib.tsb_kernel_launch_count()
+        ev0.record(s)
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            results = run()
+            walls.append(time.perf_counter() - t0)
+        ev1.record(s)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = capi.lib.tsb_kernel_launch_count() - launches0
+    return ev0.elapsed_time(ev1) * 1e-3, sum(walls), results, launches, clk.summary()
+
+
+def stage_pass(torch, wl, shape, pool, pool_seed, steps, warmup, l1_gib, layout=0, mode=None, dist=None,
+               policy=None, hbm_tier_pool=None, tier_chunks=0):
+    """Warm-up (the first pass checks every page against the synthetic generator) + `steps` timed
+    stage passes over the workload's batch on `pool`.  Returns a dict of the measurements and the
+    L1 (the caller frees it)."""
+    from paper_2603_21257_b200 import _capi, ingest
+    from paper_2603_21257_b200.stage import LoadStage
+    from paper_2603_21257_b200.tiersim import PolicyKind
+
+    mode = ingest.AUTO if mode is None else mode
+    policy = PolicyKind.Fifo if policy is None else policy
+    free, _ = torch.cuda.mem_get_info()
+    page = shape.page_bytes
+    need_pages = wl.chunks * shape.pages_per_chunk
+    num_pages = int(min((min(free - (10 << 30), l1_gib << 30)) // page, need_pages))
+    max_chunks = max(len(s) for s in wl.slots)
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=wl.queue.n + 1, max_chunks=max(max_chunks, 128),
+                             layout=layout)
+    stage = LoadStage(l1, pool)
+    slots = wl.slots
+    if hbm_tier_pool is not None and tier_chunks:
+        stage.set_hbm_tier(hbm_tier_pool)
+        slots = [[~s if k < tier_chunks else s for k, s in enumerate(sl)] for sl in wl.slots]
+    run = lambda verify=0: stage.run(wl.queue, slots, wl.config, policy=policy, mode=mode, verify_seed=verify)
+    for i in range(warmup):
+        r = run(pool_seed if i == 0 else 0)
+        if i == 0 and r.stats["verify_mismatches"]:
+            raise SystemExit(f"ingest parity failure ({wl.name}): {r.stats['verify_mismatches']} mismatching words")
+    dev_s, wall_s, res, launches, clk = timed_steps(torch, run, steps, dist, _capi)
+    req = res.requests
+    order = np.argsort(req["pick_position"])
+    out = dict(dev_s=dev_s, wall_s=wall_s, bytes=float(res.stats["bytes"]), launches=int(launches), clocks=clk,
+               stats={k: res.stats[k] for k in ("ingest_calls", "deferred_chunks", "releases", "kernel_launches")},
+               num_pages=num_pages, page=page, max_chunks=max_chunks,
+               ttft={"first_layer_ms_p50": float(np.median(req["first_layer_ms"])),
+                     "resident_ms_p50": float(np.median(req["resident_ms"])),
+                     "resident_ms_max": float(req["resident_ms"].max()),
+                     "first_layer_ms_first_request": float(req["first_layer_ms"][order[0]]),
+                     "resident_ms_first_request": float(req["resident_ms"][order[0]]),
+                     "reference_model_ms_per_request": float(
+                         len(wl.slots[0]) * (10e-6 + shape.local_chunk_bytes / 64e9) * 1e3)})
+    stage.close()
+    return out, l1
+
+
+def side_workloads(torch, args, ce_peak, hbm_peak, seed, device):
+    """configs[0], configs[2] (rank 0 of tp 1/2/4/8 on this GPU) and configs[4] as sub-lines."""
+    from paper_2603_21257_b200 import ingest
+    from paper_2603_21257_b200.workloads import WORKLOADS
+
+    out = {}
+    steps = max(3, min(args.steps, 10))
+    for key, tps in (("llama8b32k", (1,)), ("llama70b32k", (1, 2, 4, 8))):
+        wl = WORKLOADS[key]()
+        pool, desc, _, pseed = make_pool(wl.shape, wl.pool_slots, 1, 0, None, seed, "numa", device)
+        for tp in tps:
+            shape = wl.shape.with_rank(tp, 0)
+            m, l1 = stage_pass(torch, wl, shape, pool, pseed, steps, 3, 100)
+            link = m["bytes"] * steps / m["dev_s"] / 1e9
+            out[f"{wl.name}" + (f"_tp{tp}_rank0" if tp > 1 else "")] = {
+                "config": "configs[0]" if key == "llama8b32k" else f"configs[2] tp{tp} (rank 0 on this GPU)",
+                "value": link, "e2e": m["bytes"] * steps / m["wall_s"] / 1e9, "unit": UNIT,
+                "host_link_frac": link / ce_peak, "bytes_per_step": int(m["bytes"]),
+                "ms_per_step": m["dev_s"] / steps * 1e3, "ttft_load_ms": m["ttft"], "steps": steps,
+                "gpu_launches": m["launches"]}
+            del l1
+            torch.cuda.empty_cache()
+        pool.close()
+    out["queue100k"] = queue_workload(torch, hbm_peak)
+    return out
+
+
+def queue_workload(torch, hbm_peak, n=100_000):
+    """configs[4]: generate_workload(loogle, 100K, seed 0) + assign_slos {2,4,8} (the product's own
+    generator), GPU score + order for 5 policies, K3 prefix hashing of every context, K7 index."""
+    from paper_2603_21257_b200 import hasher
+    from paper_2603_21257_b200 import tiersim as t
+    from paper_2603_21257_b200.scorer import BatchScorer, DeviceQueue
+
+    spec = t.WorkloadSpec(t.builtin_profile("loogle"), qps=1.0, count=n, seed=0)
+    t0 = time.perf_counter()
+    q = t.generate_queue(spec)
+    cfg = t.ClusterConfig(l1_capacity=10**13, l2_capacity=10**13)
+    t.assign_slos_queue(q, cfg, [2.0, 4.0, 8.0], 0)
+    gen_s = time.perf_counter() - t0
+    m = t.cost_models_from_config(cfg)
+    sc = BatchScorer(torch.cuda.current_device())
+    dq = DeviceQueue(q, torch.cuda.current_device())
+    out = sc.score_device(dq, t.PolicyKind.Lstf, m, cfg)
+
+    def timed(fn, reps=20, warm=3):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) * 1e-3 / reps
+
+    gpu = {t.policy_name(p): timed(lambda: sc.score_device(dq, p, m, cfg, out=out, check_errors=False)) * 1e6
+           for p in t.PolicyKind}
+    sc.score(q, t.PolicyKind.Lstf, m, cfg)
+    t0 = time.perf_counter()
+    for _ in range(5):
+        order = sc.score(q, t.PolicyKind.Lstf, m, cfg)[3]
+    api_us = (time.perf_counter() - t0) / 5 * 1e6
+    res = {"config": "configs[4]", "requests": n, "queue_generation_s": gen_s,
+           "gpu_score_order_us": gpu, "host_api_score_order_us": api_us}
+    # K3 over every context of the queue; token ids generated on the device (doc-id prefixes shared)
+    offs = np.zeros(n + 1, np.int64)
+    np.cumsum(q.context_tokens, out=offs[1:])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d_offs = torch.from_numpy(offs).to(dev)
+    doc = torch.from_numpy(np.random.default_rng(1).integers(0, 1000, n)).to(dev)
+    sh = torch.from_numpy(q.context_tokens // 2).to(dev)
+    tok = torch.empty(int(offs[-1]), dtype=torch.int32, device=dev)
+    hasher.gen_tokens_device(0, d_offs, doc, sh, tok)
+    coff = torch.from_numpy(hasher.chunk_offsets(offs)).to(dev)
+    hout = torch.empty(int(coff[-1]), dtype=torch.int64, device=dev)
+    secs = timed(lambda: hasher.hash_prefix_chunks_device(d_offs, tok, coff, hout), reps=10)
+    nbytes = tok.numel() * 4 + hout.numel() * 8
+    res["hash"] = {"tokens": int(offs[-1]), "chunks": int(coff[-1]), "ms": secs * 1e3, "GBps": nbytes / secs / 1e9,
+                   "hbm_copy_peak_frac": nbytes / secs / 1e9 / hbm_peak, "algorithmic_bytes": int(nbytes)}
+    idx = hasher.PrefixIndex(capacity=1 << int(np.ceil(np.log2(2 * hout.numel()))))
+    slots_t = torch.arange(hout.numel(), dtype=torch.int64, device=dev)
+    ins_s = timed(lambda: idx.insert_device(hout, slots_t), reps=1, warm=0)
+    m_out = torch.empty(n, dtype=torch.int64, device=dev)
+    s_out = torch.empty_like(hout)
+    look_s = timed(lambda: idx.lookup_device(coff, hout, s_out, m_out), reps=10)
+    res["index"] = {"insert_ms": ins_s * 1e3, "lookup_ms": look_s * 1e3, "lookups_per_s": hout.numel() / look_s}
+    # the reference's own scorer + sort on one core (oracle/_ref; the cpu_baseline leg), when built
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle as po
+
+    mm = [m.load.slope, m.load.intercept, m.comp.slope, m.comp.intercept]
+    if po.ref() is not None:
+        t0 = time.perf_counter()
+        ref_order = po.ref_sort_order(q, int(t.PolicyKind.Lstf), mm, cfg)
+        res["cpu_baseline"] = {"kind": "reference", "cores": 1, "cpu_model": cpu_model(),
+                               "score_plus_sort_us": (time.perf_counter() - t0) * 1e6,
+                               "sample": "the full 100K queue, LSTF: estimate_service_cost + priority_key + "
+                                         "std::sort(PriorityKey::operator<) of the compiled reference"}
+        res["order_equal_reference"] = bool(np.array_equal(order, ref_order))
+    del tok, hout, s_out, idx
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args):
     import torch
 
@@ -350,7 +579,7 @@ def run_ours(args):
         import torch.distributed as tdist
 
         # TSB_BENCH_ONE_DEVICE=1 (a validation mode, not a measurement): every rank on cuda:0 over
-        # gloo, to exercise the multi-rank path (shared pool, head shards, reductions) on one GPU.
+        # gloo, to exercise the multi-rank path (pools, head shards, reductions) on one GPU.
         one_dev = os.environ.get("TSB_BENCH_ONE_DEVICE") == "1"
         local = 0 if one_dev else local
         torch.cuda.set_device(local)
@@ -362,7 +591,7 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    from paper_2603_21257_b200 import _capi, ingest
+    from paper_2603_21257_b200 import ingest
     from paper_2603_21257_b200.multirank import reduce_timing
     from paper_2603_21257_b200.stage import LoadStage
     from paper_2603_21257_b200.tiersim import PolicyKind
@@ -372,87 +601,28 @@ def run_ours(args):
     wl.for_rank(world, rank)  # validates the head split
     seed = 20261017
     ce_peak = measure_ce_peak(torch)
-    pool, pool_kind, shape = make_pool(wl.shape, wl.pool_slots, world, rank, dist, seed)
-    pool_seed = seed + rank if shape.tp_size == 1 and world > 1 else seed
-    pool_shape = pool.shape
+    pool, pool_kind, shape, pool_seed = make_pool(wl.shape, wl.pool_slots, world, rank, dist, seed, args.pool, dev)
     if args.emulate_tp > 1:  # one GPU standing in for rank 0 of a TP-sharded box (configs[2])
         if world > 1:
             raise SystemExit("--emulate-tp is for single-GPU runs")
         shape = wl.shape.with_rank(args.emulate_tp, 0)
+    hbm_peak, hbm_src = measured_peaks()
 
-    # The same L2 pool resident in this GPU's HBM (same slot layout and contents): the `value` arm.
-    dpool = None
-    if not args.no_hbm_arm:
-        free, _ = torch.cuda.mem_get_info()
-        if wl.pool_slots * pool_shape.chunk_bytes + (40 << 30) < free:
-            dpool = ingest.ChunkPool.create_device(pool_shape, wl.pool_slots, device=dev)
-            dpool.fill_synthetic(pool_seed)
-
-    # L1 arena: most of the remaining HBM, fewer pages than the batch needs so FIFO deferral is
-    # exercised.  Both arms share it.
-    free, total = torch.cuda.mem_get_info()
-    page = shape.page_bytes
-    need_pages = wl.chunks * shape.pages_per_chunk
-    arena_bytes = min(free - (10 << 30), args.l1_gib << 30)
-    num_pages = min(arena_bytes // page, need_pages)
-    max_chunks = max(len(s) for s in wl.slots)
-    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=wl.queue.n + 1, max_chunks=max(max_chunks, 128),
-                             layout=ingest.LAYOUTS[args.layout])
-    mode = ingest.MODES[args.mode]
-    stage_host = LoadStage(l1, pool)
-    host_slots, tier_chunks = wl.slots, 0
-    if args.hbm_tier_chunks > 0:
-        # The first K chunks of every request are already resident in an HBM tier (the value arm's
-        # device pool, which holds every slot): they bypass the host link (tsb_ingest_tiered).
-        if dpool is None:
-            raise SystemExit("--hbm-tier-chunks needs the HBM arm's device pool")
-        host_slots = [[~s if k < args.hbm_tier_chunks else s for k, s in enumerate(sl)] for sl in wl.slots]
-        tier_chunks = sum(min(args.hbm_tier_chunks, len(sl)) for sl in wl.slots)
-    run_host = lambda verify=0: stage_host.run(wl.queue, host_slots, wl.config, policy=PolicyKind.Fifo, mode=mode,
-                                               verify_seed=verify)
-
-    # ---- value: L2 pool resident in HBM, CUDA events around K stage passes ----------------------
-    hbm = None
-    if dpool is not None:
-        stage_dev = LoadStage(l1, dpool)
-        run_dev = lambda verify=0: stage_dev.run(wl.queue, wl.slots, wl.config, policy=PolicyKind.Fifo,
-                                                 verify_seed=verify)
-        for i in range(args.warmup):
-            r = run_dev(pool_seed if i == 0 else 0)
-            if i == 0 and r.stats["verify_mismatches"]:
-                raise SystemExit(f"ingest parity failure (HBM pool): {r.stats['verify_mismatches']} words")
-        d_s, d_wall, d_res, d_launch, d_clk = timed_steps(torch, run_dev, args.steps, dist, _capi)
-        d_s, d_wall, d_bytes = reduce_timing(dist, d_s, d_wall, float(d_res.stats["bytes"]),
-                                             device=coll_device(dist))
-        k1_items = max_chunks
-        k1_alg, k1_s = measure_k1_hbm(torch, l1, dpool, shape, k1_items)
-        hbm = dict(dev_s=d_s, bytes=d_bytes, launches=d_launch, clocks=d_clk, stats=d_res.stats,
-                   k1_alg=k1_alg, k1_s=k1_s, k1_items=k1_items)
-        stage_dev.close()
-        if args.hbm_tier_chunks > 0:
-            stage_host.set_hbm_tier(dpool)
-        else:
-            dpool.close()
-        torch.cuda.synchronize()
-
-    # ---- e2e: pinned host pool, every byte crosses the host link inside the timed region -------
-    for i in range(args.warmup):
-        r = run_host(pool_seed if i == 0 else 0)  # the first one checks every page
-        if i == 0 and r.stats["verify_mismatches"]:
-            raise SystemExit(f"ingest parity failure: {r.stats['verify_mismatches']} mismatching words")
-    h_s, wall_s, results, h_launch, h_clk = timed_steps(torch, run_host, args.steps, dist, _capi)
-    local_bytes = results.stats["bytes"]
-    link_bytes = local_bytes - tier_chunks * shape.local_chunk_bytes  # what crossed the host link
-    h_s, wall_s, total_bytes = reduce_timing(dist, h_s, wall_s, float(local_bytes), device=coll_device(dist))
-    host_dev_rate = args.steps * total_bytes / h_s / 1e9
+    # ---- value + e2e: the north-star hop, pinned host pool -> L1 pages ---------------------------
+    m, l1 = stage_pass(torch, wl, shape, pool, pool_seed, args.steps, args.warmup, args.l1_gib,
+                       layout=ingest.LAYOUTS[args.layout], mode=ingest.MODES[args.mode], dist=dist)
+    local_bytes = m["bytes"]
+    dev_s, wall_s, total_bytes = reduce_timing(dist, m["dev_s"], m["wall_s"], local_bytes, device=coll_device(dist))
+    value = args.steps * total_bytes / dev_s / 1e9
     e2e = args.steps * total_bytes / wall_s / 1e9
+    link_rate = args.steps * local_bytes / m["dev_s"] / 1e9  # this rank's link
 
-    # The hand-written SM ingest kernels on the same stage, first 2 requests of the batch: K1
-    # (16-byte zero-copy loads) and K1b (cp.async.bulk / TMA engine).  AUTO picks CE+K2 for
-    # full-head chunks because SM-initiated host reads cap at ~92.6% of the copy-engine rate.
-    s = torch.cuda.current_stream()
+    # the hand-written SM ingest kernels on the same stage, first 2 requests: K1 (16-byte zero-copy
+    # loads) and K1b (cp.async.bulk); AUTO picks CE+K2 for host pools (SM reads cap at ~92.5%)
     modes = {}
     if not args.no_alt_modes:
+        stage_host = LoadStage(l1, pool)
+        s = torch.cuda.current_stream()
         sub = type(wl.queue)(2, **{k: getattr(wl.queue, k)[:2] for k, _ in type(wl.queue).FIELDS})
         for name in (("zerocopy", "ce") if args.layout == "flashinfer_hnd" else ("bulk", "zerocopy", "ce")):
             stage_host.run(sub, wl.slots[:2], wl.config, mode=ingest.MODES[name])  # warm
@@ -461,89 +631,101 @@ def run_ours(args):
             r = stage_host.run(sub, wl.slots[:2], wl.config, mode=ingest.MODES[name])
             b.record(s)
             b.synchronize()
-            modes[name] = {"GBps": r.stats["bytes"] / (a.elapsed_time(b) * 1e-3) / 1e9,
-                           "host_link_frac": r.stats["bytes"] / (a.elapsed_time(b) * 1e-3) / 1e9 / ce_peak}
+            gbs = r.stats["bytes"] / (a.elapsed_time(b) * 1e-3) / 1e9
+            modes[name] = {"GBps": gbs, "host_link_frac": gbs / ce_peak}
+        stage_host.close()
         if dist:
             dist.barrier()
 
     # K2 (the CE path's paged scatter, HBM-bound), measured live on the stage's group size
     layer_bytes = 2 * shape.chunk_tokens * shape.heads_local * shape.head_dim * shape.dtype_bytes
-    k2_items = min((512 << 20) // layer_bytes, max_chunks)  # items of one request in a staging half
+    k2_items = min((512 << 20) // layer_bytes, m["max_chunks"])
     k2_alg, k2_s = measure_k2(torch, l1, shape, n_items=k2_items)
-    hbm_peak, hbm_src = measured_peaks()
-    k2_traffic = scaled_traffic("k2_ncu_summary.json", k2_alg)
     k2_roof = {"bound": "hbm", "kernel": "k_ingest_ldg (K2 paged scatter from the CE staging ring, one staging group)",
                "achieved": k2_alg / k2_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-               "frac": k2_alg / k2_s / 1e9 / hbm_peak, "traffic": k2_traffic, "peak_source": hbm_src,
-               "algorithmic_bytes_per_launch": int(k2_alg), "launch_us": k2_s * 1e6}
-    req = results.requests
-    order = np.argsort(req["pick_position"])
-    ttft = {"first_layer_ms_p50": float(np.median(req["first_layer_ms"])),
-            "resident_ms_p50": float(np.median(req["resident_ms"])),
-            "resident_ms_max": float(req["resident_ms"].max()),
-            "resident_ms_first_request": float(req["resident_ms"][order[0]]),
-            "reference_model_ms_per_request": float(len(wl.slots[0]) * (10e-6 + shape.local_chunk_bytes / 64e9) * 1e3)}
-    bt_bytes = wl.queue.n * l1.stride * 4
-    link_rate = host_dev_rate / world * link_bytes / local_bytes
-    host_link = {"achieved": link_rate, "peak": ce_peak, "unit": "GB/s",
-                 "frac": link_rate / ce_peak, "ms_per_step": h_s / args.steps * 1e3,
-                 "peak_source": "live pinned 1 GiB cudaMemcpy H2D, best of 5, this box",
-                 "kernel_launches": int(h_launch)}
-    e2e_obj = {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(link_bytes + bt_bytes + wl.queue.n * 66),
-               "d2h_bytes_per_step": int(wl.queue.n * (8 + 16)),
-               "source": "L2 pool in pinned host memory (" + pool_kind + "); host wall time of the public-API "
-                         "calls (tsb_stage_run); the KV payload is the H2D traffic"}
+               "frac": k2_alg / k2_s / 1e9 / hbm_peak, "traffic": scaled_traffic("k2_ncu_summary.json", k2_alg),
+               "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(k2_alg), "launch_us": k2_s * 1e6,
+               "share_of_step": None}
+    roofline = {"bound": "host_link",
+                "kernel": "L2->L1 hop: copy engines (cudaMemcpyBatchAsync into the HBM staging ring) + K2 paged "
+                          "scatter; achieved = this GPU's payload bytes over the link / CUDA-event time of the passes",
+                "achieved": link_rate, "peak": ce_peak, "unit": "GB/s", "frac": link_rate / ce_peak,
+                "traffic": None, "peak_source": "live pinned 1 GiB cudaMemcpy H2D, best of 5, this box",
+                "theory_gen5_x16_gbs": GEN5_X16_GBS, "frac_of_theory": link_rate / GEN5_X16_GBS,
+                "algorithmic_bytes": "payload read from the host pool once (local chunk bytes x chunks)",
+                "k2_hbm_frac": k2_roof["frac"]}
+
+    # ---- hbm_tier: the same step with the pool in HBM (peer-HBM tier kernel path, K1) -----------
+    hbm_tier = None
+    if not args.no_hbm_tier:
+        free, _ = torch.cuda.mem_get_info()
+        l1_bytes = m["num_pages"] * m["page"]
+        if wl.pool_slots * pool.shape.chunk_bytes + (24 << 30) < free + l1_bytes:
+            del l1
+            torch.cuda.empty_cache()
+            dpool = ingest.ChunkPool.create_device(pool.shape, wl.pool_slots, device=dev)
+            dpool.fill_synthetic(pool_seed)
+            hm, l1 = stage_pass(torch, wl, shape, dpool, pool_seed, args.steps, min(args.warmup, 3), args.l1_gib,
+                                layout=ingest.LAYOUTS[args.layout], dist=dist)
+            h_s, _, h_bytes = reduce_timing(dist, hm["dev_s"], hm["wall_s"], hm["bytes"], device=coll_device(dist))
+            k1_alg, k1_s = measure_k1_hbm(torch, l1, dpool, shape, hm["max_chunks"])
+            hbm_tier = {"value": args.steps * h_bytes / h_s / 1e9, "unit": UNIT,
+                        "ms_per_step": h_s / args.steps * 1e3, "gpu_launches": hm["launches"], "clocks": hm["clocks"],
+                        "source": "the same L2 pool slots held in this GPU's HBM (tsb_pool_create_device), CUDA events",
+                        "roofline": {"bound": "hbm", "kernel": "k_ingest_ldg (K1 over the HBM-resident pool)",
+                                     "achieved": k1_alg / k1_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                     "frac": k1_alg / k1_s / 1e9 / hbm_peak,
+                                     "traffic": scaled_traffic("k1hbm_ncu_summary.json", k1_alg),
+                                     "algorithmic_bytes_per_launch": int(k1_alg), "launch_us": k1_s * 1e6}}
+            dpool.close()
+    del l1
+    torch.cuda.empty_cache()
+
+    bt_bytes = wl.queue.n * (max(m["max_chunks"], 128) * shape.pages_per_chunk) * 4
     cfg = {"workload": wl.name, "description": wl.description,
-           "hbm_tier": ({"chunks_per_step": tier_chunks, "bytes_per_step": int(tier_chunks * shape.local_chunk_bytes),
-                         "note": "first K chunks of every request resident in an HBM tier (tsb_ingest_tiered); "
-                                 "e2e counts all delivered bytes, h2d only the host-link part"}
-                        if tier_chunks else None),
            "parallelism": (f"kv-head shards tp{world}" if world > 1 else
                            f"single GPU as rank 0 of a tp{args.emulate_tp} head split" if args.emulate_tp > 1
                            else "single GPU"),
-           "ingest_mode": args.mode, "policy": "fifo", "l1_layout": args.layout, "l1_pages": int(num_pages),
-           "l1_page_bytes": int(page), "l1_gib": round(num_pages * page / 2**30, 1),
+           "ingest_mode": args.mode, "policy": "fifo", "l1_layout": args.layout, "l1_pages": m["num_pages"],
+           "l1_page_bytes": m["page"], "l1_gib": round(m["num_pages"] * m["page"] / 2**30, 1),
            "bytes_per_step": int(total_bytes), "pool": pool_kind,
-           "l2_flush": "inputs larger than L2 (each step streams the whole batch: 100s of GB)"}
-    if hbm is not None:
-        value = args.steps * hbm["bytes"] / hbm["dev_s"] / 1e9
-        ms_per_step = hbm["dev_s"] / args.steps * 1e3
-        launches = hbm["launches"]
-        clocks = hbm["clocks"]
-        k1_traffic = scaled_traffic("k1hbm_ncu_summary.json", hbm["k1_alg"])
-        roofline = {"bound": "hbm", "kernel": "k_ingest_ldg (K1 over the HBM-resident pool, 4736 CTAs, 4 loads in flight per lane)",
-                    "achieved": hbm["k1_alg"] / hbm["k1_s"] / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": hbm["k1_alg"] / hbm["k1_s"] / 1e9 / hbm_peak, "traffic": k1_traffic,
-                    "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(hbm["k1_alg"]),
-                    "launch_us": hbm["k1_s"] * 1e6, "items_per_launch": hbm["k1_items"],
-                    "algorithmic_bytes": "read + write of the payload (2 x chunks x layers [1, L) x layer slice)"}
-        cfg["value_source"] = ("L2 pool resident in HBM (tsb_pool_create_device, same slots and bytes); "
-                               "CUDA events on the stage stream around the K passes")
-        cfg["hbm_arm_stage"] = {k: hbm["stats"][k] for k in ("ingest_calls", "deferred_chunks", "releases",
-                                                             "kernel_launches")}
-    else:  # HBM cannot hold pool + L1: value falls back to the host-pool device time
-        value, ms_per_step, launches, clocks, roofline = host_dev_rate, h_s / args.steps * 1e3, h_launch, h_clk, k2_roof
-        cfg["value_source"] = "L2 pool in pinned host memory (HBM too small for the pool); CUDA events"
+           "l2_flush": "inputs larger than L2 (each step streams the whole batch: 100s of GB)",
+           "value_source": "L2 pool in pinned host memory; CUDA events on the stage stream around the K passes",
+           "stage": m["stats"]}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": cfg,
-        "e2e": e2e_obj, "gpu_launches": int(launches), "roofline": roofline,
-        "roofline_k2": k2_roof, "host_link": host_link, "ttft_load_ms": ttft,
-        "stage": {k: results.stats[k] for k in ("ingest_calls", "deferred_chunks", "releases", "kernel_launches")},
-        "clocks": clocks, "clocks_e2e": h_clk,
-        "ingest_modes_2req": modes,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(local_bytes + bt_bytes + wl.queue.n * 66),
+                "d2h_bytes_per_step": int(wl.queue.n * (8 + 16)),
+                "source": "host wall time of the public-API calls (tsb_stage_run) over the same K passes: queue "
+                          "and block-table uploads, ingest, results read back; the KV payload is the H2D traffic"},
+        "gpu_launches": m["launches"], "roofline": roofline, "roofline_k2": k2_roof,
+        "host_link": {"achieved": link_rate, "peak": ce_peak, "frac": link_rate / ce_peak, "unit": UNIT},
+        "ttft_load_ms": m["ttft"], "clocks": m["clocks"], "ingest_modes_2req": modes, "hbm_tier": hbm_tier,
     }
+    if world == 1 and not args.no_side and args.workload == "qwen16x128k" and args.emulate_tp == 1:
+        pool.close()
+        line["workloads"] = side_workloads(torch, args, ce_peak, hbm_peak, seed, dev)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        sample = args.cpu_sample_chunks
-        view = pool.slot_view(0, sample)
-        gbs, nbytes, secs = cpu_scatter_baseline(wl.shape, sample, seed, threads, pool_view=view, min_seconds=10.0)
-        passes = max(2, int(round(10.0 / secs)))
-        line["cpu_baseline"] = {"value": gbs, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"{sample} chunks ({nbytes / 1e9:.2f} GB) of {wl.name} from the pinned "
-                                          f"pool, oracle scatter_ref, {threads} threads, ~{passes} passes over "
-                                          f">= 10 s of CPU work (mean)"}
+        spec = SPECS[args.workload]
+        shp, items, bt, num_pages, n_slots = reference_sample(spec, args.cpu_chunks_per_request)
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import pyoracle as po
+
+        view = po.synth_fill(7, 0, n_slots * shp.chunk_bytes // 8, threads).view(np.uint8)
+        arena = np.empty(shp.layers * 2 * num_pages * 16 * shp.heads_local * shp.head_dim * 2, np.uint8)
+        cpu_scatter(shp, view, items, bt, num_pages, threads, arena)  # first touch
+        times = []
+        while len(times) < 2 or sum(times) < 10.0:
+            times.append(cpu_scatter(shp, view, items, bt, num_pages, threads, arena))
+        nbytes = len(items) * shp.local_chunk_bytes
+        line["cpu_baseline"] = {"value": nbytes * len(times) / sum(times) / 1e9, "unit": UNIT, "cores": threads,
+                                "kind": "port", "cpu_model": cpu_model(),
+                                "sample": f"{len(items)} chunks ({nbytes / 1e9:.2f} GB) of the {spec['name']} batch "
+                                          f"in FIFO pick order, oracle scatter_ref, {threads} threads, "
+                                          f"{len(times)} passes over >= 10 s of CPU work (mean)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -557,22 +739,29 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="qwen16x128k")
+    ap.add_argument("--workload", default="qwen16x128k", choices=sorted(SPECS))
     ap.add_argument("--mode", default="auto", choices=["auto", "ce", "bulk", "zerocopy"])
+    ap.add_argument("--pool", default="numa", choices=["numa", "shared", "hostalloc"])
     ap.add_argument("--l1-gib", type=int, default=100)
     ap.add_argument("--layout", default="flash_attn", choices=["flash_attn", "flashinfer_nhd", "flashinfer_hnd"],
                     help="the consumer's L1 page layout")
-    ap.add_argument("--hbm-tier-chunks", type=int, default=0,
-                    help="e2e arm: the first K chunks of every request come from an HBM tier (not the headline)")
     ap.add_argument("--emulate-tp", type=int, default=1, help="one GPU ingests rank 0's head slice of a tpN split")
-    ap.add_argument("--no-hbm-arm", action="store_true", help="skip the HBM-resident-pool arm (value)")
-    ap.add_argument("--cpu-sample-chunks", type=int, default=128)
+    ap.add_argument("--one-device", action="store_true",
+                    help="validation: with --gpus N > 1, every rank on cuda:0 over gloo (not a measurement)")
+    ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident-pool arm")
+    ap.add_argument("--no-side", action="store_true", help="skip the configs[0]/[2]/[4] sub-lines")
+    ap.add_argument("--cpu-chunks-per-request", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt-modes", action="store_true", help="skip the K1/K1b/CE side measurements")
     args = ap.parse_args()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
-        raise SystemExit(f"--gpus {args.gpus}: launch one process per GPU with "
-                         f"`python -m torch.distributed.run --nproc-per-node {args.gpus} bench.py --gpus {args.gpus}`")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "ours" and not args.one_device:
+            import torch
+
+            if torch.cuda.device_count() < args.gpus:
+                raise SystemExit(f"--gpus {args.gpus}: only {torch.cuda.device_count()} GPUs visible "
+                                 f"(--one-device runs every rank on cuda:0 as a validation)")
+        sys.exit(launch_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:
