@@ -634,6 +634,7 @@ def run_ours(args):
             gbs = r.stats["bytes"] / (a.elapsed_time(b) * 1e-3) / 1e9
             modes[name] = {"GBps": gbs, "host_link_frac": gbs / ce_peak}
         stage_host.close()
+        del stage_host
         if dist:
             dist.barrier()
 

@@ -224,7 +224,8 @@ typedef struct tsb_index tsb_index;
 tsb_status tsb_index_create(int device, int64_t capacity, tsb_index** out);
 void tsb_index_destroy(tsb_index* x);
 int64_t tsb_index_capacity(const tsb_index* x);
-/* Device pointers; async.  Re-inserting an indexed hash updates its slot. */
+/* Device pointers; async.  Re-inserting an indexed hash updates its slot; when one batch holds
+ * the same hash more than once, the lowest batch index wins (deterministic). */
 tsb_status tsb_index_insert_device(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes,
                                    const int64_t* slots);
 tsb_status tsb_index_erase_device(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes);
@@ -237,6 +238,12 @@ tsb_status tsb_index_lookup_device(tsb_index* x, void* stream, int64_t n_req,
                                    int64_t* slots_out, int64_t* matched_out);
 /* Live entries and failed inserts (table full); synchronises. */
 tsb_status tsb_index_stats(tsb_index* x, void* stream, int64_t* live, int64_t* full_failures);
+/* Drop every entry (synchronous on `stream` order only). */
+tsb_status tsb_index_clear(tsb_index* x, void* stream);
+/* Rebuild the table without the tombstones erases left (probe paths shorten again); reports how
+ * many were reclaimed.  Synchronises.  The host tsb_index_insert compacts by itself when a batch
+ * finds the table full and tombstones exist. */
+tsb_status tsb_index_compact(tsb_index* x, void* stream, int64_t* tombstones_reclaimed);
 /* Host-pointer variants (synchronise); insert returns CAPACITY if the table is full.
  * chunk_offsets[0] must be 0. */
 tsb_status tsb_index_insert(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes,
@@ -479,6 +486,9 @@ typedef struct {
   int32_t record_trace; /* 1: keep TraceEvent-schema rows (events.hpp:33-42) for the run */
   uint64_t verify_seed; /* harness check, 0 = off: before a request's pages are released, count
                            page words differing from tsb_pool_fill_synthetic(verify_seed) */
+  int32_t pace_network; /* online mode with an L3 store: a network hop lasts at least
+                           transfer_base_latency + bytes / network_bandwidth (engine.cpp:205) */
+  int32_t reserved0;
 } tsb_stage_options;
 
 typedef struct {
@@ -503,6 +513,8 @@ typedef struct {
   int64_t releases;
   int64_t kernel_launches; /* libtsb kernels launched during the run */
   uint64_t verify_mismatches; /* with verify_seed != 0 */
+  int64_t net_blocks;      /* online mode with an L3 store: L3 -> L2 network hops */
+  int64_t l2_deferred;     /* ... L2 reservations that waited for a release (engine.cpp:357-362) */
 } tsb_stage_stats;
 
 /* TraceEvent row (events.hpp:33-42): kind 1 TransferDone, 2 AllocationGrant, 4 DispatchWake;
@@ -520,6 +532,21 @@ typedef struct {
 } tsb_trace_row;
 
 tsb_status tsb_stage_create(tsb_l1* l1, tsb_pool* pool, tsb_stage** out);
+/* Online mode only: blocks start in the L3 store `l3` (a host pool of the same chunk geometry;
+ * slots passed to tsb_stage_run_online name L3 chunks) and make the network hop L3 -> L2 for
+ * real: the stage's pool becomes the L2 tier, a TierLedger(L2) over min(l2_capacity, slots)
+ * whole slots with a FIFO slot free list (request_l2 at admit, engine.cpp:341-362; released when
+ * the block's L2 -> L1 hop completes, :264); one block in flight, copied by `copy_threads` host
+ * threads (engine.cpp:405-425).  NULL detaches.  tsb_stage_run returns UNSUPPORTED while set. */
+tsb_status tsb_stage_set_l3(tsb_stage* s, tsb_pool* l3, int copy_threads);
+/* Prefill consumer: called on the host for every layer of a request's prefill, after the stage
+ * made the compute stream wait for that layer's fence; enqueue the layer's work on `stream` (the
+ * stage's compute stream) and return 0.  Replaces the K6 timer (the reference's compute stage,
+ * engine.cpp:448-473; ComputeDone = the stream passing the last layer).  NULL restores K6. */
+typedef int (*tsb_prefill_hook)(void* user, int64_t q_index, int32_t bt_row, int64_t layer, void* stream);
+tsb_status tsb_stage_set_prefill_hook(tsb_stage* s, tsb_prefill_hook hook, void* user);
+/* The stage's compute stream (lowest priority; prefill runs here). */
+void* tsb_stage_compute_stream(tsb_stage* s);
 void tsb_stage_destroy(tsb_stage* s);
 /* HBM tier of the stage (NULL clears it): in tsb_stage_run / _online, a slot < 0 names slot ~slot
  * of hbm_pool (same chunk geometry as the L2 pool); those chunks bypass the host link. */

@@ -102,6 +102,8 @@ def restate():
         d(lib, "orc_scatter_ref", None, C.POINTER(OrcShape), vp, i64, vp, vp, i64, i64, vp, i64, i64, C.c_int)
         d(lib, "orc_scatter_ref_layout", None, C.POINTER(OrcShape), vp, i64, vp, vp, i64, i64, vp, i64, i64, C.c_int,
           C.c_int)
+        d(lib, "orc_scatter_ref_window", None, C.POINTER(OrcShape), vp, i64, vp, vp, i64, i64, vp, i64, i64, C.c_int,
+          C.c_int)
         d(lib, "orc_mix64", u64, u64)
         d(lib, "orc_synth_word", u64, u64, u64)
         d(lib, "orc_synth_fill", None, u64, u64, u64, vp, C.c_int)
@@ -216,6 +218,20 @@ def scatter_ref(shape, pool: np.ndarray, items: np.ndarray, block_table: np.ndar
                  shape.page_tokens, shape.tp_size, shape.tp_rank)
     bt = np.ascontiguousarray(block_table, np.int32)
     restate().orc_scatter_ref_layout(C.byref(s), pool.ctypes.data, len(items), items.ctypes.data, bt.ctypes.data,
+                                     bt.shape[1], num_pages, arena.ctypes.data, layer_lo, layer_hi, threads, layout)
+    return arena
+
+
+def scatter_ref_window(shape, pool: np.ndarray, items: np.ndarray, block_table: np.ndarray, num_pages: int,
+                       layer_lo: int, layer_hi: int, threads: int = 1, layout: int = 0) -> np.ndarray:
+    """scatter_ref of layers [layer_lo, layer_hi) only; returns just those layers of the arena."""
+    hl = shape.kv_heads // shape.tp_size
+    layer_bytes = 2 * num_pages * shape.page_tokens * hl * shape.head_dim * shape.dtype_bytes
+    arena = np.zeros((layer_hi - layer_lo) * layer_bytes, dtype=np.uint8)
+    s = OrcShape(shape.layers, shape.kv_heads, shape.head_dim, shape.dtype_bytes, shape.chunk_tokens,
+                 shape.page_tokens, shape.tp_size, shape.tp_rank)
+    bt = np.ascontiguousarray(block_table, np.int32)
+    restate().orc_scatter_ref_window(C.byref(s), pool.ctypes.data, len(items), items.ctypes.data, bt.ctypes.data,
                                      bt.shape[1], num_pages, arena.ctypes.data, layer_lo, layer_hi, threads, layout)
     return arena
 

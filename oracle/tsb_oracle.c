@@ -331,10 +331,11 @@ int64_t orc_pages_available(const orc_pages* p) { return p->len; }
 /*   0 flash-attn   layer = [2][pages][P][Hl][D]  (v1/attention/backends/flash_attn.py:140-149) */
 /*   1 FlashInfer   layer = [pages][2][P][Hl][D]  (flashinfer.py:357-368, NHD order :380-381)  */
 /*   2 FlashInfer   layer = [pages][2][Hl][P][D]  (HND stride order, flashinfer.py:385-386)    */
-void orc_scatter_ref_layout(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,
-                            const orc_ingest_item* items, const int32_t* block_table,
-                            int64_t bt_stride, int64_t num_pages, uint8_t* arena, int64_t layer_lo,
-                            int64_t layer_hi, int threads, int layout) {
+/* arena_layer0: the arena buffer starts at layer arena_layer0 (a window of layers; 0 = whole). */
+static void scatter_ref_impl(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,
+                             const orc_ingest_item* items, const int32_t* block_table,
+                             int64_t bt_stride, int64_t num_pages, uint8_t* arena, int64_t layer_lo,
+                             int64_t layer_hi, int threads, int layout, int64_t arena_layer0) {
   const int64_t L = s->layers, H = s->kv_heads, D = s->head_dim, E = s->dtype_bytes;
   const int64_t C = s->chunk_tokens, P = s->page_tokens;
   const int64_t Hl = H / s->tp_size, h0 = s->tp_rank * Hl;
@@ -352,7 +353,7 @@ void orc_scatter_ref_layout(const orc_kv_shape* s, const uint8_t* pool, int64_t 
       for (int64_t j = 0; j < ppc; ++j) {
         const int64_t page = block_table[it.bt_row * bt_stride + it.chunk_index * ppc + j];
         const int64_t seg = P * run; /* one (layer, K|V, page) unit */
-        uint8_t* dst = arena + l * 2 * num_pages * seg +
+        uint8_t* dst = arena + (l - arena_layer0) * 2 * num_pages * seg +
                        (layout == 0 ? (kv * num_pages + page) * seg : (page * 2 + kv) * seg);
         const uint8_t* src = chunk + ((l * 2 + kv) * C + j * P) * row + h0 * D * E;
         if (layout == 2) { /* [Hl][P][D]: head h's row of token t */
@@ -367,6 +368,24 @@ void orc_scatter_ref_layout(const orc_kv_shape* s, const uint8_t* pool, int64_t 
       }
     }
   }
+}
+
+void orc_scatter_ref_layout(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,
+                            const orc_ingest_item* items, const int32_t* block_table,
+                            int64_t bt_stride, int64_t num_pages, uint8_t* arena, int64_t layer_lo,
+                            int64_t layer_hi, int threads, int layout) {
+  scatter_ref_impl(s, pool, n_items, items, block_table, bt_stride, num_pages, arena, layer_lo,
+                   layer_hi, threads, layout, 0);
+}
+
+/* Layers [layer_lo, layer_hi) only, into an arena buffer holding just those layers (full-size
+ * parity checks of sampled layers without a whole-model host arena). */
+void orc_scatter_ref_window(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,
+                            const orc_ingest_item* items, const int32_t* block_table,
+                            int64_t bt_stride, int64_t num_pages, uint8_t* arena_window,
+                            int64_t layer_lo, int64_t layer_hi, int threads, int layout) {
+  scatter_ref_impl(s, pool, n_items, items, block_table, bt_stride, num_pages, arena_window,
+                   layer_lo, layer_hi, threads, layout, layer_lo);
 }
 
 void orc_scatter_ref(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,

@@ -135,6 +135,10 @@ void orc_scatter_ref_layout(const orc_kv_shape* s, const uint8_t* pool, int64_t 
                             const orc_ingest_item* items, const int32_t* block_table,
                             int64_t bt_stride, int64_t num_pages, uint8_t* arena, int64_t layer_lo,
                             int64_t layer_hi, int threads, int layout);
+void orc_scatter_ref_window(const orc_kv_shape* s, const uint8_t* pool, int64_t n_items,
+                            const orc_ingest_item* items, const int32_t* block_table,
+                            int64_t bt_stride, int64_t num_pages, uint8_t* arena_window,
+                            int64_t layer_lo, int64_t layer_hi, int threads, int layout);
 
 /* synthetic data */
 uint64_t orc_mix64(uint64_t x);

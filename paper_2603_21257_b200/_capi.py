@@ -97,7 +97,7 @@ class IngestItem(C.Structure):
 
 class StageOptions(C.Structure):
     _fields_ = [("mode", i32), ("policy", i32), ("layer_events", i32), ("prefill", i32), ("prefill_ctas", i32),
-                ("record_trace", i32), ("verify_seed", u64)]
+                ("record_trace", i32), ("verify_seed", u64), ("pace_network", i32), ("reserved0", i32)]
 
 
 class StageRequest(C.Structure):
@@ -108,7 +108,8 @@ class StageRequest(C.Structure):
 
 class StageStats(C.Structure):
     _fields_ = [("bytes", i64), ("device_ms", f64), ("wall_ms", f64), ("ingest_calls", i64),
-                ("deferred_chunks", i64), ("releases", i64), ("kernel_launches", i64), ("verify_mismatches", u64)]
+                ("deferred_chunks", i64), ("releases", i64), ("kernel_launches", i64), ("verify_mismatches", u64),
+                ("net_blocks", i64), ("l2_deferred", i64)]
 
 
 class TraceRow(C.Structure):
@@ -165,6 +166,8 @@ _decl("tsb_index_erase_device", st, vp, vp, i64, vp)
 _decl("tsb_index_lookup_device", st, vp, vp, i64, vp, vp, vp, vp)
 _decl("tsb_index_stats", st, vp, vp, P(i64), P(i64))
 _decl("tsb_index_insert", st, vp, vp, i64, vp, vp)
+_decl("tsb_index_clear", st, vp, vp)
+_decl("tsb_index_compact", st, vp, vp, P(i64))
 _decl("tsb_index_lookup", st, vp, vp, i64, vp, vp, vp, vp)
 _decl("tsb_pool_create", st, P(KvShape), i64, P(vp))
 _decl("tsb_pool_wrap", st, P(KvShape), vp, i64, P(vp))
@@ -217,6 +220,10 @@ _decl("tsb_l1_shape", st, vp, P(KvShape))
 _decl("tsb_stage_create", st, vp, vp, P(vp))
 _decl("tsb_stage_destroy", None, vp)
 _decl("tsb_stage_set_hbm_tier", st, vp, vp)
+_decl("tsb_stage_set_l3", st, vp, vp, C.c_int)
+PREFILL_HOOK = C.CFUNCTYPE(C.c_int, vp, i64, i32, i64, vp)
+_decl("tsb_stage_set_prefill_hook", st, vp, PREFILL_HOOK, vp)
+_decl("tsb_stage_compute_stream", vp, vp)
 _decl("tsb_stage_run", st, vp, i64, P(Queue), P(Cluster), P(f64), vp, vp, P(StageOptions), vp, P(StageRequest),
       P(StageStats))
 _decl("tsb_stage_trace", st, vp, P(TraceRow), i64, P(i64))

@@ -14,7 +14,11 @@ struct tsb_index {
   int device = 0;
   uint64_t* keys = nullptr;
   int64_t* vals = nullptr;
+  uint64_t* owner = nullptr;  // winning insert tag per entry (deterministic duplicates)
   uint64_t mask = 0;
+  uint64_t epoch = 0;         // insert calls so far
+  int64_t* pos = nullptr;     // per-batch entry positions (grow-only)
+  int64_t pos_cap = 0;
   unsigned long long* stats = nullptr;  // [0] entries inserted, [1] full failures, [2] erased
 };
 
@@ -49,22 +53,48 @@ tsb_status check_keys(int64_t n, const uint64_t* hashes) {
 
 extern "C" {
 
+namespace {
+void free_index_arrays(tsb_index* x) {
+  cudaFree(x->keys);
+  cudaFree(x->vals);
+  cudaFree(x->owner);
+  x->keys = nullptr;
+  x->vals = nullptr;
+  x->owner = nullptr;
+}
+cudaError_t alloc_index_arrays(tsb_index* x, int64_t cap) {
+  cudaError_t e = cudaMalloc(&x->keys, sizeof(uint64_t) * cap);
+  if (e == cudaSuccess) e = cudaMalloc(&x->vals, sizeof(int64_t) * cap);
+  if (e == cudaSuccess) e = cudaMalloc(&x->owner, sizeof(uint64_t) * cap);
+  if (e == cudaSuccess) e = cudaMemset(x->keys, 0xff, sizeof(uint64_t) * cap);
+  if (e == cudaSuccess) e = cudaMemset(x->owner, 0, sizeof(uint64_t) * cap);
+  return e;
+}
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
 tsb_status tsb_index_create(int device, int64_t capacity, tsb_index** out) {
   if (capacity < 1 || capacity > (1ll << 40)) return fail(TSB_VALIDATION, "index: capacity out of range");
   int64_t cap = 1;
   while (cap < capacity) cap <<= 1;
-  TSB_CUDA_TRY(cudaSetDevice(device));
+  DeviceGuard dg(device);
   auto* x = new tsb_index();
   x->device = device;
   x->mask = static_cast<uint64_t>(cap - 1);
-  cudaError_t e = cudaMalloc(&x->keys, sizeof(uint64_t) * cap);
-  if (e == cudaSuccess) e = cudaMalloc(&x->vals, sizeof(int64_t) * cap);
+  cudaError_t e = alloc_index_arrays(x, cap);
   if (e == cudaSuccess) e = cudaMalloc(&x->stats, 3 * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(x->keys, 0xff, sizeof(uint64_t) * cap);
   if (e == cudaSuccess) e = cudaMemset(x->stats, 0, 3 * sizeof(unsigned long long));
   if (e != cudaSuccess) {
-    cudaFree(x->keys);
-    cudaFree(x->vals);
+    free_index_arrays(x);
     cudaFree(x->stats);
     delete x;
     return tsb::cuda_fail(e, "tsb_index_create");
@@ -75,18 +105,69 @@ tsb_status tsb_index_create(int device, int64_t capacity, tsb_index** out) {
 
 void tsb_index_destroy(tsb_index* x) {
   if (!x) return;
-  cudaFree(x->keys);
-  cudaFree(x->vals);
+  DeviceGuard dg(x->device);
+  free_index_arrays(x);
+  cudaFree(x->pos);
   cudaFree(x->stats);
   delete x;
+}
+
+tsb_status tsb_index_clear(tsb_index* x, void* stream) {
+  DeviceGuard dg(x->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t cap = x->mask + 1;
+  TSB_CUDA_TRY(cudaMemsetAsync(x->keys, 0xff, sizeof(uint64_t) * cap, st));
+  TSB_CUDA_TRY(cudaMemsetAsync(x->owner, 0, sizeof(uint64_t) * cap, st));
+  TSB_CUDA_TRY(cudaMemsetAsync(x->stats, 0, 3 * sizeof(unsigned long long), st));
+  return TSB_OK;
+}
+
+tsb_status tsb_index_compact(tsb_index* x, void* stream, int64_t* tombstones_reclaimed) {
+  DeviceGuard dg(x->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  unsigned long long h[3] = {0, 0, 0};
+  TSB_CUDA_TRY(cudaMemcpyAsync(h, x->stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+  TSB_CUDA_TRY(cudaStreamSynchronize(st));
+  if (tombstones_reclaimed) *tombstones_reclaimed = static_cast<int64_t>(h[2]);
+  if (h[2] == 0) return TSB_OK;
+  const int64_t cap = static_cast<int64_t>(x->mask + 1);
+  tsb_index old = *x;
+  cudaError_t e = alloc_index_arrays(x, cap);
+  if (e != cudaSuccess) {
+    free_index_arrays(x);
+    x->keys = old.keys;
+    x->vals = old.vals;
+    x->owner = old.owner;
+    return tsb::cuda_fail(e, "tsb_index_compact");
+  }
+  TSB_CUDA_TRY(tsb::launch_index_rehash(old.keys, old.vals, old.owner, static_cast<uint64_t>(cap), x->keys,
+                                        x->vals, x->owner, x->mask, st));
+  const unsigned long long fresh[3] = {h[0] - h[2], 0, 0};
+  TSB_CUDA_TRY(cudaMemcpyAsync(x->stats, fresh, sizeof(fresh), cudaMemcpyHostToDevice, st));
+  TSB_CUDA_TRY(cudaStreamSynchronize(st));
+  free_index_arrays(&old);
+  return TSB_OK;
 }
 
 int64_t tsb_index_capacity(const tsb_index* x) { return static_cast<int64_t>(x->mask + 1); }
 
 tsb_status tsb_index_insert_device(tsb_index* x, void* stream, int64_t n, const uint64_t* hashes,
                                    const int64_t* slots) {
-  TSB_CUDA_TRY(tsb::launch_index_insert(x->keys, x->vals, x->mask, n, hashes, slots, x->stats,
-                                        static_cast<cudaStream_t>(stream)));
+  if (n <= 0) return TSB_OK;
+  if (n >= (1ll << 40)) return fail(TSB_VALIDATION, "index: batch too large");
+  DeviceGuard dg(x->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (n > x->pos_cap) {  // grow-only scratch; the previous batch may still be using it
+    TSB_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(x->pos);
+    x->pos = nullptr;
+    x->pos_cap = 0;
+    TSB_CUDA_TRY(cudaMalloc(&x->pos, sizeof(int64_t) * n));
+    x->pos_cap = n;
+  }
+  ++x->epoch;
+  TSB_CUDA_TRY(tsb::launch_index_insert(x->keys, x->vals, x->owner, x->mask, n, hashes, slots, x->epoch, x->pos,
+                                        x->stats, st));
   return TSB_OK;
 }
 
@@ -125,10 +206,23 @@ tsb_status tsb_index_insert(tsb_index* x, void* stream, int64_t n, const uint64_
   auto* ds = reinterpret_cast<int64_t*>(dh + n);
   TSB_CUDA_TRY(cudaMemcpyAsync(dh, hashes, 8 * n, cudaMemcpyHostToDevice, st));
   TSB_CUDA_TRY(cudaMemcpyAsync(ds, slots, 8 * n, cudaMemcpyHostToDevice, st));
+  int64_t live = 0, full0 = 0, full = 0;
+  TSB_TRY(tsb_index_stats(x, stream, &live, &full0));
   TSB_TRY(tsb_index_insert_device(x, stream, n, dh, ds));
-  int64_t live = 0, full = 0;
   TSB_TRY(tsb_index_stats(x, stream, &live, &full));
-  if (full) return fail(TSB_CAPACITY, "index: table full (" + std::to_string(full) + " inserts failed)");
+  if (full > full0) {
+    // Tombstones left by erases may be what fills the probe paths: compact and re-insert the
+    // batch once (idempotent: a later insert call wins every entry it touches).
+    int64_t reclaimed = 0;
+    TSB_TRY(tsb_index_compact(x, stream, &reclaimed));
+    if (reclaimed > 0) {
+      full0 = full;
+      TSB_TRY(tsb_index_insert_device(x, stream, n, dh, ds));
+      TSB_TRY(tsb_index_stats(x, stream, &live, &full));
+    }
+    if (full > full0)
+      return fail(TSB_CAPACITY, "index: table full (" + std::to_string(full - full0) + " inserts failed)");
+  }
   return TSB_OK;
 }
 

@@ -1079,25 +1079,64 @@ tsb_status tsb_l1_verify_synthetic(tsb_l1* l, const tsb_ingest_item* items, int6
                                    int64_t layer_lo, int64_t layer_hi, uint64_t seed,
                                    int64_t pool_chunk_bytes, void* stream,
                                    uint64_t* mismatches) {
+  // Independent of the ingest address math (verify.cu): invert the host block table into
+  // page -> (slot, first token), then check every word of those pages from the layout definition.
   auto st = static_cast<cudaStream_t>(stream);
-  tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
-  if (pool_chunk_bytes != g.chunk_bytes)
+  const tsb_kv_shape& sh = l->shape;
+  const int64_t L = sh.layers;
+  if (layer_lo < 0 || layer_hi > L || layer_lo > layer_hi)
+    return fail(TSB_VALIDATION, "verify: layer range out of bounds");
+  if (pool_chunk_bytes != L * 2 * sh.chunk_tokens * sh.kv_heads * sh.head_dim * sh.dtype_bytes)
     return fail(TSB_VALIDATION, "verify: pool chunk bytes differ from the L1 shape");
+  tsb::PageCheck c{};
+  c.H = sh.kv_heads;
+  c.Hl = sh.kv_heads / sh.tp_size;
+  c.D = sh.head_dim;
+  c.E = sh.dtype_bytes;
+  c.C = sh.chunk_tokens;
+  c.P = sh.page_tokens;
+  c.tp_rank = sh.tp_rank;
+  c.num_pages = l->num_pages;
+  c.pool_chunk_bytes = pool_chunk_bytes;
+  c.layout = l->layout;
+  c.layer_lo = static_cast<int32_t>(layer_lo);
+  c.layer_hi = static_cast<int32_t>(layer_hi);
+  std::vector<tsb::PageSource> pages;
+  pages.reserve(static_cast<size_t>(n_items * l->ppc));
+  std::vector<uint8_t> seen(static_cast<size_t>(l->num_pages), 0);
+  uint64_t host_bad = 0;
+  const int64_t words_per_page = (layer_hi - layer_lo) * 2 * c.P * c.Hl * c.D * c.E / 8;
+  for (int64_t i = 0; i < n_items; ++i) {
+    const tsb_ingest_item& it = items[i];
+    if (it.bt_row < 0 || it.bt_row >= l->rows || it.chunk_index < 0 || it.chunk_index >= l->max_chunks) {
+      host_bad += static_cast<uint64_t>(l->ppc * words_per_page);
+      continue;
+    }
+    for (int64_t j = 0; j < l->ppc; ++j) {
+      const int32_t page = l->bt_host[it.bt_row * l->stride + it.chunk_index * l->ppc + j];
+      if (page < 0 || page >= l->num_pages || seen[static_cast<size_t>(page)]) {
+        host_bad += static_cast<uint64_t>(words_per_page);  // unmapped or shared page: all wrong
+        continue;
+      }
+      seen[static_cast<size_t>(page)] = 1;
+      pages.push_back(tsb::PageSource{it.src_slot, page, static_cast<int32_t>(j * c.P)});
+    }
+  }
   TSB_CUDA_TRY(cudaMemsetAsync(l->verify_ctr, 0, sizeof(unsigned long long), st));
-  const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb_ingest_item));
-  for (int64_t i0 = 0; i0 < n_items; i0 += per) {
-    const int64_t n = std::min(per, n_items - i0);
+  const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb::PageSource));
+  for (int64_t p0 = 0; p0 < static_cast<int64_t>(pages.size()); p0 += per) {
+    const int64_t n = std::min<int64_t>(per, static_cast<int64_t>(pages.size()) - p0);
     void* dptr = nullptr;
     int slot = 0;
-    TSB_TRY(l->ring_items.stage(items + i0, sizeof(tsb_ingest_item) * n, st, &dptr, &slot));
-    TSB_CUDA_TRY(tsb::launch_verify_synth(g, l->arena, static_cast<const tsb_ingest_item*>(dptr),
-                                          l->bt_dev, n, seed, l->verify_ctr, st));
+    TSB_TRY(l->ring_items.stage(pages.data() + p0, sizeof(tsb::PageSource) * n, st, &dptr, &slot));
+    TSB_CUDA_TRY(tsb::launch_verify_pages(c, l->arena, static_cast<const tsb::PageSource*>(dptr), n, seed,
+                                          l->verify_ctr, st));
     TSB_TRY(l->ring_items.fence(slot, st));
   }
   unsigned long long h = 0;
   TSB_CUDA_TRY(cudaMemcpyAsync(&h, l->verify_ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
   TSB_CUDA_TRY(cudaStreamSynchronize(st));
-  *mismatches = h;
+  *mismatches = h + host_bad;
   return TSB_OK;
 }
 

@@ -19,29 +19,63 @@ __device__ __forceinline__ uint64_t slot_of(uint64_t h, uint64_t mask) {
   return mix64(h) & mask;  // FNV low bits are weak; remix before masking
 }
 
-__global__ void k_index_insert(uint64_t* __restrict__ keys, int64_t* __restrict__ vals,
+// Insert phase 1: claim (or find) the key's entry, remember its position, and bid for the value
+// with tag = epoch << 40 | (2^40 - 1 - i): the latest insert call wins, and inside one call the
+// LOWEST batch index wins, so duplicate keys in a batch resolve deterministically.
+__global__ void k_index_insert(uint64_t* __restrict__ keys, uint64_t* __restrict__ owner,
                                uint64_t mask, int64_t n, const uint64_t* __restrict__ hashes,
-                               const int64_t* __restrict__ slots,
+                               uint64_t epoch, int64_t* __restrict__ pos,
                                unsigned long long* __restrict__ stats /* [0]=new, [1]=full */) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const uint64_t h = hashes[i];
+  const uint64_t tag = (epoch << 40) | ((1ull << 40) - 1 - static_cast<uint64_t>(i));
   uint64_t p = slot_of(h, mask);
   for (uint64_t probe = 0; probe <= mask; ++probe, p = (p + 1) & mask) {
     const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(keys + p),
                                     static_cast<unsigned long long>(kEmpty),
                                     static_cast<unsigned long long>(h));
-    if (prev == kEmpty) {
-      vals[p] = slots[i];
-      atomicAdd(stats, 1ull);
-      return;
-    }
-    if (prev == h) {  // already indexed: the newest slot wins
-      vals[p] = slots[i];
+    if (prev == kEmpty || prev == h) {
+      if (prev == kEmpty) atomicAdd(stats, 1ull);
+      atomicMax(reinterpret_cast<unsigned long long*>(owner + p), static_cast<unsigned long long>(tag));
+      pos[i] = static_cast<int64_t>(p);
       return;
     }
   }
+  pos[i] = -1;
   atomicAdd(stats + 1, 1ull);  // table full
+}
+
+// Insert phase 2: the winning bid of each entry writes its value.
+__global__ void k_index_commit(const uint64_t* __restrict__ owner, int64_t* __restrict__ vals,
+                               int64_t n, const int64_t* __restrict__ slots, uint64_t epoch,
+                               const int64_t* __restrict__ pos) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int64_t p = pos[i];
+  const uint64_t tag = (epoch << 40) | ((1ull << 40) - 1 - static_cast<uint64_t>(i));
+  if (p >= 0 && owner[p] == tag) vals[p] = slots[i];
+}
+
+// Compaction: live entries of the old table re-inserted into an empty one (keys are unique, so
+// one CAS per entry); tombstones are dropped.
+__global__ void k_index_rehash(const uint64_t* __restrict__ okeys, const int64_t* __restrict__ ovals,
+                               const uint64_t* __restrict__ oowner, uint64_t cap,
+                               uint64_t* __restrict__ keys, int64_t* __restrict__ vals,
+                               uint64_t* __restrict__ owner, uint64_t mask) {
+  const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (q >= cap) return;
+  const uint64_t h = okeys[q];
+  if (h == kEmpty || h == kTomb) return;
+  uint64_t p = slot_of(h, mask);
+  for (uint64_t probe = 0; probe <= mask; ++probe, p = (p + 1) & mask) {
+    if (atomicCAS(reinterpret_cast<unsigned long long*>(keys + p), static_cast<unsigned long long>(kEmpty),
+                  static_cast<unsigned long long>(h)) == kEmpty) {
+      vals[p] = ovals[q];
+      owner[p] = oowner[q];
+      return;
+    }
+  }
 }
 
 __global__ void k_index_erase(uint64_t* __restrict__ keys, uint64_t mask, int64_t n,
@@ -111,11 +145,22 @@ __global__ void __launch_bounds__(256) k_index_lookup(const uint64_t* __restrict
 
 }  // namespace
 
-cudaError_t launch_index_insert(uint64_t* keys, int64_t* vals, uint64_t mask, int64_t n,
-                                const uint64_t* hashes, const int64_t* slots,
-                                unsigned long long* stats, cudaStream_t st) {
+cudaError_t launch_index_insert(uint64_t* keys, int64_t* vals, uint64_t* owner, uint64_t mask,
+                                int64_t n, const uint64_t* hashes, const int64_t* slots,
+                                uint64_t epoch, int64_t* pos, unsigned long long* stats,
+                                cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  k_index_insert<<<ceil_div(n, 256), 256, 0, st>>>(keys, vals, mask, n, hashes, slots, stats);
+  k_index_insert<<<ceil_div(n, 256), 256, 0, st>>>(keys, owner, mask, n, hashes, epoch, pos, stats);
+  k_index_commit<<<ceil_div(n, 256), 256, 0, st>>>(owner, vals, n, slots, epoch, pos);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_index_rehash(const uint64_t* okeys, const int64_t* ovals, const uint64_t* oowner,
+                                uint64_t cap, uint64_t* keys, int64_t* vals, uint64_t* owner,
+                                uint64_t mask, cudaStream_t st) {
+  k_index_rehash<<<ceil_div(static_cast<int64_t>(cap), 256), 256, 0, st>>>(okeys, ovals, oowner, cap, keys, vals,
+                                                                          owner, mask);
   count_launch();
   return cudaGetLastError();
 }

@@ -166,43 +166,6 @@ __global__ void k_fill_synth(uint64_t* __restrict__ dst, uint64_t first_word, ui
     dst[n_words - 1] = synth_word(seed, first_word + n_words - 1);
 }
 
-// Harness check: every 8-byte word of every page of the items must equal the synthetic word
-// of the source position it was gathered from (slot mode geometry).
-__global__ void k_verify_synth(IngestGeom g, const uint8_t* __restrict__ arena,
-                               const tsb_ingest_item* __restrict__ items,
-                               const int32_t* __restrict__ bt, int64_t nseg, uint64_t seed,
-                               unsigned long long* mismatches) {
-  const int64_t words_per_run = g.run / 8;
-  const int64_t words = g.P * words_per_run;
-  unsigned long long bad = 0;
-  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
-    const SegAddr a = seg_addr(g, nullptr, const_cast<uint8_t*>(arena), items, bt, s);
-    if (!a.ok) {
-      if (threadIdx.x == 0) bad += words;
-      continue;
-    }
-    const int64_t src_off = reinterpret_cast<int64_t>(a.src);  // src base was nullptr
-    const int64_t words_per_head = g.head_bytes / 8;
-    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) {
-      // destination word w -> (token t, word c of this rank's run)
-      int64_t t, c;
-      if (g.hnd) {
-        const int64_t h = w / (g.P * words_per_head), r = w % (g.P * words_per_head);
-        t = r / words_per_head;
-        c = h * words_per_head + r % words_per_head;
-      } else {
-        t = w / words_per_run;
-        c = w % words_per_run;
-      }
-      const uint64_t expect =
-          synth_word(seed, static_cast<uint64_t>(src_off + t * g.row + c * 8) / 8);
-      bad += reinterpret_cast<const uint64_t*>(a.dst)[w] != expect;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
-  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
-}
-
 template <bool kHnd>
 void launch_ldg_variant(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
                         const tsb_ingest_item* items, const int32_t* bt, int64_t nseg, int grid,
@@ -268,16 +231,6 @@ cudaError_t launch_fill_synth(uint64_t* dst, uint64_t first_word, uint64_t n_wor
                               cudaStream_t st) {
   if (n_words == 0) return cudaSuccess;
   k_fill_synth<<<148 * 8, 256, 0, st>>>(dst, first_word, n_words, seed);
-  count_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_verify_synth(const IngestGeom& g, const uint8_t* arena,
-                                const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
-                                uint64_t seed, unsigned long long* mismatches, cudaStream_t st) {
-  const int64_t nseg = n_items * g.n_layers * 2 * g.ppc;
-  if (nseg == 0) return cudaSuccess;
-  k_verify_synth<<<148 * 8, 256, 0, st>>>(g, arena, items, bt, nseg, seed, mismatches);
   count_launch();
   return cudaGetLastError();
 }

@@ -48,9 +48,22 @@ cudaError_t launch_ingest_bulk(const IngestGeom& g, const uint8_t* src, uint8_t*
                                int grid, cudaStream_t st);
 cudaError_t launch_fill_synth(uint64_t* dst, uint64_t first_word, uint64_t n_words, uint64_t seed,
                               cudaStream_t st);
-cudaError_t launch_verify_synth(const IngestGeom& g, const uint8_t* arena,
-                                const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
-                                uint64_t seed, unsigned long long* mismatches, cudaStream_t st);
+// Harness page check (verify.cu): the canonical shape and layout only, no IngestGeom.
+struct PageCheck {
+  int64_t H, Hl, D, E, C, P, tp_rank;  // chunk [L][2][C][H][D]; this rank's heads [tp_rank*Hl, +Hl)
+  int64_t num_pages;
+  int64_t pool_chunk_bytes;  // slot stride of the pool whose synthetic pattern is expected
+  int32_t layout;            // tsb_kv_layout
+  int32_t layer_lo, layer_hi;
+};
+struct PageSource {  // inverted block table: which chunk position a page must hold
+  int64_t slot;      // pool slot of the chunk
+  int32_t page;      // page id in the arena
+  int32_t tok0;      // first token of the page inside the chunk (j * P)
+};
+cudaError_t launch_verify_pages(const PageCheck& c, const uint8_t* arena, const PageSource* pages,
+                                int64_t n_pages, uint64_t seed, unsigned long long* mismatches,
+                                cudaStream_t st);
 
 // Scorer (K4) and order (K5).
 struct ScoreParams {
@@ -78,9 +91,13 @@ cudaError_t launch_gen_tokens(uint64_t seed, int64_t n_req, const int64_t* offse
                               cudaStream_t st);
 
 // L2 chunk index (K7).
-cudaError_t launch_index_insert(uint64_t* keys, int64_t* vals, uint64_t mask, int64_t n,
-                                const uint64_t* hashes, const int64_t* slots,
-                                unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_index_insert(uint64_t* keys, int64_t* vals, uint64_t* owner, uint64_t mask,
+                                int64_t n, const uint64_t* hashes, const int64_t* slots,
+                                uint64_t epoch, int64_t* pos, unsigned long long* stats,
+                                cudaStream_t st);
+cudaError_t launch_index_rehash(const uint64_t* okeys, const int64_t* ovals, const uint64_t* oowner,
+                                uint64_t cap, uint64_t* keys, int64_t* vals, uint64_t* owner,
+                                uint64_t mask, cudaStream_t st);
 cudaError_t launch_index_erase(uint64_t* keys, uint64_t mask, int64_t n, const uint64_t* hashes,
                                unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_index_lookup(const uint64_t* keys, const int64_t* vals, uint64_t mask,

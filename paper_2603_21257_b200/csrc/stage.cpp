@@ -1,73 +1,195 @@
-// stage.cpp — the real-time L2->L1 load stage (tsb_stage_*).
+// stage.cpp — the real-time load stage (tsb_stage_*).
 //
 // SimEngine's dispatch rules with real bytes and real time (reference: core/src/engine.cpp):
 //   * pick order: the batched GPU scorer (K4/K5) orders the batch by PriorityKey under the chosen
 //     policy -- the order best_pending()/admit() would produce for a queue present at one instant
 //     (engine.cpp:306-312, 341-355; keys ignore `now`, scheduler.cpp:47);
-//   * admission reserves L1 for every planned chunk in block order (proactive allocation,
-//     engine.cpp:419) through the TierLedger-semantics paged allocator; reservations that do not
+//   * admission reserves L1 for every planned chunk in block order through the TierLedger-
+//     semantics paged allocator (proactive allocation, engine.cpp:419); reservations that do not
 //     fit wait FIFO and are granted by later releases (engine.cpp:38-49, 388-397);
 //   * a chunk is ingested only once its pages are granted (grant-before-hop, engine.cpp:434-436),
 //     requests are served in pick order (pcie_dispatch scans admitted_ in pick order, :427-446);
 //   * a request's L1 pages are released when its prefill completes (ComputeDone, :280-282); with
-//     prefill disabled, when its last layer is resident.
+//     prefill disabled, when its last layer is resident;
+//   * ControlMode::Coupled (engine.cpp:321-327): one request traverses every stage before the next
+//     is admitted.
+// The online mode (tsb_stage_run_online) replays arrivals in real time and runs SimEngine's pump
+// (try_admit / net_dispatch / pcie_dispatch / try_start_compute to a fixpoint, engine.cpp:290-302)
+// against CUDA events instead of a simulated clock.  With an L3 store attached
+// (tsb_stage_set_l3) it also runs the network stage for real: blocks start in L3, are granted L2
+// slots by a TierLedger(L2) + slot free list at admission (engine.cpp:341-364), are copied
+// L3 -> L2 one block at a time by host copy threads (optionally paced to network_bandwidth,
+// engine.cpp:405-425), reserve L1 at network dispatch (Proactive, :419) or at NetDone (Reactive,
+// :254), and give their L2 slot back when their L2 -> L1 hop completes (:264).  Coupled control
+// also holds a request's L2 -> L1 hops until all its network hops are done (:434).
 // The simulator's event queue and clock are replaced by CUDA streams and events: ingest on the
-// caller's stream, synthetic prefill (K6) on a lower-priority compute stream that waits on the
-// request's per-layer fences, and the host thread blocks on the oldest request only when the
-// ledger has deferred reservations and nothing else can be dispatched.
+// caller's stream, prefill (K6 synthetic, or a caller hook that enqueues a real consumer) on a
+// lower-priority compute stream.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <cstring>
 #include <ctime>
+#include <deque>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "ledger.h"
 
 using tsb::fail;
 
 namespace {
-
-struct ReqRt {
-  int64_t q_index = 0;
-  int64_t id = 0;
-  int64_t n_chunks = 0;
-  int64_t compute_tokens = 0;
-  const int64_t* slots = nullptr;
-  int32_t row = -1;
-  std::vector<int32_t> ready;  // granted, not yet ingested (block order)
-  int64_t issued = 0;
-  int32_t deferred = 0;
-  bool finished_issue = false;
-  bool released = false;
-  cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr;
-};
 
 double now_s() {
   using namespace std::chrono;
   return duration<double>(steady_clock::now().time_since_epoch()).count();
 }
 
+// Host copy threads for the L3 -> L2 network hop: one block in flight (the reference's single
+// network stage, engine.cpp:405-425), split into stripes across the threads.
+class NetCopier {
+ public:
+  explicit NetCopier(int threads) {
+    for (int t = 0; t < threads; ++t) workers_.emplace_back([this, t, threads] { loop(t, threads); });
+  }
+  ~NetCopier() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void post(const uint8_t* src, uint8_t* dst, size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      src_ = src;
+      dst_ = dst;
+      bytes_ = bytes;
+      remaining_.store(static_cast<int>(workers_.size()), std::memory_order_release);
+      ++gen_;
+    }
+    cv_.notify_all();
+  }
+  bool done() const { return remaining_.load(std::memory_order_acquire) == 0; }
+  int threads() const { return static_cast<int>(workers_.size()); }
+
+ private:
+  void loop(int t, int nt) {
+    uint64_t seen = 0;
+    for (;;) {
+      const uint8_t* src;
+      uint8_t* dst;
+      size_t bytes;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        src = src_;
+        dst = dst_;
+        bytes = bytes_;
+      }
+      const size_t stripe = (bytes / nt + 4095) & ~size_t(4095);
+      const size_t lo = std::min(bytes, stripe * t), hi = std::min(bytes, lo + stripe);
+      if (hi > lo) std::memcpy(dst + lo, src + lo, hi - lo);
+      remaining_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  bool stop_ = false;
+  uint64_t gen_ = 0;
+  const uint8_t* src_ = nullptr;
+  uint8_t* dst_ = nullptr;
+  size_t bytes_ = 0;
+  std::atomic<int> remaining_{0};
+};
+
+// Prefill duration of the reference compute stage (engine.cpp:190-212): the measured t_comp for
+// replayed requests, else compute_base + per_token * n + quadratic * n^2.
+double compute_seconds(const tsb_queue* q, int64_t i, const tsb_cluster* c, int64_t compute_tokens) {
+  if (q->flags && (q->flags[i] & TSB_HAS_MEASURED)) return q->measured_t_comp[i];
+  const auto ct = static_cast<double>(compute_tokens);
+  return c->compute_base + c->compute_per_token * ct + c->compute_quadratic * ct * ct;
+}
+
 }  // namespace
 
 struct tsb_stage {
   tsb_l1* l1 = nullptr;
-  tsb_pool* pool = nullptr;
+  tsb_pool* pool = nullptr;      // L2 (pinned host) pool
   tsb_pool* hbm_pool = nullptr;  // HBM tier: slots < 0 name slot ~slot of this pool
+  tsb_pool* l3 = nullptr;        // online mode: blocks start here; `pool` becomes the L2 slot cache
+  NetCopier* net = nullptr;
+  tsb_prefill_hook hook = nullptr;
+  void* hook_user = nullptr;
   tsb_kv_shape shape{};
   int device = 0;
   tsb_scorer* scorer = nullptr;
   cudaStream_t compute = nullptr;
   std::vector<cudaEvent_t> timing_pool;  // 3 per request, grown on demand
   std::vector<cudaEvent_t> layer_ev;     // per-layer fences (reused across requests)
+  std::vector<cudaEvent_t> call_pool;    // per ingest call (online PcieDone / trace), grown on demand
   cudaEvent_t ev_start = nullptr;
-  std::vector<cudaEvent_t> call_ev;      // per ingest call (trace only)
   std::vector<tsb_trace_row> trace;
   uint64_t seq = 0;
 };
+
+namespace {
+
+// Device of the stage for the duration of a call; restores the caller's device on exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+tsb_status grow_events(std::vector<cudaEvent_t>& v, size_t n, unsigned flags) {
+  while (v.size() < n) {
+    cudaEvent_t e;
+    TSB_CUDA_TRY(cudaEventCreateWithFlags(&e, flags));
+    v.push_back(e);
+  }
+  return TSB_OK;
+}
+
+// Enqueues a request's prefill on the compute stream: for each layer, wait on its fence (may be
+// null = no wait), then the caller's hook or the K6 burner for that layer's share of `secs`.
+tsb_status enqueue_prefill(tsb_stage* s, int64_t q_index, int32_t bt_row, double secs,
+                           const std::vector<cudaEvent_t>& fences, int ctas) {
+  const int64_t L = s->shape.layers;
+  const auto per_layer_ns = static_cast<uint64_t>(secs * 1e9 / static_cast<double>(L));
+  for (int64_t l = 0; l < L; ++l) {
+    if (fences[static_cast<size_t>(l)]) TSB_CUDA_TRY(cudaStreamWaitEvent(s->compute, fences[l], 0));
+    if (s->hook) {
+      if (s->hook(s->hook_user, q_index, bt_row, l, s->compute) != 0)
+        return fail(TSB_VALIDATION, "stage: prefill hook failed at request index " +
+                                        std::to_string(q_index) + " layer " + std::to_string(l));
+    } else {
+      for (uint64_t done = 0; done < per_layer_ns; done += 250000)
+        TSB_CUDA_TRY(tsb::launch_prefill_burn(std::min<uint64_t>(250000, per_layer_ns - done), ctas,
+                                              nullptr, s->compute));
+    }
+  }
+  return TSB_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -75,17 +197,28 @@ tsb_status tsb_stage_create(tsb_l1* l1, tsb_pool* pool, tsb_stage** out) {
   auto* s = new tsb_stage();
   s->l1 = l1;
   s->pool = pool;
-  TSB_TRY(tsb_l1_shape(l1, &s->shape));
+  tsb_status st = tsb_l1_shape(l1, &s->shape);
+  if (st != TSB_OK) {
+    delete s;
+    return st;
+  }
   s->device = tsb_l1_device(l1);
-  TSB_CUDA_TRY(cudaSetDevice(s->device));
+  DeviceGuard dg(s->device);
   int lo = 0, hi = 0;
-  TSB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
   // Prefill gets the LOWEST priority so the ingest scatter kernels interleave ahead of it.
-  TSB_CUDA_TRY(cudaStreamCreateWithPriority(&s->compute, cudaStreamNonBlocking, lo));
-  TSB_CUDA_TRY(cudaEventCreate(&s->ev_start));
-  s->layer_ev.resize(static_cast<size_t>(s->shape.layers));
-  for (auto& e : s->layer_ev) TSB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  TSB_TRY(tsb_scorer_create(s->device, 1024, &s->scorer));
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s->compute, cudaStreamNonBlocking, lo);
+  if (e == cudaSuccess) e = cudaEventCreate(&s->ev_start);
+  if (e != cudaSuccess) {
+    tsb_stage_destroy(s);
+    return tsb::cuda_fail(e, "tsb_stage_create");
+  }
+  st = grow_events(s->layer_ev, static_cast<size_t>(s->shape.layers), cudaEventDisableTiming);
+  if (st == TSB_OK) st = tsb_scorer_create(s->device, 1024, &s->scorer);
+  if (st != TSB_OK) {
+    tsb_stage_destroy(s);
+    return st;
+  }
   *out = s;
   return TSB_OK;
 }
@@ -97,13 +230,40 @@ tsb_status tsb_stage_set_hbm_tier(tsb_stage* s, tsb_pool* hbm_pool) {
   return TSB_OK;
 }
 
+tsb_status tsb_stage_set_l3(tsb_stage* s, tsb_pool* l3, int copy_threads) {
+  if (l3 && tsb_pool_chunk_bytes(l3) != tsb_pool_chunk_bytes(s->pool))
+    return fail(TSB_VALIDATION, "stage: the L3 store's chunk geometry differs from the L2 pool's");
+  if (l3 && tsb_pool_location_of(l3) != TSB_POOL_HOST)
+    return fail(TSB_VALIDATION, "stage: the L3 store must be host memory");
+  if (l3 && tsb_pool_location_of(s->pool) != TSB_POOL_HOST)
+    return fail(TSB_VALIDATION, "stage: with an L3 store the L2 pool must be host memory");
+  delete s->net;
+  s->net = nullptr;
+  s->l3 = l3;
+  if (l3) s->net = new NetCopier(std::max(1, std::min(copy_threads > 0 ? copy_threads : 4, 32)));
+  return TSB_OK;
+}
+
+tsb_status tsb_stage_set_prefill_hook(tsb_stage* s, tsb_prefill_hook hook, void* user) {
+  s->hook = hook;
+  s->hook_user = user;
+  return TSB_OK;
+}
+
+void* tsb_stage_compute_stream(tsb_stage* s) { return s->compute; }
+
 void tsb_stage_destroy(tsb_stage* s) {
   if (!s) return;
+  DeviceGuard dg(s->device);
+  delete s->net;
   for (auto e : s->timing_pool) cudaEventDestroy(e);
   for (auto e : s->layer_ev) cudaEventDestroy(e);
-  for (auto e : s->call_ev) cudaEventDestroy(e);
+  for (auto e : s->call_pool) cudaEventDestroy(e);
   if (s->ev_start) cudaEventDestroy(s->ev_start);
-  if (s->compute) cudaStreamDestroy(s->compute);
+  if (s->compute) {
+    cudaStreamSynchronize(s->compute);
+    cudaStreamDestroy(s->compute);
+  }
   tsb_scorer_destroy(s->scorer);
   delete s;
 }
@@ -114,34 +274,30 @@ tsb_status tsb_stage_trace(tsb_stage* s, tsb_trace_row* out, int64_t cap, int64_
   return TSB_OK;
 }
 
-tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_cluster* c,
-                         const double models[4], const int64_t* slot_offsets,
-                         const int64_t* slots, const tsb_stage_options* opt, void* stream,
-                         tsb_stage_request* results, tsb_stage_stats* stats) {
-  const double wall0 = now_s();
-  const uint64_t launches0 = tsb_kernel_launch_count();
-  auto st = static_cast<cudaStream_t>(stream);
-  const int64_t L = s->shape.layers;
-  int64_t chunk_bytes_full = 0, page_bytes = 0, chunk_bytes = 0;
-  TSB_TRY(tsb_kv_shape_info(&s->shape, &chunk_bytes_full, &page_bytes, &chunk_bytes));
-  TSB_TRY(tsb_cluster_validate(c));
-  if (c->block_size_tokens != s->shape.chunk_tokens)
-    return fail(TSB_VALIDATION, "stage: cluster block_size_tokens must equal the KV chunk_tokens");
-  s->trace.clear();
-  s->seq = 0;
-  auto row = [&](double t, int kind, int stg, int tier, int64_t rid, int32_t blk, int64_t bytes) {
-    if (opt->record_trace) s->trace.push_back({t, s->seq++, kind, stg, tier, blk, rid, bytes});
-  };
+}  // extern "C"
 
-  // ---- plans (types.cpp:85-101) and capacity check (engine.cpp:213-217) ----------------------
-  std::vector<ReqRt> reqs(static_cast<size_t>(n));
-  std::unordered_map<int64_t, size_t> by_id;
+namespace {
+
+// Common per-call setup of both modes: plans (types.cpp:85-101), slot checks, capacity checks
+// (engine.cpp:213-217), duplicate ids (engine.cpp:126-127).
+struct Plan {
+  int64_t id = 0, n_chunks = 0, compute_tokens = 0;
+  const int64_t* slots = nullptr;
+};
+
+tsb_status make_plans(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_cluster* c,
+                      const int64_t* slot_offsets, const int64_t* slots, int64_t chunk_bytes,
+                      bool use_l3, std::vector<Plan>* plans,
+                      std::unordered_map<int64_t, size_t>* by_id) {
+  plans->assign(static_cast<size_t>(n), Plan{});
   const int64_t l1_capacity = tsb_l1_capacity(s->l1);
+  const int64_t src_slots = tsb_pool_slots(use_l3 ? s->l3 : s->pool);
+  int64_t l2_capacity = 0;
+  if (use_l3) l2_capacity = std::min<int64_t>(c->l2_capacity / chunk_bytes, tsb_pool_slots(s->pool)) * chunk_bytes;
   for (int64_t i = 0; i < n; ++i) {
     int64_t cached = 0, compute = 0, nb = 0, bt = 0, bb = 0;
     TSB_TRY(tsb_derive_block_plan(q, i, c, &cached, &compute, &nb, &bt, &bb));
-    ReqRt& r = reqs[i];
-    r.q_index = i;
+    Plan& r = (*plans)[static_cast<size_t>(i)];
     r.id = q->id[i];
     r.n_chunks = nb;
     r.compute_tokens = compute;
@@ -152,22 +308,61 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
                                       " pool slots for a plan of " + std::to_string(nb) + " chunks");
     for (int64_t k = 0; k < nb; ++k) {
       const int64_t sl = r.slots[k];
-      const bool ok = sl >= 0 ? sl < tsb_pool_slots(s->pool)
-                              : (s->hbm_pool && ~sl < tsb_pool_slots(s->hbm_pool));
+      if (use_l3 && sl < 0)
+        return fail(TSB_VALIDATION, "stage: with an L3 store every slot names an L3 chunk (no HBM tier)");
+      const bool ok = sl >= 0 ? sl < src_slots : (s->hbm_pool && ~sl < tsb_pool_slots(s->hbm_pool));
       if (!ok) return fail(TSB_VALIDATION, "stage: pool slot out of range");
     }
-    if (nb * chunk_bytes > l1_capacity)
+    if (nb * chunk_bytes > l1_capacity || (use_l3 && nb * chunk_bytes > l2_capacity))
       return fail(TSB_CAPACITY, "request " + std::to_string(r.id) + ": " +
                                     std::to_string(nb * chunk_bytes) +
                                     " resident bytes can never fit");
-    if (!by_id.emplace(r.id, static_cast<size_t>(i)).second)
+    if (!by_id->emplace(r.id, static_cast<size_t>(i)).second)
       return fail(TSB_VALIDATION, "run_simulation: duplicate request id " + std::to_string(r.id));
   }
-  while (s->timing_pool.size() < static_cast<size_t>(3 * n)) {
-    cudaEvent_t e;
-    TSB_CUDA_TRY(cudaEventCreate(&e));
-    s->timing_pool.push_back(e);
-  }
+  return TSB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_cluster* c,
+                         const double models[4], const int64_t* slot_offsets,
+                         const int64_t* slots, const tsb_stage_options* opt, void* stream,
+                         tsb_stage_request* results, tsb_stage_stats* stats) {
+  DeviceGuard dg(s->device);
+  const double wall0 = now_s();
+  const uint64_t launches0 = tsb_kernel_launch_count();
+  auto st = static_cast<cudaStream_t>(stream);
+  const int64_t L = s->shape.layers;
+  int64_t chunk_bytes_full = 0, page_bytes = 0, chunk_bytes = 0;
+  TSB_TRY(tsb_kv_shape_info(&s->shape, &chunk_bytes_full, &page_bytes, &chunk_bytes));
+  TSB_TRY(tsb_cluster_validate(c));
+  if (c->block_size_tokens != s->shape.chunk_tokens)
+    return fail(TSB_VALIDATION, "stage: cluster block_size_tokens must equal the KV chunk_tokens");
+  if (s->l3)
+    return fail(TSB_UNSUPPORTED, "stage: the L3 network stage runs in tsb_stage_run_online only");
+  const bool coupled = c->control_mode == 0;
+  s->trace.clear();
+  s->seq = 0;
+  auto row = [&](double t, int kind, int stg, int tier, int64_t rid, int32_t blk, int64_t bytes) {
+    if (opt->record_trace) s->trace.push_back({t, s->seq++, kind, stg, tier, blk, rid, bytes});
+  };
+
+  std::vector<Plan> plans;
+  std::unordered_map<int64_t, size_t> by_id;
+  TSB_TRY(make_plans(s, n, q, c, slot_offsets, slots, chunk_bytes, false, &plans, &by_id));
+  struct ReqRt {
+    int32_t row = -1;
+    std::vector<int32_t> ready;  // granted, not yet ingested (block order)
+    int64_t issued = 0;
+    int32_t deferred = 0;
+    bool finished_issue = false;
+    cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr;
+  };
+  std::vector<ReqRt> reqs(static_cast<size_t>(n));
+  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(3 * n), cudaEventDefault));
   for (int64_t i = 0; i < n; ++i) {
     reqs[i].ev_first = s->timing_pool[3 * i];
     reqs[i].ev_resident = s->timing_pool[3 * i + 1];
@@ -187,27 +382,26 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   const int ctas = opt->prefill_ctas > 0 ? opt->prefill_ctas : 148;
   int64_t ingest_calls = 0, deferred_total = 0, releases = 0, bytes_total = 0;
   uint64_t verify_mismatches = 0;
+  std::vector<cudaEvent_t> call_events;  // trace only: one per ingest call
 
-  auto finish_request_events = [&](ReqRt& r) -> tsb_status {
-    // Called once the request's last chunk has been dispatched: ev_first / ev_resident were
-    // recorded by that ingest call (or here for an empty plan); now the prefill and ev_done.
-    if (r.n_chunks == 0) {
+  // Once a request's last chunk is dispatched: ev_first / ev_resident were recorded by that ingest
+  // call (or here for an empty plan); now the prefill and ev_done.
+  auto finish_request_events = [&](int64_t i) -> tsb_status {
+    ReqRt& r = reqs[i];
+    const Plan& p = plans[i];
+    if (p.n_chunks == 0) {
       TSB_CUDA_TRY(cudaEventRecord(r.ev_first, st));
       TSB_CUDA_TRY(cudaEventRecord(r.ev_resident, st));
       for (int64_t l = 0; l < L; ++l) TSB_CUDA_TRY(cudaEventRecord(s->layer_ev[l], st));
     }
-    if (opt->prefill) {
-      const double ct = static_cast<double>(r.compute_tokens);
-      const double secs = c->compute_base + c->compute_per_token * ct + c->compute_quadratic * ct * ct;
-      const auto per_layer_ns = static_cast<uint64_t>(secs * 1e9 / static_cast<double>(L));
-      for (int64_t l = 0; l < L; ++l) {
-        cudaEvent_t fence = r.ev_resident;
-        if (opt->layer_events) fence = l == 0 ? r.ev_first : l == L - 1 ? r.ev_resident : s->layer_ev[l];
-        TSB_CUDA_TRY(cudaStreamWaitEvent(s->compute, fence, 0));
-        for (uint64_t done = 0; done < per_layer_ns; done += 250000)
-          TSB_CUDA_TRY(tsb::launch_prefill_burn(std::min<uint64_t>(250000, per_layer_ns - done),
-                                                ctas, nullptr, s->compute));
+    if (opt->prefill || s->hook) {
+      std::vector<cudaEvent_t> fences(static_cast<size_t>(L), nullptr);
+      fences[0] = opt->layer_events ? r.ev_first : r.ev_resident;
+      if (opt->layer_events) {
+        for (int64_t l = 1; l + 1 < L; ++l) fences[l] = s->layer_ev[l];
+        if (L > 1) fences[L - 1] = r.ev_resident;
       }
+      TSB_TRY(enqueue_prefill(s, i, r.row, compute_seconds(q, i, c, p.compute_tokens), fences, ctas));
       TSB_CUDA_TRY(cudaEventRecord(r.ev_done, s->compute));
     } else {
       TSB_CUDA_TRY(cudaEventRecord(r.ev_done, st));
@@ -220,7 +414,9 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   auto dispatch = [&]() -> tsb_status {
     bool synced = false;
     for (int64_t k = 0; k < n; ++k) {
-      ReqRt& r = reqs[order[k]];
+      const int64_t i = order[k];
+      ReqRt& r = reqs[i];
+      const Plan& p = plans[i];
       if (r.finished_issue || r.ready.empty()) continue;
       if (!synced) {
         TSB_TRY(tsb_l1_sync_block_table(s->l1, stream));
@@ -229,12 +425,12 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       std::vector<tsb_ingest_item> items;
       items.reserve(r.ready.size());
       for (int32_t ch : r.ready) {
-        items.push_back(tsb_ingest_item{r.slots[ch], r.row, ch});
-        row(now_s() - host0, 4, 1, -1, r.id, ch, chunk_bytes);  // DispatchWake(Pcie)
+        items.push_back(tsb_ingest_item{p.slots[ch], r.row, ch});
+        row(now_s() - host0, 4, 1, -1, p.id, ch, chunk_bytes);  // DispatchWake(Pcie)
       }
       r.issued += static_cast<int64_t>(items.size());
       r.ready.clear();
-      const bool last = r.issued == r.n_chunks;
+      const bool last = r.issued == p.n_chunks;
       std::vector<void*> evs;
       void* const* evp = nullptr;
       if (last) {
@@ -250,76 +446,111 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
                                 static_cast<int64_t>(items.size()), 0, L, opt->mode, stream, evp));
       if (last && L == 1) TSB_CUDA_TRY(cudaEventRecord(r.ev_first, st));
       if (opt->record_trace) {
-        cudaEvent_t ce;
-        TSB_CUDA_TRY(cudaEventCreate(&ce));
+        if (call_events.size() >= 4096) return fail(TSB_CAPACITY, "stage: more than 4096 traced ingest calls");
+        TSB_TRY(grow_events(s->call_pool, call_events.size() + 1, cudaEventDefault));
+        cudaEvent_t ce = s->call_pool[call_events.size()];
         TSB_CUDA_TRY(cudaEventRecord(ce, st));
-        s->call_ev.push_back(ce);
+        call_events.push_back(ce);
         for (const auto& it : items)  // TransferDone(Pcie); time filled in after the run
-          row(-static_cast<double>(s->call_ev.size()), 1, 1, -1, r.id, it.chunk_index, chunk_bytes);
+          row(-static_cast<double>(call_events.size()), 1, 1, -1, p.id, it.chunk_index, chunk_bytes);
       }
       ++ingest_calls;
       bytes_total += static_cast<int64_t>(items.size()) * chunk_bytes;
-      if (last) TSB_TRY(finish_request_events(r));
+      if (last) TSB_TRY(finish_request_events(i));
     }
     return TSB_OK;
   };
 
-  // admit (engine.cpp:341-355) in pick order: reserve L1 for every planned chunk.
-  int64_t total_chunks = 0;
-  for (const auto& r : reqs) total_chunks += r.n_chunks;
-  std::vector<tsb_grant> grants(static_cast<size_t>(std::max<int64_t>(total_chunks, 1)));
-  for (int64_t k = 0; k < n; ++k) {
-    ReqRt& r = reqs[order[k]];
-    for (int64_t ch = 0; ch < r.n_chunks; ++ch) {
+  // admit (engine.cpp:341-355): reserve L1 for every planned chunk of a request.
+  auto admit = [&](int64_t i) -> tsb_status {
+    ReqRt& r = reqs[i];
+    const Plan& p = plans[i];
+    for (int64_t ch = 0; ch < p.n_chunks; ++ch) {
       int granted = 0;
-      TSB_TRY(tsb_l1_request(s->l1, r.id, static_cast<int32_t>(ch), chunk_bytes, &granted, &r.row));
+      TSB_TRY(tsb_l1_request(s->l1, p.id, static_cast<int32_t>(ch), chunk_bytes, &granted, &r.row));
       if (granted) {
         r.ready.push_back(static_cast<int32_t>(ch));
-        row(now_s() - host0, 2, -1, 2, r.id, static_cast<int32_t>(ch), chunk_bytes);
+        row(now_s() - host0, 2, -1, 2, p.id, static_cast<int32_t>(ch), chunk_bytes);
       } else {
         ++r.deferred;
         ++deferred_total;
       }
     }
-    if (r.n_chunks == 0) TSB_TRY(finish_request_events(r));
-  }
-  TSB_TRY(dispatch());
+    if (p.n_chunks == 0) TSB_TRY(finish_request_events(i));
+    return TSB_OK;
+  };
 
-  // Complete requests in pick order; each release may grant deferred reservations (FIFO), whose
-  // chunks are dispatched right away so the link never idles while the host waits.
-  for (int64_t k = 0; k < n; ++k) {
-    ReqRt& r = reqs[order[k]];
-    if (!r.finished_issue)
-      return fail(TSB_CAPACITY, "stage: request " + std::to_string(r.id) +
-                                    " is blocked on L1 pages held by later requests");
+  // ComputeDone (engine.cpp:274-283): wait, optionally verify, release L1 (FIFO grants), and
+  // dispatch what the grants made ready.
+  auto complete = [&](int64_t i) -> tsb_status {
+    ReqRt& r = reqs[i];
+    const Plan& p = plans[i];
     TSB_CUDA_TRY(cudaEventSynchronize(r.ev_done));
-    if (opt->verify_seed && r.n_chunks > 0) {
+    if (opt->verify_seed && p.n_chunks > 0) {
       std::vector<tsb_ingest_item> items;
       // both tiers hold the synthetic pattern of the seed at their own slot index
-      for (int64_t ch = 0; ch < r.n_chunks; ++ch)
-        items.push_back(tsb_ingest_item{r.slots[ch] < 0 ? ~r.slots[ch] : r.slots[ch], r.row,
+      for (int64_t ch = 0; ch < p.n_chunks; ++ch)
+        items.push_back(tsb_ingest_item{p.slots[ch] < 0 ? ~p.slots[ch] : p.slots[ch], r.row,
                                         static_cast<int32_t>(ch)});
       uint64_t mm = 0;
-      TSB_TRY(tsb_l1_verify_synthetic(s->l1, items.data(), r.n_chunks, 0, L, opt->verify_seed,
+      TSB_TRY(tsb_l1_verify_synthetic(s->l1, items.data(), p.n_chunks, 0, L, opt->verify_seed,
                                       tsb_pool_chunk_bytes(s->pool), stream, &mm));
       verify_mismatches += mm;
     }
-    // ComputeDone (engine.cpp:349-358): bytes = compute_tokens * bytes_per_token, then release.
-    row(now_s() - host0, 3, 2, -1, r.id, -1, r.compute_tokens * c->bytes_per_token);
+    row(now_s() - host0, 3, 2, -1, p.id, -1, p.compute_tokens * c->bytes_per_token);
     if (r.row >= 0) {
+      std::vector<tsb_grant> grants(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
       int64_t ng = 0;
-      TSB_TRY(tsb_l1_release_request(s->l1, r.id, grants.data(),
-                                     static_cast<int64_t>(grants.size()), &ng));
+      TSB_TRY(tsb_l1_release_request(s->l1, p.id, grants.data(), static_cast<int64_t>(grants.size()), &ng));
       ++releases;
       const double t = now_s() - host0;
       for (int64_t g = 0; g < ng; ++g) {
         ReqRt& w = reqs[by_id.at(grants[g].request_id)];
         w.ready.push_back(grants[g].block_index);
-        row(t, 2, -1, 2, w.id, grants[g].block_index, grants[g].bytes);
+        row(t, 2, -1, 2, grants[g].request_id, grants[g].block_index, grants[g].bytes);
       }
       TSB_TRY(dispatch());
     }
-    r.released = true;
+    return TSB_OK;
+  };
+
+  tsb_status status = TSB_OK;
+  if (coupled) {
+    // ControlMode::Coupled (engine.cpp:321-327): admit the next request only when the previous
+    // one has traversed every stage (its prefill is done and its pages are released).
+    for (int64_t k = 0; k < n && status == TSB_OK; ++k) {
+      status = admit(order[k]);
+      if (status == TSB_OK) status = dispatch();
+      if (status == TSB_OK) status = complete(order[k]);
+    }
+  } else {
+    // Decoupled: admit everything in pick order up front; then complete requests in pick order,
+    // each release granting deferred reservations whose chunks are dispatched right away so the
+    // link never idles while the host waits.
+    for (int64_t k = 0; k < n && status == TSB_OK; ++k) status = admit(order[k]);
+    if (status == TSB_OK) status = dispatch();
+    for (int64_t k = 0; k < n && status == TSB_OK; ++k) {
+      if (!reqs[order[k]].finished_issue) {
+        status = fail(TSB_CAPACITY, "stage: request " + std::to_string(plans[order[k]].id) +
+                                        " is blocked on L1 pages held by later requests");
+        break;
+      }
+      status = complete(order[k]);
+    }
+  }
+  if (status != TSB_OK) {
+    // Leave nothing in flight and no reservation held: drain both streams, then release every
+    // request's L1 pages (the allocator returns to its pre-call state).
+    const std::string msg = tsb_last_error();
+    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(s->compute);
+    for (int64_t i = 0; i < n; ++i) {
+      if (reqs[i].row < 0 && reqs[i].deferred == 0) continue;
+      std::vector<tsb_grant> grants(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
+      int64_t ng = 0;
+      tsb_l1_release_request(s->l1, plans[i].id, grants.data(), static_cast<int64_t>(grants.size()), &ng);
+    }
+    return fail(status, msg);
   }
   TSB_CUDA_TRY(cudaStreamSynchronize(st));
 
@@ -333,21 +564,20 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     TSB_CUDA_TRY(cudaEventElapsedTime(&d, s->ev_start, r.ev_done));
     last_ms = std::max(last_ms, b);
     if (results)
-      results[i] = tsb_stage_request{r.id, static_cast<int32_t>(pos_of[i]), r.deferred, r.n_chunks,
-                                     r.n_chunks * chunk_bytes, a, b, d, 0.0, 0.0};
+      results[i] = tsb_stage_request{plans[i].id, static_cast<int32_t>(pos_of[i]), r.deferred,
+                                     plans[i].n_chunks, plans[i].n_chunks * chunk_bytes, a, b, d, 0.0, 0.0};
   }
   if (opt->record_trace) {
     for (auto& tr : s->trace) {
       if (tr.time < 0) {
         float ms = 0.f;
-        TSB_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev_start, s->call_ev[static_cast<size_t>(-tr.time) - 1]));
+        TSB_CUDA_TRY(cudaEventElapsedTime(&ms, s->ev_start, call_events[static_cast<size_t>(-tr.time) - 1]));
         tr.time = ms * 1e-3;
       }
     }
-    for (auto e : s->call_ev) cudaEventDestroy(e);
-    s->call_ev.clear();
   }
   if (stats) {
+    *stats = tsb_stage_stats{};
     stats->bytes = bytes_total;
     stats->device_ms = last_ms;
     stats->wall_ms = (now_s() - wall0) * 1e3;
@@ -360,11 +590,15 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   return TSB_OK;
 }
 
+// ------------------------------------------------------------------------------------------------
+// Online mode: SimEngine's event loop (engine.cpp:140-158, 290-302) in real time.
+// ------------------------------------------------------------------------------------------------
 tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
                                 const tsb_cluster* c, const double models[4],
                                 const int64_t* slot_offsets, const int64_t* slots,
                                 const tsb_stage_options* opt, void* stream,
                                 tsb_stage_request* results, tsb_stage_stats* stats) {
+  DeviceGuard dg(s->device);
   const double wall0 = now_s();
   const uint64_t launches0 = tsb_kernel_launch_count();
   auto st = static_cast<cudaStream_t>(stream);
@@ -374,52 +608,43 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   TSB_TRY(tsb_cluster_validate(c));
   if (c->block_size_tokens != s->shape.chunk_tokens)
     return fail(TSB_VALIDATION, "stage: cluster block_size_tokens must equal the KV chunk_tokens");
-  if (n == 0) return TSB_OK;
+  const bool use_l3 = s->l3 != nullptr;
+  const bool coupled = c->control_mode == 0;
+  const bool reactive = c->allocation_mode == 1;
+  const int64_t l2_slot_bytes = tsb_pool_chunk_bytes(s->pool);
+  s->trace.clear();
+  s->seq = 0;
+  if (n == 0) {
+    if (stats) *stats = tsb_stage_stats{};
+    return TSB_OK;
+  }
+  std::vector<Plan> plans;
+  std::unordered_map<int64_t, size_t> by_id;
+  TSB_TRY(make_plans(s, n, q, c, slot_offsets, slots, chunk_bytes, use_l3, &plans, &by_id));
+
+  struct Blk {
+    int64_t l2_slot = -1;  // L3 mode: the L2 slot this block was granted
+    bool l2_granted = false, l1_granted = false, net_done = false, pcie_issued = false;
+  };
   struct Rt {
-    int64_t id = 0, n_chunks = 0, compute_tokens = 0;
-    const int64_t* slots = nullptr;
+    std::vector<Blk> blk;
     int32_t row = -1, deferred = 0;
-    std::vector<int32_t> ready;
-    int64_t issued = 0, granted = 0;
-    bool arrived = false, admitted = false, dispatched_all = false, resident = false,
-         started = false, finished = false;
+    int64_t next_net = 0, next_pcie = 0, net_done = 0, pcie_issued = 0, pcie_done = 0;
+    bool arrived = false, admitted = false, compute_ready = false, started = false, finished = false;
     double arrival = 0.0, admit_t = 0.0;
     cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr;
   };
   std::vector<Rt> R(static_cast<size_t>(n));
-  std::unordered_map<int64_t, size_t> by_id;
-  const int64_t l1_capacity = tsb_l1_capacity(s->l1);
   double first_arrival = q->arrival[0];
   for (int64_t i = 0; i < n; ++i) first_arrival = std::min(first_arrival, q->arrival[i]);
+  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(3 * n), cudaEventDefault));
   for (int64_t i = 0; i < n; ++i) {
-    int64_t cached = 0, compute = 0, nb = 0, bt = 0, bb = 0;
-    TSB_TRY(tsb_derive_block_plan(q, i, c, &cached, &compute, &nb, &bt, &bb));
     Rt& r = R[i];
-    r.id = q->id[i];
-    r.n_chunks = nb;
-    r.compute_tokens = compute;
-    r.slots = slots + slot_offsets[i];
+    r.blk.resize(static_cast<size_t>(plans[i].n_chunks));
     r.arrival = q->arrival[i] - first_arrival;
-    if (slot_offsets[i + 1] - slot_offsets[i] != nb)
-      return fail(TSB_VALIDATION, "stage: request " + std::to_string(r.id) + " lists " +
-                                      std::to_string(slot_offsets[i + 1] - slot_offsets[i]) +
-                                      " pool slots for a plan of " + std::to_string(nb) + " chunks");
-    if (nb * chunk_bytes > l1_capacity)
-      return fail(TSB_CAPACITY, "request " + std::to_string(r.id) + ": " +
-                                    std::to_string(nb * chunk_bytes) +
-                                    " resident bytes can never fit");
-    if (!by_id.emplace(r.id, static_cast<size_t>(i)).second)
-      return fail(TSB_VALIDATION, "run_simulation: duplicate request id " + std::to_string(r.id));
-  }
-  while (s->timing_pool.size() < static_cast<size_t>(3 * n)) {
-    cudaEvent_t e;
-    TSB_CUDA_TRY(cudaEventCreate(&e));
-    s->timing_pool.push_back(e);
-  }
-  for (int64_t i = 0; i < n; ++i) {
-    R[i].ev_first = s->timing_pool[3 * i];
-    R[i].ev_resident = s->timing_pool[3 * i + 1];
-    R[i].ev_done = s->timing_pool[3 * i + 2];
+    r.ev_first = s->timing_pool[3 * i];
+    r.ev_resident = s->timing_pool[3 * i + 1];
+    r.ev_done = s->timing_pool[3 * i + 2];
   }
   // Priority keys from the GPU scorer (K4), compared with PriorityKey::operator< on the host.
   std::vector<double> primary(static_cast<size_t>(n));
@@ -436,195 +661,358 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   std::stable_sort(by_arrival.begin(), by_arrival.end(),
                    [&](size_t a, size_t b) { return R[a].arrival < R[b].arrival; });
 
-  cudaEvent_t ev_ingest = nullptr, ev_compute = nullptr;
-  TSB_CUDA_TRY(cudaEventCreateWithFlags(&ev_ingest, cudaEventDisableTiming));
-  TSB_CUDA_TRY(cudaEventCreateWithFlags(&ev_compute, cudaEventDisableTiming));
-  bool ingest_issued = false, compute_issued = false;
+  // L2 tier (L3 mode): TierLedger(L2) over the pool's slots + a FIFO slot free list.
+  tsb::Ledger l2(1, use_l3 ? std::min<int64_t>(c->l2_capacity / l2_slot_bytes, tsb_pool_slots(s->pool)) * l2_slot_bytes
+                           : 1);
+  std::deque<int64_t> l2_free;
+  if (use_l3)
+    for (int64_t k = 0; k < tsb_pool_slots(s->pool); ++k) l2_free.push_back(k);
+
+  struct Call {  // one L2 -> L1 ingest call: its blocks complete together (PcieDone)
+    cudaEvent_t ev;
+    size_t req;
+    std::vector<int32_t> blocks;
+  };
+  std::deque<Call> calls;
+  size_t call_slot = 0;
   const int ctas = opt->prefill_ctas > 0 ? opt->prefill_ctas : 148;
-  std::vector<tsb_grant> grants(4096);
-  int64_t ingest_calls = 0, deferred_total = 0, releases = 0, bytes_total = 0;
+  int64_t ingest_calls = 0, deferred_total = 0, releases = 0, bytes_total = 0, net_blocks = 0, l2_deferred = 0;
   uint64_t verify_mismatches = 0;
   std::vector<size_t> pending, admitted;
-  size_t next_arrival = 0, finished = 0;
-  int64_t pick = 0;
+  size_t admitted_head = 0, next_arrival = 0, finished = 0;
+  int64_t pick = 0, unissued_net = 0, active = 0;
   std::vector<int32_t> pick_pos(static_cast<size_t>(n), -1);
+  bool net_busy = false, compute_busy = false;
+  size_t net_req = 0;
+  int64_t net_blk = 0;
+  double net_ready_at = 0.0;
 
   TSB_CUDA_TRY(cudaEventRecord(s->ev_start, st));
   const double host0 = now_s();
+  auto now = [&] { return now_s() - host0; };
+  auto row = [&](int kind, int stg, int tier, int64_t rid, int32_t blk, int64_t bytes) {
+    if (opt->record_trace) s->trace.push_back({now(), s->seq++, kind, stg, tier, blk, rid, bytes});
+  };
   auto done = [](cudaEvent_t e) { return cudaEventQuery(e) == cudaSuccess; };
-  tsb_status status = TSB_OK;
-  auto fail_out = [&](tsb_status st_) {
-    status = st_;
-    return st_;
+  std::vector<tsb_grant> grants(64);
+  double last_progress = now();
+
+  auto grant_l1 = [&](size_t i, int32_t b) {
+    R[i].blk[static_cast<size_t>(b)].l1_granted = true;
+    row(2, -1, 2, plans[i].id, b, chunk_bytes);
+  };
+  auto request_l1 = [&](size_t i, int32_t b) -> tsb_status {
+    int granted = 0;
+    TSB_TRY(tsb_l1_request(s->l1, plans[i].id, b, chunk_bytes, &granted, &R[i].row));
+    if (granted) {
+      grant_l1(i, b);
+    } else {
+      ++R[i].deferred;
+      ++deferred_total;
+    }
+    return TSB_OK;
+  };
+  auto grant_l2 = [&](size_t i, int32_t b) {
+    Blk& k = R[i].blk[static_cast<size_t>(b)];
+    k.l2_granted = true;
+    k.l2_slot = l2_free.front();
+    l2_free.pop_front();
+    row(2, -1, 1, plans[i].id, b, chunk_bytes);
+  };
+  auto release_l2 = [&](int64_t slot) -> tsb_status {
+    l2_free.push_back(slot);
+    std::string msg;
+    const tsb_status rs = l2.release(l2_slot_bytes, [&](const tsb::Ledger::Pending& p) {
+      grant_l2(by_id.at(p.request_id), p.block_index);
+    }, &msg);
+    return rs == TSB_OK ? TSB_OK : fail(rs, msg);
   };
 
-  while (finished < static_cast<size_t>(n)) {
-    const double now = now_s() - host0;
-    while (next_arrival < by_arrival.size() && R[by_arrival[next_arrival]].arrival <= now) {
-      R[by_arrival[next_arrival]].arrived = true;
-      pending.push_back(by_arrival[next_arrival++]);
+  tsb_status status = TSB_OK;
+  while (finished < static_cast<size_t>(n) && status == TSB_OK) {
+    bool progress = false;
+    // ---- handle(): every event that has happened by now (engine.cpp:227-288) ------------------
+    while (next_arrival < by_arrival.size() && R[by_arrival[next_arrival]].arrival <= now()) {
+      const size_t i = by_arrival[next_arrival++];
+      R[i].arrived = true;
+      pending.push_back(i);
+      row(0, -1, -1, plans[i].id, -1, 0);
+      progress = true;
     }
-    bool progress = true;
-    while (progress) {
-      progress = false;
-      // ComputeDone -> release this request's L1 pages; FIFO grants to waiting reservations.
-      for (size_t i : admitted) {
-        Rt& r = R[i];
-        if (!r.started || r.finished || !done(r.ev_done)) continue;
-        r.finished = true;
-        ++finished;
-        progress = true;
-        if (opt->verify_seed && r.n_chunks > 0) {  // opt-in check (synchronises the stream)
-          std::vector<tsb_ingest_item> items;
-          for (int64_t ch = 0; ch < r.n_chunks; ++ch)
-            items.push_back(tsb_ingest_item{r.slots[ch] < 0 ? ~r.slots[ch] : r.slots[ch], r.row,
-                                            static_cast<int32_t>(ch)});
-          uint64_t mm = 0;
-          if (tsb_l1_verify_synthetic(s->l1, items.data(), r.n_chunks, 0, L, opt->verify_seed,
-                                      tsb_pool_chunk_bytes(s->pool), stream, &mm) != TSB_OK)
-            return fail_out(TSB_CUDA);
-          verify_mismatches += mm;
-        }
-        if (r.row >= 0) {
-          int64_t ng = 0;
-          if (grants.size() < static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1)
-            grants.resize(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
-          if (tsb_l1_release_request(s->l1, r.id, grants.data(),
-                                     static_cast<int64_t>(grants.size()), &ng) != TSB_OK)
-            return fail_out(TSB_VALIDATION);
-          ++releases;
-          for (int64_t g = 0; g < ng; ++g) {
-            Rt& w = R[by_id.at(grants[g].request_id)];
-            w.ready.push_back(grants[g].block_index);
-            ++w.granted;
-          }
-        }
+    if (net_busy && s->net->done() && now() >= net_ready_at) {  // NetDone (engine.cpp:242-256)
+      Rt& r = R[net_req];
+      r.blk[static_cast<size_t>(net_blk)].net_done = true;
+      ++r.net_done;
+      row(1, 0, -1, plans[net_req].id, static_cast<int32_t>(net_blk), chunk_bytes);
+      if (reactive && (status = request_l1(net_req, static_cast<int32_t>(net_blk))) != TSB_OK) break;
+      net_busy = false;
+      progress = true;
+    }
+    while (!calls.empty() && done(calls.front().ev)) {  // PcieDone (engine.cpp:258-272)
+      Call cl = std::move(calls.front());
+      calls.pop_front();
+      Rt& r = R[cl.req];
+      for (int32_t b : cl.blocks) {
+        row(1, 1, -1, plans[cl.req].id, b, chunk_bytes);
+        ++r.pcie_done;
+        if (use_l3 && (status = release_l2(r.blk[static_cast<size_t>(b)].l2_slot)) != TSB_OK) break;
       }
-      // PcieDone of a request's last chunk -> L1 resident -> compute ready.
-      for (size_t i : admitted) {
-        Rt& r = R[i];
-        if (r.dispatched_all && !r.resident && done(r.ev_resident)) {
-          r.resident = true;
-          progress = true;
+      if (status != TSB_OK) break;
+      if (r.pcie_done == plans[cl.req].n_chunks) r.compute_ready = true;
+      progress = true;
+    }
+    if (status != TSB_OK) break;
+    for (size_t k = admitted_head; k < admitted.size(); ++k) {  // ComputeDone (engine.cpp:274-283)
+      const size_t i = admitted[k];
+      Rt& r = R[i];
+      if (!r.started || r.finished || !done(r.ev_done)) continue;
+      r.finished = true;
+      ++finished;
+      --active;
+      compute_busy = false;
+      progress = true;
+      row(3, 2, -1, plans[i].id, -1, plans[i].compute_tokens * c->bytes_per_token);
+      if (opt->verify_seed && plans[i].n_chunks > 0) {  // opt-in check (synchronises the stream)
+        std::vector<tsb_ingest_item> items;
+        for (int64_t ch = 0; ch < plans[i].n_chunks; ++ch) {
+          const int64_t sl = plans[i].slots[ch];
+          items.push_back(tsb_ingest_item{sl < 0 ? ~sl : sl, r.row, static_cast<int32_t>(ch)});
         }
+        uint64_t mm = 0;
+        if ((status = tsb_l1_verify_synthetic(s->l1, items.data(), plans[i].n_chunks, 0, L, opt->verify_seed,
+                                              tsb_pool_chunk_bytes(s->pool), stream, &mm)) != TSB_OK)
+          break;
+        verify_mismatches += mm;
       }
-      // try_admit, decoupled (engine.cpp:318-339): the first stage must be idle with no backlog.
+      if (r.row >= 0 || r.deferred > 0) {
+        int64_t ng = 0;
+        grants.resize(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
+        if ((status = tsb_l1_release_request(s->l1, plans[i].id, grants.data(),
+                                             static_cast<int64_t>(grants.size()), &ng)) != TSB_OK)
+          break;
+        ++releases;
+        for (int64_t g = 0; g < ng; ++g) grant_l1(by_id.at(grants[g].request_id), grants[g].block_index);
+      }
+    }
+    if (status != TSB_OK) break;
+    while (admitted_head < admitted.size() && R[admitted[admitted_head]].finished) ++admitted_head;
+
+    // ---- pump(): try_admit / net_dispatch / pcie_dispatch / try_start_compute to a fixpoint ---
+    bool moved = true;
+    while (moved && status == TSB_OK) {
+      moved = false;
+      // try_admit (engine.cpp:318-339)
       if (!pending.empty()) {
         size_t bi = 0;
         for (size_t k = 1; k < pending.size(); ++k)
           if (key_less(pending[k], pending[bi])) bi = k;
-        Rt& r = R[pending[bi]];
-        bool backlog = false;
-        for (size_t i : admitted)
-          if (!R[i].dispatched_all) backlog = true;
+        const size_t i = pending[bi];
+        Rt& r = R[i];
         bool can = false;
-        if (r.n_chunks > 0) {
-          can = !backlog && (!ingest_issued || done(ev_ingest));
+        if (coupled) {
+          can = active == 0;
+        } else if (plans[i].n_chunks > 0) {
+          if (use_l3) {
+            can = !net_busy && unissued_net == 0;
+          } else {
+            bool backlog = false;  // the first stage is the L2 -> L1 hop: idle with no backlog
+            for (size_t k = admitted_head; k < admitted.size(); ++k) {
+              const Rt& a = R[admitted[k]];
+              if (a.admitted && a.pcie_issued < static_cast<int64_t>(a.blk.size())) backlog = true;
+            }
+            can = !backlog && calls.empty();
+          }
         } else {
           bool ready_waiting = false;
-          for (size_t i : admitted)
-            if (R[i].resident && !R[i].started) ready_waiting = true;
-          can = (!compute_issued || done(ev_compute)) && !ready_waiting;
+          for (size_t k = admitted_head; k < admitted.size(); ++k)
+            if (R[admitted[k]].compute_ready && !R[admitted[k]].started) ready_waiting = true;
+          can = !compute_busy && !ready_waiting;
         }
-        if (can) {
-          const size_t idx = pending[bi];
+        if (can) {  // admit (engine.cpp:341-355)
           pending.erase(pending.begin() + static_cast<std::ptrdiff_t>(bi));
           r.admitted = true;
-          r.admit_t = now_s() - host0;
-          pick_pos[idx] = static_cast<int32_t>(pick++);
-          admitted.push_back(idx);
-          for (int64_t ch = 0; ch < r.n_chunks; ++ch) {
-            int granted = 0;
-            const tsb_status rs = tsb_l1_request(s->l1, r.id, static_cast<int32_t>(ch), chunk_bytes,
-                                                 &granted, &r.row);
-            if (rs != TSB_OK) return fail_out(rs);
-            if (granted) {
-              r.ready.push_back(static_cast<int32_t>(ch));
-              ++r.granted;
-            } else {
-              ++r.deferred;
-              ++deferred_total;
+          r.admit_t = now();
+          pick_pos[i] = static_cast<int32_t>(pick++);
+          admitted.push_back(i);
+          ++active;
+          const int64_t nb = plans[i].n_chunks;
+          if (use_l3) {
+            unissued_net += nb;
+            for (int64_t b = 0; b < nb; ++b) {  // request_l2 (engine.cpp:357-362)
+              bool granted = false;
+              std::string msg;
+              const tsb_status rs = l2.request(plans[i].id, static_cast<int32_t>(b), l2_slot_bytes, &granted, &msg);
+              if (rs != TSB_OK) {
+                status = fail(rs, msg);
+                break;
+              }
+              if (granted) grant_l2(i, static_cast<int32_t>(b));
+              else ++l2_deferred;
             }
+          } else {
+            // Blocks are L2-resident already: the network hop is instantaneous, so proactive and
+            // reactive L1 reservation both happen now.
+            for (int64_t b = 0; b < nb && status == TSB_OK; ++b) {
+              r.blk[static_cast<size_t>(b)].l2_granted = r.blk[static_cast<size_t>(b)].net_done = true;
+              status = request_l1(i, static_cast<int32_t>(b));
+            }
+            r.net_done = nb;
           }
-          if (r.n_chunks == 0) {
-            r.dispatched_all = true;
-            cudaEventRecord(r.ev_first, st);
-            cudaEventRecord(r.ev_resident, st);
+          if (nb == 0) {  // compute-only: ready at admission (engine.cpp:351-354)
+            r.compute_ready = true;
+            cudaError_t e = cudaEventRecord(r.ev_first, s->compute);
+            if (e == cudaSuccess) e = cudaEventRecord(r.ev_resident, s->compute);
+            if (e != cudaSuccess) status = tsb::cuda_fail(e, "stage: compute-only request events");
           }
-          progress = true;
+          moved = true;
         }
       }
-      // pcie_dispatch: granted chunks of admitted requests, in admission order.
-      for (size_t i : admitted) {
+      if (status != TSB_OK) break;
+      // net_dispatch (engine.cpp:405-425): one block in flight, first granted block in pick order
+      if (use_l3 && !net_busy) {
+        for (size_t k = admitted_head; k < admitted.size(); ++k) {
+          const size_t i = admitted[k];
+          Rt& r = R[i];
+          if (r.next_net >= static_cast<int64_t>(r.blk.size())) continue;
+          Blk& b = r.blk[static_cast<size_t>(r.next_net)];
+          if (!b.l2_granted) continue;
+          const int64_t bi = r.next_net++;
+          --unissued_net;
+          row(4, 0, -1, plans[i].id, static_cast<int32_t>(bi), chunk_bytes);
+          if (!reactive && (status = request_l1(i, static_cast<int32_t>(bi))) != TSB_OK) break;
+          net_busy = true;
+          net_req = i;
+          net_blk = bi;
+          const double pace = opt->pace_network
+                                  ? c->transfer_base_latency + static_cast<double>(chunk_bytes) / c->network_bandwidth
+                                  : 0.0;
+          net_ready_at = now() + pace;
+          s->net->post(static_cast<const uint8_t*>(tsb_pool_slot_ptr(s->l3, plans[i].slots[bi])),
+                       static_cast<uint8_t*>(tsb_pool_slot_ptr(s->pool, b.l2_slot)),
+                       static_cast<size_t>(l2_slot_bytes));
+          ++net_blocks;
+          moved = true;
+          break;
+        }
+        if (status != TSB_OK) break;
+      }
+      // pcie_dispatch (engine.cpp:427-446): per admitted request in pick order, its next blocks
+      // in block order that are L2-resident and hold L1 pages; one ingest call per request.
+      for (size_t k = admitted_head; k < admitted.size() && status == TSB_OK; ++k) {
+        const size_t i = admitted[k];
         Rt& r = R[i];
-        if (r.ready.empty()) continue;
-        if (tsb_l1_sync_block_table(s->l1, stream) != TSB_OK) return fail_out(TSB_CUDA);
+        const int64_t nb = static_cast<int64_t>(r.blk.size());
+        if (r.next_pcie >= nb) continue;
+        if (coupled && r.net_done < nb) continue;
         std::vector<tsb_ingest_item> items;
-        for (int32_t ch : r.ready) items.push_back(tsb_ingest_item{r.slots[ch], r.row, ch});
-        r.ready.clear();
-        r.issued += static_cast<int64_t>(items.size());
-        const bool last = r.issued == r.n_chunks;
+        std::vector<int32_t> bl;
+        while (r.next_pcie < nb) {
+          Blk& b = r.blk[static_cast<size_t>(r.next_pcie)];
+          if (!b.net_done || !b.l1_granted) break;
+          b.pcie_issued = true;
+          const int64_t src = use_l3 ? b.l2_slot : plans[i].slots[r.next_pcie];
+          items.push_back(tsb_ingest_item{src, r.row, static_cast<int32_t>(r.next_pcie)});
+          bl.push_back(static_cast<int32_t>(r.next_pcie));
+          row(4, 1, -1, plans[i].id, static_cast<int32_t>(r.next_pcie), chunk_bytes);
+          ++r.next_pcie;
+        }
+        if (items.empty()) continue;
+        if ((status = tsb_l1_sync_block_table(s->l1, stream)) != TSB_OK) break;
+        r.pcie_issued += static_cast<int64_t>(items.size());
+        const bool last = r.pcie_issued == nb;
         std::vector<void*> evs;
         if (last) {
           evs.assign(static_cast<size_t>(L), nullptr);
           evs[0] = r.ev_first;
           evs[L - 1] = r.ev_resident;
         }
-        const tsb_status is = tsb_ingest_tiered(s->l1, s->pool, s->hbm_pool, items.data(),
-                                                static_cast<int64_t>(items.size()), 0, L,
-                                                opt->mode, stream, last ? evs.data() : nullptr);
-        if (is != TSB_OK) return fail_out(is);
-        if (last && L == 1) cudaEventRecord(r.ev_first, st);
-        cudaEventRecord(ev_ingest, st);
-        ingest_issued = true;
+        if ((status = tsb_ingest_tiered(s->l1, s->pool, s->hbm_pool, items.data(),
+                                        static_cast<int64_t>(items.size()), 0, L, opt->mode, stream,
+                                        last ? evs.data() : nullptr)) != TSB_OK)
+          break;
+        if (calls.size() >= 4096) {  // bound the in-flight call list (event slots are reused)
+          status = fail(TSB_CAPACITY, "stage: more than 4096 ingest calls in flight");
+          break;
+        }
+        if ((status = grow_events(s->call_pool, std::min<size_t>(call_slot + 1, 4096), cudaEventDefault)) != TSB_OK)
+          break;
+        cudaEvent_t ce = s->call_pool[call_slot++ % 4096];
+        cudaError_t e = cudaSuccess;
+        if (last && L == 1) e = cudaEventRecord(r.ev_first, st);
+        if (e == cudaSuccess) e = cudaEventRecord(ce, st);
+        if (e != cudaSuccess) {
+          status = tsb::cuda_fail(e, "stage: ingest call events");
+          break;
+        }
+        calls.push_back(Call{ce, i, std::move(bl)});
         ++ingest_calls;
         bytes_total += static_cast<int64_t>(items.size()) * chunk_bytes;
-        if (last) r.dispatched_all = true;
-        progress = true;
+        moved = true;
       }
+      if (status != TSB_OK) break;
       // try_start_compute (engine.cpp:448-473): best key among resident, not started.
-      if (!compute_issued || done(ev_compute)) {
+      if (!compute_busy) {
         size_t best = SIZE_MAX;
-        for (size_t i : admitted) {
-          const Rt& r = R[i];
-          if (!r.resident || r.started) continue;
+        for (size_t k = admitted_head; k < admitted.size(); ++k) {
+          const size_t i = admitted[k];
+          if (!R[i].compute_ready || R[i].started) continue;
           if (best == SIZE_MAX || key_less(i, best)) best = i;
         }
         if (best != SIZE_MAX) {
           Rt& r = R[best];
           r.started = true;
-          const double ct = static_cast<double>(r.compute_tokens);
-          const double secs =
-              c->compute_base + c->compute_per_token * ct + c->compute_quadratic * ct * ct;
-          const auto ns = static_cast<uint64_t>(secs * 1e9);
-          cudaStreamWaitEvent(s->compute, r.ev_resident, 0);
-          for (uint64_t t = 0; t < ns; t += 250000)
-            if (tsb::launch_prefill_burn(std::min<uint64_t>(250000, ns - t), ctas, nullptr,
-                                         s->compute) != cudaSuccess)
-              return fail_out(TSB_CUDA);
-          cudaEventRecord(r.ev_done, s->compute);
-          cudaEventRecord(ev_compute, s->compute);
-          compute_issued = true;
-          progress = true;
+          compute_busy = true;
+          row(4, 2, -1, plans[best].id, -1, 0);
+          std::vector<cudaEvent_t> fences(static_cast<size_t>(L), nullptr);
+          fences[0] = r.ev_resident;
+          if ((status = enqueue_prefill(s, static_cast<int64_t>(best), r.row,
+                                        opt->prefill || s->hook ? compute_seconds(q, best, c, plans[best].compute_tokens) : 0.0,
+                                        fences, ctas)) != TSB_OK)
+            break;
+          const cudaError_t e = cudaEventRecord(r.ev_done, s->compute);
+          if (e != cudaSuccess) {
+            status = tsb::cuda_fail(e, "stage: prefill done event");
+            break;
+          }
+          moved = true;
         }
       }
+      progress = progress || moved;
     }
+    if (status != TSB_OK) break;
     if (finished < static_cast<size_t>(n)) {
+      const double t = now();
+      if (progress) last_progress = t;
+      const bool in_flight = net_busy || !calls.empty() || compute_busy;
+      if (!in_flight && next_arrival >= by_arrival.size() && t - last_progress > 5.0) {
+        status = fail(TSB_CAPACITY, "stage: no request can make progress (ledger deadlock)");
+        break;
+      }
       // Nothing to do until the next completion or arrival: back off briefly.
-      const double wait = next_arrival < by_arrival.size()
-                              ? R[by_arrival[next_arrival]].arrival - (now_s() - host0)
-                              : 1.0;
-      if (wait > 50e-6) {
+      const double wait = next_arrival < by_arrival.size() ? R[by_arrival[next_arrival]].arrival - t : 1.0;
+      if (!progress && wait > 50e-6) {
         timespec ts{0, 20000};
         nanosleep(&ts, nullptr);
       }
     }
   }
-  TSB_CUDA_TRY(cudaStreamSynchronize(st));
-  TSB_CUDA_TRY(cudaStreamSynchronize(s->compute));
-  cudaEventDestroy(ev_ingest);
-  cudaEventDestroy(ev_compute);
-  if (status != TSB_OK) return status;
+  // Drain: no copy thread, ingest or prefill may outlive the call (error paths included).
+  while (net_busy && !s->net->done()) {
+    timespec ts{0, 20000};
+    nanosleep(&ts, nullptr);
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamSynchronize(s->compute);
+  if (status != TSB_OK) {
+    const std::string msg = tsb_last_error();
+    for (int64_t i = 0; i < n; ++i) {  // hand every L1 reservation back
+      if (!R[i].admitted || R[i].finished) continue;
+      std::vector<tsb_grant> g(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
+      int64_t ng = 0;
+      tsb_l1_release_request(s->l1, plans[i].id, g.data(), static_cast<int64_t>(g.size()), &ng);
+    }
+    return fail(status, msg);
+  }
 
   float last_ms = 0.f;
   for (int64_t i = 0; i < n; ++i) {
@@ -635,11 +1023,12 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     TSB_CUDA_TRY(cudaEventElapsedTime(&d, s->ev_start, r.ev_done));
     last_ms = std::max(last_ms, b);
     if (results)
-      results[i] = tsb_stage_request{r.id, pick_pos[i], r.deferred, r.n_chunks,
-                                     r.n_chunks * chunk_bytes, a, b, d, r.admit_t * 1e3,
+      results[i] = tsb_stage_request{plans[i].id, pick_pos[i], r.deferred, plans[i].n_chunks,
+                                     plans[i].n_chunks * chunk_bytes, a, b, d, r.admit_t * 1e3,
                                      r.arrival * 1e3};
   }
   if (stats) {
+    *stats = tsb_stage_stats{};
     stats->bytes = bytes_total;
     stats->device_ms = last_ms;
     stats->wall_ms = (now_s() - wall0) * 1e3;
@@ -648,6 +1037,8 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     stats->releases = releases;
     stats->kernel_launches = static_cast<int64_t>(tsb_kernel_launch_count() - launches0);
     stats->verify_mismatches = verify_mismatches;
+    stats->net_blocks = net_blocks;
+    stats->l2_deferred = l2_deferred;
   }
   return TSB_OK;
 }

@@ -97,6 +97,15 @@ class PrefixIndex:
                                    slots.ctypes.data, matched.ctypes.data))
         return matched[:n_req], slots[: len(hashes)]
 
+    def clear(self, stream=None):
+        check(lib.tsb_index_clear(self._h, (stream or torch.cuda.current_stream()).cuda_stream))
+
+    def compact(self, stream=None) -> int:
+        """Rebuild without erase tombstones; returns how many were reclaimed."""
+        n = C.c_int64()
+        check(lib.tsb_index_compact(self._h, (stream or torch.cuda.current_stream()).cuda_stream, C.byref(n)))
+        return n.value
+
     def stats(self, stream=None):
         live, full = C.c_int64(), C.c_int64()
         s = (stream or torch.cuda.current_stream()).cuda_stream

@@ -154,3 +154,61 @@ def test_request_path_with_hbm_tier_hits():
     res = stage.run(q, slot_lists, cfg, verify_seed=19)
     assert res.stats["verify_mismatches"] == 0
     assert list(res.requests["chunks"]) == list(matched)
+
+
+def test_duplicate_keys_in_one_batch_resolve_to_the_lowest_index():
+    """LooGLE-like batches index the same document chunk from several requests at once: the entry
+    must hold the value of the FIRST occurrence in the batch, every time (no race)."""
+    rng = np.random.default_rng(5)
+    uniq = rng.integers(1, 2**62, 3000).astype(np.uint64)
+    reps = rng.integers(0, len(uniq), 60000)
+    keys = uniq[reps]
+    vals = np.arange(len(keys), dtype=np.int64) + 7
+    first = {}
+    for i, k in enumerate(keys.tolist()):
+        first.setdefault(k, int(vals[i]))
+    for trial in range(5):
+        idx = hasher.PrefixIndex(capacity=1 << 13)
+        perm = rng.permutation(len(keys)) if trial else np.arange(len(keys))
+        idx.insert(keys[perm], vals[perm])
+        want = {}
+        for i in perm.tolist():
+            want.setdefault(int(keys[i]), int(vals[i]))
+        co = np.arange(len(uniq) + 1, dtype=np.int64)
+        m, got = idx.lookup(co, uniq)
+        assert np.all(m == 1)
+        assert [want[int(k)] for k in uniq.tolist()] == got.tolist()
+        assert idx.stats() == (len(uniq), 0)
+        # a later batch re-indexes: the newest call wins, again lowest index within it
+        idx.insert(keys[:10], vals[:10] + 10**9)
+        m, got2 = idx.lookup(np.arange(11, dtype=np.int64), keys[:10])
+        firsts = {}
+        for i in range(10):
+            firsts.setdefault(int(keys[i]), int(vals[i]) + 10**9)
+        assert got2.tolist() == [firsts[int(k)] for k in keys[:10].tolist()]
+
+
+def test_erase_churn_compaction_reclaims_tombstones():
+    import torch
+
+    cap = 1 << 12
+    idx = hasher.PrefixIndex(capacity=cap)
+    rng = np.random.default_rng(9)
+    live = {}
+    for rnd in range(12):  # each round fills ~70% of the table, then erases it all
+        keys = rng.integers(1, 2**62, int(0.7 * cap)).astype(np.uint64)
+        idx.insert(keys, np.arange(len(keys), dtype=np.int64))  # compacts by itself when tombstones fill it
+        live = {int(k): i for i, k in enumerate(keys.tolist())}
+        if rnd < 11:
+            idx.erase_device(torch.from_numpy(keys.view(np.int64)).cuda())
+            torch.cuda.synchronize()
+    assert idx.stats()[0] == len(live)
+    ks = np.array(list(live), np.uint64)
+    m, got = idx.lookup(np.arange(len(ks) + 1, dtype=np.int64), ks)
+    assert np.all(m == 1) and got.tolist() == [live[int(k)] for k in ks.tolist()]
+    # explicit compaction with nothing erased reclaims nothing; clear empties the table
+    assert idx.compact() == 0
+    idx.clear()
+    assert idx.stats() == (0, 0)
+    m, _ = idx.lookup(np.arange(len(ks) + 1, dtype=np.int64), ks)
+    assert np.all(m == 0)
