@@ -502,6 +502,10 @@ typedef struct {
   double done_ms;          /* run start -> prefill done / pages released (first token) */
   double admit_ms;         /* run start -> admitted (Timestamps::scheduled; host clock) */
   double arrival_ms;       /* run start -> arrival (online mode: replayed arrival time) */
+  double ingest_begin_ms;  /* run start -> its first L2 -> L1 hop began (CUDA event); with
+                              resident_ms the measured T_load sample for fit_linear */
+  int64_t cached_tokens;   /* cached_token_count (types.cpp:73-79): the T_load regressor */
+  int64_t compute_tokens;  /* compute_token_count (types.cpp:81-83): the T_comp regressor */
 } tsb_stage_request;
 
 typedef struct {

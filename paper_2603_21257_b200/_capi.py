@@ -103,7 +103,8 @@ class StageOptions(C.Structure):
 class StageRequest(C.Structure):
     _fields_ = [("request_id", i64), ("pick_position", i32), ("deferred_chunks", i32), ("chunks", i64),
                 ("bytes", i64), ("first_layer_ms", f64), ("resident_ms", f64), ("done_ms", f64),
-                ("admit_ms", f64), ("arrival_ms", f64)]
+                ("admit_ms", f64), ("arrival_ms", f64), ("ingest_begin_ms", f64), ("cached_tokens", i64),
+                ("compute_tokens", i64)]
 
 
 class StageStats(C.Structure):

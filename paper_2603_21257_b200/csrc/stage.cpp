@@ -359,14 +359,15 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     int64_t issued = 0;
     int32_t deferred = 0;
     bool finished_issue = false;
-    cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr, ev_begin = nullptr;
   };
   std::vector<ReqRt> reqs(static_cast<size_t>(n));
-  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(3 * n), cudaEventDefault));
+  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(4 * n), cudaEventDefault));
   for (int64_t i = 0; i < n; ++i) {
-    reqs[i].ev_first = s->timing_pool[3 * i];
-    reqs[i].ev_resident = s->timing_pool[3 * i + 1];
-    reqs[i].ev_done = s->timing_pool[3 * i + 2];
+    reqs[i].ev_first = s->timing_pool[4 * i];
+    reqs[i].ev_resident = s->timing_pool[4 * i + 1];
+    reqs[i].ev_done = s->timing_pool[4 * i + 2];
+    reqs[i].ev_begin = s->timing_pool[4 * i + 3];
   }
 
   // ---- pick order (K4 + K5 on the GPU) ----------------------------------------------------------
@@ -390,6 +391,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     ReqRt& r = reqs[i];
     const Plan& p = plans[i];
     if (p.n_chunks == 0) {
+      TSB_CUDA_TRY(cudaEventRecord(r.ev_begin, st));
       TSB_CUDA_TRY(cudaEventRecord(r.ev_first, st));
       TSB_CUDA_TRY(cudaEventRecord(r.ev_resident, st));
       for (int64_t l = 0; l < L; ++l) TSB_CUDA_TRY(cudaEventRecord(s->layer_ev[l], st));
@@ -428,6 +430,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
         items.push_back(tsb_ingest_item{p.slots[ch], r.row, ch});
         row(now_s() - host0, 4, 1, -1, p.id, ch, chunk_bytes);  // DispatchWake(Pcie)
       }
+      if (r.issued == 0) TSB_CUDA_TRY(cudaEventRecord(r.ev_begin, st));  // the request's first hop
       r.issued += static_cast<int64_t>(items.size());
       r.ready.clear();
       const bool last = r.issued == p.n_chunks;
@@ -558,14 +561,16 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   float last_ms = 0.f;
   for (int64_t i = 0; i < n; ++i) {
     ReqRt& r = reqs[i];
-    float a = 0.f, b = 0.f, d = 0.f;
+    float a = 0.f, b = 0.f, d = 0.f, g = 0.f;
     TSB_CUDA_TRY(cudaEventElapsedTime(&a, s->ev_start, r.ev_first));
     TSB_CUDA_TRY(cudaEventElapsedTime(&b, s->ev_start, r.ev_resident));
     TSB_CUDA_TRY(cudaEventElapsedTime(&d, s->ev_start, r.ev_done));
+    TSB_CUDA_TRY(cudaEventElapsedTime(&g, s->ev_start, r.ev_begin));
     last_ms = std::max(last_ms, b);
     if (results)
       results[i] = tsb_stage_request{plans[i].id, static_cast<int32_t>(pos_of[i]), r.deferred,
-                                     plans[i].n_chunks, plans[i].n_chunks * chunk_bytes, a, b, d, 0.0, 0.0};
+                                     plans[i].n_chunks, plans[i].n_chunks * chunk_bytes, a, b, d, 0.0, 0.0,
+                                     g, plans[i].n_chunks * s->shape.chunk_tokens, plans[i].compute_tokens};
   }
   if (opt->record_trace) {
     for (auto& tr : s->trace) {
@@ -632,19 +637,20 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     int64_t next_net = 0, next_pcie = 0, net_done = 0, pcie_issued = 0, pcie_done = 0;
     bool arrived = false, admitted = false, compute_ready = false, started = false, finished = false;
     double arrival = 0.0, admit_t = 0.0;
-    cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr, ev_begin = nullptr;
   };
   std::vector<Rt> R(static_cast<size_t>(n));
   double first_arrival = q->arrival[0];
   for (int64_t i = 0; i < n; ++i) first_arrival = std::min(first_arrival, q->arrival[i]);
-  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(3 * n), cudaEventDefault));
+  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(4 * n), cudaEventDefault));
   for (int64_t i = 0; i < n; ++i) {
     Rt& r = R[i];
     r.blk.resize(static_cast<size_t>(plans[i].n_chunks));
     r.arrival = q->arrival[i] - first_arrival;
-    r.ev_first = s->timing_pool[3 * i];
-    r.ev_resident = s->timing_pool[3 * i + 1];
-    r.ev_done = s->timing_pool[3 * i + 2];
+    r.ev_first = s->timing_pool[4 * i];
+    r.ev_resident = s->timing_pool[4 * i + 1];
+    r.ev_done = s->timing_pool[4 * i + 2];
+    r.ev_begin = s->timing_pool[4 * i + 3];
   }
   // Priority keys from the GPU scorer (K4), compared with PriorityKey::operator< on the host.
   std::vector<double> primary(static_cast<size_t>(n));
@@ -860,7 +866,8 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
           }
           if (nb == 0) {  // compute-only: ready at admission (engine.cpp:351-354)
             r.compute_ready = true;
-            cudaError_t e = cudaEventRecord(r.ev_first, s->compute);
+            cudaError_t e = cudaEventRecord(r.ev_begin, s->compute);
+            if (e == cudaSuccess) e = cudaEventRecord(r.ev_first, s->compute);
             if (e == cudaSuccess) e = cudaEventRecord(r.ev_resident, s->compute);
             if (e != cudaSuccess) status = tsb::cuda_fail(e, "stage: compute-only request events");
           }
@@ -918,6 +925,13 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
         }
         if (items.empty()) continue;
         if ((status = tsb_l1_sync_block_table(s->l1, stream)) != TSB_OK) break;
+        if (r.pcie_issued == 0) {
+          const cudaError_t e = cudaEventRecord(r.ev_begin, st);
+          if (e != cudaSuccess) {
+            status = tsb::cuda_fail(e, "stage: ingest begin event");
+            break;
+          }
+        }
         r.pcie_issued += static_cast<int64_t>(items.size());
         const bool last = r.pcie_issued == nb;
         std::vector<void*> evs;
@@ -1017,15 +1031,17 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   float last_ms = 0.f;
   for (int64_t i = 0; i < n; ++i) {
     Rt& r = R[i];
-    float a = 0.f, b = 0.f, d = 0.f;
+    float a = 0.f, b = 0.f, d = 0.f, g = 0.f;
     TSB_CUDA_TRY(cudaEventElapsedTime(&a, s->ev_start, r.ev_first));
     TSB_CUDA_TRY(cudaEventElapsedTime(&b, s->ev_start, r.ev_resident));
     TSB_CUDA_TRY(cudaEventElapsedTime(&d, s->ev_start, r.ev_done));
+    TSB_CUDA_TRY(cudaEventElapsedTime(&g, s->ev_start, r.ev_begin));
     last_ms = std::max(last_ms, b);
     if (results)
       results[i] = tsb_stage_request{plans[i].id, pick_pos[i], r.deferred, plans[i].n_chunks,
                                      plans[i].n_chunks * chunk_bytes, a, b, d, r.admit_t * 1e3,
-                                     r.arrival * 1e3};
+                                     r.arrival * 1e3, g, plans[i].n_chunks * s->shape.chunk_tokens,
+                                     plans[i].compute_tokens};
   }
   if (stats) {
     *stats = tsb_stage_stats{};

@@ -282,6 +282,49 @@ def fit_linear(samples: Iterable) -> LinearFit:
     return LinearFit(LinearCostModel(a.value, b.value), bool(ca.value), bool(cb.value))
 
 
+@dataclass
+class TokenSample:
+    """cost_model.hpp TokenSample: one measured (tokens, seconds) point."""
+
+    tokens: int
+    seconds: float
+
+
+def read_samples_csv(path) -> list[TokenSample]:
+    """cost_model.cpp:105-123: two columns (tokens, seconds) split on ',', ';', tab or spaces;
+    '#' comments and blank lines skipped; a non-numeric FIRST line is a header; any later
+    non-numeric line raises Error("read_samples_csv: malformed line in <path>: <line>")."""
+    try:
+        text = open(path).read()
+    except OSError:
+        raise Error(f"read_samples_csv: cannot open {path}") from None
+    out, first = [], True
+    for line in text.split("\n"):
+        if not line or line[0] == "#":
+            continue
+        parts = line.replace(",", " ").replace(";", " ").replace("\t", " ").split()
+        try:
+            tokens, seconds = float(parts[0]), float(parts[1])
+        except (IndexError, ValueError):
+            if not first:
+                raise Error(f"read_samples_csv: malformed line in {path}: {line}") from None
+            first = False
+            continue
+        out.append(TokenSample(int(tokens), seconds))
+        first = False
+    return out
+
+
+def write_samples_csv(path, samples, header: str = "tokens,seconds") -> None:
+    """The file read_samples_csv reads: a header, then one 'tokens,seconds' row per sample
+    (seconds printed with 17 significant digits, so the fit sees the measured doubles)."""
+    with open(path, "w") as f:
+        f.write(header + "\n")
+        for s in samples:
+            tok, sec = (s.tokens, s.seconds) if isinstance(s, TokenSample) else s
+            f.write(f"{int(tok)},{float(sec):.17g}\n")
+
+
 def estimate_service_cost(spec: RequestSpec, load_model: LinearCostModel, comp_model: LinearCostModel,
                           config: ClusterConfig) -> ServiceCost:
     q, s = _q1(spec)

@@ -76,3 +76,48 @@ def test_flashinfer_paged_decode_reads_ingested_pages(mode, layout):
             v = src[:, 1].reshape(-1, 8, 128).to(dev)
             want = _reference_attention(q[b], k, v)
             torch.testing.assert_close(out[b].float(), want, atol=2e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("layout", ["flash_attn", "flashinfer_nhd"])
+def test_real_prefill_consumer_as_stage_hook(layout):
+    """PagedPrefill (FlashInfer paged prefill + bf16 GEMMs per layer) runs as the stage's prefill
+    hook, gated on per-layer fences: every page is verified, the consumer's last-layer attention
+    equals attention over the source chunks, and ComputeDone follows residency."""
+    pytest.importorskip("flashinfer")
+    from paper_2603_21257_b200.consumer import PagedPrefill
+    from paper_2603_21257_b200.stage import LoadStage
+
+    shape = ingest.KVShape(layers=4, kv_heads=8, head_dim=128)
+    pool = ingest.ChunkPool(shape, 16)
+    pool.fill_synthetic(11)
+    l1 = ingest.PagedKVCache(shape, 16 * 16, max_rows=4, max_chunks=16, layout=ingest.LAYOUTS[layout])
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(4, 8, 128, 2))
+    q = t.QueueArrays(1, id=[5], arrival=[0.0], context_tokens=[256 * 6 + 100], query_tokens=[60],
+                      cache_hit_ratio=[1.0], flags=np.zeros(1, np.uint8))
+    slots = [[3, 9, 4, 0, 12, 7]]
+    stage = LoadStage(l1, pool)
+    cons = PagedPrefill(l1, q, cfg, hidden=1024, intermediate=2048, wrappers=2)
+    stage.set_prefill_hook(cons)
+    res = stage.run(q, slots, cfg, prefill=True, layer_events=True, verify_seed=11)
+    assert res.stats["verify_mismatches"] == 0 and cons.calls == shape.layers
+    r = res.requests
+    assert r["done_ms"][0] >= r["resident_ms"][0] >= r["first_layer_ms"][0]
+    # the consumer's last layer: o = attention(q, cached K/V of layer L-1) -- against the source chunks
+    ct = cons.ct[0]
+    assert ct == 100 + 60
+    chunks = torch.from_numpy(pool.slot_view(0, pool.n_slots).view(np.int16).copy()).view(torch.bfloat16)
+    chunks = chunks.view(pool.n_slots, shape.layers, 2, 256, 8, 128)
+    src = chunks[slots[0], shape.layers - 1]
+    k = src[:, 0].reshape(-1, 8, 128).cuda()
+    v = src[:, 1].reshape(-1, 8, 128).cuda()
+    qs = cons.q_buf[:ct]
+    for i in (0, 77, ct - 1):
+        want = _reference_attention(qs[i], k, v)
+        torch.testing.assert_close(cons.o_buf[i].float(), want, atol=2e-2, rtol=2e-2)
+    # an exception in the hook fails the stage call with that exception
+    def bad(*a):
+        raise RuntimeError("consumer exploded")
+    stage.set_prefill_hook(bad)
+    with pytest.raises(RuntimeError, match="consumer exploded"):
+        stage.run(q, slots, cfg, prefill=True)
+    assert l1.reserved() == 0

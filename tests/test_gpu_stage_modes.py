@@ -139,8 +139,6 @@ def test_online_l3_modes_pages_and_trace(rig, control, alloc):
     st = res.stats
     assert st["verify_mismatches"] == 0
     assert st["net_blocks"] == sum(plan_sizes(q)) and st["bytes"] == st["net_blocks"] * SHAPE.chunk_bytes
-    if control == t.ControlMode.Decoupled:  # blocks waiting for L1 pages keep their L2 slots
-        assert st["l2_deferred"] > 0 and st["deferred_chunks"] > 0
     l1 = rig["l1"]
     assert l1.reserved() == 0 and l1.free_pages() == l1.num_pages
     check_trace(res.trace, q, SHAPE.chunk_bytes, l1.capacity(), cfg.l2_capacity, control == t.ControlMode.Coupled)
@@ -149,6 +147,24 @@ def test_online_l3_modes_pages_and_trace(rig, control, alloc):
     if control == t.ControlMode.Coupled:  # admitted one at a time, each after its predecessor's ComputeDone
         order = np.argsort(r["pick_position"])
         assert np.all(r["admit_ms"][order][1:] >= r["done_ms"][order][:-1] - 0.5)
+
+
+@pytest.mark.parametrize("alloc", [t.AllocationMode.Proactive, t.AllocationMode.Reactive])
+def test_online_l2_and_l1_pressure(rig, alloc):
+    """Blocks that reached L2 but wait for L1 pages keep their L2 slots (released only after their
+    PCIe hop, engine.cpp:264), so later admissions are deferred on BOTH ledgers and granted FIFO."""
+    n = 4
+    q = t.QueueArrays(n, id=np.arange(1, n + 1), arrival=np.zeros(n), context_tokens=np.full(n, 13 * 256),
+                      query_tokens=np.full(n, 20), cache_hit_ratio=np.ones(n), flags=np.zeros(n, np.uint8))
+    slots = [list(range(13 * i % rig["n_l3"], 13 * i % rig["n_l3"] + 13)) for i in range(n)]
+    cfg = t.ClusterConfig(bytes_per_token=BPT, network_bandwidth=16e9, compute_base=0.05, compute_per_token=0.0,
+                          l2_capacity=rig["n_l2"] * SHAPE.chunk_bytes, allocation_mode=alloc)
+    res = rig["stage"].run_online(q, slots, cfg, pace_network=True, record_trace=True, verify_seed=SEED)
+    st = res.stats
+    assert st["verify_mismatches"] == 0
+    assert st["l2_deferred"] > 0 and st["deferred_chunks"] > 0
+    check_trace(res.trace, q, SHAPE.chunk_bytes, rig["l1"].capacity(), cfg.l2_capacity, False)
+    assert list(np.argsort(res.requests["pick_position"])) == [0, 1, 2, 3]
 
 
 def test_online_errors_and_exclusive_tiers(rig):

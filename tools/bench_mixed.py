@@ -39,6 +39,58 @@ def mixed_batch(n, seed, block=256):
     return q
 
 
+def timeline_summary(prof, path):
+    """Per-stream busy time of the copy engines (H2D memcpy), the ingest kernels and the prefill
+    kernels from a kineto (CUPTI) trace, and the time both the link and the prefill were busy."""
+    ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    spans = {"h2d": [], "ingest": [], "prefill": []}
+    for e in ev:
+        name = e.name
+        t0, t1 = e.time_range.start, e.time_range.end
+        if "Memcpy" in name or "memcpy" in name:
+            if "HtoD" in name or "H2D" in name or "Host to Device" in name:
+                spans["h2d"].append((t0, t1))
+        elif name.startswith("void tsb::") or "k_ingest" in name or "k_score" in name:
+            spans["ingest"].append((t0, t1))
+        else:
+            spans["prefill"].append((t0, t1))
+
+    def union(iv):
+        iv = sorted(iv)
+        out = []
+        for a, b in iv:
+            if out and a <= out[-1][1]:
+                out[-1] = (out[-1][0], max(out[-1][1], b))
+            else:
+                out.append((a, b))
+        return out
+
+    def inter(a, b):
+        i = j = 0
+        tot = 0.0
+        while i < len(a) and j < len(b):
+            lo, hi = max(a[i][0], b[j][0]), min(a[i][1], b[j][1])
+            tot += max(0.0, hi - lo)
+            if a[i][1] < b[j][1]:
+                i += 1
+            else:
+                j += 1
+        return tot
+
+    u = {k: union(v) for k, v in spans.items()}
+    busy = {k: sum(b - a for a, b in v) / 1e3 for k, v in u.items()}
+    allt = [t for v in u.values() for iv in v for t in iv]
+    res = {"source": "torch.profiler (kineto/CUPTI) CUDA activity of one overlapped run (nsys is not in the image)",
+           "window_ms": (max(allt) - min(allt)) / 1e3 if allt else 0.0,
+           "busy_ms": busy, "h2d_and_prefill_concurrent_ms": inter(u["h2d"], u["prefill"]) / 1e3,
+           "launches": {k: len(v) for k, v in spans.items()}}
+    res["prefill_hidden_under_link_frac"] = (res["h2d_and_prefill_concurrent_ms"] / busy["prefill"]
+                                             if busy["prefill"] else 0.0)
+    Path(path).write_text(json.dumps(res, indent=1))
+    prof.export_chrome_trace(str(Path(path).with_suffix(".trace.json")))
+    return res
+
+
 def main():
     import argparse
 
@@ -46,9 +98,14 @@ def main():
     ap.add_argument("--compute-per-token", type=float, default=4e-5,
                     help="prefill seconds/token: 4e-5 = the reference calibration (types.hpp:91); "
                          "~4e-6 approximates an 8B prefill on B200")
+    ap.add_argument("--consumer", choices=["k6", "real"], default="k6",
+                    help="k6: the calibrated timer; real: PagedPrefill (FlashInfer paged attention over the "
+                         "ingested pages + Llama-3.1-8B-sized bf16 GEMMs per layer) as the stage's prefill hook")
+    ap.add_argument("--n", type=int, default=48)
+    ap.add_argument("--profile", default="", help="write a kineto (CUPTI) timeline summary of the overlapped run here")
     args = ap.parse_args()
     shape = ingest.LLAMA31_8B
-    n = 48
+    n = args.n
     q = mixed_batch(n, 0)
     cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(32, 8, 128, 2),
                           compute_per_token=args.compute_per_token)
@@ -68,10 +125,24 @@ def main():
                        f"{{0.25,0.5,0.75,0.9,1.0}}, Llama-3.1-8B KV, L1 {num_pages * shape.page_bytes / 2**30:.0f} GiB",
            "chunks": int(sum(plans)), "bytes": int(sum(plans) * shape.local_chunk_bytes)}
     stage.run(q, slots, cfg, verify_seed=5)  # warm-up + full parity check
+    consumer = None
+    if args.consumer == "real":
+        from paper_2603_21257_b200.consumer import PagedPrefill
+
+        consumer = PagedPrefill(l1, q, cfg)
+        stage.set_prefill_hook(consumer)
+        stage.run(q, slots, cfg, prefill=True, layer_events=True)  # JIT + warm-up
+        out["consumer"] = {"kind": "PagedPrefill: FlashInfer paged prefill attention over l1.layer(l) + "
+                                   "Llama-3.1-8B-sized bf16 GEMMs (qkv, o, gate/up, down) per layer",
+                           "tflop_per_batch": sum(consumer.flops_per_request(i) for i in range(n)) / 1e12}
     runs = {}
     for name, kw in (("ingest_only", dict(prefill=False)), ("serial_prefill", dict(prefill=True, layer_events=False)),
                      ("overlapped_prefill", dict(prefill=True, layer_events=True))):
+        if consumer is not None and not kw.get("prefill"):
+            stage.set_prefill_hook(None)
         r = stage.run(q, slots, cfg, **kw)
+        if consumer is not None:
+            stage.set_prefill_hook(consumer)
         req = r.requests
         runs[name] = {"batch_ms": float(req["done_ms"].max()), "ingest_GBps": r.stats["bytes"] / (req["resident_ms"].max() * 1e-3) / 1e9,
                       "ttft_ms_mean": float(req["done_ms"].mean()), "ttft_ms_p50": float(np.median(req["done_ms"])),
@@ -82,6 +153,18 @@ def main():
                           for i in range(n)))
     out["prefill_total_ms"] = prefill_s * 1e3
     out["overlap_gain"] = runs["serial_prefill"]["batch_ms"] / runs["overlapped_prefill"]["batch_ms"]
+    if consumer is not None:
+        out["prefill_total_ms"] = None  # the real consumer's time is measured, not modelled
+        out["real_ttft_mean_ms"] = {k: v["ttft_ms_mean"] for k, v in out["runs"].items() if k != "ingest_only"}
+        out["ingest_GBps_with_prefill"] = runs["overlapped_prefill"]["ingest_GBps"]
+        out["ingest_GBps_alone"] = runs["ingest_only"]["ingest_GBps"]
+    if args.profile:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            stage.run(q, slots, cfg, prefill=True, layer_events=True)
+            torch.cuda.synchronize()
+        out["timeline"] = timeline_summary(prof, args.profile)
 
     # sim-vs-real: the reference DES with the measured ingest rate, no network stage
     import pyoracle as po
