@@ -142,9 +142,13 @@ class BatchScorer {
   }
   tsb_scorer* handle() { return s_.get(); }
 
+  /// One scorer per (host thread, current device): a rank bound to cuda:k scores on cuda:k.
   static BatchScorer& shared() {
-    static thread_local BatchScorer s(0);
-    return s;
+    const int dev = tsb_current_device();
+    static thread_local std::unordered_map<int, std::unique_ptr<BatchScorer>> per_dev;
+    auto& s = per_dev[dev];
+    if (!s) s = std::make_unique<BatchScorer>(dev);
+    return *s;
   }
 
  private:
@@ -153,6 +157,45 @@ class BatchScorer {
   };
   std::unique_ptr<tsb_scorer, Del> s_;
 };
+
+namespace detail {
+/// Priority keys the GPU scorer already computed, by request id.  A key depends only on the
+/// request's fields, its CostMap entry and the policy (never on `now`, scheduler.cpp:47), so an
+/// engine that calls pick_next in its pump loop pays the GPU round trip once per request, not once
+/// per pick; each pick is then the reference's O(n) argmin over cached keys.
+struct CachedKey {
+  double arrival, hit, deadline, t_load, t_comp, primary;
+  std::int64_t ctx, query;
+  bool has_deadline, has_cost, has_measured;
+  PolicyKind policy;
+};
+inline std::unordered_map<std::int64_t, CachedKey>& key_cache() {
+  static thread_local std::unordered_map<std::int64_t, CachedKey> m;
+  return m;
+}
+inline CachedKey key_fields(const RequestSpec& s, PolicyKind policy, const CostMap& costs) {
+  CachedKey k{};
+  k.arrival = s.arrival_time;
+  k.hit = s.cache_hit_ratio;
+  k.ctx = s.context_tokens;
+  k.query = s.query_tokens;
+  k.has_deadline = s.deadline.has_value();
+  k.deadline = s.deadline.value_or(0.0);
+  const auto it = costs.find(s.id);
+  k.has_cost = it != costs.end();
+  k.t_load = k.has_cost ? it->second.t_load : 0.0;
+  k.t_comp = k.has_cost ? it->second.t_comp : 0.0;
+  k.has_measured = s.measured_cost.has_value();
+  k.policy = policy;
+  return k;
+}
+inline bool same_fields(const CachedKey& a, const CachedKey& b) {
+  return a.arrival == b.arrival && a.hit == b.hit && a.ctx == b.ctx && a.query == b.query &&
+         a.has_deadline == b.has_deadline && a.deadline == b.deadline && a.has_cost == b.has_cost &&
+         a.t_load == b.t_load && a.t_comp == b.t_comp && a.has_measured == b.has_measured &&
+         a.policy == b.policy;
+}
+}  // namespace detail
 
 /// The pick_next drain of a fixed queue in one GPU pass: ids in pick order.
 inline std::vector<std::int64_t> schedule_order(std::span<const RequestSpec> queue, PolicyKind policy,
@@ -163,14 +206,48 @@ inline std::vector<std::int64_t> schedule_order(std::span<const RequestSpec> que
   return ids;
 }
 
-/// scheduler.cpp:75-91, on the GPU.
+/// scheduler.cpp:75-91.  Keys of requests not seen before (or whose fields, cost or policy
+/// changed) are computed by the GPU scorer in one batch; the argmin (first minimum wins) runs over
+/// the cached keys, as the reference's scan does.
 inline std::optional<std::size_t> best_request_index(std::span<const RequestSpec> queue,
                                                      PolicyKind policy, const CostMap& costs,
                                                      double now) {
   (void)now;
   if (queue.empty()) return std::nullopt;
-  const auto r = BatchScorer::shared().score(queue, policy, CostModelPair{}, ClusterConfig{}, &costs);
-  return static_cast<std::size_t>(r.order[0]);
+  auto& cache = detail::key_cache();
+  if (cache.size() > 4 * queue.size() + 4096) cache.clear();  // bounded: drop finished requests
+  std::vector<RequestSpec> fresh;
+  std::vector<detail::CachedKey> fresh_fields;
+  std::vector<const detail::CachedKey*> keys(queue.size(), nullptr);
+  for (std::size_t i = 0; i < queue.size(); ++i) {
+    const detail::CachedKey f = detail::key_fields(queue[i], policy, costs);
+    const auto it = cache.find(queue[i].id);
+    if (it != cache.end() && detail::same_fields(it->second, f)) {
+      keys[i] = &it->second;
+    } else {
+      fresh.push_back(queue[i]);
+      fresh_fields.push_back(f);
+    }
+  }
+  if (!fresh.empty()) {
+    const auto r = BatchScorer::shared().score(fresh, policy, CostModelPair{}, ClusterConfig{}, &costs);
+    for (std::size_t k = 0; k < fresh.size(); ++k) {
+      fresh_fields[k].primary = r.primary[k];
+      cache[fresh[k].id] = fresh_fields[k];
+    }
+    for (std::size_t i = 0; i < queue.size(); ++i)
+      if (!keys[i]) keys[i] = &cache.at(queue[i].id);
+  }
+  std::size_t best = 0;
+  PriorityKey best_key{keys[0]->primary, queue[0].arrival_time, queue[0].id};
+  for (std::size_t i = 1; i < queue.size(); ++i) {
+    const PriorityKey k{keys[i]->primary, queue[i].arrival_time, queue[i].id};
+    if (k < best_key) {
+      best = i;
+      best_key = k;
+    }
+  }
+  return best;
 }
 
 /// scheduler.cpp:93-100

@@ -40,6 +40,9 @@ typedef enum {
 
 const char* tsb_last_error(void);
 const char* tsb_version(void);
+/* The calling thread's current CUDA device (cudaGetDevice; 0 if none), for header-only C++
+ * callers that keep one object per device. */
+int tsb_current_device(void);
 /* Number of device kernels this library has launched since load (evidence counter). */
 uint64_t tsb_kernel_launch_count(void);
 

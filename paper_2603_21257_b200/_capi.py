@@ -134,6 +134,7 @@ st = C.c_int
 _decl("tsb_last_error", C.c_char_p)
 _decl("tsb_version", C.c_char_p)
 _decl("tsb_kernel_launch_count", u64)
+_decl("tsb_current_device", C.c_int)
 _decl("tsb_cluster_default", None, P(Cluster))
 _decl("tsb_cluster_validate", st, P(Cluster))
 _decl("tsb_kv_bytes_per_token", st, i64, i64, i64, i64, P(i64))

@@ -46,6 +46,10 @@ extern "C" {
 const char* tsb_last_error(void) { return tsb::g_last_error.c_str(); }
 const char* tsb_version(void) { return "tsb 0.1.0 sm_100a"; }
 uint64_t tsb_kernel_launch_count(void) { return tsb::g_launches.load(); }
+int tsb_current_device(void) {
+  int d = 0;
+  return cudaGetDevice(&d) == cudaSuccess ? d : 0;
+}
 
 // ---------------------------------------------------------------------------------------
 // ClusterConfig (types.hpp:82-97, validate types.cpp:56-71)
@@ -337,7 +341,7 @@ tsb_status scorer_check_errors(tsb_scorer* s, cudaStream_t st, int64_t* err_inde
 extern "C" {
 
 tsb_status tsb_scorer_create(int device, int64_t capacity, tsb_scorer** out) {
-  TSB_CUDA_TRY(cudaSetDevice(device));
+  tsb::DeviceGuard dg(device);
   auto* s = new tsb_scorer();
   s->device = device;
   cudaError_t e = cudaMalloc(&s->err, 3 * sizeof(unsigned long long));
@@ -358,6 +362,8 @@ tsb_status tsb_scorer_create(int device, int64_t capacity, tsb_scorer** out) {
 }
 
 void tsb_scorer_destroy(tsb_scorer* s) {
+  if (!s) return;
+  tsb::DeviceGuard dg(s->device);
   scorer_free(s);
   delete s;
 }
@@ -368,6 +374,7 @@ tsb_status tsb_score_queue_device(tsb_scorer* s, void* stream, int64_t n, const 
                                   int64_t* order, int64_t* err_index) {
   if (policy < TSB_FIFO || policy > TSB_LSTF) return fail(TSB_VALIDATION, "unknown policy");
   if (n < 0) return fail(TSB_VALIDATION, "score_queue: n must be >= 0");
+  tsb::DeviceGuard dg(s->device);
   if (c->block_size_tokens < 1)
     return fail(TSB_VALIDATION, "cluster: block_size_tokens must be >= 1");
   TSB_TRY(scorer_reserve(s, n));
@@ -387,6 +394,7 @@ tsb_status tsb_score_queue_device(tsb_scorer* s, void* stream, int64_t n, const 
 }
 
 tsb_status tsb_scorer_check(tsb_scorer* s, void* stream, int64_t* err_index) {
+  tsb::DeviceGuard dg(s->device);
   return scorer_check_errors(s, static_cast<cudaStream_t>(stream), err_index);
 }
 
@@ -395,6 +403,7 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
                            double* t_load, double* t_comp, double* primary, int64_t* order) {
   auto st = static_cast<cudaStream_t>(stream);
   if (n == 0) return TSB_OK;
+  tsb::DeviceGuard dg(s->device);
   // Pack the SoA queue into one device block: 7 x 8-byte arrays + flags.
   const size_t w = sizeof(int64_t) * static_cast<size_t>(n);
   if (n > s->host_cap) {  // grow-only buffers: no allocation (and no implicit sync) per call
@@ -488,35 +497,51 @@ tsb_status tsb_hash_prefix_chunks(void* stream, int64_t n_req, const int64_t* of
   *n_hashes = total;
   if (total == 0) return TSB_OK;
   const int64_t ntok = offsets[n_req] - offsets[0];
-  int64_t *doff = nullptr, *dcoff = nullptr;
-  int32_t* dtok = nullptr;
-  uint64_t* dout = nullptr;
-  tsb_status rc = TSB_OK;
-  cudaError_t e = cudaMalloc(&doff, sizeof(int64_t) * (n_req + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&dcoff, sizeof(int64_t) * (n_req + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&dtok, sizeof(int32_t) * std::max<int64_t>(ntok, 1));
-  if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(uint64_t) * total);
+  // Grow-only device buffers per (host thread, device): no cudaMalloc / cudaFree (and no implicit
+  // device synchronisation) per call once the largest batch has been seen.
+  int dev = 0;
+  TSB_CUDA_TRY(cudaGetDevice(&dev));
+  struct HashBufs {
+    int64_t* off = nullptr;
+    int64_t* coff = nullptr;
+    int32_t* tok = nullptr;
+    uint64_t* out = nullptr;
+    int64_t n_req = 0, ntok = 0, total = 0;
+  };
+  thread_local std::vector<HashBufs> per_dev;
+  if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(static_cast<size_t>(dev) + 1);
+  HashBufs& b = per_dev[static_cast<size_t>(dev)];
+  auto grow = [&](auto** p, int64_t& cap, int64_t need, size_t elem) -> cudaError_t {
+    if (need <= cap) return cudaSuccess;
+    cudaFree(*p);
+    *p = nullptr;
+    cap = 0;
+    const int64_t n = std::max<int64_t>(need, cap + cap / 2);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), elem * static_cast<size_t>(n));
+    if (e == cudaSuccess) cap = n;
+    return e;
+  };
+  int64_t n_cap = b.n_req, n_cap2 = b.n_req;
+  cudaError_t e = grow(&b.off, n_cap, n_req + 1, sizeof(int64_t));
+  if (e == cudaSuccess) e = grow(&b.coff, n_cap2, n_req + 1, sizeof(int64_t));
+  if (e == cudaSuccess) b.n_req = std::min(n_cap, n_cap2);
+  if (e == cudaSuccess) e = grow(&b.tok, b.ntok, std::max<int64_t>(ntok, 1), sizeof(int32_t));
+  if (e == cudaSuccess) e = grow(&b.out, b.total, total, sizeof(uint64_t));
   if (e == cudaSuccess) {
     std::vector<int64_t> rel(offsets, offsets + n_req + 1);
     for (auto& v : rel) v -= offsets[0];
-    e = cudaMemcpyAsync(doff, rel.data(), sizeof(int64_t) * (n_req + 1), cudaMemcpyHostToDevice, st);
+    e = cudaMemcpyAsync(b.off, rel.data(), sizeof(int64_t) * (n_req + 1), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(dcoff, coff.data(), sizeof(int64_t) * (n_req + 1),
-                          cudaMemcpyHostToDevice, st);
+      e = cudaMemcpyAsync(b.coff, coff.data(), sizeof(int64_t) * (n_req + 1), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(dtok, tokens + offsets[0], sizeof(int32_t) * ntok,
-                          cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = tsb::launch_hash_prefix(n_req, doff, dtok, dcoff, dout, st);
+      e = cudaMemcpyAsync(b.tok, tokens + offsets[0], sizeof(int32_t) * ntok, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = tsb::launch_hash_prefix(n_req, b.off, b.tok, b.coff, b.out, st);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(out, dout, sizeof(uint64_t) * total, cudaMemcpyDeviceToHost, st);
+      e = cudaMemcpyAsync(out, b.out, sizeof(uint64_t) * total, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
-  if (e != cudaSuccess) rc = tsb::cuda_fail(e, "tsb_hash_prefix_chunks");
-  cudaFree(doff);
-  cudaFree(dcoff);
-  cudaFree(dtok);
-  cudaFree(dout);
-  return rc;
+  if (e != cudaSuccess) return tsb::cuda_fail(e, "tsb_hash_prefix_chunks");
+  return TSB_OK;
 }
 
 tsb_status tsb_gen_tokens_device(void* stream, uint64_t seed, int64_t n_req,

@@ -151,8 +151,8 @@ tsb_status tsb_pool_create_device(int device, const tsb_kv_shape* shape, int64_t
                                   tsb_pool** out) {
   tsb_pool* p = nullptr;
   TSB_TRY(new_device_pool(shape, device, n_slots, &p));
-  cudaError_t e = cudaSetDevice(device);
-  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->dev),
+  tsb::DeviceGuard dg(device);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->dev),
                                        static_cast<size_t>(p->chunk_bytes) * n_slots);
   if (e != cudaSuccess) {
     delete p;
@@ -325,6 +325,7 @@ int tsb_pool_numa_node(const tsb_pool* p) {
 
 void tsb_pool_destroy(tsb_pool* p) {
   if (!p) return;
+  tsb::DeviceGuard dg(p->location == TSB_POOL_DEVICE && p->owned ? p->device : -1);
   if (p->location == TSB_POOL_DEVICE) {
     if (p->owned) cudaFree(p->dev);
     if (p->ipc) cudaIpcCloseMemHandle(p->dev);
@@ -344,6 +345,7 @@ int64_t tsb_pool_chunk_bytes(const tsb_pool* p) { return p->chunk_bytes; }
 
 tsb_status tsb_pool_fill_synthetic(tsb_pool* p, uint64_t seed, int64_t first, int64_t n,
                                    void* stream) {
+  tsb::DeviceGuard dg(p->location == TSB_POOL_DEVICE ? p->device : -1);
   if (first < 0 || n < 0 || first + n > p->slots)
     return fail(TSB_VALIDATION, "pool_fill_synthetic: slot range out of bounds");
   auto st = static_cast<cudaStream_t>(stream);
@@ -451,7 +453,7 @@ tsb_status tsb_l1_create(int device, const tsb_kv_shape* shape, int64_t num_page
   if (num_pages < 1 || num_pages > INT32_MAX)
     return fail(TSB_VALIDATION, "l1: num_pages must be in [1, 2^31)");
   if (max_rows < 1 || max_chunks < 1) return fail(TSB_VALIDATION, "l1: max_rows/max_chunks must be >= 1");
-  TSB_CUDA_TRY(cudaSetDevice(device));
+  tsb::DeviceGuard dg(device);
   auto* l = new tsb_l1();
   l->device = device;
   l->shape = *shape;
@@ -502,6 +504,8 @@ tsb_status tsb_l1_create(int device, const tsb_kv_shape* shape, int64_t num_page
 }
 
 void tsb_l1_destroy(tsb_l1* l) {
+  if (!l) return;
+  tsb::DeviceGuard dg(l->device);
   l1_free(l);
   delete l;
 }
@@ -614,6 +618,7 @@ const int32_t* tsb_l1_block_table_device(const tsb_l1* l) { return l->bt_dev; }
 int64_t tsb_l1_block_table_stride(const tsb_l1* l) { return l->stride; }
 
 tsb_status tsb_l1_sync_block_table(tsb_l1* l, void* stream) {
+  tsb::DeviceGuard dg(l->device);
   auto st = static_cast<cudaStream_t>(stream);
   int64_t r = 0;
   while (r < l->rows) {
@@ -951,6 +956,7 @@ extern "C" {
 tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
                       int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
                       void* const* layer_events) {
+  tsb::DeviceGuard dg(l->device);
   auto st = static_cast<cudaStream_t>(stream);
   const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb_ingest_item));
   if (n_items > per)
@@ -979,6 +985,7 @@ tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, i
 tsb_status tsb_ingest_tiered(tsb_l1* l, tsb_pool* pool, tsb_pool* hbm_pool,
                              const tsb_ingest_item* items, int64_t n_items, int64_t layer_lo,
                              int64_t layer_hi, int mode, void* stream, void* const* layer_events) {
+  tsb::DeviceGuard dg(l->device);
   std::vector<tsb_ingest_item> host, tier;
   for (int64_t k = 0; k < n_items; ++k) {
     if (items[k].src_slot >= 0) {
@@ -1031,6 +1038,7 @@ tsb_status tsb_ingest_tiered(tsb_l1* l, tsb_pool* pool, tsb_pool* hbm_pool,
 tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
                              int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
                              void* stream, void* const* layer_events) {
+  tsb::DeviceGuard dg(l->device);
   return ingest_impl(l, pool, items_dev, nullptr, n_items, layer_lo, layer_hi, mode,
                      static_cast<cudaStream_t>(stream), layer_events);
 }
@@ -1054,6 +1062,7 @@ tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes) {
 tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_item* items_dev,
                               int64_t n_items, int64_t layer_lo, int64_t layer_hi,
                               void* stream) {
+  tsb::DeviceGuard dg(l->device);
   if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
     return fail(TSB_VALIDATION, "scatter: layer range must satisfy 0 <= lo < hi <= layers");
   tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
@@ -1067,6 +1076,7 @@ tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_i
 tsb_status tsb_scatter_device_packed(tsb_l1* l, const void* staging,
                                      const tsb_ingest_item* items_dev, int64_t n_items,
                                      int64_t layer_lo, int64_t layer_hi, void* stream) {
+  tsb::DeviceGuard dg(l->device);
   if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
     return fail(TSB_VALIDATION, "scatter: layer range must satisfy 0 <= lo < hi <= layers");
   const tsb::IngestGeom g = make_staged_geom(l, layer_lo, layer_hi - layer_lo);
@@ -1079,6 +1089,7 @@ tsb_status tsb_l1_verify_synthetic(tsb_l1* l, const tsb_ingest_item* items, int6
                                    int64_t layer_lo, int64_t layer_hi, uint64_t seed,
                                    int64_t pool_chunk_bytes, void* stream,
                                    uint64_t* mismatches) {
+  tsb::DeviceGuard dg(l->device);
   // Independent of the ingest address math (verify.cu): invert the host block table into
   // page -> (slot, first token), then check every word of those pages from the layout definition.
   auto st = static_cast<cudaStream_t>(stream);

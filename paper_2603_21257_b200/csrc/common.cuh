@@ -22,6 +22,21 @@ void count_launch(uint64_t n = 1);
     if (_e != cudaSuccess) return ::tsb::cuda_fail(_e, #expr);     \
   } while (0)
 
+// Runs a C-ABI call on an object's device and restores the caller's current device on exit, so
+// no entry point leaves the calling thread switched to another GPU.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 #define TSB_TRY(expr)                       \
   do {                                      \
     tsb_status _s = (expr);                 \

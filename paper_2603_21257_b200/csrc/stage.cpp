@@ -147,17 +147,6 @@ struct tsb_stage {
 
 namespace {
 
-// Device of the stage for the duration of a call; restores the caller's device on exit.
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
 
 tsb_status grow_events(std::vector<cudaEvent_t>& v, size_t n, unsigned flags) {
   while (v.size() < n) {
@@ -203,7 +192,7 @@ tsb_status tsb_stage_create(tsb_l1* l1, tsb_pool* pool, tsb_stage** out) {
     return st;
   }
   s->device = tsb_l1_device(l1);
-  DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s->device);
   int lo = 0, hi = 0;
   cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
   // Prefill gets the LOWEST priority so the ingest scatter kernels interleave ahead of it.
@@ -254,7 +243,7 @@ void* tsb_stage_compute_stream(tsb_stage* s) { return s->compute; }
 
 void tsb_stage_destroy(tsb_stage* s) {
   if (!s) return;
-  DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s->device);
   delete s->net;
   for (auto e : s->timing_pool) cudaEventDestroy(e);
   for (auto e : s->layer_ev) cudaEventDestroy(e);
@@ -331,7 +320,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
                          const double models[4], const int64_t* slot_offsets,
                          const int64_t* slots, const tsb_stage_options* opt, void* stream,
                          tsb_stage_request* results, tsb_stage_stats* stats) {
-  DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s->device);
   const double wall0 = now_s();
   const uint64_t launches0 = tsb_kernel_launch_count();
   auto st = static_cast<cudaStream_t>(stream);
@@ -603,7 +592,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
                                 const int64_t* slot_offsets, const int64_t* slots,
                                 const tsb_stage_options* opt, void* stream,
                                 tsb_stage_request* results, tsb_stage_stats* stats) {
-  DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s->device);
   const double wall0 = now_s();
   const uint64_t launches0 = tsb_kernel_launch_count();
   auto st = static_cast<cudaStream_t>(stream);

@@ -230,6 +230,34 @@ static void gpu_cases() {
     EXPECT(r.stats.verify_mismatches == 0 && r.stats.deferred_chunks > 0 && l1.reserved() == 0);
     EXPECT(r.stats.bytes == 9 * 256 * cfg.bytes_per_token);
   });
+  run("gpu: pick_next drain == schedule_order, keys computed once per request", [] {
+    std::vector<RequestSpec> q;
+    for (int i = 0; i < 300; ++i) {
+      RequestSpec r = spec(1000 + i, 0.001 * ((i * 37) % 300), 256 * (1 + (i * 13) % 40));
+      r.cache_hit_ratio = (i % 3) ? 0.9 : 0.5;
+      r.deadline = r.arrival_time + 1.0 + 0.01 * (i % 17);
+      q.push_back(r);
+    }
+    CostMap costs;
+    for (int i = 0; i < 300; i += 3) costs[1000 + i] = ServiceCost{0.001 * (i % 7), 0.002};
+    for (PolicyKind p : {PolicyKind::Lstf, PolicyKind::SjfCost}) {
+      const auto want = schedule_order(q, p, costs);
+      std::vector<RequestSpec> work = q;
+      const uint64_t l0 = tsb_kernel_launch_count();
+      std::vector<std::int64_t> got;
+      while (auto r = pick_next(work, p, costs, 0.0)) got.push_back(r->id);
+      const uint64_t launches = tsb_kernel_launch_count() - l0;
+      EXPECT(got == want);
+      EXPECT(launches < 20);  // one scoring pass for the whole drain, not 300
+      // a new arrival is scored on its own and slots into the cached order
+      work = q;
+      RequestSpec late = spec(5000, 0.0, 256);
+      late.deadline = 0.01;
+      work.push_back(late);
+      const auto first = pick_next(work, p, costs, 0.0);
+      EXPECT(first && (p != PolicyKind::Lstf || first->id == 5000));
+    }
+  });
   run("gpu: prefix hasher", [] {
     std::vector<std::int64_t> off = {0, 600, 1112};
     std::vector<std::int32_t> tok(1112);
