@@ -554,6 +554,10 @@ typedef int (*tsb_prefill_hook)(void* user, int64_t q_index, int32_t bt_row, int
 tsb_status tsb_stage_set_prefill_hook(tsb_stage* s, tsb_prefill_hook hook, void* user);
 /* The stage's compute stream (lowest priority; prefill runs here). */
 void* tsb_stage_compute_stream(tsb_stage* s);
+/* Run prefill on the caller's stream instead (not destroyed by the stage; NULL = a stage-owned
+ * lowest-priority stream again): a consumer whose framework owns stream lifetimes (e.g. a torch
+ * stream) keeps its work and host buffers tied to a stream that outlives the stage. */
+tsb_status tsb_stage_set_compute_stream(tsb_stage* s, void* stream);
 void tsb_stage_destroy(tsb_stage* s);
 /* HBM tier of the stage (NULL clears it): in tsb_stage_run / _online, a slot < 0 names slot ~slot
  * of hbm_pool (same chunk geometry as the L2 pool); those chunks bypass the host link. */

@@ -226,6 +226,7 @@ _decl("tsb_stage_set_l3", st, vp, vp, C.c_int)
 PREFILL_HOOK = C.CFUNCTYPE(C.c_int, vp, i64, i32, i64, vp)
 _decl("tsb_stage_set_prefill_hook", st, vp, PREFILL_HOOK, vp)
 _decl("tsb_stage_compute_stream", vp, vp)
+_decl("tsb_stage_set_compute_stream", st, vp, vp)
 _decl("tsb_stage_run", st, vp, i64, P(Queue), P(Cluster), P(f64), vp, vp, P(StageOptions), vp, P(StageRequest),
       P(StageStats))
 _decl("tsb_stage_trace", st, vp, P(TraceRow), i64, P(i64))

@@ -32,9 +32,15 @@ def ingest_samples(requests: np.ndarray) -> list[TokenSample]:
 
 
 def compute_samples(requests: np.ndarray) -> list[TokenSample]:
-    """(compute tokens, prefill seconds) per request -- valid when prefill starts at residency
-    (layer_events off), so done - resident is the prefill alone."""
-    return [TokenSample(int(r["compute_tokens"]), float(r["done_ms"] - r["resident_ms"]) * 1e-3) for r in requests]
+    """(compute tokens, prefill seconds) per request, for runs whose prefill starts once the request
+    is resident (layer_events off).  Prefills run one at a time in pick order on the compute
+    stream, so a request's prefill starts at max(its residency, the previous prefill's end)."""
+    out, prev_done = [], 0.0
+    for r in requests[np.argsort(requests["pick_position"], kind="stable")]:
+        start = max(float(r["resident_ms"]), prev_done)
+        out.append(TokenSample(int(r["compute_tokens"]), (float(r["done_ms"]) - start) * 1e-3))
+        prev_done = float(r["done_ms"])
+    return out
 
 
 @dataclass

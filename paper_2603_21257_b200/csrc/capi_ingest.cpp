@@ -392,6 +392,8 @@ struct tsb_l1 {
   uint8_t* staging = nullptr;  // CE staging (lazy)
   int64_t staging_bytes = 0;
   cudaStream_t ce_stream = nullptr;
+  cudaStream_t k2_stream = nullptr;  // K2 at the greatest stream priority: ahead of prefill kernels
+  cudaEvent_t ev_k2_done = nullptr;
   cudaEvent_t ev_fence = nullptr;
   // two-tier ingest: the HBM-tier part runs on its own stream beside the host part; the host
   // part's first layer fence waits for it (fence_dep, consumed once)
@@ -421,6 +423,8 @@ void l1_free(tsb_l1* l) {
   for (auto& e : l->ev_k2)
     if (e) cudaEventDestroy(e);
   if (l->ce_stream) cudaStreamDestroy(l->ce_stream);
+  if (l->k2_stream) cudaStreamDestroy(l->k2_stream);
+  if (l->ev_k2_done) cudaEventDestroy(l->ev_k2_done);
   if (l->ev_tier_start) cudaEventDestroy(l->ev_tier_start);
   if (l->ev_tier_done) cudaEventDestroy(l->ev_tier_done);
   if (l->tier_stream) cudaStreamDestroy(l->tier_stream);
@@ -654,13 +658,85 @@ tsb_status tsb_ingest_set_scatter(int impl, int ctas) {
 
 namespace {
 
-// K2: HBM staging -> pages, with the SM load/store kernel or the bulk-copy (TMA engine) kernel.
-cudaError_t launch_scatter(const tsb::IngestGeom& g, const uint8_t* src, uint8_t* arena,
-                           const tsb_ingest_item* items, const int32_t* bt, int64_t n,
-                           cudaStream_t st) {
-  if (g_knobs.scatter_impl == 1 && g.seg_bytes * 2 <= tsb::kBulkSmem && !g.hnd)
-    return tsb::launch_ingest_bulk(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st);
-  return tsb::launch_ingest_ldg(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st, true);
+// K1b CTAs per SM from an HBM / NVLink source: as many rings as fit in 228 KB of shared memory.
+int tma_ctas_per_sm(const tsb::IngestGeom& g) {
+  const int64_t stages = std::min<int64_t>(tsb::kTmaMaxStages, tsb::kBulkSmem / g.seg_bytes);
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (stages * g.seg_bytes + 2048))));
+}
+
+// ---- tensor maps for K1b (cuTensorMapEncodeTiled through the runtime's driver entry point) ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// Source map whose box is one page segment.  base = slot 0 of the pool (or the staging ring),
+// rows = every token row [outer][2][C] of it, pitch = bytes per token row.  NHD: 2D map over
+// 8-byte columns, box (run/8, P) at column head_off/8.  HND: 3D map ordered (D, token rows, heads)
+// with strides (pitch, D*E), box (D*E/8, P, H_local) -> shared memory [H_local][P][D].
+tsb_status make_segment_map(const tsb::IngestGeom& g, const void* base, int64_t rows, CUtensorMap* m,
+                            tsb::TmaSrc* ts, int64_t layers, int64_t C) {
+  const EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(TSB_UNSUPPORTED, "ingest bulk: cuTensorMapEncodeTiled is unavailable");
+  if (g.run % 16 || g.head_bytes % 16 || g.row % 16 || g.run / 8 > 256 || g.head_bytes / 8 > 256 || g.P > 256 ||
+      g.run / g.head_bytes > 256 || rows >= (int64_t{1} << 31))
+    return fail(TSB_UNSUPPORTED, "ingest bulk: page segment exceeds one TMA box (rows <= 2 KiB, < 2^31 rows)");
+  ts->layers = layers;
+  ts->C = C;
+  ts->x0 = static_cast<int32_t>(g.head_off / 8);
+  ts->head0 = static_cast<int32_t>(g.head_off / g.head_bytes);
+  CUresult r;
+  if (g.hnd) {
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.head_bytes / 8), static_cast<cuuint64_t>(rows),
+                                static_cast<cuuint64_t>(g.row / g.head_bytes)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.row), static_cast<cuuint64_t>(g.head_bytes)};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(g.head_bytes / 8), static_cast<cuuint32_t>(g.P),
+                               static_cast<cuuint32_t>(g.run / g.head_bytes)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.row / 8), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.row)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(g.run / 8), static_cast<cuuint32_t>(g.P)};
+    const cuuint32_t es[2] = {1, 1};
+    r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS)
+    return fail(TSB_UNSUPPORTED, "ingest bulk: cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return TSB_OK;
+}
+
+// K2: HBM staging -> pages, with the SM load/store kernel or the tensor-map TMA kernel (K1b).
+tsb_status launch_scatter(const tsb::IngestGeom& g, const uint8_t* src, uint8_t* arena,
+                          const tsb_ingest_item* items, const int32_t* bt, int64_t n, cudaStream_t st,
+                          int device) {
+  if (g_knobs.scatter_impl == 1) {
+    CUtensorMap m;
+    tsb::TmaSrc ts{};
+    TSB_TRY(make_segment_map(g, src, n * g.n_layers * 2 * (g.kv_src / g.row), &m, &ts, g.n_layers,
+                             g.kv_src / g.row));
+    int sms = 148;
+    TSB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    TSB_CUDA_TRY(tsb::launch_ingest_tma(m, g, ts, arena, items, bt, n, sms * tma_ctas_per_sm(g), st));
+    return TSB_OK;
+  }
+  TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st, true));
+  return TSB_OK;
 }
 
 }  // namespace
@@ -749,6 +825,12 @@ tsb_status ensure_staging(tsb_l1* l) {
   l->staging_bytes = g_knobs.staging_bytes;
   TSB_CUDA_TRY(cudaMalloc(&l->staging, l->staging_bytes));
   TSB_CUDA_TRY(cudaStreamCreateWithFlags(&l->ce_stream, cudaStreamNonBlocking));
+  // K2 runs at the greatest priority so that, while a prefill occupies the SMs, the scatter
+  // that drains the staging ring gets the next free SM slots and the copy engines never stall.
+  int lo_prio = 0, hi_prio = 0;
+  TSB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  TSB_CUDA_TRY(cudaStreamCreateWithPriority(&l->k2_stream, cudaStreamNonBlocking, hi_prio));
+  TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_k2_done, cudaEventDisableTiming));
   TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_fence, cudaEventDisableTiming));
   for (int b = 0; b < 2; ++b) {
     TSB_CUDA_TRY(cudaEventCreateWithFlags(&l->ev_ce[b], cudaEventDisableTiming));
@@ -858,6 +940,8 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
   // Host reads are ordered after the work already queued on `st` (stream semantics).
   TSB_CUDA_TRY(cudaEventRecord(l->ev_fence, st));
   TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_fence, 0));
+  TSB_CUDA_TRY(cudaStreamWaitEvent(l->k2_stream, l->ev_fence, 0));
+  cudaStream_t ks = l->k2_stream;
   int64_t layer = lo;
   while (layer < hi) {
     int64_t span_end = hi;  // exclusive end of the layers before (and including) the next fence
@@ -878,14 +962,17 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
       if (l->k2_used[b]) TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_k2[b], 0));
       TSB_TRY(ce_copy_layers(l, pool, items_host + i0, n, layer, nl, stage));
       TSB_CUDA_TRY(cudaEventRecord(l->ev_ce[b], l->ce_stream));
-      TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_ce[b], 0));
-      TSB_CUDA_TRY(launch_scatter(g, stage, l->arena, items_dev + i0, l->bt_dev, n, st));
-      TSB_CUDA_TRY(cudaEventRecord(l->ev_k2[b], st));
+      TSB_CUDA_TRY(cudaStreamWaitEvent(ks, l->ev_ce[b], 0));
+      TSB_TRY(launch_scatter(g, stage, l->arena, items_dev + i0, l->bt_dev, n, ks, l->device));
+      TSB_CUDA_TRY(cudaEventRecord(l->ev_k2[b], ks));
       l->k2_used[b] = true;
     }
     layer += nl;
-    if (layer_events && layer_events[layer - 1 - lo]) TSB_TRY(record_fence(l, layer_events[layer - 1 - lo], st));
+    if (layer_events && layer_events[layer - 1 - lo]) TSB_TRY(record_fence(l, layer_events[layer - 1 - lo], ks));
   }
+  // The caller's stream resumes after the last scatter (stream semantics for what follows).
+  TSB_CUDA_TRY(cudaEventRecord(l->ev_k2_done, ks));
+  TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_k2_done, 0));
   return TSB_OK;
 }
 
@@ -911,13 +998,17 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
     } else {
       if (g.seg_bytes * 2 > tsb::kBulkSmem)
         return fail(TSB_UNSUPPORTED, "ingest bulk: page segment too large for the smem ring");
-      if (g.hnd)
-        return fail(TSB_UNSUPPORTED, "ingest bulk: HND pages need a per-head transpose; use zerocopy or ce");
-      // The K1b ring fills an SM's shared memory: one resident CTA per SM.
+      // K1b: one tensor-map TMA load per page segment, NHD or HND (the map does the transpose).
+      // From a host pool the link saturates with a small grid; from HBM / NVLink, every SM runs
+      // as many rings as its shared memory holds.
+      CUtensorMap m;
+      tsb::TmaSrc ts{};
+      const int64_t C = l->shape.chunk_tokens;
+      TSB_TRY(make_segment_map(g, pool->dev, pool->slots * l->shape.layers * 2 * C, &m, &ts, l->shape.layers, C));
       int sms = 148;
       if (on_device) TSB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, l->device));
-      TSB_CUDA_TRY(tsb::launch_ingest_bulk(g, pool->dev, l->arena, items_dev, l->bt_dev, n_items,
-                                           on_device ? sms : g_knobs.bulk_ctas, st));
+      TSB_CUDA_TRY(tsb::launch_ingest_tma(m, g, ts, l->arena, items_dev, l->bt_dev, n_items,
+                                          on_device ? sms * tma_ctas_per_sm(g) : g_knobs.bulk_ctas, st));
     }
     if (layer_events && layer_events[l1 - 1 - lo]) TSB_TRY(record_fence(l, layer_events[l1 - 1 - lo], st));
     l0 = l1;
@@ -1068,8 +1159,8 @@ tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_i
   tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
   g.staged = 1;  // item i's layers [lo, hi) at staging + i * (hi - lo) * layer bytes
   g.item_stride = (layer_hi - layer_lo) * g.layer_src;
-  TSB_CUDA_TRY(launch_scatter(g, static_cast<const uint8_t*>(staging), l->arena, items_dev,
-                              l->bt_dev, n_items, static_cast<cudaStream_t>(stream)));
+  TSB_TRY(launch_scatter(g, static_cast<const uint8_t*>(staging), l->arena, items_dev, l->bt_dev, n_items,
+                         static_cast<cudaStream_t>(stream), l->device));
   return TSB_OK;
 }
 
@@ -1080,8 +1171,8 @@ tsb_status tsb_scatter_device_packed(tsb_l1* l, const void* staging,
   if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
     return fail(TSB_VALIDATION, "scatter: layer range must satisfy 0 <= lo < hi <= layers");
   const tsb::IngestGeom g = make_staged_geom(l, layer_lo, layer_hi - layer_lo);
-  TSB_CUDA_TRY(launch_scatter(g, static_cast<const uint8_t*>(staging), l->arena, items_dev,
-                              l->bt_dev, n_items, static_cast<cudaStream_t>(stream)));
+  TSB_TRY(launch_scatter(g, static_cast<const uint8_t*>(staging), l->arena, items_dev, l->bt_dev, n_items,
+                         static_cast<cudaStream_t>(stream), l->device));
   return TSB_OK;
 }
 

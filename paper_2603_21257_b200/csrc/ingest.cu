@@ -8,6 +8,10 @@
 // of the layer's [2][num_pages][P][H_local][D] arena.  Segments are numbered so consecutive
 // ids read consecutive source bytes (layer-major inside a chunk), which keeps host reads
 // sequential.  No tensor cores: a pure gather/scatter bounded by the host link (K1) or HBM (K2).
+#include <cuda.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -92,59 +96,73 @@ __global__ void __launch_bounds__(256) k_ingest_ldg(IngestGeom g, const uint8_t*
   }
 }
 
-// K1b: the TMA/bulk-copy engine does the moving.  One warp per CTA; a ring of kStages
-// segment buffers in shared memory.  Lane 0 (or lanes 0..P-1 for head-sharded runs) issues
-// cp.async.bulk host->smem completing on the stage mbarrier, then one cp.async.bulk
-// smem->HBM per segment.  Almost no SM issue bandwidth is used, so prefill keeps the SMs.
-template <int kStages>
-__global__ void __launch_bounds__(32) k_ingest_bulk(IngestGeom g, const uint8_t* __restrict__ src,
-                                                    uint8_t* __restrict__ arena,
-                                                    const tsb_ingest_item* __restrict__ items,
-                                                    const int32_t* __restrict__ bt,
-                                                    int64_t nseg) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t full[kStages];
-  const int lane = threadIdx.x;
-  const bool contig = g.run == g.row;
+// K1b: the TMA engine does the moving, from a tensor map.  The source is a 2D (NHD pages) or 3D
+// (HND pages) tensor map over the pool -- or over the CE staging ring -- whose box is exactly one
+// page segment: P token rows x this rank's run for NHD, or [H_local][P][D] for HND, where the map's
+// dimension order (D, token rows, heads) makes the TMA unit perform the per-head transpose on the
+// way into shared memory.  So one UTMALDG brings a whole (layer, K|V, page) segment, at any head
+// shard (TP8: one 4 KiB box instead of 16 row copies), and one cp.async.bulk stores it to the page.
+// One warp per CTA, lane 0 issues; a ring of `stages` segment buffers completes on mbarriers.
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* m, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* m, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool kHnd>
+__global__ void __launch_bounds__(32) k_ingest_tma(const __grid_constant__ CUtensorMap src_map, IngestGeom g,
+                                                   TmaSrc ts, uint8_t* __restrict__ arena,
+                                                   const tsb_ingest_item* __restrict__ items,
+                                                   const int32_t* __restrict__ bt, int64_t nseg, int stages) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[kTmaMaxStages];
   const uint32_t seg = static_cast<uint32_t>(g.seg_bytes);
-  if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-  }
-  __syncwarp();
-
-  auto issue = [&](int64_t s, int stage) {
-    const SegAddr a = seg_addr(g, src, arena, items, bt, s);
-    uint8_t* buf = smem + static_cast<int64_t>(stage) * seg;
-    if (lane == 0) mbar_arrive_expect_tx(&full[stage], seg);
-    __syncwarp();
-    if (contig) {
-      if (lane == 0) bulk_g2s(buf, a.src, seg, &full[stage]);
-    } else {
-      for (int t = lane; t < g.P; t += 32)
-        bulk_g2s(buf + t * g.run, a.src + t * g.row, static_cast<uint32_t>(g.run), &full[stage]);
-    }
+  if (threadIdx.x != 0) return;  // one thread drives the TMA unit
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&src_map)) : "memory");
+  for (int st = 0; st < stages; ++st) mbar_init(&full[st], 1);
+  mbar_fence_init();
+  const int64_t spi = static_cast<int64_t>(g.n_layers) * 2 * g.ppc;
+  // token-row coordinate of segment s in the source map: rows are [slot][L][2][C] (pool) or
+  // [item][n_layers][2][C] (staging ring)
+  auto row_of = [&](int64_t s) -> int {
+    const int64_t i = s / spi, r = s - i * spi;
+    const int64_t l = r / (2 * g.ppc), kv = (r / g.ppc) & 1, j = r % g.ppc;
+    const int64_t outer = g.staged ? i * g.n_layers + l : items[i].src_slot * ts.layers + g.layer_lo + l;
+    return static_cast<int>((outer * 2 + kv) * ts.C + j * g.P);
   };
-
+  auto issue = [&](int64_t s, int st) {
+    uint8_t* buf = smem + static_cast<int64_t>(st) * seg;
+    mbar_arrive_expect_tx(&full[st], seg);
+    if (kHnd)
+      tma_load_3d(buf, &src_map, 0, row_of(s), ts.head0, &full[st]);
+    else
+      tma_load_2d(buf, &src_map, ts.x0, row_of(s), &full[st]);
+  };
   int64_t next = blockIdx.x;
-  for (int st = 0; st < kStages && next < nseg; ++st, next += gridDim.x) issue(next, st);
+  for (int st = 0; st < stages && next < nseg; ++st, next += gridDim.x) issue(next, st);
   int k = 0;
   for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x, ++k) {
-    const int stage = k % kStages;
-    mbar_wait(&full[stage], (k / kStages) & 1);
-    if (lane == 0) {
-      const SegAddr a = seg_addr(g, src, arena, items, bt, s);
-      if (a.ok) bulk_s2g(a.dst, smem + static_cast<int64_t>(stage) * seg, seg);
-      bulk_commit();
-    }
+    const int st = k % stages;
+    mbar_wait(&full[st], (k / stages) & 1);
+    const SegAddr a = seg_addr(g, nullptr, arena, items, bt, s);
+    if (a.ok) bulk_s2g(a.dst, smem + static_cast<int64_t>(st) * seg, seg);
+    bulk_commit();
     if (next < nseg) {
-      if (lane == 0) bulk_wait_read0();  // the stage's smem has been read by the store
-      __syncwarp();
-      issue(next, stage);
+      bulk_wait_read0();  // the stage's smem has been read by its store
+      issue(next, st);
       next += gridDim.x;
     }
   }
-  if (lane == 0) bulk_wait0();
+  bulk_wait0();
 }
 
 __global__ void k_fill_synth(uint64_t* __restrict__ dst, uint64_t first_word, uint64_t n_words,
@@ -202,27 +220,25 @@ cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_ingest_bulk(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
-                               const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
-                               int grid, cudaStream_t st) {
+cudaError_t launch_ingest_tma(const CUtensorMap& src_map, const IngestGeom& g, const TmaSrc& ts, uint8_t* arena,
+                              const tsb_ingest_item* items, const int32_t* bt, int64_t n_items, int grid,
+                              cudaStream_t st) {
   const int64_t nseg = n_items * g.n_layers * 2 * g.ppc;
   if (nseg == 0) return cudaSuccess;
-  // ring depth: as many stages of one segment as fit in kBulkSmem (6 for 32 KiB segments)
   static std::atomic<uint64_t> attr_set{0};
   if (first_on_device(attr_set)) {
-    cudaError_t e = cudaFuncSetAttribute(k_ingest_bulk<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_ingest_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_ingest_bulk<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_ingest_bulk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+      e = cudaFuncSetAttribute(k_ingest_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
     if (e != cudaSuccess) return e;
   }
-  if (g.seg_bytes * 6 <= kBulkSmem)
-    k_ingest_bulk<6><<<grid, 32, 6 * g.seg_bytes, st>>>(g, src, arena, items, bt, nseg);
-  else if (g.seg_bytes * 3 <= kBulkSmem)
-    k_ingest_bulk<3><<<grid, 32, 3 * g.seg_bytes, st>>>(g, src, arena, items, bt, nseg);
+  // ring depth: as many segment buffers as fit (6 for 32 KiB segments, 16 for TP8's 4 KiB)
+  const int stages = static_cast<int>(std::min<int64_t>(kTmaMaxStages, kBulkSmem / g.seg_bytes));
+  const size_t smem = static_cast<size_t>(stages) * g.seg_bytes;
+  if (g.hnd)
+    k_ingest_tma<true><<<grid, 32, smem, st>>>(src_map, g, ts, arena, items, bt, nseg, stages);
   else
-    k_ingest_bulk<2><<<grid, 32, 2 * g.seg_bytes, st>>>(g, src, arena, items, bt, nseg);
+    k_ingest_tma<false><<<grid, 32, smem, st>>>(src_map, g, ts, arena, items, bt, nseg, stages);
   count_launch();
   return cudaGetLastError();
 }

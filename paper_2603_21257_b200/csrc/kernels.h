@@ -1,6 +1,7 @@
 // kernels.h — launch interface of the sm_100a kernels (internal to libtsb.so).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,11 +42,20 @@ struct IngestGeom {
 cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
                               const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
                               int grid, cudaStream_t st, bool hbm_source);
-// Shared memory of the K1b ring (bytes); a segment must fit twice (<= 100 KiB).
+// K1b: one tensor-map TMA load per page segment (ingest.cu).  TmaSrc carries what the map's
+// coordinates need beyond IngestGeom: the pool's layer count and chunk tokens (rows are
+// [slot][L][2][C]) and this rank's first head (HND maps) or first u64 column (NHD maps).
 constexpr int kBulkSmem = 200 * 1024;
-cudaError_t launch_ingest_bulk(const IngestGeom& g, const uint8_t* src, uint8_t* arena,
-                               const tsb_ingest_item* items, const int32_t* bt, int64_t n_items,
-                               int grid, cudaStream_t st);
+constexpr int kTmaMaxStages = 16;
+struct TmaSrc {
+  int64_t layers;  // L of the source chunks (slot mode)
+  int64_t C;       // chunk tokens
+  int32_t x0;      // NHD map: first 8-byte column of this rank's run in a token row
+  int32_t head0;   // HND map: first head of this rank
+};
+cudaError_t launch_ingest_tma(const CUtensorMap& src_map, const IngestGeom& g, const TmaSrc& ts, uint8_t* arena,
+                              const tsb_ingest_item* items, const int32_t* bt, int64_t n_items, int grid,
+                              cudaStream_t st);
 cudaError_t launch_fill_synth(uint64_t* dst, uint64_t first_word, uint64_t n_words, uint64_t seed,
                               cudaStream_t st);
 // Harness page check (verify.cu): the canonical shape and layout only, no IngestGeom.

@@ -137,6 +137,7 @@ struct tsb_stage {
   int device = 0;
   tsb_scorer* scorer = nullptr;
   cudaStream_t compute = nullptr;
+  bool own_compute = true;  // false: the caller's stream (tsb_stage_set_compute_stream)
   std::vector<cudaEvent_t> timing_pool;  // 3 per request, grown on demand
   std::vector<cudaEvent_t> layer_ev;     // per-layer fences (reused across requests)
   std::vector<cudaEvent_t> call_pool;    // per ingest call (online PcieDone / trace), grown on demand
@@ -241,6 +242,22 @@ tsb_status tsb_stage_set_prefill_hook(tsb_stage* s, tsb_prefill_hook hook, void*
 
 void* tsb_stage_compute_stream(tsb_stage* s) { return s->compute; }
 
+tsb_status tsb_stage_set_compute_stream(tsb_stage* s, void* stream) {
+  tsb::DeviceGuard dg(s->device);
+  TSB_CUDA_TRY(cudaStreamSynchronize(s->compute));
+  if (s->own_compute) TSB_CUDA_TRY(cudaStreamDestroy(s->compute));
+  if (stream) {
+    s->compute = static_cast<cudaStream_t>(stream);
+    s->own_compute = false;
+    return TSB_OK;
+  }
+  int lo = 0, hi = 0;
+  TSB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  TSB_CUDA_TRY(cudaStreamCreateWithPriority(&s->compute, cudaStreamNonBlocking, lo));
+  s->own_compute = true;
+  return TSB_OK;
+}
+
 void tsb_stage_destroy(tsb_stage* s) {
   if (!s) return;
   tsb::DeviceGuard dg(s->device);
@@ -251,7 +268,7 @@ void tsb_stage_destroy(tsb_stage* s) {
   if (s->ev_start) cudaEventDestroy(s->ev_start);
   if (s->compute) {
     cudaStreamSynchronize(s->compute);
-    cudaStreamDestroy(s->compute);
+    if (s->own_compute) cudaStreamDestroy(s->compute);
   }
   tsb_scorer_destroy(s->scorer);
   delete s;

@@ -63,10 +63,17 @@ class LoadStage:
 
         self.hook_error = None
         self._hook = capi.PREFILL_HOOK(tramp)  # kept alive with the stage
+        # Prefill runs on a torch-owned lowest-priority stream: torch tensors the consumer touches
+        # there (pinned staging included) may outlive the stage without referencing a dead stream.
+        if getattr(self, "_compute", None) is None:
+            self._compute = torch.cuda.Stream(device=torch.device("cuda", self.l1.device), priority=0)
+            check(lib.tsb_stage_set_compute_stream(self._h, self._compute.cuda_stream))
         check(lib.tsb_stage_set_prefill_hook(self._h, self._hook, None))
 
     @property
-    def compute_stream(self) -> torch.cuda.ExternalStream:
+    def compute_stream(self):
+        if getattr(self, "_compute", None) is not None:
+            return self._compute
         return torch.cuda.ExternalStream(lib.tsb_stage_compute_stream(self._h), device=torch.device("cuda", self.l1.device))
 
     def close(self):

@@ -44,7 +44,7 @@ def test_fit_of_csv_samples_equals_reference(tmp_path, ref_lib):
 
 def test_calibration_from_stage_requests(tmp_path):
     """The request rows a stage run returns -> CSVs -> fitted models (no device: synthetic rows)."""
-    dt = np.dtype([("chunks", np.int64), ("cached_tokens", np.int64), ("compute_tokens", np.int64),
+    dt = np.dtype([("pick_position", np.int32), ("chunks", np.int64), ("cached_tokens", np.int64), ("compute_tokens", np.int64),
                    ("ingest_begin_ms", np.float64), ("resident_ms", np.float64), ("done_ms", np.float64)])
     n = 40
     rows = np.zeros(n, dt)
@@ -54,7 +54,13 @@ def test_calibration_from_stage_requests(tmp_path):
     rows["compute_tokens"] = rng.integers(30, 4000, n)
     rows["ingest_begin_ms"] = np.arange(n) * 100.0
     rows["resident_ms"] = rows["ingest_begin_ms"] + (2.4e-6 * rows["cached_tokens"] + 5e-4) * 1e3
-    rows["done_ms"] = rows["resident_ms"] + (1e-5 * rows["compute_tokens"] + 2e-3) * 1e3
+    rows["pick_position"] = np.arange(n)
+    # prefills queue on one compute stream: request k starts at max(resident_k, done_{k-1})
+    prev = 0.0
+    for k in range(n):
+        start = max(rows["resident_ms"][k], prev)
+        rows["done_ms"][k] = start + (1e-5 * rows["compute_tokens"][k] + 2e-3) * 1e3
+        prev = rows["done_ms"][k]
 
     class R:
         requests = rows

@@ -525,16 +525,47 @@ def test_ingest_layouts_bit_exact(oracle, layout, mode, tp):
     rows = [l1.request(5, c, shape.page_bytes * 16)[1] for c in range(7)]
     l1.sync_block_table()
     items = ingest.items_numpy([3, 4, 5, 6, 0, 1, 7], rows, range(7))
-    if mode == "bulk" and lay == ingest.LAYOUT_FLASHINFER_HND:
-        with pytest.raises(t.Unsupported):
-            ingest.ingest(l1, pool, items, mode=ingest.BULK)
-        return
     ingest.ingest(l1, pool, items, mode=ingest.MODES[mode])
     torch.cuda.synchronize()
     want = oracle.scatter_ref(shape, pool.slot_view(0, 8), items, l1.block_table(), num_pages, layout=lay)
     assert np.array_equal(arena.cpu().numpy(), want)
     assert ingest.verify_synthetic(l1, pool, items, seed=17) == 0
     assert tuple(l1.layer(0).shape)[:2] == (num_pages, 2)
+
+
+@pytest.mark.parametrize("layout", ["flash_attn", "flashinfer_nhd", "flashinfer_hnd"])
+@pytest.mark.parametrize("tp", [(1, 0), (2, 1), (8, 6)])
+@pytest.mark.parametrize("source", ["host", "device"])
+def test_k1b_tensor_map_tma_bit_exact(oracle, layout, tp, source):
+    """K1b: one tensor-map TMA load per page segment (2D map for NHD, 3D (D, rows, heads) map for HND
+    pages -- the TMA unit does the per-head transpose), from a host or an HBM pool, and as K2 from
+    the CE staging ring (tsb_ingest_set_scatter(1)): bit-exact against scatter_ref."""
+    lay = ingest.LAYOUTS[layout]
+    shape = SMALL.with_rank(*tp)
+    pool = ingest.ChunkPool(SMALL, 8) if source == "host" else ingest.ChunkPool.create_device(SMALL, 8)
+    pool.fill_synthetic(23)
+    host = ingest.ChunkPool(SMALL, 8)
+    host.fill_synthetic(23)
+    num_pages = 200
+    arena = torch.zeros(shape.layers * 2 * num_pages * 16 * shape.heads_local * 128 * 2, dtype=torch.uint8,
+                        device="cuda")
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=2, max_chunks=12, arena=arena, layout=lay)
+    rows = [l1.request(5, c, shape.page_bytes * 16)[1] for c in range(7)]
+    l1.sync_block_table()
+    items = ingest.items_numpy([3, 4, 5, 6, 0, 1, 7], rows, range(7))
+    want = oracle.scatter_ref(shape, host.slot_view(0, 8), items, l1.block_table(), num_pages, layout=lay)
+    ingest.ingest(l1, pool, items, mode=ingest.BULK)
+    torch.cuda.synchronize()
+    assert np.array_equal(arena.cpu().numpy(), want)
+    if source == "host":  # K2 on the TMA kernel, over the packed CE staging ring
+        arena.zero_()
+        t.check(_capi.lib.tsb_ingest_set_scatter(1, 0))
+        try:
+            ingest.ingest(l1, pool, items, mode=ingest.CE)
+            torch.cuda.synchronize()
+        finally:
+            t.check(_capi.lib.tsb_ingest_set_scatter(0, 0))
+        assert np.array_equal(arena.cpu().numpy(), want)
 
 
 def test_layout_fixed_once_reserved():

@@ -32,7 +32,7 @@ def _case(seed):
                           dtype_bytes=int(rng.choice([1, 2])), chunk_tokens=chunk, page_tokens=page)
     shape = full.with_rank(tp, int(rng.integers(tp)))
     layout = int(rng.integers(3))
-    modes = ["auto", "ce", "zerocopy"] + ([] if layout == ingest.LAYOUT_FLASHINFER_HND else ["bulk"])
+    modes = ["auto", "ce", "zerocopy", "bulk"]
     return rng, full, shape, layout, str(rng.choice(modes)), int(rng.integers(5))
 
 

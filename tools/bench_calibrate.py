@@ -76,7 +76,12 @@ def main():
     stage.run(q, slots, base, prefill=True, verify_seed=3)
     cal_runs = [stage.run(q, slots, base, prefill=True) for _ in range(2)]
     cal = calibrate.calibrate(cal_runs, base, args.out, fit_compute=True)
-    link = float(np.mean([r.stats["bytes"] / (r.requests["resident_ms"].max() * 1e-3) for r in cal_runs]))
+    if consumer is not None:
+        stage.set_prefill_hook(None)
+    alone = stage.run(q, slots, base)  # ingest only: the link rate without prefill interference
+    if consumer is not None:
+        stage.set_prefill_hook(consumer)
+    link = alone.stats["bytes"] / (alone.requests["resident_ms"].max() * 1e-3)
     box = t.ClusterConfig(bytes_per_token=bpt, l1_capacity=10**13, l2_capacity=10**13, network_bandwidth=1e15,
                           transfer_base_latency=0.0, pcie_bandwidth=bpt / cal.models.load.slope,
                           compute_per_token=cal.models.comp.slope, compute_base=cal.models.comp.intercept)

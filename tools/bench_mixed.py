@@ -40,52 +40,40 @@ def mixed_batch(n, seed, block=256):
 
 
 def timeline_summary(prof, path):
-    """Per-stream busy time of the copy engines (H2D memcpy), the ingest kernels and the prefill
-    kernels from a kineto (CUPTI) trace, and the time both the link and the prefill were busy."""
+    """From a kineto (CUPTI) trace of one overlapped run: busy time of the ingest kernels (K2; the
+    batched host->device copies are not reported as memcpy activity by CUPTI), of the prefill
+    kernels, the ingest window [first K2 start, last K2 end], and how much prefill ran inside it."""
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
-    spans = {"h2d": [], "ingest": [], "prefill": []}
+    spans = {"ingest": [], "prefill": [], "memcpy": []}
     for e in ev:
-        name = e.name
         t0, t1 = e.time_range.start, e.time_range.end
-        if "Memcpy" in name or "memcpy" in name:
-            if "HtoD" in name or "H2D" in name or "Host to Device" in name:
-                spans["h2d"].append((t0, t1))
-        elif name.startswith("void tsb::") or "k_ingest" in name or "k_score" in name:
+        if "emcpy" in e.name:
+            spans["memcpy"].append((t0, t1))
+        elif "tsb::" in e.name:
             spans["ingest"].append((t0, t1))
         else:
             spans["prefill"].append((t0, t1))
 
     def union(iv):
-        iv = sorted(iv)
         out = []
-        for a, b in iv:
+        for a, b in sorted(iv):
             if out and a <= out[-1][1]:
                 out[-1] = (out[-1][0], max(out[-1][1], b))
             else:
                 out.append((a, b))
         return out
 
-    def inter(a, b):
-        i = j = 0
-        tot = 0.0
-        while i < len(a) and j < len(b):
-            lo, hi = max(a[i][0], b[j][0]), min(a[i][1], b[j][1])
-            tot += max(0.0, hi - lo)
-            if a[i][1] < b[j][1]:
-                i += 1
-            else:
-                j += 1
-        return tot
-
     u = {k: union(v) for k, v in spans.items()}
     busy = {k: sum(b - a for a, b in v) / 1e3 for k, v in u.items()}
+    w0 = min(a for a, _ in u["ingest"]) if u["ingest"] else 0
+    w1 = max(b for _, b in u["ingest"]) if u["ingest"] else 0
+    inside = sum(max(0, min(b, w1) - max(a, w0)) for a, b in u["prefill"]) / 1e3
     allt = [t for v in u.values() for iv in v for t in iv]
     res = {"source": "torch.profiler (kineto/CUPTI) CUDA activity of one overlapped run (nsys is not in the image)",
-           "window_ms": (max(allt) - min(allt)) / 1e3 if allt else 0.0,
-           "busy_ms": busy, "h2d_and_prefill_concurrent_ms": inter(u["h2d"], u["prefill"]) / 1e3,
+           "run_window_ms": (max(allt) - min(allt)) / 1e3 if allt else 0.0, "busy_ms": busy,
+           "ingest_window_ms": (w1 - w0) / 1e3, "prefill_busy_inside_ingest_window_ms": inside,
+           "prefill_share_of_ingest_window": inside / ((w1 - w0) / 1e3) if w1 > w0 else 0.0,
            "launches": {k: len(v) for k, v in spans.items()}}
-    res["prefill_hidden_under_link_frac"] = (res["h2d_and_prefill_concurrent_ms"] / busy["prefill"]
-                                             if busy["prefill"] else 0.0)
     Path(path).write_text(json.dumps(res, indent=1))
     prof.export_chrome_trace(str(Path(path).with_suffix(".trace.json")))
     return res

@@ -26,11 +26,11 @@ def hbm_peak():
     return measured_peaks()[0]
 
 
-def run(shape, n_chunks, mode, reps, seed=3):
+def run(shape, n_chunks, mode, reps, seed=3, layout=0):
     pool = ingest.ChunkPool.create_device(shape, n_chunks)
     pool.fill_synthetic(seed)
     ppc = shape.pages_per_chunk
-    l1 = ingest.PagedKVCache(shape, n_chunks * ppc, max_rows=1, max_chunks=n_chunks)
+    l1 = ingest.PagedKVCache(shape, n_chunks * ppc, max_rows=1, max_chunks=n_chunks, layout=layout)
     for c in range(n_chunks):
         assert l1.request(1, c, shape.page_bytes * ppc)[0]
     l1.sync_block_table()
@@ -63,13 +63,15 @@ def main():
     cases = [("llama8b32k", ingest.LLAMA31_8B, 128, (1, 0)),
              ("qwen32b_64chunks", ingest.QWEN25_32B, 64, (1, 0)),
              ("llama70b32k_tp8", ingest.LLAMA3_70B, 128, (8, 0)),
+             ("llama70b32k_tp4", ingest.LLAMA3_70B, 128, (4, 1)),
              ("llama70b32k_tp2", ingest.LLAMA3_70B, 128, (2, 0))]
     for name, shape, n, tp in cases:
         shape = shape.with_rank(*tp)
-        for mname in ("zerocopy", "bulk"):
-            payload, secs, bad = run(shape, n, ingest.MODES[mname], args.reps)
+        for layout in ("flash_attn", "flashinfer_hnd"):
+          for mname in ("zerocopy", "bulk"):
+            payload, secs, bad = run(shape, n, ingest.MODES[mname], args.reps, layout=ingest.LAYOUTS[layout])
             gbs = payload / secs / 1e9
-            print(json.dumps(dict(workload=name, source="device_pool_local_hbm", mode=mname, tp=tp[0],
+            print(json.dumps(dict(workload=name, source="device_pool_local_hbm", mode=mname, tp=tp[0], layout=layout,
                                   payload_bytes=payload, ms=secs * 1e3, payload_GBps=round(gbs, 1),
                                   hbm_GBps=round(2 * gbs, 1), hbm_peak_GBps=peak,
                                   frac=round(2 * gbs / peak, 4), verify_mismatches=int(bad))), flush=True)
