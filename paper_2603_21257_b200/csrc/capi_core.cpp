@@ -363,7 +363,7 @@ tsb_status tsb_scorer_create(int device, int64_t capacity, tsb_scorer** out) {
 
 void tsb_scorer_destroy(tsb_scorer* s) {
   if (!s) return;
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   scorer_free(s);
   delete s;
 }
@@ -374,7 +374,7 @@ tsb_status tsb_score_queue_device(tsb_scorer* s, void* stream, int64_t n, const 
                                   int64_t* order, int64_t* err_index) {
   if (policy < TSB_FIFO || policy > TSB_LSTF) return fail(TSB_VALIDATION, "unknown policy");
   if (n < 0) return fail(TSB_VALIDATION, "score_queue: n must be >= 0");
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   if (c->block_size_tokens < 1)
     return fail(TSB_VALIDATION, "cluster: block_size_tokens must be >= 1");
   TSB_TRY(scorer_reserve(s, n));
@@ -394,7 +394,7 @@ tsb_status tsb_score_queue_device(tsb_scorer* s, void* stream, int64_t n, const 
 }
 
 tsb_status tsb_scorer_check(tsb_scorer* s, void* stream, int64_t* err_index) {
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   return scorer_check_errors(s, static_cast<cudaStream_t>(stream), err_index);
 }
 
@@ -403,7 +403,7 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
                            double* t_load, double* t_comp, double* primary, int64_t* order) {
   auto st = static_cast<cudaStream_t>(stream);
   if (n == 0) return TSB_OK;
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   // Pack the SoA queue into one device block: 7 x 8-byte arrays + flags.
   const size_t w = sizeof(int64_t) * static_cast<size_t>(n);
   if (n > s->host_cap) {  // grow-only buffers: no allocation (and no implicit sync) per call

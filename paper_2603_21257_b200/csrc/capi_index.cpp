@@ -95,7 +95,7 @@ tsb_status tsb_index_create(int device, int64_t capacity, tsb_index** out) {
 
 void tsb_index_destroy(tsb_index* x) {
   if (!x) return;
-  tsb::DeviceGuard dg(x->device);
+  tsb::DeviceGuard dg(x ? x->device : -1);
   free_index_arrays(x);
   cudaFree(x->pos);
   cudaFree(x->stats);
@@ -103,7 +103,7 @@ void tsb_index_destroy(tsb_index* x) {
 }
 
 tsb_status tsb_index_clear(tsb_index* x, void* stream) {
-  tsb::DeviceGuard dg(x->device);
+  tsb::DeviceGuard dg(x ? x->device : -1);
   auto st = static_cast<cudaStream_t>(stream);
   const size_t cap = x->mask + 1;
   TSB_CUDA_TRY(cudaMemsetAsync(x->keys, 0xff, sizeof(uint64_t) * cap, st));
@@ -113,7 +113,7 @@ tsb_status tsb_index_clear(tsb_index* x, void* stream) {
 }
 
 tsb_status tsb_index_compact(tsb_index* x, void* stream, int64_t* tombstones_reclaimed) {
-  tsb::DeviceGuard dg(x->device);
+  tsb::DeviceGuard dg(x ? x->device : -1);
   auto st = static_cast<cudaStream_t>(stream);
   unsigned long long h[3] = {0, 0, 0};
   TSB_CUDA_TRY(cudaMemcpyAsync(h, x->stats, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -145,7 +145,7 @@ tsb_status tsb_index_insert_device(tsb_index* x, void* stream, int64_t n, const 
                                    const int64_t* slots) {
   if (n <= 0) return TSB_OK;
   if (n >= (1ll << 40)) return fail(TSB_VALIDATION, "index: batch too large");
-  tsb::DeviceGuard dg(x->device);
+  tsb::DeviceGuard dg(x ? x->device : -1);
   auto st = static_cast<cudaStream_t>(stream);
   if (n > x->pos_cap) {  // grow-only scratch; the previous batch may still be using it
     TSB_CUDA_TRY(cudaStreamSynchronize(st));

@@ -509,7 +509,7 @@ tsb_status tsb_l1_create(int device, const tsb_kv_shape* shape, int64_t num_page
 
 void tsb_l1_destroy(tsb_l1* l) {
   if (!l) return;
-  tsb::DeviceGuard dg(l->device);
+  tsb::DeviceGuard dg(l ? l->device : -1);
   l1_free(l);
   delete l;
 }
@@ -622,7 +622,7 @@ const int32_t* tsb_l1_block_table_device(const tsb_l1* l) { return l->bt_dev; }
 int64_t tsb_l1_block_table_stride(const tsb_l1* l) { return l->stride; }
 
 tsb_status tsb_l1_sync_block_table(tsb_l1* l, void* stream) {
-  tsb::DeviceGuard dg(l->device);
+  tsb::DeviceGuard dg(l ? l->device : -1);
   auto st = static_cast<cudaStream_t>(stream);
   int64_t r = 0;
   while (r < l->rows) {
@@ -1047,7 +1047,7 @@ extern "C" {
 tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
                       int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
                       void* const* layer_events) {
-  tsb::DeviceGuard dg(l->device);
+  tsb::DeviceGuard dg(l ? l->device : -1);
   auto st = static_cast<cudaStream_t>(stream);
   const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb_ingest_item));
   if (n_items > per)
@@ -1076,7 +1076,7 @@ tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, i
 tsb_status tsb_ingest_tiered(tsb_l1* l, tsb_pool* pool, tsb_pool* hbm_pool,
                              const tsb_ingest_item* items, int64_t n_items, int64_t layer_lo,
                              int64_t layer_hi, int mode, void* stream, void* const* layer_events) {
-  tsb::DeviceGuard dg(l->device);
+  tsb::DeviceGuard dg(l ? l->device : -1);
   std::vector<tsb_ingest_item> host, tier;
   for (int64_t k = 0; k < n_items; ++k) {
     if (items[k].src_slot >= 0) {
@@ -1129,7 +1129,7 @@ tsb_status tsb_ingest_tiered(tsb_l1* l, tsb_pool* pool, tsb_pool* hbm_pool,
 tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev,
                              int64_t n_items, int64_t layer_lo, int64_t layer_hi, int mode,
                              void* stream, void* const* layer_events) {
-  tsb::DeviceGuard dg(l->device);
+  tsb::DeviceGuard dg(l ? l->device : -1);
   return ingest_impl(l, pool, items_dev, nullptr, n_items, layer_lo, layer_hi, mode,
                      static_cast<cudaStream_t>(stream), layer_events);
 }
@@ -1153,7 +1153,7 @@ tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes) {
 tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_item* items_dev,
                               int64_t n_items, int64_t layer_lo, int64_t layer_hi,
                               void* stream) {
-  tsb::DeviceGuard dg(l->device);
+  tsb::DeviceGuard dg(l ? l->device : -1);
   if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
     return fail(TSB_VALIDATION, "scatter: layer range must satisfy 0 <= lo < hi <= layers");
   tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
@@ -1167,7 +1167,7 @@ tsb_status tsb_scatter_device(tsb_l1* l, const void* staging, const tsb_ingest_i
 tsb_status tsb_scatter_device_packed(tsb_l1* l, const void* staging,
                                      const tsb_ingest_item* items_dev, int64_t n_items,
                                      int64_t layer_lo, int64_t layer_hi, void* stream) {
-  tsb::DeviceGuard dg(l->device);
+  tsb::DeviceGuard dg(l ? l->device : -1);
   if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
     return fail(TSB_VALIDATION, "scatter: layer range must satisfy 0 <= lo < hi <= layers");
   const tsb::IngestGeom g = make_staged_geom(l, layer_lo, layer_hi - layer_lo);
@@ -1180,7 +1180,7 @@ tsb_status tsb_l1_verify_synthetic(tsb_l1* l, const tsb_ingest_item* items, int6
                                    int64_t layer_lo, int64_t layer_hi, uint64_t seed,
                                    int64_t pool_chunk_bytes, void* stream,
                                    uint64_t* mismatches) {
-  tsb::DeviceGuard dg(l->device);
+  tsb::DeviceGuard dg(l ? l->device : -1);
   // Independent of the ingest address math (verify.cu): invert the host block table into
   // page -> (slot, first token), then check every word of those pages from the layout definition.
   auto st = static_cast<cudaStream_t>(stream);

@@ -125,44 +125,70 @@ __global__ void __launch_bounds__(32) k_ingest_tma(const __grid_constant__ CUten
                                                    const int32_t* __restrict__ bt, int64_t nseg, int stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[kTmaMaxStages];
+  // Addresses of this CTA's segments, 64 iterations in a ring: the whole warp resolves 32 of them
+  // at a time (item and block-table loads in parallel), so lane 0's TMA loop never waits on a
+  // dependent global load.
+  __shared__ int32_t row_tab[64];
+  __shared__ uint8_t* dst_tab[64];
+  const int lane = threadIdx.x;
   const uint32_t seg = static_cast<uint32_t>(g.seg_bytes);
-  if (threadIdx.x != 0) return;  // one thread drives the TMA unit
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&src_map)) : "memory");
-  for (int st = 0; st < stages; ++st) mbar_init(&full[st], 1);
-  mbar_fence_init();
+  const int64_t grid = gridDim.x;
   const int64_t spi = static_cast<int64_t>(g.n_layers) * 2 * g.ppc;
-  // token-row coordinate of segment s in the source map: rows are [slot][L][2][C] (pool) or
-  // [item][n_layers][2][C] (staging ring)
-  auto row_of = [&](int64_t s) -> int {
+  auto resolve = [&](int64_t k) {  // iteration k of this CTA -> table slot k % 64
+    const int64_t s = blockIdx.x + k * grid;
+    if (s >= nseg) return;
     const int64_t i = s / spi, r = s - i * spi;
     const int64_t l = r / (2 * g.ppc), kv = (r / g.ppc) & 1, j = r % g.ppc;
+    // token-row coordinate in the source map: rows are [slot][L][2][C] (pool) or
+    // [item][n_layers][2][C] (staging ring)
     const int64_t outer = g.staged ? i * g.n_layers + l : items[i].src_slot * ts.layers + g.layer_lo + l;
-    return static_cast<int>((outer * 2 + kv) * ts.C + j * g.P);
+    row_tab[k & 63] = static_cast<int32_t>((outer * 2 + kv) * ts.C + j * g.P);
+    const SegAddr a = seg_addr(g, nullptr, arena, items, bt, s);
+    dst_tab[k & 63] = a.ok ? a.dst : nullptr;
   };
-  auto issue = [&](int64_t s, int st) {
+  auto issue = [&](int64_t k) {
+    const int st = static_cast<int>(k % stages);
     uint8_t* buf = smem + static_cast<int64_t>(st) * seg;
     mbar_arrive_expect_tx(&full[st], seg);
     if (kHnd)
-      tma_load_3d(buf, &src_map, 0, row_of(s), ts.head0, &full[st]);
+      tma_load_3d(buf, &src_map, 0, row_tab[k & 63], ts.head0, &full[st]);
     else
-      tma_load_2d(buf, &src_map, ts.x0, row_of(s), &full[st]);
+      tma_load_2d(buf, &src_map, ts.x0, row_tab[k & 63], &full[st]);
   };
-  int64_t next = blockIdx.x;
-  for (int st = 0; st < stages && next < nseg; ++st, next += gridDim.x) issue(next, st);
-  int k = 0;
-  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x, ++k) {
-    const int st = k % stages;
-    mbar_wait(&full[st], (k / stages) & 1);
-    const SegAddr a = seg_addr(g, nullptr, arena, items, bt, s);
-    if (a.ok) bulk_s2g(a.dst, smem + static_cast<int64_t>(st) * seg, seg);
-    bulk_commit();
-    if (next < nseg) {
-      bulk_wait_read0();  // the stage's smem has been read by its store
-      issue(next, st);
-      next += gridDim.x;
+  if (lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&src_map)) : "memory");
+    for (int st = 0; st < stages; ++st) mbar_init(&full[st], 1);
+    mbar_fence_init();
+  }
+  resolve(lane);
+  resolve(32 + lane);
+  __syncwarp();
+  if (lane == 0)
+    for (int64_t k = 0; k < stages && blockIdx.x + k * grid < nseg; ++k) issue(k);
+  // Iteration k consumes this CTA's k-th segment from stage k % stages.  A stage is refilled
+  // kLag - 1 iterations after its store was committed (wait_group.read kLag-1), so up to kLag
+  // stores read shared memory while the next loads are already in flight.
+  constexpr int kLag = 3;
+  for (int64_t k = 0; blockIdx.x + k * grid < nseg; ++k) {
+    if ((k & 31) == 0 && k > 0) {  // all of this block's and the next block's entries resolved
+      __syncwarp();
+      resolve(k + 32 + lane);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      const int st = static_cast<int>(k % stages);
+      mbar_wait(&full[st], static_cast<uint32_t>((k / stages) & 1));
+      uint8_t* dst = dst_tab[k & 63];
+      if (dst) bulk_s2g(dst, smem + static_cast<int64_t>(st) * seg, seg);
+      bulk_commit();
+      const int64_t j = k - (kLag - 1);  // its store is now at most kLag-1 groups from the newest
+      if (j >= 0 && blockIdx.x + (j + stages) * grid < nseg) {
+        bulk_wait_read<kLag - 1>();
+        issue(j + stages);
+      }
     }
   }
-  bulk_wait0();
+  if (lane == 0) bulk_wait0();
 }
 
 __global__ void k_fill_synth(uint64_t* __restrict__ dst, uint64_t first_word, uint64_t n_words,

@@ -193,7 +193,7 @@ tsb_status tsb_stage_create(tsb_l1* l1, tsb_pool* pool, tsb_stage** out) {
     return st;
   }
   s->device = tsb_l1_device(l1);
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   int lo = 0, hi = 0;
   cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
   // Prefill gets the LOWEST priority so the ingest scatter kernels interleave ahead of it.
@@ -243,7 +243,7 @@ tsb_status tsb_stage_set_prefill_hook(tsb_stage* s, tsb_prefill_hook hook, void*
 void* tsb_stage_compute_stream(tsb_stage* s) { return s->compute; }
 
 tsb_status tsb_stage_set_compute_stream(tsb_stage* s, void* stream) {
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   TSB_CUDA_TRY(cudaStreamSynchronize(s->compute));
   if (s->own_compute) TSB_CUDA_TRY(cudaStreamDestroy(s->compute));
   if (stream) {
@@ -260,7 +260,7 @@ tsb_status tsb_stage_set_compute_stream(tsb_stage* s, void* stream) {
 
 void tsb_stage_destroy(tsb_stage* s) {
   if (!s) return;
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   delete s->net;
   for (auto e : s->timing_pool) cudaEventDestroy(e);
   for (auto e : s->layer_ev) cudaEventDestroy(e);
@@ -337,7 +337,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
                          const double models[4], const int64_t* slot_offsets,
                          const int64_t* slots, const tsb_stage_options* opt, void* stream,
                          tsb_stage_request* results, tsb_stage_stats* stats) {
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   const double wall0 = now_s();
   const uint64_t launches0 = tsb_kernel_launch_count();
   auto st = static_cast<cudaStream_t>(stream);
@@ -609,7 +609,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
                                 const int64_t* slot_offsets, const int64_t* slots,
                                 const tsb_stage_options* opt, void* stream,
                                 tsb_stage_request* results, tsb_stage_stats* stats) {
-  tsb::DeviceGuard dg(s->device);
+  tsb::DeviceGuard dg(s ? s->device : -1);
   const double wall0 = now_s();
   const uint64_t launches0 = tsb_kernel_launch_count();
   auto st = static_cast<cudaStream_t>(stream);

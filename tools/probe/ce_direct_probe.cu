@@ -64,8 +64,9 @@ int main(int argc, char** argv) {
         // batches of <= 4096 entries per call (a staging-group-sized call)
         for (size_t i0 = 0; i0 < n; i0 += 4096) {
           const size_t k = std::min<size_t>(4096, n - i0);
-          size_t fi = 0;
-          CK(cudaMemcpyBatchAsync(dst.data() + i0, src.data() + i0, sz.data() + i0, k, &attr, &fi, 1, &fi, s));
+          size_t attr_idx = 0, fail_idx = 0;
+          CK(cudaMemcpyBatchAsync(dst.data() + i0, src.data() + i0, sz.data() + i0, k, &attr, &attr_idx, 1, &fail_idx,
+                                  s));
         }
         CK(cudaEventRecord(b, s));
         CK(cudaEventSynchronize(b));
