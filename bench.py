@@ -691,7 +691,8 @@ def run_ours(args):
         stage_host = LoadStage(l1, pool)
         s = torch.cuda.current_stream()
         sub = type(wl.queue)(2, **{k: getattr(wl.queue, k)[:2] for k, _ in type(wl.queue).FIELDS})
-        for name in (("zerocopy", "ce") if args.layout == "flashinfer_hnd" else ("bulk", "zerocopy", "ce")):
+        for name in (("bulk", "zerocopy", "ce") if args.layout == "flashinfer_hnd" or shape.tp_size > 1
+                     else ("bulk", "zerocopy", "ce", "ce_direct")):
             stage_host.run(sub, wl.slots[:2], wl.config, mode=ingest.MODES[name])  # warm
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(s)

@@ -407,15 +407,21 @@ typedef enum {
                               lists whose consecutive-slot runs carry >= 3.1 MB per copy,
                               else ZEROCOPY; device pool or device items: ZEROCOPY */
   TSB_INGEST_ZEROCOPY = 1, /* K1: SM 16B loads from mapped host memory, scatter to pages */
-  TSB_INGEST_BULK = 2,     /* K1b: cp.async.bulk host->smem->pages, one issuing lane/CTA
-                              (not for TSB_LAYOUT_FLASHINFER_HND: UNSUPPORTED) */
-  TSB_INGEST_CE = 3        /* copy engine H2D into an HBM staging ring, then K2 scatter;
+  TSB_INGEST_BULK = 2,     /* K1b: one tensor-map TMA load (UTMALDG) per page segment into a
+                              shared-memory ring, one cp.async.bulk store per segment; NHD via a
+                              2D map, HND via a 3D (D, rows, heads) map that transposes */
+  TSB_INGEST_CE = 3,       /* copy engine H2D into an HBM staging ring, then K2 scatter;
                               host reads run on an internal copy stream ordered after the
                               work queued on `stream` before the call.  Consecutive layers up
                               to the next requested fence share a staging group when they
                               fit.  Head-sharded shapes copy only this rank's heads: one
                               strided cudaMemcpy3DAsync per run of consecutive slots per
-                              group */
+                              group.  K2 runs on an internal greatest-priority stream */
+  TSB_INGEST_CE_DIRECT = 4 /* copy engines straight into the pages, no SM work at all: one
+                              cudaMemcpyBatchAsync entry per (layer, K|V, run of consecutive
+                              pages); for full-head chunks into flash-attn / NHD pages (the
+                              page segment is contiguous on both sides), else UNSUPPORTED.
+                              What the stage uses while a prefill shares the SMs */
 } tsb_ingest_mode;
 
 /* One pcie_dispatch with real bytes (engine.cpp:427-446; PcieDone engine.cpp:258-272).
@@ -436,6 +442,9 @@ tsb_status tsb_ingest_tiered(tsb_l1* l1, tsb_pool* pool, tsb_pool* hbm_pool,
 /* The kernel path tsb_ingest takes for these items and mode (AUTO resolved; other modes returned
  * as given) -- which mechanism carries the pcie_dispatch hop (engine.cpp:427-446).  items: host
  * array or NULL (device items). */
+/* 1 if TSB_INGEST_CE_DIRECT can serve this L1 / pool pair (full heads, host pool, flash-attn or
+ * NHD pages).  The load stage uses it whenever a prefill shares the GPU, so ingest needs no SMs. */
+int tsb_ingest_ce_direct_supported(const tsb_l1* l1, const tsb_pool* pool);
 tsb_status tsb_ingest_resolve_mode(const tsb_l1* l1, const tsb_pool* pool,
                                    const tsb_ingest_item* items, int64_t n_items, int mode,
                                    int* resolved);

@@ -119,7 +119,7 @@ class TraceRow(C.Structure):
 
 
 HAS_DEADLINE, HAS_MEASURED = 1, 2
-INGEST_AUTO, INGEST_ZEROCOPY, INGEST_BULK, INGEST_CE = range(4)
+INGEST_AUTO, INGEST_ZEROCOPY, INGEST_BULK, INGEST_CE, INGEST_CE_DIRECT = range(5)
 POOL_HOST, POOL_DEVICE = 0, 1
 
 
@@ -212,6 +212,7 @@ _decl("tsb_ingest", st, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, P(vp)
 _decl("tsb_ingest_device", st, vp, vp, vp, i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_set_ce", st, C.c_int, i64)
 _decl("tsb_ingest_tiered", st, vp, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, P(vp))
+_decl("tsb_ingest_ce_direct_supported", C.c_int, vp, vp)
 _decl("tsb_ingest_resolve_mode", st, vp, vp, P(IngestItem), i64, C.c_int, P(C.c_int))
 _decl("tsb_ingest_set_scatter", st, C.c_int, C.c_int)
 _decl("tsb_scatter_device", st, vp, vp, vp, i64, i64, i64, vp)

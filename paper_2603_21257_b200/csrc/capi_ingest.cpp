@@ -658,12 +658,6 @@ tsb_status tsb_ingest_set_scatter(int impl, int ctas) {
 
 namespace {
 
-// K1b CTAs per SM from an HBM / NVLink source: as many rings as fit in 228 KB of shared memory.
-int tma_ctas_per_sm(const tsb::IngestGeom& g) {
-  const int64_t stages = std::min<int64_t>(tsb::kTmaMaxStages, tsb::kBulkSmem / g.seg_bytes);
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, (228 * 1024) / (stages * g.seg_bytes + 2048))));
-}
-
 // ---- tensor maps for K1b (cuTensorMapEncodeTiled through the runtime's driver entry point) ----
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -732,7 +726,7 @@ tsb_status launch_scatter(const tsb::IngestGeom& g, const uint8_t* src, uint8_t*
                              g.kv_src / g.row));
     int sms = 148;
     TSB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    TSB_CUDA_TRY(tsb::launch_ingest_tma(m, g, ts, arena, items, bt, n, sms * tma_ctas_per_sm(g), st));
+    TSB_CUDA_TRY(tsb::launch_ingest_tma(m, g, ts, arena, items, bt, n, sms * tsb::tma_ctas_per_sm(g.seg_bytes), st));
     return TSB_OK;
   }
   TSB_CUDA_TRY(tsb::launch_ingest_ldg(g, src, arena, items, bt, n, g_knobs.scatter_ctas, st, true));
@@ -976,6 +970,75 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
   return TSB_OK;
 }
 
+// CE-direct: the copy engines write the pages themselves.  For full-head chunks a (layer, K|V,
+// page j) segment is P contiguous token rows in the chunk and one contiguous page plane, so one
+// batched-memcpy entry moves it; consecutive pages of a chunk that landed on consecutive page ids
+// (flash-attn planes) merge into one entry.  Measured on B200 (profiles/r02_ce_direct_probe.jsonl):
+// 32 KiB entries run at 54.5 GB/s, 512 KiB at 54.7 -- with every SM busy or not.
+bool ce_direct_ok(const tsb_l1* l, const tsb_pool* pool) {
+  return pool->location == TSB_POOL_HOST && l->shape.tp_size == 1 && l->layout != TSB_LAYOUT_FLASHINFER_HND;
+}
+
+tsb_status ingest_ce_direct(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_host, int64_t n_items,
+                            int64_t lo, int64_t hi, cudaStream_t st, void* const* layer_events) {
+  if (!ce_direct_ok(l, pool))
+    return fail(TSB_UNSUPPORTED, "ingest CE direct: full-head chunks from a host pool into flash-attn / NHD pages only");
+  if (!items_host) return fail(TSB_UNSUPPORTED, "ingest CE direct needs host-visible items (use tsb_ingest)");
+  TSB_TRY(ensure_staging(l));  // the copy stream and its events (no staging memory is touched)
+  TSB_CUDA_TRY(cudaEventRecord(l->ev_fence, st));
+  TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_fence, 0));
+  const tsb::IngestGeom g = make_geom(l, 0, 1);
+  const int64_t ppc = l->ppc, seg = g.seg_bytes;
+  const bool planes = l->layout == TSB_LAYOUT_FLASH_ATTN;  // consecutive pages are contiguous
+  std::vector<void*> dst, src;
+  std::vector<size_t> sz;
+  dst.reserve(8192);
+  src.reserve(8192);
+  sz.reserve(8192);
+  auto flush = [&]() -> tsb_status {
+    if (dst.empty()) return TSB_OK;
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.srcLocHint.type = cudaMemLocationTypeHost;
+    attr.dstLocHint.type = cudaMemLocationTypeDevice;
+    attr.dstLocHint.id = l->device;
+    size_t attr_idx = 0, fail_idx = 0;
+    TSB_CUDA_TRY(cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), dst.size(), &attr, &attr_idx, 1, &fail_idx,
+                                      l->ce_stream));
+    dst.clear();
+    src.clear();
+    sz.clear();
+    return TSB_OK;
+  };
+  for (int64_t layer = lo; layer < hi; ++layer) {
+    for (int64_t i = 0; i < n_items; ++i) {
+      const tsb_ingest_item& it = items_host[i];
+      const int32_t* pages = l->bt_host + it.bt_row * l->stride + static_cast<int64_t>(it.chunk_index) * ppc;
+      const uint8_t* chunk = pool->host + it.src_slot * g.chunk_bytes + layer * g.layer_src;
+      for (int64_t kv = 0; kv < 2; ++kv) {
+        int64_t j = 0;
+        while (j < ppc) {
+          int64_t e = j + 1;  // extend over consecutive page ids (contiguous in flash-attn planes)
+          while (planes && e < ppc && pages[e] == pages[e - 1] + 1) ++e;
+          dst.push_back(l->arena + layer * g.layer_dst + kv * g.kv_dst + static_cast<int64_t>(pages[j]) * g.page_dst);
+          src.push_back(const_cast<uint8_t*>(chunk + kv * g.kv_src + j * g.P * g.row));
+          sz.push_back(static_cast<size_t>((e - j) * seg));
+          j = e;
+        }
+      }
+      if (dst.size() >= 8192) TSB_TRY(flush());
+    }
+    if (layer_events && layer_events[layer - lo]) {
+      TSB_TRY(flush());
+      TSB_TRY(record_fence(l, layer_events[layer - lo], l->ce_stream));
+    }
+  }
+  TSB_TRY(flush());
+  TSB_CUDA_TRY(cudaEventRecord(l->ev_k2_done, l->ce_stream));
+  TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_k2_done, 0));
+  return TSB_OK;
+}
+
 tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev, int64_t n_items,
                      int64_t lo, int64_t hi, int mode, cudaStream_t st, void* const* layer_events) {
   // One launch per span of layers ending at a requested fence (or at hi): per-layer fences give
@@ -1008,7 +1071,7 @@ tsb_status ingest_sm(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
       int sms = 148;
       if (on_device) TSB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, l->device));
       TSB_CUDA_TRY(tsb::launch_ingest_tma(m, g, ts, l->arena, items_dev, l->bt_dev, n_items,
-                                          on_device ? sms * tma_ctas_per_sm(g) : g_knobs.bulk_ctas, st));
+                                          on_device ? sms * tsb::tma_ctas_per_sm(g.seg_bytes) : g_knobs.bulk_ctas, st));
     }
     if (layer_events && layer_events[l1 - 1 - lo]) TSB_TRY(record_fence(l, layer_events[l1 - 1 - lo], st));
     l0 = l1;
@@ -1035,6 +1098,8 @@ tsb_status ingest_impl(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_d
       return ingest_sm(l, pool, items_dev, n_items, lo, hi, mode, st, layer_events);
     case TSB_INGEST_CE:
       return ingest_ce(l, pool, items_dev, items_host, n_items, lo, hi, st, layer_events);
+    case TSB_INGEST_CE_DIRECT:
+      return ingest_ce_direct(l, pool, items_host, n_items, lo, hi, st, layer_events);
     default:
       return fail(TSB_VALIDATION, "ingest: unknown mode " + std::to_string(mode));
   }
@@ -1043,6 +1108,10 @@ tsb_status ingest_impl(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_d
 }  // namespace
 
 extern "C" {
+
+int tsb_ingest_ce_direct_supported(const tsb_l1* l1, const tsb_pool* pool) {
+  return l1 && pool && ce_direct_ok(l1, pool) ? 1 : 0;
+}
 
 tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, int64_t n_items,
                       int64_t layer_lo, int64_t layer_hi, int mode, void* stream,
@@ -1137,7 +1206,7 @@ tsb_status tsb_ingest_device(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* i
 tsb_status tsb_ingest_resolve_mode(const tsb_l1* l, const tsb_pool* pool,
                                    const tsb_ingest_item* items, int64_t n_items, int mode,
                                    int* resolved) {
-  if (mode < TSB_INGEST_AUTO || mode > TSB_INGEST_CE)
+  if (mode < TSB_INGEST_AUTO || mode > TSB_INGEST_CE_DIRECT)
     return fail(TSB_VALIDATION, "ingest: unknown mode " + std::to_string(mode));
   *resolved = resolve_mode(l, pool, mode, items, n_items);
   return TSB_OK;

@@ -259,7 +259,7 @@ cudaError_t launch_ingest_tma(const CUtensorMap& src_map, const IngestGeom& g, c
     if (e != cudaSuccess) return e;
   }
   // ring depth: as many segment buffers as fit (6 for 32 KiB segments, 16 for TP8's 4 KiB)
-  const int stages = static_cast<int>(std::min<int64_t>(kTmaMaxStages, kBulkSmem / g.seg_bytes));
+  const int stages = tma_ring_stages(g.seg_bytes);
   const size_t smem = static_cast<size_t>(stages) * g.seg_bytes;
   if (g.hnd)
     k_ingest_tma<true><<<grid, 32, smem, st>>>(src_map, g, ts, arena, items, bt, nseg, stages);

@@ -47,6 +47,19 @@ cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* 
 // [slot][L][2][C]) and this rank's first head (HND maps) or first u64 column (NHD maps).
 constexpr int kBulkSmem = 200 * 1024;
 constexpr int kTmaMaxStages = 16;
+// Ring depth per CTA: ~96 KiB of segments (6..16 stages, within kBulkSmem), so small head-shard
+// segments run 2-3 rings per SM and full-head 32 KiB segments one 6-deep ring.
+inline int tma_ring_stages(int64_t seg_bytes) {
+  int64_t st = 98304 / seg_bytes;
+  st = st < 6 ? 6 : st > kTmaMaxStages ? kTmaMaxStages : st;
+  while (st > 2 && st * seg_bytes > kBulkSmem) --st;
+  return static_cast<int>(st);
+}
+inline int tma_ctas_per_sm(int64_t seg_bytes) {
+  const int64_t ring = tma_ring_stages(seg_bytes) * seg_bytes + 2048;
+  const int64_t n = (228 * 1024) / ring;
+  return static_cast<int>(n < 1 ? 1 : n > 4 ? 4 : n);
+}
 struct TmaSrc {
   int64_t layers;  // L of the source chunks (slot mode)
   int64_t C;       // chunk tokens

@@ -158,6 +158,15 @@ tsb_status grow_events(std::vector<cudaEvent_t>& v, size_t n, unsigned flags) {
   return TSB_OK;
 }
 
+// The ingest mode a run uses: while a prefill shares the GPU (K6 or a consumer hook) and the
+// caller left the choice to AUTO, the copy engines write the pages directly when the geometry
+// allows -- ingest then takes no SM time from prefill and prefill cannot stall it.
+int ingest_mode(const tsb_stage* s, const tsb_stage_options* opt) {
+  if (opt->mode == TSB_INGEST_AUTO && (opt->prefill || s->hook) && tsb_ingest_ce_direct_supported(s->l1, s->pool))
+    return TSB_INGEST_CE_DIRECT;
+  return opt->mode;
+}
+
 // Enqueues a request's prefill on the compute stream: for each layer, wait on its fence (may be
 // null = no wait), then the caller's hook or the K6 burner for that layer's share of `secs`.
 tsb_status enqueue_prefill(tsb_stage* s, int64_t q_index, int32_t bt_row, double secs,
@@ -350,6 +359,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   if (s->l3)
     return fail(TSB_UNSUPPORTED, "stage: the L3 network stage runs in tsb_stage_run_online only");
   const bool coupled = c->control_mode == 0;
+  const int mode = ingest_mode(s, opt);
   s->trace.clear();
   s->seq = 0;
   auto row = [&](double t, int kind, int stg, int tier, int64_t rid, int32_t blk, int64_t bytes) {
@@ -452,7 +462,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
         evp = evs.data();
       }
       TSB_TRY(tsb_ingest_tiered(s->l1, s->pool, s->hbm_pool, items.data(),
-                                static_cast<int64_t>(items.size()), 0, L, opt->mode, stream, evp));
+                                static_cast<int64_t>(items.size()), 0, L, mode, stream, evp));
       if (last && L == 1) TSB_CUDA_TRY(cudaEventRecord(r.ev_first, st));
       if (opt->record_trace) {
         if (call_events.size() >= 4096) return fail(TSB_CAPACITY, "stage: more than 4096 traced ingest calls");
@@ -622,6 +632,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   const bool use_l3 = s->l3 != nullptr;
   const bool coupled = c->control_mode == 0;
   const bool reactive = c->allocation_mode == 1;
+  const int mode = ingest_mode(s, opt);
   const int64_t l2_slot_bytes = tsb_pool_chunk_bytes(s->pool);
   s->trace.clear();
   s->seq = 0;
@@ -947,7 +958,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
           evs[L - 1] = r.ev_resident;
         }
         if ((status = tsb_ingest_tiered(s->l1, s->pool, s->hbm_pool, items.data(),
-                                        static_cast<int64_t>(items.size()), 0, L, opt->mode, stream,
+                                        static_cast<int64_t>(items.size()), 0, L, mode, stream,
                                         last ? evs.data() : nullptr)) != TSB_OK)
           break;
         if (calls.size() >= 4096) {  // bound the in-flight call list (event slots are reused)

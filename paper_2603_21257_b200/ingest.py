@@ -20,7 +20,8 @@ from ._capi import lib
 from .tiersim import Tier, check
 
 ZEROCOPY, BULK, CE, AUTO = capi.INGEST_ZEROCOPY, capi.INGEST_BULK, capi.INGEST_CE, capi.INGEST_AUTO
-MODES = {"auto": AUTO, "zerocopy": ZEROCOPY, "bulk": BULK, "ce": CE}
+CE_DIRECT = capi.INGEST_CE_DIRECT
+MODES = {"auto": AUTO, "zerocopy": ZEROCOPY, "bulk": BULK, "ce": CE, "ce_direct": CE_DIRECT}
 # Page layouts of the L1 arena (tsb_kv_layout): the consumer's KV-cache layout.
 LAYOUT_FLASH_ATTN, LAYOUT_FLASHINFER_NHD, LAYOUT_FLASHINFER_HND = 0, 1, 2
 LAYOUTS = {"flash_attn": LAYOUT_FLASH_ATTN, "flashinfer_nhd": LAYOUT_FLASHINFER_NHD,

@@ -509,6 +509,40 @@ def test_ingest_sparse_layer_events(oracle, mode):
     assert np.array_equal(l1.arena.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("layout", ["flash_attn", "flashinfer_nhd", "flashinfer_hnd"])
+@pytest.mark.parametrize("tp", [(1, 0), (2, 1)])
+def test_ce_direct_bit_exact(oracle, layout, tp):
+    """CE-direct: the copy engines write the pages (one batched entry per run of consecutive pages),
+    no kernel launched; flash-attn / NHD pages of full-head chunks, else UNSUPPORTED."""
+    lay = ingest.LAYOUTS[layout]
+    shape = SMALL.with_rank(*tp)
+    pool = ingest.ChunkPool(SMALL, 8)
+    pool.fill_synthetic(29)
+    num_pages = 200
+    arena = torch.zeros(shape.layers * 2 * num_pages * 16 * shape.heads_local * 128 * 2, dtype=torch.uint8,
+                        device="cuda")
+    l1 = ingest.PagedKVCache(shape, num_pages, max_rows=2, max_chunks=12, arena=arena, layout=lay)
+    rows = [l1.request(5, c, shape.page_bytes * 16)[1] for c in range(7)]
+    bt = l1.block_table()
+    bt[rows[0], 16:48] = bt[rows[0], 16:48][::-1].copy()  # chunks 1-2: pages in reverse (no merging)
+    l1.sync_block_table()
+    items = ingest.items_numpy([3, 4, 5, 6, 0, 1, 7], rows, range(7))
+    supported = tp[0] == 1 and layout != "flashinfer_hnd"
+    assert bool(_capi.lib.tsb_ingest_ce_direct_supported(l1.handle, pool.handle)) == supported
+    if not supported:
+        with pytest.raises(t.Unsupported):
+            ingest.ingest(l1, pool, items, mode=ingest.CE_DIRECT)
+        return
+    evs = [torch.cuda.Event() for _ in range(shape.layers)]
+    launches = _capi.lib.tsb_kernel_launch_count()
+    ingest.ingest(l1, pool, items, mode=ingest.CE_DIRECT, layer_events=evs)
+    evs[0].synchronize()
+    torch.cuda.synchronize()
+    assert _capi.lib.tsb_kernel_launch_count() == launches  # no SM work
+    want = oracle.scatter_ref(shape, pool.slot_view(0, 8), items, l1.block_table(), num_pages, layout=lay)
+    assert np.array_equal(arena.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("layout", ["flashinfer_nhd", "flashinfer_hnd"])
 @pytest.mark.parametrize("mode", ["zerocopy", "bulk", "ce", "auto"])
 @pytest.mark.parametrize("tp", [(1, 0), (2, 1), (8, 6)])
