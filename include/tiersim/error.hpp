@@ -65,6 +65,7 @@ inline void check(tsb_status s) {
     case TSB_CAPACITY: throw CapacityError(tsb_last_error());
     case TSB_MISSING_DEADLINE: throw MissingDeadline(tsb_last_error());
     case TSB_DEGENERATE_FIT: throw DegenerateFit(tsb_last_error());
+    case TSB_UNKNOWN_PROFILE: throw UnknownProfile(tsb_last_error());
     default: throw DeviceError(tsb_last_error());
   }
 }

@@ -15,6 +15,7 @@
 #include "tiersim/engine.hpp"
 #include "tiersim/scheduler.hpp"
 #include "tiersim/types.hpp"
+#include "tiersim/workload.hpp"
 
 using namespace tiersim;
 
@@ -79,6 +80,42 @@ static void host_cases() {
     EXPECT(derive_block_plan(spec(3, 0, 28100, 10, 0.0), cfg).empty());
     const auto st = make_request_state(spec(4, 1.5, 1000, 7, 0.5), cfg);
     EXPECT(st.cached_tokens == 256 && st.compute_tokens == 1000 + 7 - 256 && st.ts.arrival == 1.5);
+  });
+  run("workload: generate_workload / assign_slos through the kept API", [] {
+    WorkloadSpec w;
+    w.profile = builtin_profile("loogle");
+    w.count = 500;
+    w.qps = 4.0;
+    w.seed = 9;
+    w.hit_ratio_source = HitRatioSource::uniform_choice({0.25, 0.5, 1.0});
+    const auto a = generate_workload(w), b = generate_workload(w);
+    EXPECT(a.size() == 500 && a.front().id == 1 && a.back().id == 500 && a[0].dataset_tag == "loogle");
+    bool ok = true;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+      ok = ok && a[i].context_tokens == b[i].context_tokens && a[i].arrival_time == b[i].arrival_time;
+      ok = ok && a[i].context_tokens >= 1 && a[i].query_tokens >= 1;
+      ok = ok && (i == 0 || a[i].arrival_time - a[i - 1].arrival_time >= 1e-6 * 0.999999);
+      ok = ok && (a[i].cache_hit_ratio == 0.25 || a[i].cache_hit_ratio == 0.5 || a[i].cache_hit_ratio == 1.0);
+    }
+    EXPECT(ok);
+    ClusterConfig cfg;
+    cfg.l1_capacity = cfg.l2_capacity = 10'000'000'000'000;
+    const std::vector<double> f = {2.0, 4.0, 8.0};
+    const auto s = assign_slos(a, cfg, cost_models_from_config(cfg), f, 3);
+    bool dl = true;
+    for (std::size_t i = 0; i < s.size(); ++i) {
+      const double solo = solo_baseline_ttft(a[i], cfg);
+      const double fac = (*s[i].deadline - a[i].arrival_time) / solo;
+      dl = dl && s[i].deadline.has_value() && fac > 1.99 && fac < 8.01;
+    }
+    EXPECT(dl);
+    bool threw = false;
+    try {
+      builtin_profile("nope");
+    } catch (const UnknownProfile&) {
+      threw = true;
+    }
+    EXPECT(threw);
   });
   run("geometry: kv_bytes_per_token", [] {
     EXPECT(kv_bytes_per_token(32, 8, 128, 2) == 131072);

@@ -1,6 +1,7 @@
 """Small, single-purpose workloads for ncu (one GPU, short):  python tools/prof_targets.py <what>
 
-what: scorer | hash | index | ingest-ce | ingest-bulk | ingest-zerocopy | ingest-tp8 | ingest-hbm | ingest-hbm-tp8
+what: scorer | hash | index | ingest-ce | ingest-bulk | ingest-zerocopy | ingest-tp8 | ingest-hbm | ingest-hbm-tp8 |
+      bulk-hbm | bulk-hbm-tp8 | bulk-hbm-tp8-hnd | ingest-ce-direct
 """
 from __future__ import annotations
 
@@ -29,6 +30,22 @@ def ingest_once(shape, n_chunks, mode, reps=2):
     evs = [torch.cuda.Event() for _ in range(shape.layers)]
     for _ in range(reps):
         ingest.ingest(l1, pool, items, mode=mode, layer_events=evs)
+    torch.cuda.synchronize()
+    assert ingest.verify_synthetic(l1, pool, items, 3) == 0
+
+
+def ingest_hbm_bulk(shape, n_chunks, layout=0, reps=2):
+    """K1b (tensor-map TMA) over an HBM-resident pool, whole layer range in one launch."""
+    pool = ingest.ChunkPool.create_device(shape, n_chunks)
+    pool.fill_synthetic(3)
+    l1 = ingest.PagedKVCache(shape, n_chunks * shape.pages_per_chunk, 1, n_chunks, layout=layout)
+    cb = shape.page_bytes * shape.pages_per_chunk
+    for c in range(n_chunks):
+        g, row = l1.request(1, c, cb)
+    l1.sync_block_table()
+    items = ingest.items_numpy(np.random.default_rng(0).permutation(n_chunks), [row] * n_chunks, np.arange(n_chunks))
+    for _ in range(reps):
+        ingest.ingest(l1, pool, items, mode=ingest.BULK)
     torch.cuda.synchronize()
     assert ingest.verify_synthetic(l1, pool, items, 3) == 0
 
@@ -84,6 +101,14 @@ if __name__ == "__main__":
         ingest_once(ingest.LLAMA3_70B.with_rank(8, 7), 128, ingest.ZEROCOPY)
     elif what == "ingest-hbm":
         ingest_hbm(ingest.LLAMA31_8B, 128)
+    elif what == "bulk-hbm-tp8":
+        ingest_hbm_bulk(ingest.LLAMA3_70B.with_rank(8, 7), 128)
+    elif what == "bulk-hbm-tp8-hnd":
+        ingest_hbm_bulk(ingest.LLAMA3_70B.with_rank(8, 7), 128, layout=ingest.LAYOUT_FLASHINFER_HND)
+    elif what == "bulk-hbm":
+        ingest_hbm_bulk(ingest.LLAMA31_8B, 128)
+    elif what == "ingest-ce-direct":
+        ingest_once(ingest.LLAMA31_8B, 128, ingest.CE_DIRECT)
     elif what == "ingest-hbm-tp8":
         ingest_hbm(ingest.LLAMA3_70B.with_rank(8, 7), 128)
     else:
