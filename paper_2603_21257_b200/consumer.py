@@ -28,7 +28,7 @@ from .tiersim import ClusterConfig, QueueArrays
 
 class PagedPrefill:
     def __init__(self, l1: PagedKVCache, queue: QueueArrays, config: ClusterConfig, hidden: int = 4096,
-                 q_heads: int = 32, intermediate: int = 14336, token_block: int = 8192, wrappers: int = 4,
+                 q_heads: int = 32, intermediate: int = 14336, token_block: int = 8192, wrappers: int = 8,
                  seed: int = 0):
         import flashinfer
 

@@ -139,7 +139,8 @@ struct tsb_stage {
   cudaStream_t compute = nullptr;
   bool own_compute = true;  // false: the caller's stream (tsb_stage_set_compute_stream)
   std::vector<cudaEvent_t> timing_pool;  // 3 per request, grown on demand
-  std::vector<cudaEvent_t> layer_ev;     // per-layer fences (reused across requests)
+  std::vector<cudaEvent_t> layer_ev;     // per-layer fences of compute-only requests
+  std::vector<cudaEvent_t> layer_pool;   // per-(request, layer) fences, grown on demand
   std::vector<cudaEvent_t> call_pool;    // per ingest call (online PcieDone / trace), grown on demand
   cudaEvent_t ev_start = nullptr;
   std::vector<tsb_trace_row> trace;
@@ -273,6 +274,7 @@ void tsb_stage_destroy(tsb_stage* s) {
   delete s->net;
   for (auto e : s->timing_pool) cudaEventDestroy(e);
   for (auto e : s->layer_ev) cudaEventDestroy(e);
+  for (auto e : s->layer_pool) cudaEventDestroy(e);
   for (auto e : s->call_pool) cudaEventDestroy(e);
   if (s->ev_start) cudaEventDestroy(s->ev_start);
   if (s->compute) {
@@ -416,7 +418,8 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       std::vector<cudaEvent_t> fences(static_cast<size_t>(L), nullptr);
       fences[0] = opt->layer_events ? r.ev_first : r.ev_resident;
       if (opt->layer_events) {
-        for (int64_t l = 1; l + 1 < L; ++l) fences[l] = s->layer_ev[l];
+        for (int64_t l = 1; l + 1 < L; ++l)
+          fences[l] = p.n_chunks ? s->layer_pool[static_cast<size_t>(i * L + l)] : s->layer_ev[l];
         if (L > 1) fences[L - 1] = r.ev_resident;
       }
       TSB_TRY(enqueue_prefill(s, i, r.row, compute_seconds(q, i, c, p.compute_tokens), fences, ctas));
@@ -429,6 +432,8 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   };
 
   // pcie_dispatch (engine.cpp:427-446): serve granted chunks of admitted requests in pick order.
+  std::vector<int64_t> issued_last;
+  if (opt->layer_events) TSB_TRY(grow_events(s->layer_pool, static_cast<size_t>(n * L), cudaEventDisableTiming));
   auto dispatch = [&]() -> tsb_status {
     bool synced = false;
     for (int64_t k = 0; k < n; ++k) {
@@ -453,10 +458,11 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       std::vector<void*> evs;
       void* const* evp = nullptr;
       if (last) {
-        // Timing events double as the layer-0 and last-layer fences.
+        // Timing events double as the layer-0 and last-layer fences; the layers between get this
+        // request's own fences (its prefill is enqueued after later requests' ingest).
         evs.assign(static_cast<size_t>(L), nullptr);
         if (opt->layer_events)
-          for (int64_t l = 1; l + 1 < L; ++l) evs[l] = s->layer_ev[l];
+          for (int64_t l = 1; l + 1 < L; ++l) evs[l] = s->layer_pool[static_cast<size_t>(i * L + l)];
         evs[0] = r.ev_first;
         evs[L - 1] = r.ev_resident;
         evp = evs.data();
@@ -475,8 +481,13 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       }
       ++ingest_calls;
       bytes_total += static_cast<int64_t>(items.size()) * chunk_bytes;
-      if (last) TSB_TRY(finish_request_events(i));
+      if (last) issued_last.push_back(i);
     }
+    // Every ready chunk of every request is queued on the link before any prefill is enqueued:
+    // a consumer hook may block the host (planning, waiting on its own resources), and the link
+    // must not idle meanwhile.
+    for (const int64_t i : issued_last) TSB_TRY(finish_request_events(i));
+    issued_last.clear();
     return TSB_OK;
   };
 
