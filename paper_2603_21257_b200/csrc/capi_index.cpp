@@ -81,10 +81,14 @@ tsb_status tsb_index_create(int device, int64_t capacity, tsb_index** out) {
   x->device = device;
   x->mask = static_cast<uint64_t>(cap - 1);
   cudaError_t e = alloc_index_arrays(x, cap);
+  // insert-position scratch sized for a batch as large as the table (grown if a batch is larger)
+  if (e == cudaSuccess) e = cudaMalloc(&x->pos, sizeof(int64_t) * cap);
+  if (e == cudaSuccess) x->pos_cap = cap;
   if (e == cudaSuccess) e = cudaMalloc(&x->stats, 3 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(x->stats, 0, 3 * sizeof(unsigned long long));
   if (e != cudaSuccess) {
     free_index_arrays(x);
+    cudaFree(x->pos);
     cudaFree(x->stats);
     delete x;
     return tsb::cuda_fail(e, "tsb_index_create");
