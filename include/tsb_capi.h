@@ -463,6 +463,17 @@ tsb_status tsb_scatter_device(tsb_l1* l1, const void* staging, const tsb_ingest_
 tsb_status tsb_scatter_device_packed(tsb_l1* l1, const void* staging,
                                      const tsb_ingest_item* items_dev, int64_t n_items,
                                      int64_t layer_lo, int64_t layer_hi, void* stream);
+/* Chunk replication inside L1 (K8): a chunk resident in one request's pages copied into another
+ * request's granted pages, HBM -> HBM, for layers [layer_lo, layer_hi) -- instead of moving the
+ * same L2 chunk over the host link again (LooGLE-like batches read each document chunk from many
+ * requests).  Both rows' pages must be granted and the source's bytes written by work already
+ * queued on `stream`.  Items are range-checked; async. */
+typedef struct {
+  int32_t src_row, src_chunk; /* block_table row / chunk index holding the bytes */
+  int32_t dst_row, dst_chunk; /* where they go */
+} tsb_page_copy;
+tsb_status tsb_l1_copy_chunks(tsb_l1* l1, const tsb_page_copy* items, int64_t n_items, int64_t layer_lo,
+                              int64_t layer_hi, void* stream);
 /* Tuning knobs for measurement (0 = default); no reference counterpart (the reference models
  * the hop's cost only, engine.cpp:206-207). */
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas);
@@ -500,7 +511,9 @@ typedef struct {
                            page words differing from tsb_pool_fill_synthetic(verify_seed) */
   int32_t pace_network; /* online mode with an L3 store: a network hop lasts at least
                            transfer_base_latency + bytes / network_bandwidth (engine.cpp:205) */
-  int32_t reserved0;
+  int32_t reuse_l1;     /* batch mode: a chunk whose L2 slot is already resident in another live
+                           request's pages is replicated HBM -> HBM (K8) instead of crossing the
+                           link again; the holder's release waits for the copies */
 } tsb_stage_options;
 
 typedef struct {
@@ -531,6 +544,7 @@ typedef struct {
   uint64_t verify_mismatches; /* with verify_seed != 0 */
   int64_t net_blocks;      /* online mode with an L3 store: L3 -> L2 network hops */
   int64_t l2_deferred;     /* ... L2 reservations that waited for a release (engine.cpp:357-362) */
+  int64_t reused_chunks;   /* reuse_l1: chunks replicated from L1 instead of the host link */
 } tsb_stage_stats;
 
 /* TraceEvent row (events.hpp:33-42): kind 1 TransferDone, 2 AllocationGrant, 4 DispatchWake;

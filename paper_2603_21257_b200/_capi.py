@@ -97,7 +97,7 @@ class IngestItem(C.Structure):
 
 class StageOptions(C.Structure):
     _fields_ = [("mode", i32), ("policy", i32), ("layer_events", i32), ("prefill", i32), ("prefill_ctas", i32),
-                ("record_trace", i32), ("verify_seed", u64), ("pace_network", i32), ("reserved0", i32)]
+                ("record_trace", i32), ("verify_seed", u64), ("pace_network", i32), ("reuse_l1", i32)]
 
 
 class StageRequest(C.Structure):
@@ -110,7 +110,7 @@ class StageRequest(C.Structure):
 class StageStats(C.Structure):
     _fields_ = [("bytes", i64), ("device_ms", f64), ("wall_ms", f64), ("ingest_calls", i64),
                 ("deferred_chunks", i64), ("releases", i64), ("kernel_launches", i64), ("verify_mismatches", u64),
-                ("net_blocks", i64), ("l2_deferred", i64)]
+                ("net_blocks", i64), ("l2_deferred", i64), ("reused_chunks", i64)]
 
 
 class TraceRow(C.Structure):
@@ -215,6 +215,11 @@ _decl("tsb_ingest_tiered", st, vp, vp, vp, P(IngestItem), i64, i64, i64, C.c_int
 _decl("tsb_ingest_ce_direct_supported", C.c_int, vp, vp)
 _decl("tsb_ingest_resolve_mode", st, vp, vp, P(IngestItem), i64, C.c_int, P(C.c_int))
 _decl("tsb_ingest_set_scatter", st, C.c_int, C.c_int)
+class PageCopy(C.Structure):
+    _fields_ = [("src_row", i32), ("src_chunk", i32), ("dst_row", i32), ("dst_chunk", i32)]
+
+
+_decl("tsb_l1_copy_chunks", st, vp, P(PageCopy), i64, i64, i64, vp)
 _decl("tsb_scatter_device", st, vp, vp, vp, i64, i64, i64, vp)
 _decl("tsb_scatter_device_packed", st, vp, vp, vp, i64, i64, i64, vp)
 _decl("tsb_ingest_set_grid", st, C.c_int, C.c_int, C.c_int)

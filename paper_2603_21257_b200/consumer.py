@@ -28,7 +28,7 @@ from .tiersim import ClusterConfig, QueueArrays
 
 class PagedPrefill:
     def __init__(self, l1: PagedKVCache, queue: QueueArrays, config: ClusterConfig, hidden: int = 4096,
-                 q_heads: int = 32, intermediate: int = 14336, token_block: int = 8192, wrappers: int = 8,
+                 q_heads: int = 32, intermediate: int = 14336, token_block: int = 8192, wrappers: int = 0,
                  seed: int = 0):
         import flashinfer
 
@@ -57,6 +57,8 @@ class PagedPrefill:
         self.kv_tuple = l1.layout == LAYOUT_FLASH_ATTN
         # A ring of wrappers: each holds one request's plan (host pinned staging + device
         # metadata); a wrapper is re-planned only after the prefill that used it has finished.
+        # Default: one per request up to 32, so planning never waits on the GPU.
+        wrappers = wrappers or max(2, min(32, queue.n))
         self.wrappers = [flashinfer.BatchPrefillWithPagedKVCacheWrapper(
             torch.empty(128 << 20, dtype=torch.uint8, device=dev), layout) for _ in range(wrappers)]
         self.done = [None] * wrappers

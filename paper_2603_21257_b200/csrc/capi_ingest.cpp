@@ -1109,6 +1109,31 @@ tsb_status ingest_impl(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_d
 
 extern "C" {
 
+tsb_status tsb_l1_copy_chunks(tsb_l1* l, const tsb_page_copy* items, int64_t n_items, int64_t layer_lo,
+                              int64_t layer_hi, void* stream) {
+  tsb::DeviceGuard dg(l ? l->device : -1);
+  if (layer_lo < 0 || layer_hi > l->shape.layers || layer_lo >= layer_hi)
+    return fail(TSB_VALIDATION, "copy_chunks: layer range must satisfy 0 <= lo < hi <= layers");
+  const int64_t per = static_cast<int64_t>(UploadRing::kSlotBytes / sizeof(tsb_page_copy));
+  if (n_items > per) return fail(TSB_VALIDATION, "copy_chunks: at most " + std::to_string(per) + " items per call");
+  for (int64_t k = 0; k < n_items; ++k) {
+    const tsb_page_copy& it = items[k];
+    if (it.src_row < 0 || it.src_row >= l->rows || it.dst_row < 0 || it.dst_row >= l->rows || it.src_chunk < 0 ||
+        it.src_chunk >= l->max_chunks || it.dst_chunk < 0 || it.dst_chunk >= l->max_chunks)
+      return fail(TSB_VALIDATION, "copy_chunks: item " + std::to_string(k) + " is outside the block table");
+  }
+  if (n_items == 0) return TSB_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  void* dptr = nullptr;
+  int slot = 0;
+  TSB_TRY(l->ring_items.stage(items, sizeof(tsb_page_copy) * n_items, st, &dptr, &slot));
+  const tsb::IngestGeom g = make_geom(l, layer_lo, layer_hi);
+  TSB_CUDA_TRY(tsb::launch_page_copy(g, l->arena, static_cast<const tsb_page_copy*>(dptr), l->bt_dev, n_items,
+                                     g_knobs.scatter_ctas, st));
+  TSB_TRY(l->ring_items.fence(slot, st));
+  return TSB_OK;
+}
+
 int tsb_ingest_ce_direct_supported(const tsb_l1* l1, const tsb_pool* pool) {
   return l1 && pool && ce_direct_ok(l1, pool) ? 1 : 0;
 }

@@ -191,6 +191,39 @@ __global__ void __launch_bounds__(32) k_ingest_tma(const __grid_constant__ CUten
   if (lane == 0) bulk_wait0();
 }
 
+// K8: chunk replication inside L1.  A chunk already resident in one request's pages is copied
+// into another request's pages (HBM -> HBM) instead of crossing the host link again -- LooGLE-like
+// batches read each document chunk from several requests.  Warp per (item, layer, K|V, page)
+// plane; both sides use the arena's layout, so a plane is one contiguous seg_bytes copy.
+__global__ void __launch_bounds__(256) k_page_copy(IngestGeom g, uint8_t* __restrict__ arena,
+                                                   const tsb_page_copy* __restrict__ items,
+                                                   const int32_t* __restrict__ bt, int64_t nseg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t spi = static_cast<int64_t>(g.n_layers) * 2 * g.ppc;
+  const int nvec = static_cast<int>(g.seg_bytes >> 4);
+  for (int64_t s = warp; s < nseg; s += nwarps) {
+    const int64_t i = s / spi, r = s - i * spi;
+    const int64_t l = g.layer_lo + r / (2 * g.ppc), kv = (r / g.ppc) & 1, j = r % g.ppc;
+    const tsb_page_copy it = items[i];
+    const int32_t ps = bt[static_cast<int64_t>(it.src_row) * g.bt_stride + static_cast<int64_t>(it.src_chunk) * g.ppc + j];
+    const int32_t pd = bt[static_cast<int64_t>(it.dst_row) * g.bt_stride + static_cast<int64_t>(it.dst_chunk) * g.ppc + j];
+    if (ps < 0 || pd < 0 || ps >= g.num_pages || pd >= g.num_pages) continue;
+    const uint8_t* src = arena + l * g.layer_dst + kv * g.kv_dst + static_cast<int64_t>(ps) * g.page_dst;
+    uint8_t* dst = arena + l * g.layer_dst + kv * g.kv_dst + static_cast<int64_t>(pd) * g.page_dst;
+    for (int v0 = lane; v0 < nvec; v0 += 32 * 4) {
+      int4 buf[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v0 + u * 32 < nvec) buf[u] = ld_stream(src + static_cast<int64_t>(v0 + u * 32) * 16);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v0 + u * 32 < nvec) st_stream(dst + static_cast<int64_t>(v0 + u * 32) * 16, buf[u]);
+    }
+  }
+}
+
 __global__ void k_fill_synth(uint64_t* __restrict__ dst, uint64_t first_word, uint64_t n_words,
                              uint64_t seed) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -265,6 +298,15 @@ cudaError_t launch_ingest_tma(const CUtensorMap& src_map, const IngestGeom& g, c
     k_ingest_tma<true><<<grid, 32, smem, st>>>(src_map, g, ts, arena, items, bt, nseg, stages);
   else
     k_ingest_tma<false><<<grid, 32, smem, st>>>(src_map, g, ts, arena, items, bt, nseg, stages);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_page_copy(const IngestGeom& g, uint8_t* arena, const tsb_page_copy* items, const int32_t* bt,
+                             int64_t n_items, int grid, cudaStream_t st) {
+  const int64_t nseg = n_items * g.n_layers * 2 * g.ppc;
+  if (nseg == 0) return cudaSuccess;
+  k_page_copy<<<grid, 256, 0, st>>>(g, arena, items, bt, nseg);
   count_launch();
   return cudaGetLastError();
 }

@@ -69,6 +69,9 @@ struct TmaSrc {
 cudaError_t launch_ingest_tma(const CUtensorMap& src_map, const IngestGeom& g, const TmaSrc& ts, uint8_t* arena,
                               const tsb_ingest_item* items, const int32_t* bt, int64_t n_items, int grid,
                               cudaStream_t st);
+// K8: copy resident chunks' pages to other rows' pages (HBM -> HBM), layers of g.
+cudaError_t launch_page_copy(const IngestGeom& g, uint8_t* arena, const tsb_page_copy* items, const int32_t* bt,
+                             int64_t n_items, int grid, cudaStream_t st);
 cudaError_t launch_fill_synth(uint64_t* dst, uint64_t first_word, uint64_t n_words, uint64_t seed,
                               cudaStream_t st);
 // Harness page check (verify.cu): the canonical shape and layout only, no IngestGeom.

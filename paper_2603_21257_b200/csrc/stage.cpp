@@ -377,16 +377,26 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     int64_t issued = 0;
     int32_t deferred = 0;
     bool finished_issue = false;
+    bool read_by_copy = false;  // reuse_l1: ev_reader guards this request's pages until copied
     cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr, ev_begin = nullptr;
+    cudaEvent_t ev_reader = nullptr;
   };
   std::vector<ReqRt> reqs(static_cast<size_t>(n));
-  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(4 * n), cudaEventDefault));
+  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(5 * n), cudaEventDefault));
   for (int64_t i = 0; i < n; ++i) {
-    reqs[i].ev_first = s->timing_pool[4 * i];
-    reqs[i].ev_resident = s->timing_pool[4 * i + 1];
-    reqs[i].ev_done = s->timing_pool[4 * i + 2];
-    reqs[i].ev_begin = s->timing_pool[4 * i + 3];
+    reqs[i].ev_first = s->timing_pool[5 * i];
+    reqs[i].ev_resident = s->timing_pool[5 * i + 1];
+    reqs[i].ev_done = s->timing_pool[5 * i + 2];
+    reqs[i].ev_begin = s->timing_pool[5 * i + 3];
+    reqs[i].ev_reader = s->timing_pool[5 * i + 4];
   }
+  // reuse_l1: L2 slot -> a live request's (row, chunk) whose pages hold that chunk (issued).
+  struct Holder {
+    int64_t req;
+    int32_t row, chunk;
+  };
+  std::unordered_map<int64_t, std::vector<Holder>> holders;  // every live holder, oldest first
+  int64_t reused_chunks = 0;
 
   // ---- pick order (K4 + K5 on the GPU) ----------------------------------------------------------
   std::vector<int64_t> order(static_cast<size_t>(n));
@@ -432,6 +442,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   };
 
   // pcie_dispatch (engine.cpp:427-446): serve granted chunks of admitted requests in pick order.
+  constexpr size_t kPrefillLag = 2;
   std::vector<int64_t> issued_last;
   if (opt->layer_events) TSB_TRY(grow_events(s->layer_pool, static_cast<size_t>(n * L), cudaEventDisableTiming));
   auto dispatch = [&]() -> tsb_status {
@@ -446,15 +457,40 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
         synced = true;
       }
       std::vector<tsb_ingest_item> items;
+      std::vector<tsb_page_copy> copies;
+      std::vector<int64_t> copy_from;  // holder request of each copy
       items.reserve(r.ready.size());
       for (int32_t ch : r.ready) {
-        items.push_back(tsb_ingest_item{p.slots[ch], r.row, ch});
+        const int64_t sl = p.slots[ch];
+        const auto h = opt->reuse_l1 && sl >= 0 ? holders.find(sl) : holders.end();
+        if (h != holders.end() && !h->second.empty()) {
+          const Holder& src = h->second.front();
+          copies.push_back(tsb_page_copy{src.row, src.chunk, r.row, ch});
+          copy_from.push_back(src.req);
+        } else {
+          items.push_back(tsb_ingest_item{sl, r.row, ch});
+        }
         row(now_s() - host0, 4, 1, -1, p.id, ch, chunk_bytes);  // DispatchWake(Pcie)
       }
       if (r.issued == 0) TSB_CUDA_TRY(cudaEventRecord(r.ev_begin, st));  // the request's first hop
-      r.issued += static_cast<int64_t>(items.size());
+      r.issued += static_cast<int64_t>(r.ready.size());
+      if (opt->reuse_l1)
+        for (int32_t ch : r.ready)
+          if (p.slots[ch] >= 0) holders[p.slots[ch]].push_back(Holder{i, r.row, ch});
       r.ready.clear();
       const bool last = r.issued == p.n_chunks;
+      if (!copies.empty()) {
+        // K8 first: its sources were written by earlier work on this stream; then the link part.
+        for (int64_t c0 = 0; c0 < static_cast<int64_t>(copies.size()); c0 += 65536)
+          TSB_TRY(tsb_l1_copy_chunks(s->l1, copies.data() + c0,
+                                     std::min<int64_t>(65536, static_cast<int64_t>(copies.size()) - c0), 0, L,
+                                     stream));
+        for (const int64_t h : copy_from) {  // the holders' pages stay until these copies ran
+          TSB_CUDA_TRY(cudaEventRecord(reqs[h].ev_reader, st));
+          reqs[h].read_by_copy = true;
+        }
+        reused_chunks += static_cast<int64_t>(copies.size());
+      }
       std::vector<void*> evs;
       void* const* evp = nullptr;
       if (last) {
@@ -469,7 +505,12 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       }
       TSB_TRY(tsb_ingest_tiered(s->l1, s->pool, s->hbm_pool, items.data(),
                                 static_cast<int64_t>(items.size()), 0, L, mode, stream, evp));
-      if (last && L == 1) TSB_CUDA_TRY(cudaEventRecord(r.ev_first, st));
+      if (last && (L == 1 || !copies.empty())) TSB_CUDA_TRY(cudaEventRecord(r.ev_first, st));
+      if (last && !copies.empty()) {  // the fences must also cover the replicated chunks
+        for (int64_t l = 1; opt->layer_events && l + 1 < L; ++l)
+          TSB_CUDA_TRY(cudaEventRecord(s->layer_pool[static_cast<size_t>(i * L + l)], st));
+        TSB_CUDA_TRY(cudaEventRecord(r.ev_resident, st));
+      }
       if (opt->record_trace) {
         if (call_events.size() >= 4096) return fail(TSB_CAPACITY, "stage: more than 4096 traced ingest calls");
         TSB_TRY(grow_events(s->call_pool, call_events.size() + 1, cudaEventDefault));
@@ -481,11 +522,19 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       }
       ++ingest_calls;
       bytes_total += static_cast<int64_t>(items.size()) * chunk_bytes;
-      if (last) issued_last.push_back(i);
+      if (last) {
+        issued_last.push_back(i);
+        // A request's prefill is enqueued once the ingest of the next kPrefillLag requests is
+        // queued too: a consumer hook runs on this host thread (planning, possibly waiting on its
+        // own resources) and the link must have work queued meanwhile.  Without prefill the
+        // request's completion is recorded right away.
+        const size_t lag = (opt->prefill || s->hook) ? kPrefillLag : 0;
+        while (issued_last.size() > lag) {
+          TSB_TRY(finish_request_events(issued_last.front()));
+          issued_last.erase(issued_last.begin());
+        }
+      }
     }
-    // Every ready chunk of every request is queued on the link before any prefill is enqueued:
-    // a consumer hook may block the host (planning, waiting on its own resources), and the link
-    // must not idle meanwhile.
     for (const int64_t i : issued_last) TSB_TRY(finish_request_events(i));
     issued_last.clear();
     return TSB_OK;
@@ -528,6 +577,15 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       verify_mismatches += mm;
     }
     row(now_s() - host0, 3, 2, -1, p.id, -1, p.compute_tokens * c->bytes_per_token);
+    if (opt->reuse_l1) {  // its pages stop being a copy source; pending copies from them finish first
+      for (int64_t ch = 0; ch < p.n_chunks; ++ch) {
+        const auto h = p.slots[ch] >= 0 ? holders.find(p.slots[ch]) : holders.end();
+        if (h == holders.end()) continue;
+        auto& v = h->second;
+        v.erase(std::remove_if(v.begin(), v.end(), [&](const Holder& x) { return x.req == i; }), v.end());
+      }
+      if (r.read_by_copy) TSB_CUDA_TRY(cudaEventSynchronize(r.ev_reader));
+    }
     if (r.row >= 0) {
       std::vector<tsb_grant> grants(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
       int64_t ng = 0;
@@ -618,6 +676,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     stats->releases = releases;
     stats->kernel_launches = static_cast<int64_t>(tsb_kernel_launch_count() - launches0);
     stats->verify_mismatches = verify_mismatches;
+    stats->reused_chunks = reused_chunks;
   }
   return TSB_OK;
 }

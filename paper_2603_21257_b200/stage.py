@@ -101,7 +101,8 @@ class LoadStage:
     def run(self, queue: QueueArrays, slot_lists: Sequence[Sequence[int]], config: ClusterConfig,
             models: Optional[CostModelPair] = None, policy: int = PolicyKind.Fifo, mode: int = AUTO,
             layer_events: bool = False, prefill: bool = False, prefill_ctas: int = 0, record_trace: bool = False,
-            verify_seed: int = 0, stream=None, pace_network: bool = False, _fn=None) -> StageResult:
+            verify_seed: int = 0, stream=None, pace_network: bool = False, reuse_l1: bool = False,
+            _fn=None) -> StageResult:
         fn = _fn or lib.tsb_stage_run
         models = models or cost_models_from_config(config)
         offs = np.zeros(len(slot_lists) + 1, np.int64)
@@ -109,7 +110,7 @@ class LoadStage:
         slots = np.concatenate([np.asarray(s, np.int64) for s in slot_lists]) if len(slot_lists) else np.zeros(0, np.int64)
         slots = np.ascontiguousarray(slots, np.int64)
         opt = capi.StageOptions(int(mode), int(policy), int(layer_events), int(prefill), int(prefill_ctas),
-                                int(record_trace), int(verify_seed), int(pace_network), 0)
+                                int(record_trace), int(verify_seed), int(pace_network), int(reuse_l1))
         res = (capi.StageRequest * max(queue.n, 1))()
         stats = capi.StageStats()
         qs = queue.struct()

@@ -170,3 +170,57 @@ def test_stage_synthetic_prefill_overlap():
     assert np.all(r["done_ms"] >= r["resident_ms"])
     prefill_s = cfg.compute_base + cfg.compute_per_token * 500
     assert r["done_ms"].max() * 1e-3 >= 6 * prefill_s * 0.9
+
+
+@pytest.mark.parametrize("layer_events", [False, True])
+def test_stage_reuse_l1_replicates_resident_chunks(layer_events):
+    """reuse_l1: requests reading the same document chunks get them from a live holder's pages
+    (K8, HBM -> HBM) instead of the host link; every page is still verified, the holders' pages are
+    released only after the copies, and the result equals the link-only run."""
+    shape = ingest.KVShape(layers=4, kv_heads=8, head_dim=128)
+    pool = ingest.ChunkPool(shape, 24)
+    pool.fill_synthetic(9)
+    l1 = ingest.PagedKVCache(shape, 20 * 16, max_rows=16, max_chunks=16)  # L1 pressure: deferral
+    cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(4, 8, 128, 2), compute_base=1e-4,
+                          compute_per_token=1e-7)
+    n = 8
+    q = t.QueueArrays(n, id=np.arange(1, n + 1), arrival=np.arange(n) * 1e-3, context_tokens=np.full(n, 256 * 6),
+                      query_tokens=np.full(n, 10), cache_hit_ratio=np.ones(n), flags=np.zeros(n, np.uint8))
+    docs = [list(range(0, 6)), list(range(10, 16)), list(range(3, 9))]  # doc 2 overlaps doc 0
+    slots = [docs[i % 3] for i in range(n)]
+    stage = LoadStage(l1, pool)
+    base = stage.run(q, slots, cfg, prefill=True, layer_events=layer_events, verify_seed=9)
+    res = stage.run(q, slots, cfg, prefill=True, layer_events=layer_events, verify_seed=9, reuse_l1=True)
+    assert base.stats["verify_mismatches"] == 0 and res.stats["verify_mismatches"] == 0
+    assert base.stats["reused_chunks"] == 0 and res.stats["reused_chunks"] > n * 6 // 2
+    assert res.stats["bytes"] == base.stats["bytes"] == n * 6 * shape.local_chunk_bytes
+    assert l1.reserved() == 0 and l1.free_pages() == l1.num_pages
+    r = res.requests
+    assert np.all(r["done_ms"] >= r["resident_ms"]) and np.all(r["resident_ms"] >= r["first_layer_ms"])
+
+
+def test_copy_chunks_api(oracle):
+    """tsb_l1_copy_chunks (K8) against scatter_ref: chunks ingested into row A, replicated into row B."""
+    import ctypes as C
+
+    from paper_2603_21257_b200 import _capi
+
+    shape = ingest.KVShape(layers=3, kv_heads=8, head_dim=128)
+    pool = ingest.ChunkPool(shape, 6)
+    pool.fill_synthetic(4)
+    l1 = ingest.PagedKVCache(shape, 12 * 16, max_rows=3, max_chunks=6)
+    cb = shape.page_bytes * 16
+    ra = [l1.request(1, c, cb)[1] for c in range(4)][0]
+    rb = [l1.request(2, c, cb)[1] for c in range(4)][0]
+    l1.sync_block_table()
+    ingest.ingest(l1, pool, ingest.items_numpy([5, 1, 2, 0], [ra] * 4, range(4)))
+    items = (_capi.PageCopy * 4)(*[_capi.PageCopy(ra, c, rb, 3 - c) for c in range(4)])
+    t.check(_capi.lib.tsb_l1_copy_chunks(l1.handle, items, 4, 0, 3, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = oracle.scatter_ref(shape, pool.slot_view(0, 6),
+                              ingest.items_numpy([5, 1, 2, 0, 0, 2, 1, 5], [ra] * 4 + [rb] * 4, [0, 1, 2, 3] * 2),
+                              l1.block_table(), l1.num_pages)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+    bad = (_capi.PageCopy * 1)(_capi.PageCopy(ra, 0, 7, 0))
+    with pytest.raises(t.ValidationError, match="outside the block table"):
+        t.check(_capi.lib.tsb_l1_copy_chunks(l1.handle, bad, 1, 0, 3, None))
