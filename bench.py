@@ -420,7 +420,7 @@ def timed_steps(torch, run, steps, dist, capi):
 
 
 def stage_pass(torch, wl, shape, pool, pool_seed, steps, warmup, l1_gib, layout=0, mode=None, dist=None,
-               policy=None, hbm_tier_pool=None, tier_chunks=0):
+               policy=None, hbm_tier_pool=None, tier_chunks=0, reuse_l1=False):
     """Warm-up (the first pass checks every page against the synthetic generator) + `steps` timed
     stage passes over the workload's batch on `pool`.  Returns a dict of the measurements and the
     L1 (the caller frees it)."""
@@ -442,7 +442,8 @@ def stage_pass(torch, wl, shape, pool, pool_seed, steps, warmup, l1_gib, layout=
     if hbm_tier_pool is not None and tier_chunks:
         stage.set_hbm_tier(hbm_tier_pool)
         slots = [[~s if k < tier_chunks else s for k, s in enumerate(sl)] for sl in wl.slots]
-    run = lambda verify=0: stage.run(wl.queue, slots, wl.config, policy=policy, mode=mode, verify_seed=verify)
+    run = lambda verify=0: stage.run(wl.queue, slots, wl.config, policy=policy, mode=mode, verify_seed=verify,
+                                     reuse_l1=reuse_l1)
     for i in range(warmup):
         r = run(pool_seed if i == 0 else 0)
         if i == 0 and r.stats["verify_mismatches"]:
@@ -451,7 +452,8 @@ def stage_pass(torch, wl, shape, pool, pool_seed, steps, warmup, l1_gib, layout=
     req = res.requests
     order = np.argsort(req["pick_position"])
     out = dict(dev_s=dev_s, wall_s=wall_s, bytes=float(res.stats["bytes"]), launches=int(launches), clocks=clk,
-               stats={k: res.stats[k] for k in ("ingest_calls", "deferred_chunks", "releases", "kernel_launches")},
+               stats={k: res.stats[k] for k in ("ingest_calls", "deferred_chunks", "releases", "kernel_launches",
+                                                "reused_chunks")},
                num_pages=num_pages, page=page, max_chunks=max_chunks,
                ttft={"first_layer_ms_p50": float(np.median(req["first_layer_ms"])),
                      "resident_ms_p50": float(np.median(req["resident_ms"])),
@@ -724,6 +726,24 @@ def run_ours(args):
                 "algorithmic_bytes": "payload read from the host pool once (local chunk bytes x chunks)",
                 "k2_hbm_frac": k2_roof["frac"]}
 
+    # ---- l1_reuse: the same step, chunks already resident in a live request's pages replicated
+    # HBM -> HBM (K8) instead of crossing the link again (not the headline) ----------------------
+    l1_reuse = None
+    if not args.no_l1_reuse:
+        del l1
+        torch.cuda.empty_cache()
+        rm, l1 = stage_pass(torch, wl, shape, pool, pool_seed, args.steps, min(args.warmup, 3), args.l1_gib,
+                            layout=ingest.LAYOUTS[args.layout], mode=ingest.MODES[args.mode], dist=dist, reuse_l1=True)
+        r_s, r_wall, r_bytes = reduce_timing(dist, rm["dev_s"], rm["wall_s"], rm["bytes"], device=coll_device(dist))
+        reused = rm["stats"]["reused_chunks"]
+        l1_reuse = {"value": args.steps * r_bytes / r_s / 1e9, "e2e": args.steps * r_bytes / r_wall / 1e9, "unit": UNIT,
+                    "ms_per_step": r_s / args.steps * 1e3, "reused_chunks_per_step": reused,
+                    "link_bytes_per_step": int(rm["bytes"] - reused * shape.local_chunk_bytes),
+                    "delivered_bytes_per_step": int(rm["bytes"]), "ttft_load_ms": rm["ttft"],
+                    "gpu_launches": rm["launches"],
+                    "source": "stage option reuse_l1: a chunk whose L2 slot is resident in a live request's pages is "
+                              "copied HBM -> HBM by K8 (tsb_l1_copy_chunks); every page verified in the warm-up"}
+
     # ---- hbm_tier: the same step with the pool in HBM (peer-HBM tier kernel path, K1) -----------
     hbm_tier = None
     if not args.no_hbm_tier:
@@ -772,6 +792,7 @@ def run_ours(args):
         "gpu_launches": m["launches"], "roofline": roofline, "roofline_k2": k2_roof,
         "host_link": {"achieved": link_rate, "peak": ce_peak, "frac": link_rate / ce_peak, "unit": UNIT},
         "ttft_load_ms": m["ttft"], "clocks": m["clocks"], "ingest_modes_2req": modes, "hbm_tier": hbm_tier,
+        "l1_reuse": l1_reuse,
     }
     if world == 1 and not args.no_side and args.workload == "qwen16x128k" and args.emulate_tp == 1:
         pool.close()
@@ -818,6 +839,7 @@ def main():
     ap.add_argument("--one-device", action="store_true",
                     help="validation: with --gpus N > 1, every rank on cuda:0 over gloo (not a measurement)")
     ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident-pool arm")
+    ap.add_argument("--no-l1-reuse", action="store_true", help="skip the reuse_l1 arm")
     ap.add_argument("--no-side", action="store_true", help="skip the configs[0]/[2]/[4] sub-lines")
     ap.add_argument("--cpu-chunks-per-request", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
