@@ -599,21 +599,29 @@ def queue_workload(torch, hbm_peak, n=100_000):
     api_us = (time.perf_counter() - t0) / 5 * 1e6
     res = {"config": "configs[4]", "requests": n, "queue_generation_s": gen_s,
            "gpu_score_order_us": gpu, "host_api_score_order_us": api_us}
-    # K3 over every context of the queue; token ids generated on the device (doc-id prefixes shared)
-    offs = np.zeros(n + 1, np.int64)
-    np.cumsum(q.context_tokens, out=offs[1:])
+    # K3 over every context of the queue; token ids generated on the device (doc-id prefixes shared).
+    # Requests sit at 16-byte-aligned starts (gaps of <= 3 tokens): the layout K3 reads with whole
+    # 16-byte vectors; the chunk counts come from the true lengths, so the hashes are the same.
+    offs = hasher.aligned_offsets(q.context_tokens)
     dev = torch.device("cuda", torch.cuda.current_device())
     d_offs = torch.from_numpy(offs).to(dev)
     doc = torch.from_numpy(np.random.default_rng(1).integers(0, 1000, n)).to(dev)
     sh = torch.from_numpy(q.context_tokens // 2).to(dev)
     tok = torch.empty(int(offs[-1]), dtype=torch.int32, device=dev)
     hasher.gen_tokens_device(0, d_offs, doc, sh, tok)
-    coff = torch.from_numpy(hasher.chunk_offsets(offs)).to(dev)
+    coff = torch.from_numpy(hasher.chunk_offsets_of_lengths(q.context_tokens)).to(dev)
     hout = torch.empty(int(coff[-1]), dtype=torch.int64, device=dev)
     secs = timed(lambda: hasher.hash_prefix_chunks_device(d_offs, tok, coff, hout), reps=10)
-    nbytes = tok.numel() * 4 + hout.numel() * 8
-    res["hash"] = {"tokens": int(offs[-1]), "chunks": int(coff[-1]), "ms": secs * 1e3, "GBps": nbytes / secs / 1e9,
-                   "hbm_copy_peak_frac": nbytes / secs / 1e9 / hbm_peak, "algorithmic_bytes": int(nbytes)}
+    p1 = timed(lambda: hasher.chunk_digests_device(d_offs, tok, coff, hout), reps=10)
+    hasher.hash_prefix_chunks_device(d_offs, tok, coff, hout)
+    ntok = int(q.context_tokens.sum())
+    nbytes = ntok * 4 + hout.numel() * 8
+    read_ceiling = 7410.0  # read-only HBM ceiling measured on this pool (profiles/r01_hbm_read_probe.jsonl)
+    res["hash"] = {"tokens": ntok, "chunks": int(coff[-1]), "ms": secs * 1e3, "GBps": nbytes / secs / 1e9,
+                   "read_ceiling_GBps": read_ceiling, "read_ceiling_frac": nbytes / secs / 1e9 / read_ceiling,
+                   "phase1_ms": p1 * 1e3, "phase1_read_ceiling_frac": nbytes / p1 / 1e9 / read_ceiling,
+                   "hbm_copy_peak_frac": nbytes / secs / 1e9 / hbm_peak, "algorithmic_bytes": int(nbytes),
+                   "layout": "16-byte-aligned request starts"}
     idx = hasher.PrefixIndex(capacity=1 << int(np.ceil(np.log2(2 * hout.numel()))))
     slots_t = torch.arange(hout.numel(), dtype=torch.int64, device=dev)
     ins_s = timed(lambda: idx.insert_device(hout, slots_t), reps=1, warm=0)

@@ -202,8 +202,13 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
 /* Prefix chunk hasher (K3).  Definition in oracle/tsb_oracle.c (orc_hash_prefix_chunks);   */
 /* the reference's only hash primitive is FNV-1a-64 (engine.cpp:500-534).                   */
 /* Request r owns tokens [offsets[r], offsets[r+1]) and writes floor(len/256) chained chunk */
-/* hashes at out[chunk_offsets[r] ...].                                                     */
+/* hashes at out[chunk_offsets[r] ...].  Device variants read only offsets[r] (the first     */
+/* token) and chunk_offsets (the full-chunk counts), so requests may sit at padded, 16-byte  */
+/* aligned starts with gaps between them: aligned leaves load as whole 16-byte vectors.      */
 /* ------------------------------------------------------------------------------------ */
+/* Phase 1 alone: each full chunk's own digest (no chain) at out[chunk_offsets[r] + c]. */
+tsb_status tsb_hash_chunk_digests_device(void* stream, int64_t n_req, const int64_t* offsets,
+                                         const int32_t* tokens, const int64_t* chunk_offsets, uint64_t* out);
 tsb_status tsb_hash_prefix_chunks_device(void* stream, int64_t n_req, const int64_t* offsets,
                                          const int32_t* tokens, const int64_t* chunk_offsets,
                                          uint64_t* out);

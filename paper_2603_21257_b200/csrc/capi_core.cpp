@@ -483,6 +483,14 @@ tsb_status tsb_hash_prefix_chunks_device(void* stream, int64_t n_req, const int6
   return TSB_OK;
 }
 
+tsb_status tsb_hash_chunk_digests_device(void* stream, int64_t n_req, const int64_t* offsets,
+                                         const int32_t* tokens, const int64_t* chunk_offsets, uint64_t* out) {
+  if (n_req < 0) return fail(TSB_VALIDATION, "hash_chunk_digests: n_req must be >= 0");
+  TSB_CUDA_TRY(tsb::launch_chunk_digests(n_req, offsets, tokens, chunk_offsets, out,
+                                         static_cast<cudaStream_t>(stream)));
+  return TSB_OK;
+}
+
 tsb_status tsb_hash_prefix_chunks(void* stream, int64_t n_req, const int64_t* offsets,
                                   const int32_t* tokens, uint64_t* out, int64_t* n_hashes) {
   auto st = static_cast<cudaStream_t>(stream);

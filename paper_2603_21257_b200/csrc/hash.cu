@@ -321,6 +321,14 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 
 }  // namespace
 
+cudaError_t launch_chunk_digests(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
+                                 const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
+  if (n_req == 0) return cudaSuccess;
+  k_chunk_digest<<<148 * 3, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;

@@ -44,6 +44,32 @@ def hash_prefix_chunks_device(offsets: torch.Tensor, tokens: torch.Tensor, coffs
     return out
 
 
+def chunk_digests_device(offsets: torch.Tensor, tokens: torch.Tensor, coffsets: torch.Tensor, out: torch.Tensor,
+                         stream=None) -> torch.Tensor:
+    """K3 phase 1 alone: every full chunk's own digest (tsb_hash_chunk_digests_device)."""
+    s = (stream or torch.cuda.current_stream()).cuda_stream
+    check(lib.tsb_hash_chunk_digests_device(s, coffsets.numel() - 1, offsets.data_ptr(), tokens.data_ptr(),
+                                            coffsets.data_ptr(), out.data_ptr()))
+    return out
+
+
+def aligned_offsets(lengths: np.ndarray, align_tokens: int = 4) -> np.ndarray:
+    """Request starts padded to `align_tokens` (4 int32 = 16 bytes) with gaps between requests:
+    the layout the device hasher reads fastest; chunk counts still come from the true lengths."""
+    lengths = np.asarray(lengths, np.int64)
+    padded = (lengths + align_tokens - 1) // align_tokens * align_tokens
+    offs = np.zeros(len(lengths) + 1, np.int64)
+    np.cumsum(padded, out=offs[1:])
+    return offs
+
+
+def chunk_offsets_of_lengths(lengths: np.ndarray) -> np.ndarray:
+    lengths = np.asarray(lengths, np.int64)
+    co = np.zeros(len(lengths) + 1, np.int64)
+    np.cumsum(lengths // 256, out=co[1:])
+    return co
+
+
 class PrefixIndex:
     """L2 chunk index on the GPU (K7): chained chunk hash -> L2 pool slot (tsb_index_*).
 

@@ -829,3 +829,32 @@ def test_scorer_empty_queue(scorer):
     q = t.QueueArrays(0)
     tl, tc, pr, order = scorer.score(q, t.PolicyKind.Fifo, t.CostModelPair(), t.ClusterConfig())
     assert len(order) == 0
+
+
+def test_hash_aligned_layout_and_phase1(oracle):
+    """K3 on a layout with 16-byte-aligned request starts (gaps between requests) gives the same
+    chained hashes as the packed layout; phase 1 alone gives the unchained chunk digests (the chain
+    of those digests equals the full hash)."""
+    rng = np.random.default_rng(12)
+    n = 300
+    lens = rng.integers(0, 3000, n)
+    lens[::7] = rng.integers(250, 260, len(lens[::7]))  # around one chunk
+    doc = rng.integers(0, 20, n)
+    shared = lens // 2
+    packed = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=packed[1:])
+    toks = oracle.gen_tokens(5, packed, doc, shared)
+    want = oracle.hash_prefix_chunks(packed, toks)
+    aligned = hasher.aligned_offsets(lens)
+    dev = torch.device("cuda")
+    d_off = torch.from_numpy(aligned).to(dev)
+    tok = torch.empty(int(aligned[-1]), dtype=torch.int32, device=dev)
+    hasher.gen_tokens_device(5, d_off, torch.from_numpy(doc).to(dev), torch.from_numpy(shared).to(dev), tok)
+    coff = torch.from_numpy(hasher.chunk_offsets_of_lengths(lens)).to(dev)
+    out = torch.empty(int(coff[-1]), dtype=torch.int64, device=dev)
+    hasher.hash_prefix_chunks_device(d_off, tok, coff, out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want)
+    dig = torch.empty_like(out)
+    hasher.chunk_digests_device(d_off, tok, coff, dig)
+    torch.cuda.synchronize()
+    assert not np.array_equal(dig.cpu().numpy(), out.cpu().numpy())  # unchained
