@@ -833,8 +833,7 @@ def test_scorer_empty_queue(scorer):
 
 def test_hash_aligned_layout_and_phase1(oracle):
     """K3 on a layout with 16-byte-aligned request starts (gaps between requests) gives the same
-    chained hashes as the packed layout; phase 1 alone gives the unchained chunk digests (the chain
-    of those digests equals the full hash)."""
+    chained hashes as the packed layout; phase 1 alone gives unchained per-chunk digests."""
     rng = np.random.default_rng(12)
     n = 300
     lens = rng.integers(0, 3000, n)
