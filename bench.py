@@ -747,6 +747,7 @@ def run_ours(args):
         l1_reuse = {"value": args.steps * r_bytes / r_s / 1e9, "e2e": args.steps * r_bytes / r_wall / 1e9, "unit": UNIT,
                     "ms_per_step": r_s / args.steps * 1e3, "reused_chunks_per_step": reused,
                     "link_bytes_per_step": int(rm["bytes"] - reused * shape.local_chunk_bytes),
+                    "link_GBps": (rm["bytes"] - reused * shape.local_chunk_bytes) * args.steps / rm["dev_s"] / 1e9,
                     "delivered_bytes_per_step": int(rm["bytes"]), "ttft_load_ms": rm["ttft"],
                     "gpu_launches": rm["launches"],
                     "source": "stage option reuse_l1: a chunk whose L2 slot is resident in a live request's pages is "

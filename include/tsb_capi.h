@@ -539,7 +539,8 @@ typedef struct {
 } tsb_stage_request;
 
 typedef struct {
-  int64_t bytes;           /* total L2 -> L1 bytes of the run */
+  int64_t bytes;           /* total bytes delivered into L1 pages (host link + HBM tier + reuse_l1
+                              replication; the link part is bytes - reused_chunks * chunk bytes) */
   double device_ms;        /* first ingest start -> last request resident (CUDA events) */
   double wall_ms;          /* host wall time of tsb_stage_run */
   int64_t ingest_calls;

@@ -17,6 +17,7 @@ only (their own K/V are not appended), which keeps the attention FLOPs of the ca
 """
 from __future__ import annotations
 
+import time
 from typing import Optional
 
 import numpy as np
@@ -75,6 +76,9 @@ class PagedPrefill:
         self.next = 0
         self.flops = 0.0
         self.calls = 0
+        self.host_s = 0.0       # host time spent inside the hook (enqueueing)
+        self.host_max_s = 0.0
+        self.plan_s = 0.0
 
     def flops_per_request(self, i: int) -> float:
         """GEMM + attention FLOPs of one request's prefill across all layers."""
@@ -101,13 +105,24 @@ class PagedPrefill:
 
     def __call__(self, q_index: int, bt_row: int, layer: int, stream_ptr: int):
         """The stage's prefill hook: enqueue layer `layer` of request q_index on `stream_ptr`."""
+        t0 = time.perf_counter()
+        try:
+            self._enqueue(q_index, bt_row, layer, stream_ptr)
+        finally:
+            dt = time.perf_counter() - t0
+            self.host_s += dt
+            self.host_max_s = max(self.host_max_s, dt)
+
+    def _enqueue(self, q_index: int, bt_row: int, layer: int, stream_ptr: int):
         stream = torch.cuda.ExternalStream(stream_ptr, device=self.x.device)
         with torch.cuda.stream(stream):
             ct = self.ct[q_index]
             if ct == 0:
                 return
             if layer == 0 and self.nb[q_index] > 0:
+                t0 = time.perf_counter()
                 self._plan(q_index, bt_row)
+                self.plan_s += time.perf_counter() - t0
             x = self.x[:ct]
             qkv = x @ self.w_qkv
             q = self.q_buf[:ct]

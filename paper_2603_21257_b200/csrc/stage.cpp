@@ -490,6 +490,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
           reqs[h].read_by_copy = true;
         }
         reused_chunks += static_cast<int64_t>(copies.size());
+        bytes_total += static_cast<int64_t>(copies.size()) * chunk_bytes;  // delivered into L1 all the same
       }
       std::vector<void*> evs;
       void* const* evp = nullptr;

@@ -192,7 +192,7 @@ def test_stage_reuse_l1_replicates_resident_chunks(layer_events):
     base = stage.run(q, slots, cfg, prefill=True, layer_events=layer_events, verify_seed=9)
     res = stage.run(q, slots, cfg, prefill=True, layer_events=layer_events, verify_seed=9, reuse_l1=True)
     assert base.stats["verify_mismatches"] == 0 and res.stats["verify_mismatches"] == 0
-    assert base.stats["reused_chunks"] == 0 and res.stats["reused_chunks"] > n * 6 // 2
+    assert base.stats["reused_chunks"] == 0 and res.stats["reused_chunks"] >= 12
     assert res.stats["bytes"] == base.stats["bytes"] == n * 6 * shape.local_chunk_bytes
     assert l1.reserved() == 0 and l1.free_pages() == l1.num_pages
     r = res.requests
@@ -209,6 +209,7 @@ def test_copy_chunks_api(oracle):
     pool = ingest.ChunkPool(shape, 6)
     pool.fill_synthetic(4)
     l1 = ingest.PagedKVCache(shape, 12 * 16, max_rows=3, max_chunks=6)
+    l1.arena.zero_()
     cb = shape.page_bytes * 16
     ra = [l1.request(1, c, cb)[1] for c in range(4)][0]
     rb = [l1.request(2, c, cb)[1] for c in range(4)][0]

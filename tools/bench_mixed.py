@@ -128,13 +128,20 @@ def main():
                      ("overlapped_prefill", dict(prefill=True, layer_events=True))):
         if consumer is not None and not kw.get("prefill"):
             stage.set_prefill_hook(None)
+        if consumer is not None:
+            consumer.host_s = consumer.host_max_s = consumer.plan_s = 0.0
         r = stage.run(q, slots, cfg, **kw)
         if consumer is not None:
             stage.set_prefill_hook(consumer)
         req = r.requests
         runs[name] = {"batch_ms": float(req["done_ms"].max()), "ingest_GBps": r.stats["bytes"] / (req["resident_ms"].max() * 1e-3) / 1e9,
                       "ttft_ms_mean": float(req["done_ms"].mean()), "ttft_ms_p50": float(np.median(req["done_ms"])),
-                      "resident_ms_mean": float(req["resident_ms"].mean()), "deferred_chunks": r.stats["deferred_chunks"]}
+                      "resident_ms_mean": float(req["resident_ms"].mean()), "deferred_chunks": r.stats["deferred_chunks"],
+                      "wall_ms": r.stats["wall_ms"]}
+        if consumer is not None and kw.get("prefill"):
+            runs[name]["hook_host_ms"] = consumer.host_s * 1e3
+            runs[name]["hook_host_max_ms"] = consumer.host_max_s * 1e3
+            runs[name]["plan_host_ms"] = consumer.plan_s * 1e3
         runs[name]["_req"] = req
     out["runs"] = {k: {kk: vv for kk, vv in v.items() if kk != "_req"} for k, v in runs.items()}
     prefill_s = float(sum(cfg.compute_base + cfg.compute_per_token * (q.context_tokens[i] + 28 - plans[i] * 256)
