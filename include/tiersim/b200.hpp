@@ -138,8 +138,18 @@ class LoadStage {
   };
   /// HBM tier (this GPU's or a peer's device pool): a slot s < 0 names slot ~s of it.
   void set_hbm_tier(ChunkPool* tier) { check(tsb_stage_set_hbm_tier(s_.get(), tier ? tier->handle() : nullptr)); }
+  /// Online mode: blocks start in an L3 host store and make the network hop L3 -> L2 for real into
+  /// this stage's pool, under TierLedger(L2) + a slot free list (engine.cpp:341-364, 405-425).
+  void set_l3(ChunkPool* l3, int copy_threads = 4) {
+    check(tsb_stage_set_l3(s_.get(), l3 ? l3->handle() : nullptr, copy_threads));
+  }
+  /// A real prefill consumer: hook(user, q_index, bt_row, layer, stream) enqueues one layer after
+  /// the stage made `stream` wait for that layer's fence (called from the stage's enqueue thread).
+  void set_prefill_hook(tsb_prefill_hook hook, void* user) { check(tsb_stage_set_prefill_hook(s_.get(), hook, user)); }
+  void set_compute_stream(void* stream) { check(tsb_stage_set_compute_stream(s_.get(), stream)); }
   /// slots[i][c] = pool slot of request i's planned chunk c (< 0: slot ~s of the HBM tier).
-  /// Real-time replay of arrivals with SimEngine's decoupled control loop (tsb_stage_run_online).
+  /// Real-time replay of arrivals with SimEngine's control loop under config.control_mode /
+  /// allocation_mode (tsb_stage_run_online).
   Result run_online(std::span<const RequestSpec> batch, const std::vector<std::vector<int64_t>>& slots,
                     const ClusterConfig& config, const CostModelPair& models, tsb_stage_options opt,
                     void* stream = nullptr) {

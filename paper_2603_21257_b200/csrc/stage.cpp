@@ -34,6 +34,8 @@
 #include <cstring>
 #include <ctime>
 #include <deque>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -113,6 +115,86 @@ class NetCopier {
   uint8_t* dst_ = nullptr;
   size_t bytes_ = 0;
   std::atomic<int> remaining_{0};
+};
+
+// The prefill enqueuer: a host thread of its own.  A real consumer's prefill is thousands of
+// kernel launches per batch (cuBLAS + attention per layer); enqueued from the dispatch thread they
+// fill the device's launch queue and block that thread, so the link would idle.  Here the stage
+// thread only posts "enqueue request i's prefill"; the worker does the waits on the per-layer
+// fences, the hook calls and the ComputeDone event, and marks the request enqueued (an event
+// queried before it is recorded would read as complete, so completions check the mark first).
+class PrefillWorker {
+ public:
+  PrefillWorker(int device, int64_t n) : device_(device), enqueued_(new std::atomic<uint8_t>[n]) {
+    for (int64_t i = 0; i < n; ++i) enqueued_[i].store(0);
+    th_ = std::thread([this] { loop(); });
+  }
+  ~PrefillWorker() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    th_.join();
+  }
+  void post(int64_t i, std::function<tsb_status()> job) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      jobs_.emplace_back(i, std::move(job));
+    }
+    cv_.notify_all();
+  }
+  bool enqueued(int64_t i) const { return enqueued_[i].load(std::memory_order_acquire) != 0; }
+  // Blocks until request i's prefill is enqueued (or the worker failed); returns the status.
+  tsb_status wait(int64_t i) {
+    std::unique_lock<std::mutex> g(m_);
+    done_cv_.wait(g, [&] { return enqueued(i) || status_ != TSB_OK; });
+    return status_ != TSB_OK ? fail(status_.load(), msg_) : TSB_OK;
+  }
+  // Blocks until every posted job ran; returns the first failure.
+  tsb_status drain() {
+    std::unique_lock<std::mutex> g(m_);
+    done_cv_.wait(g, [&] { return (jobs_.empty() && !busy_) || status_ != TSB_OK; });
+    return status_ != TSB_OK ? fail(status_.load(), msg_) : TSB_OK;
+  }
+  tsb_status status() const { return status_; }
+
+ private:
+  void loop() {
+    cudaSetDevice(device_);
+    for (;;) {
+      std::pair<int64_t, std::function<tsb_status()>> job;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || !jobs_.empty(); });
+        if (jobs_.empty()) return;  // stop requested and nothing left
+        job = std::move(jobs_.front());
+        jobs_.pop_front();
+        busy_ = true;
+      }
+      const tsb_status prev = status_.load();
+      const tsb_status st = prev == TSB_OK ? job.second() : prev;
+      {
+        std::lock_guard<std::mutex> g(m_);
+        busy_ = false;
+        if (st != TSB_OK && status_ == TSB_OK) {
+          status_ = st;
+          msg_ = tsb_last_error();
+        }
+        if (st == TSB_OK) enqueued_[job.first].store(1, std::memory_order_release);
+      }
+      done_cv_.notify_all();
+    }
+  }
+  int device_;
+  std::unique_ptr<std::atomic<uint8_t>[]> enqueued_;
+  std::thread th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  std::deque<std::pair<int64_t, std::function<tsb_status()>>> jobs_;
+  bool stop_ = false, busy_ = false;
+  std::atomic<tsb_status> status_{TSB_OK};
+  std::string msg_;
 };
 
 // Prefill duration of the reference compute stage (engine.cpp:190-212): the measured t_comp for
@@ -413,8 +495,12 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   uint64_t verify_mismatches = 0;
   std::vector<cudaEvent_t> call_events;  // trace only: one per ingest call
 
+  const bool with_prefill = opt->prefill || s->hook;
+  std::unique_ptr<PrefillWorker> worker;
+  if (with_prefill) worker = std::make_unique<PrefillWorker>(s->device, n);
+
   // Once a request's last chunk is dispatched: ev_first / ev_resident were recorded by that ingest
-  // call (or here for an empty plan); now the prefill and ev_done.
+  // call (or here for an empty plan); now the prefill (posted to the worker) and ev_done.
   auto finish_request_events = [&](int64_t i) -> tsb_status {
     ReqRt& r = reqs[i];
     const Plan& p = plans[i];
@@ -432,8 +518,14 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
           fences[l] = p.n_chunks ? s->layer_pool[static_cast<size_t>(i * L + l)] : s->layer_ev[l];
         if (L > 1) fences[L - 1] = r.ev_resident;
       }
-      TSB_TRY(enqueue_prefill(s, i, r.row, compute_seconds(q, i, c, p.compute_tokens), fences, ctas));
-      TSB_CUDA_TRY(cudaEventRecord(r.ev_done, s->compute));
+      const double secs = compute_seconds(q, i, c, p.compute_tokens);
+      const int32_t row_i = r.row;
+      cudaEvent_t ev_done = r.ev_done;
+      worker->post(i, [s, i, row_i, secs, fences, ctas, ev_done]() -> tsb_status {
+        TSB_TRY(enqueue_prefill(s, i, row_i, secs, fences, ctas));
+        TSB_CUDA_TRY(cudaEventRecord(ev_done, s->compute));
+        return TSB_OK;
+      });
     } else {
       TSB_CUDA_TRY(cudaEventRecord(r.ev_done, st));
     }
@@ -442,7 +534,6 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   };
 
   // pcie_dispatch (engine.cpp:427-446): serve granted chunks of admitted requests in pick order.
-  constexpr size_t kPrefillLag = 2;
   std::vector<int64_t> issued_last;
   if (opt->layer_events) TSB_TRY(grow_events(s->layer_pool, static_cast<size_t>(n * L), cudaEventDisableTiming));
   auto dispatch = [&]() -> tsb_status {
@@ -523,18 +614,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       }
       ++ingest_calls;
       bytes_total += static_cast<int64_t>(items.size()) * chunk_bytes;
-      if (last) {
-        issued_last.push_back(i);
-        // A request's prefill is enqueued once the ingest of the next kPrefillLag requests is
-        // queued too: a consumer hook runs on this host thread (planning, possibly waiting on its
-        // own resources) and the link must have work queued meanwhile.  Without prefill the
-        // request's completion is recorded right away.
-        const size_t lag = (opt->prefill || s->hook) ? kPrefillLag : 0;
-        while (issued_last.size() > lag) {
-          TSB_TRY(finish_request_events(issued_last.front()));
-          issued_last.erase(issued_last.begin());
-        }
-      }
+      if (last) issued_last.push_back(i);
     }
     for (const int64_t i : issued_last) TSB_TRY(finish_request_events(i));
     issued_last.clear();
@@ -565,6 +645,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   auto complete = [&](int64_t i) -> tsb_status {
     ReqRt& r = reqs[i];
     const Plan& p = plans[i];
+    if (worker) TSB_TRY(worker->wait(i));  // its ComputeDone event is recorded
     TSB_CUDA_TRY(cudaEventSynchronize(r.ev_done));
     if (opt->verify_seed && p.n_chunks > 0) {
       std::vector<tsb_ingest_item> items;
@@ -627,6 +708,8 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       status = complete(order[k]);
     }
   }
+  if (worker && status == TSB_OK) status = worker->drain();
+  worker.reset();  // joins: no hook runs after this call returns
   if (status != TSB_OK) {
     // Leave nothing in flight and no reservation held: drain both streams, then release every
     // request's L1 pages (the allocator returns to its pre-call state).
@@ -781,6 +864,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   int64_t net_blk = 0;
   double net_ready_at = 0.0;
 
+  PrefillWorker worker(s->device, n);  // the compute stage's enqueuer (see PrefillWorker)
   TSB_CUDA_TRY(cudaEventRecord(s->ev_start, st));
   const double host0 = now_s();
   auto now = [&] { return now_s() - host0; };
@@ -856,10 +940,14 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
       progress = true;
     }
     if (status != TSB_OK) break;
+    if ((status = worker.status()) != TSB_OK) {
+      status = worker.drain();
+      break;
+    }
     for (size_t k = admitted_head; k < admitted.size(); ++k) {  // ComputeDone (engine.cpp:274-283)
       const size_t i = admitted[k];
       Rt& r = R[i];
-      if (!r.started || r.finished || !done(r.ev_done)) continue;
+      if (!r.started || r.finished || !worker.enqueued(static_cast<int64_t>(i)) || !done(r.ev_done)) continue;
       r.finished = true;
       ++finished;
       --active;
@@ -1067,15 +1155,15 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
           row(4, 2, -1, plans[best].id, -1, 0);
           std::vector<cudaEvent_t> fences(static_cast<size_t>(L), nullptr);
           fences[0] = r.ev_resident;
-          if ((status = enqueue_prefill(s, static_cast<int64_t>(best), r.row,
-                                        opt->prefill || s->hook ? compute_seconds(q, best, c, plans[best].compute_tokens) : 0.0,
-                                        fences, ctas)) != TSB_OK)
-            break;
-          const cudaError_t e = cudaEventRecord(r.ev_done, s->compute);
-          if (e != cudaSuccess) {
-            status = tsb::cuda_fail(e, "stage: prefill done event");
-            break;
-          }
+          const double secs = opt->prefill || s->hook ? compute_seconds(q, best, c, plans[best].compute_tokens) : 0.0;
+          const int64_t bi = static_cast<int64_t>(best);
+          const int32_t row_i = r.row;
+          cudaEvent_t ev_done = r.ev_done;
+          worker.post(bi, [s, bi, row_i, secs, fences, ctas, ev_done]() -> tsb_status {
+            TSB_TRY(enqueue_prefill(s, bi, row_i, secs, fences, ctas));
+            TSB_CUDA_TRY(cudaEventRecord(ev_done, s->compute));
+            return TSB_OK;
+          });
           moved = true;
         }
       }
@@ -1099,6 +1187,10 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     }
   }
   // Drain: no copy thread, ingest or prefill may outlive the call (error paths included).
+  {
+    const tsb_status ws = worker.drain();
+    if (status == TSB_OK) status = ws;
+  }
   while (net_busy && !s->net->done()) {
     timespec ts{0, 20000};
     nanosleep(&ts, nullptr);

@@ -295,6 +295,33 @@ static void gpu_cases() {
       EXPECT(first && (p != PolicyKind::Lstf || first->id == 5000));
     }
   });
+  run("gpu: online stage with an L3 store, coupled + reactive, a C prefill hook", [] {
+    KvShape shape;
+    shape.layers = 4;
+    ChunkPool l3(shape, 12), l2(shape, 6);
+    check(tsb_pool_fill_synthetic(l3.handle(), 55, 0, 12, nullptr));
+    check(tsb_pool_fill_synthetic(l2.handle(), 1, 0, 6, nullptr));
+    PagedAllocator l1(0, shape, 8 * 16, 8, 8);
+    LoadStage stage(l1, l2);
+    stage.set_l3(&l3, 2);
+    static int calls = 0;
+    calls = 0;
+    stage.set_prefill_hook([](void*, int64_t, int32_t, int64_t, void*) -> int { return ++calls > 0 ? 0 : 1; }, nullptr);
+    ClusterConfig cfg;
+    cfg.bytes_per_token = kv_bytes_per_token(4, 8, 128, 2);
+    cfg.l2_capacity = 6 * 256 * cfg.bytes_per_token;
+    cfg.control_mode = ControlMode::Coupled;
+    cfg.allocation_mode = AllocationMode::Reactive;
+    std::vector<RequestSpec> batch = {spec(1, 0.0, 256 * 5), spec(2, 0.001, 256 * 4), spec(3, 0.002, 256 * 6)};
+    std::vector<std::vector<int64_t>> slots = {{0, 1, 2, 3, 4}, {7, 8, 9, 10}, {11, 5, 6, 0, 1, 2}};
+    tsb_stage_options opt{};
+    opt.mode = TSB_INGEST_AUTO;
+    opt.prefill = 1;
+    opt.verify_seed = 55;
+    const auto r = stage.run_online(batch, slots, cfg, cost_models_from_config(cfg), opt);
+    EXPECT(r.stats.verify_mismatches == 0 && r.stats.net_blocks == 15 && l1.reserved() == 0);
+    EXPECT(calls == 3 * 4);  // every layer of every request went through the hook
+  });
   run("gpu: prefix hasher", [] {
     std::vector<std::int64_t> off = {0, 600, 1112};
     std::vector<std::int32_t> tok(1112);
