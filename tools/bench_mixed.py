@@ -39,6 +39,41 @@ def mixed_batch(n, seed, block=256):
     return q
 
 
+def stage_overlap(req, layer_events):
+    """Device-clock spans from the stage's own CUDA events: ingest of request k is
+    [ingest_begin, resident]; its prefill runs on the one compute stream after the previous prefill,
+    from its first layer (layer-pipelined) or its residency (serial) to done.  Reports how long the
+    link and the prefill were busy at the same time, and how many prefills began before their own
+    request was fully resident (layer pipelining at work)."""
+    def union(iv):
+        out = []
+        for a, b in sorted(iv):
+            if out and a <= out[-1][1]:
+                out[-1] = (out[-1][0], max(out[-1][1], b))
+            else:
+                out.append((a, b))
+        return out
+
+    order = np.argsort(req["pick_position"], kind="stable")
+    ingest = [(float(r["ingest_begin_ms"]), float(r["resident_ms"])) for r in req if r["chunks"] > 0]
+    prefill, prev, early = [], 0.0, 0
+    for k in order:
+        r = req[k]
+        ready = float(r["first_layer_ms"] if layer_events else r["resident_ms"])
+        start = max(ready, prev)
+        prefill.append((start, float(r["done_ms"])))
+        early += int(start < float(r["resident_ms"]) - 1e-3)
+        prev = float(r["done_ms"])
+    ui, up = union(ingest), union(prefill)
+    both = 0.0
+    for a, b in ui:
+        for c, d in up:
+            both += max(0.0, min(b, d) - max(a, c))
+    return {"link_busy_ms": sum(b - a for a, b in ui), "prefill_busy_ms": sum(b - a for a, b in up),
+            "link_and_prefill_concurrent_ms": both, "prefills_started_before_own_residency": early,
+            "source": "stage CUDA events (ingest_begin / first_layer / resident / done per request)"}
+
+
 def timeline_summary(prof, path):
     """From a kineto (CUPTI) trace of one overlapped run: busy time of the ingest kernels (K2; the
     batched host->device copies are not reported as memcpy activity by CUPTI), of the prefill
@@ -143,6 +178,8 @@ def main():
             runs[name]["hook_host_max_ms"] = consumer.host_max_s * 1e3
             runs[name]["plan_host_ms"] = consumer.plan_s * 1e3
         runs[name]["_req"] = req
+        if kw.get("prefill"):
+            runs[name]["overlap"] = stage_overlap(req, kw.get("layer_events", False))
     out["runs"] = {k: {kk: vv for kk, vv in v.items() if kk != "_req"} for k, v in runs.items()}
     prefill_s = float(sum(cfg.compute_base + cfg.compute_per_token * (q.context_tokens[i] + 28 - plans[i] * 256)
                           for i in range(n)))
