@@ -534,7 +534,6 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
   };
 
   // pcie_dispatch (engine.cpp:427-446): serve granted chunks of admitted requests in pick order.
-  std::vector<int64_t> issued_last;
   if (opt->layer_events) TSB_TRY(grow_events(s->layer_pool, static_cast<size_t>(n * L), cudaEventDisableTiming));
   auto dispatch = [&]() -> tsb_status {
     bool synced = false;
@@ -614,10 +613,10 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
       }
       ++ingest_calls;
       bytes_total += static_cast<int64_t>(items.size()) * chunk_bytes;
-      if (last) issued_last.push_back(i);
+      // Completion right away: without prefill ev_done is recorded now; with prefill the request
+      // is posted to the enqueue thread, so this loop never waits on the consumer.
+      if (last) TSB_TRY(finish_request_events(i));
     }
-    for (const int64_t i : issued_last) TSB_TRY(finish_request_events(i));
-    issued_last.clear();
     return TSB_OK;
   };
 
