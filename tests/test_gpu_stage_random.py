@@ -81,6 +81,13 @@ def test_random_stage_runs_verify(seed):
     assert st == 0
     want = po.sort_order(pr, q.arrival, q.id)
     assert list(np.argsort(res.requests["pick_position"])) == list(want)
+    # the same batch with reuse_l1 (K8 replication from live holders) and a K6 prefill sharing the GPU
+    # (AUTO then resolves to CE-direct where the geometry allows)
+    res2 = stage.run(q, slot_lists, cfg, policy=policy, verify_seed=1000 + seed, reuse_l1=True, prefill=True,
+                     layer_events=bool(seed % 2))
+    assert res2.stats["verify_mismatches"] == 0, (seed, "reuse", layout)
+    assert res2.stats["bytes"] == res.stats["bytes"]
+    assert l1.reserved() == 0 and l1.free_pages() == num_pages
 
 
 @pytest.mark.parametrize("seed", range(12))
