@@ -203,25 +203,35 @@ def main():
 
     if po.ref() is not None:
         rate = runs["ingest_only"]["ingest_GBps"] * 1e9
-        sim_cfg = t.ClusterConfig(bytes_per_token=cfg.bytes_per_token, network_bandwidth=1e18, pcie_bandwidth=rate,
-                                  transfer_base_latency=0.0, l1_capacity=num_pages * shape.page_bytes,
-                                  l2_capacity=10**15, compute_base=cfg.compute_base,
-                                  compute_per_token=cfg.compute_per_token)
-        ttft = np.zeros(n)
-        mean = C.c_double()
-        models = t.cost_models_from_config(sim_cfg)
-        st = po.ref().ref_run_simulation(n, C.byref(po.queue_struct(q)), C.byref(po.cluster_struct(sim_cfg)), 0,
-                                         (C.c_double * 4)(models.load.slope, models.load.intercept,
-                                                          models.comp.slope, models.comp.intercept),
-                                         0, ttft.ctypes.data, C.byref(mean))
-        if st == 0:
+
+        def des(compute_base, compute_per_token):
+            sim_cfg = t.ClusterConfig(bytes_per_token=cfg.bytes_per_token, network_bandwidth=1e18, pcie_bandwidth=rate,
+                                      transfer_base_latency=0.0, l1_capacity=num_pages * shape.page_bytes,
+                                      l2_capacity=10**15, compute_base=compute_base, compute_per_token=compute_per_token)
+            ttft = np.zeros(n)
+            mean = C.c_double()
+            models = t.cost_models_from_config(sim_cfg)
+            st = po.ref().ref_run_simulation(n, C.byref(po.queue_struct(q)), C.byref(po.cluster_struct(sim_cfg)), 0,
+                                             (C.c_double * 4)(models.load.slope, models.load.intercept,
+                                                              models.comp.slope, models.comp.intercept),
+                                             0, ttft.ctypes.data, C.byref(mean))
+            if st != 0:
+                return {"error": po.ref().ref_last_error().decode()}
             real = runs["serial_prefill"]["_req"]["done_ms"] * 1e-3
             err = np.abs(real - ttft) / ttft
-            out["sim_vs_real"] = {"mode": "serial prefill vs DES (coupled stages per request are decoupled in both)",
-                                  "sim_mean_ttft_ms": mean.value * 1e3, "real_mean_ttft_ms": float(real.mean() * 1e3),
-                                  "mean_abs_rel_err": float(err.mean()), "max_abs_rel_err": float(err.max())}
-        else:
-            out["sim_vs_real"] = {"error": po.ref().ref_last_error().decode()}
+            return {"sim_mean_ttft_ms": mean.value * 1e3, "real_mean_ttft_ms": float(real.mean() * 1e3),
+                    "mean_abs_rel_err": float(err.mean()), "max_abs_rel_err": float(err.max()),
+                    "compute_model": [compute_base, compute_per_token]}
+
+        out["sim_vs_real"] = {"mode": "serial prefill vs DES (coupled stages per request are decoupled in both)",
+                              **des(cfg.compute_base, cfg.compute_per_token)}
+        if consumer is not None:
+            # the real consumer's own cost: fit (compute tokens, prefill seconds) of the serial run
+            from paper_2603_21257_b200 import calibrate
+
+            fit = t.fit_linear((x.tokens, x.seconds) for x in calibrate.compute_samples(runs["serial_prefill"]["_req"]))
+            out["sim_vs_real_calibrated"] = {"mode": "DES with T_comp fitted to this run's prefills (fit_linear)",
+                                             **des(fit.model.intercept, fit.model.slope)}
     print(json.dumps(out), flush=True)
 
 
