@@ -483,6 +483,12 @@ tsb_status tsb_hash_prefix_chunks_device(void* stream, int64_t n_req, const int6
   return TSB_OK;
 }
 
+tsb_status tsb_hash_set_grid(int ctas_per_sm) {
+  if (ctas_per_sm < 0 || ctas_per_sm > 8) return fail(TSB_VALIDATION, "hash_set_grid: 0..8 CTAs per SM");
+  tsb::set_hash_grid(ctas_per_sm);
+  return TSB_OK;
+}
+
 tsb_status tsb_hash_chunk_digests_device(void* stream, int64_t n_req, const int64_t* offsets,
                                          const int32_t* tokens, const int64_t* chunk_offsets, uint64_t* out) {
   if (n_req < 0) return fail(TSB_VALIDATION, "hash_chunk_digests: n_req must be >= 0");

@@ -182,7 +182,7 @@ __device__ __forceinline__ uint64_t tree16x2(uint64_t v0, uint64_t v1, int j) {
 
 // Rotating software pipeline of two rounds: the loads of round u + 2 are issued as soon as round
 // u has been folded, so a warp keeps 1-2 rounds (2 KiB each) in flight while it computes.
-__global__ void __launch_bounds__(kHashThreads, 3) k_chunk_digest(
+__global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
     int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
     const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -321,10 +321,14 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 
 }  // namespace
 
+// Phase-1 CTAs per SM (3 shipped; tsb_hash_set_grid for measurement).
+static int g_digest_ctas_per_sm = 3;
+void set_hash_grid(int ctas_per_sm) { g_digest_ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : 3; }
+
 cudaError_t launch_chunk_digests(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                  const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
-  k_chunk_digest<<<148 * 3, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  k_chunk_digest<<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
   return cudaGetLastError();
 }
@@ -334,7 +338,7 @@ cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int3
   if (n_req == 0) return cudaSuccess;
   // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
   // 3 CTAs of 8 warps per SM (4 measured no faster)
-  k_chunk_digest<<<148 * 3, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  k_chunk_digest<<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
   k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();
