@@ -206,9 +206,8 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
 /* token) and chunk_offsets (the full-chunk counts), so requests may sit at padded, 16-byte  */
 /* aligned starts with gaps between them: aligned leaves load as whole 16-byte vectors.      */
 /* ------------------------------------------------------------------------------------ */
-/* Measurement knob: phase-1 CTAs per SM (0 = default 3) and tree variant (0: shuffle tree on every
- * lane, 1: leaf digests staged in shared memory, one lane folds a chunk's tree). */
-tsb_status tsb_hash_set_grid(int ctas_per_sm, int variant);
+/* Measurement knob: phase-1 CTAs per SM (0 = default 3). */
+tsb_status tsb_hash_set_grid(int ctas_per_sm);
 /* Phase 1 alone: each full chunk's own digest (no chain) at out[chunk_offsets[r] + c]. */
 tsb_status tsb_hash_chunk_digests_device(void* stream, int64_t n_req, const int64_t* offsets,
                                          const int32_t* tokens, const int64_t* chunk_offsets, uint64_t* out);

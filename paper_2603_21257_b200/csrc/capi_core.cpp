@@ -483,10 +483,9 @@ tsb_status tsb_hash_prefix_chunks_device(void* stream, int64_t n_req, const int6
   return TSB_OK;
 }
 
-tsb_status tsb_hash_set_grid(int ctas_per_sm, int variant) {
+tsb_status tsb_hash_set_grid(int ctas_per_sm) {
   if (ctas_per_sm < 0 || ctas_per_sm > 8) return fail(TSB_VALIDATION, "hash_set_grid: 0..8 CTAs per SM");
-  if (variant < 0 || variant > 1) return fail(TSB_VALIDATION, "hash_set_grid: variant 0 or 1");
-  tsb::set_hash_grid(ctas_per_sm, variant);
+  tsb::set_hash_grid(ctas_per_sm);
   return TSB_OK;
 }
 

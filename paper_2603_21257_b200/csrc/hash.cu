@@ -182,7 +182,6 @@ __device__ __forceinline__ uint64_t tree16x2(uint64_t v0, uint64_t v1, int j) {
 
 // Rotating software pipeline of two rounds: the loads of round u + 2 are issued as soon as round
 // u has been folded, so a warp keeps 1-2 rounds (2 KiB each) in flight while it computes.
-template <bool kLaneTree>
 __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
     int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
     const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
@@ -203,11 +202,6 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
   cur.cb = chunk_offsets[cur.r];
   cur.nb = chunk_offsets[cur.r + 1];
   cur.tb = offsets[cur.r];
-  // kLaneTree: leaf digests of 32 chunks are staged in shared memory ([chunk][leaf], rows padded
-  // to 18 words: conflict-free 8-byte writes by half-warps and 16-byte row reads by lanes), then
-  // lane k folds chunk k's 4-level tree alone -- 15 pairs per chunk in one lane instead of four
-  // shuffle levels on every lane.
-  __shared__ __align__(16) uint64_t dig[kLaneTree ? kHashWarps : 1][32][18];
   Leaf f[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
@@ -217,8 +211,7 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
       load_leaf(tokens + base + j * 4, f[u]);
     }
   }
-  int g = 0;
-  for (int64_t c = first; c < c_end; c += kStride, ++g) {
+  for (int64_t c = first; c < c_end; c += kStride) {
     uint64_t v[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -229,35 +222,9 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
         load_leaf(tokens + base + j * 4, f[u]);
       }
     }
-    if (!kLaneTree) {
-      const uint64_t d = tree16x2(v[0], v[1], j);
-      const int64_t cc = c + 2 * j + half;  // lane 0: round 0's chunk, lane 1: round 1's
-      if (j < 2 && cc < c_end) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
-    } else {
-      const int gs = g & 7;  // this group's 4 slots: 4*gs + 2u + half
-      dig[w][4 * gs + half][j] = v[0];
-      dig[w][4 * gs + 2 + half][j] = v[1];
-      if (gs == 7 || c + kStride >= c_end) {  // 32 chunks staged (or the warp's last group)
-        __syncwarp();
-        const int64_t ck = (c - gs * kStride) + (lane >> 2) * kStride + (lane & 3);
-        if ((lane >> 2) <= gs && ck < c_end) {
-          uint64_t t[16];
-          const ulonglong2* row = reinterpret_cast<const ulonglong2*>(dig[w][lane]);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const ulonglong2 x = row[q];
-            t[2 * q] = x.x;
-            t[2 * q + 1] = x.y;
-          }
-#pragma unroll
-          for (int width = 16; width > 1; width >>= 1)
-#pragma unroll
-            for (int i = 0; i < width / 2; ++i) t[i] = fpair(t[2 * i], t[2 * i + 1]);
-          st_evict_last(out + ck, t[0]);
-        }
-        __syncwarp();
-      }
-    }
+    const uint64_t d = tree16x2(v[0], v[1], j);
+    const int64_t cc = c + 2 * j + half;  // lane 0: round 0's chunk, lane 1: round 1's
+    if (j < 2 && cc < c_end) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
   }
 }
 
@@ -356,19 +323,12 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 
 // Phase-1 CTAs per SM (3 shipped; tsb_hash_set_grid for measurement).
 static int g_digest_ctas_per_sm = 3;
-static int g_digest_variant = 0;  // 0: shuffle tree on every lane, 1: lane-per-chunk tree
-void set_hash_grid(int ctas_per_sm, int variant) {
-  g_digest_ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : 3;
-  g_digest_variant = variant;
-}
+void set_hash_grid(int ctas_per_sm) { g_digest_ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : 3; }
 
 cudaError_t launch_chunk_digests(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                  const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
-  if (g_digest_variant == 1)
-    k_chunk_digest<true><<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
-  else
-    k_chunk_digest<false><<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  k_chunk_digest<<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
   return cudaGetLastError();
 }
@@ -378,10 +338,7 @@ cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int3
   if (n_req == 0) return cudaSuccess;
   // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
   // 3 CTAs of 8 warps per SM (4 measured no faster)
-  if (g_digest_variant == 1)
-    k_chunk_digest<true><<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
-  else
-    k_chunk_digest<false><<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
+  k_chunk_digest<<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
   count_launch();
   k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
   count_launch();

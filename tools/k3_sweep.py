@@ -49,18 +49,18 @@ def main():
         hasher.gen_tokens_device(0, d_offs, doc, sh, tok)
         out = torch.empty(int(coff[-1]), dtype=torch.int64, device=dev)
         nbytes = int(lens.sum()) * 4 + out.numel() * 8
-        for cps, var in ((3, 0), (4, 0), (3, 1), (4, 1), (2, 1)):
-            t.check(_capi.lib.tsb_hash_set_grid(cps, var))
+        for cps in (2, 3, 4):
+            t.check(_capi.lib.tsb_hash_set_grid(cps))
             p1 = timed(lambda: hasher.chunk_digests_device(d_offs, tok, coff, out))
             full = timed(lambda: hasher.hash_prefix_chunks_device(d_offs, tok, coff, out))
             h = out.cpu().numpy()
             ref = h if ref is None else ref
-            print(json.dumps({"layout": layout, "ctas_per_sm": cps, "tree": ["shuffle", "lane"][var], "phase1_ms": p1 * 1e3, "total_ms": full * 1e3,
+            print(json.dumps({"layout": layout, "ctas_per_sm": cps, "phase1_ms": p1 * 1e3, "total_ms": full * 1e3,
                               "phase1_read_ceiling_frac": nbytes / p1 / 1e9 / CEIL,
                               "total_read_ceiling_frac": nbytes / full / 1e9 / CEIL,
                               "hashes_equal_first_case": bool(np.array_equal(h, ref))}), flush=True)
         del tok
-    t.check(_capi.lib.tsb_hash_set_grid(0, 0))
+    t.check(_capi.lib.tsb_hash_set_grid(0))
 
 
 if __name__ == "__main__":
