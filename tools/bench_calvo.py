@@ -48,7 +48,7 @@ def main():
     ap.add_argument("--n", type=int, default=60)
     ap.add_argument("--qps", type=float, default=6.0)
     ap.add_argument("--net-gbps", type=float, default=25.0)
-    ap.add_argument("--l2-slots", type=int, default=96)
+    ap.add_argument("--l2-slots", type=int, default=320)
     ap.add_argument("--l1-gib", type=int, default=24)
     ap.add_argument("--compute-per-token", type=float, default=4e-6)
     ap.add_argument("--seed", type=int, default=1)
@@ -59,10 +59,10 @@ def main():
     bpt = t.kv_bytes_per_token(32, 8, 128, 2)
     q = t.generate_queue(t.WorkloadSpec(t.builtin_profile("loogle"), qps=args.qps, count=args.n, seed=args.seed,
                                         hit_ratio_source=t.HitRatioSource.uniform_choice([0.25, 0.5, 0.75, 1.0])))
-    q.context_tokens[:] = np.minimum(q.context_tokens, 96 * 1024)
+    q.context_tokens[:] = np.minimum(q.context_tokens, 64 * 1024)
     plans = [int(np.floor(q.context_tokens[i] * q.cache_hit_ratio[i] / 256)) for i in range(q.n)]
-    # L3: 16 documents of up to max-plan chunks; request i reads a prefix of document i % 16
-    n_docs, doc_len = 16, max(plans) + 1
+    # L3: 6 documents of up to max-plan chunks; request i reads a prefix of document i % 6
+    n_docs, doc_len = 6, max(plans) + 1
     l3 = ingest.ChunkPool(shape, n_docs * doc_len)
     l3.fill_synthetic(11)
     slots = [list(range((i % n_docs) * doc_len, (i % n_docs) * doc_len + nb)) for i, nb in enumerate(plans)]
@@ -87,7 +87,7 @@ def main():
     t.assign_slos_queue(q, box, [2.0, 4.0, 8.0], 7)
     dl = q.deadline - q.arrival
     out = {"workload": f"{q.n} LooGLE-profile requests (generate_workload seed {args.seed}), {args.qps} QPS, hits "
-                       "{0.25,0.5,0.75,1.0}, 16 shared documents in L3, Llama-3.1-8B KV",
+                       "{0.25,0.5,0.75,1.0}, contexts capped at 64K, 6 shared documents in L3, Llama-3.1-8B KV",
            "tiers": {"l3_to_l2": f"host copy threads paced to {args.net_gbps} GB/s", "l2_slots": args.l2_slots,
                      "l1_gib": args.l1_gib, "l2_to_l1_measured_GBps": link / 1e9},
            "compute": f"K6 {args.compute_per_token:g} s/token + 2 ms", "runs": {}}
