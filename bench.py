@@ -254,6 +254,37 @@ def measure_k2(torch, l1, shape, n_items=128, reps=20):
     return 2 * n_items * n_layers * local_layer, avg_s
 
 
+def measure_k8(torch, l1, shape, n_items, reps=10):
+    """K8 (tsb_l1_copy_chunks, HBM -> HBM chunk replication) timed alone with CUDA events: n_items
+    chunks of one row copied into another row, all layers; algorithmic bytes = read + write."""
+    from paper_2603_21257_b200 import _capi
+    from paper_2603_21257_b200.tiersim import check
+
+    cb = shape.page_bytes * shape.pages_per_chunk
+    ra = rb = -1
+    for c in range(n_items):
+        g, ra = l1.request((1 << 40) + 2, c, cb)
+        assert g
+    for c in range(n_items):
+        g, rb = l1.request((1 << 40) + 3, c, cb)
+        assert g
+    l1.sync_block_table()
+    items = (_capi.PageCopy * n_items)(*[_capi.PageCopy(ra, c, rb, c) for c in range(n_items)])
+    s = torch.cuda.current_stream()
+    launch = lambda: check(_capi.lib.tsb_l1_copy_chunks(l1.handle, items, n_items, 0, shape.layers, s.cuda_stream))
+    for _ in range(3):
+        launch()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(reps):
+        launch()
+    b.record(s)
+    b.synchronize()
+    l1.release_request((1 << 40) + 3)
+    l1.release_request((1 << 40) + 2)
+    return 2 * n_items * shape.local_chunk_bytes, a.elapsed_time(b) * 1e-3 / reps
+
+
 def measure_k1_hbm(torch, l1, pool, shape, n_items, reps=10):
     """K1 (k_ingest_ldg, HBM grid) reading the HBM-resident pool, timed alone with CUDA events:
     layers [1, L) of a request's n_items chunks; algorithmic bytes = read + write of the payload."""
@@ -744,12 +775,19 @@ def run_ours(args):
                             layout=ingest.LAYOUTS[args.layout], mode=ingest.MODES[args.mode], dist=dist, reuse_l1=True)
         r_s, r_wall, r_bytes = reduce_timing(dist, rm["dev_s"], rm["wall_s"], rm["bytes"], device=coll_device(dist))
         reused = rm["stats"]["reused_chunks"]
+        k8_items = max(1, min(rm["max_chunks"], rm["num_pages"] // (2 * shape.pages_per_chunk)))
+        k8_alg, k8_s = measure_k8(torch, l1, shape, k8_items)
+        hbm_peak8, _ = measured_peaks()
         l1_reuse = {"value": args.steps * r_bytes / r_s / 1e9, "e2e": args.steps * r_bytes / r_wall / 1e9, "unit": UNIT,
                     "ms_per_step": r_s / args.steps * 1e3, "reused_chunks_per_step": reused,
                     "link_bytes_per_step": int(rm["bytes"] - reused * shape.local_chunk_bytes),
                     "link_GBps": (rm["bytes"] - reused * shape.local_chunk_bytes) * args.steps / rm["dev_s"] / 1e9,
                     "delivered_bytes_per_step": int(rm["bytes"]), "ttft_load_ms": rm["ttft"],
                     "gpu_launches": rm["launches"],
+                    "roofline_k8": {"bound": "hbm", "kernel": "k_page_copy (K8: chunk replication inside L1)",
+                                    "achieved": k8_alg / k8_s / 1e9, "peak": hbm_peak8, "unit": "GB/s",
+                                    "frac": k8_alg / k8_s / 1e9 / hbm_peak8, "algorithmic_bytes_per_launch": int(k8_alg),
+                                    "launch_us": k8_s * 1e6, "chunks_per_launch": k8_items},
                     "source": "stage option reuse_l1: a chunk whose L2 slot is resident in a live request's pages is "
                               "copied HBM -> HBM by K8 (tsb_l1_copy_chunks); every page verified in the warm-up"}
 
