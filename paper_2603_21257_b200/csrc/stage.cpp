@@ -391,8 +391,9 @@ tsb_status make_plans(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_clu
   plans->assign(static_cast<size_t>(n), Plan{});
   const int64_t l1_capacity = tsb_l1_capacity(s->l1);
   const int64_t src_slots = tsb_pool_slots(use_l3 ? s->l3 : s->pool);
-  int64_t l2_capacity = 0;
-  if (use_l3) l2_capacity = std::min<int64_t>(c->l2_capacity / chunk_bytes, tsb_pool_slots(s->pool)) * chunk_bytes;
+  // L2 (L3 mode) is counted in whole pool slots, as the online stage's TierLedger(L2) grants them
+  int64_t l2_slots = 0;
+  if (use_l3) l2_slots = std::min<int64_t>(c->l2_capacity / tsb_pool_chunk_bytes(s->pool), tsb_pool_slots(s->pool));
   for (int64_t i = 0; i < n; ++i) {
     int64_t cached = 0, compute = 0, nb = 0, bt = 0, bb = 0;
     TSB_TRY(tsb_derive_block_plan(q, i, c, &cached, &compute, &nb, &bt, &bb));
@@ -412,7 +413,7 @@ tsb_status make_plans(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_clu
       const bool ok = sl >= 0 ? sl < src_slots : (s->hbm_pool && ~sl < tsb_pool_slots(s->hbm_pool));
       if (!ok) return fail(TSB_VALIDATION, "stage: pool slot out of range");
     }
-    if (nb * chunk_bytes > l1_capacity || (use_l3 && nb * chunk_bytes > l2_capacity))
+    if (nb * chunk_bytes > l1_capacity || (use_l3 && nb > l2_slots))
       return fail(TSB_CAPACITY, "request " + std::to_string(r.id) + ": " +
                                     std::to_string(nb * chunk_bytes) +
                                     " resident bytes can never fit");
