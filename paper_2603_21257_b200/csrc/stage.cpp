@@ -1067,7 +1067,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
           net_req = i;
           net_blk = bi;
           const double pace = opt->pace_network
-                                  ? c->transfer_base_latency + static_cast<double>(chunk_bytes) / c->network_bandwidth
+                                  ? c->transfer_base_latency + static_cast<double>(l2_slot_bytes) / c->network_bandwidth
                                   : 0.0;
           net_ready_at = now() + pace;
           s->net->post(static_cast<const uint8_t*>(tsb_pool_slot_ptr(s->l3, plans[i].slots[bi])),
