@@ -24,17 +24,10 @@ from paper_2603_21257_b200.scorer import BatchScorer, DeviceQueue  # noqa: E402
 
 
 def loogle_queue(n, seed):
-    """LooGLE-like lengths (lognormal mean 28100 / cv 0.5; query mean 28), Poisson arrivals,
-    hits from {0.25..1.0}, deadlines = arrival + factor x (2 ms + 40 us/token)."""
-    rng = np.random.default_rng(seed)
-    sig = np.sqrt(np.log1p(0.25))
-    ctx = np.maximum(1, np.round(np.exp(np.log(28100) - 0.5 * sig**2 + sig * rng.standard_normal(n)))).astype(np.int64)
-    qry = np.maximum(1, np.round(np.exp(np.log(28) - 0.5 * sig**2 + sig * rng.standard_normal(n)))).astype(np.int64)
-    arr = np.cumsum(np.maximum(rng.exponential(1.0, n), 1e-6))
-    hit = rng.choice([0.25, 0.5, 0.75, 0.9, 1.0], n)
-    dl = arr + rng.choice([2.0, 4.0, 8.0], n) * (2e-3 + 4e-5 * ctx)
-    return t.QueueArrays(n, id=np.arange(1, n + 1), arrival=arr, context_tokens=ctx, query_tokens=qry,
-                         cache_hit_ratio=hit, flags=np.ones(n, np.uint8), deadline=dl)
+    """generate_workload(loogle, n, seed) -- the product's own generator, bit-identical to the
+    reference's (workload.cpp:70-99) -- with assign_slos {2, 4, 8} deadlines (workload.cpp:117-135)."""
+    q = t.generate_queue(t.WorkloadSpec(t.builtin_profile("loogle"), qps=1.0, count=n, seed=seed))
+    return t.assign_slos_queue(q, t.ClusterConfig(l1_capacity=10**13, l2_capacity=10**13), [2.0, 4.0, 8.0], seed)
 
 
 def timed(fn, reps=20, warm=3):
