@@ -161,6 +161,7 @@ _decl("tsb_hash_prefix_chunks_device", st, vp, i64, vp, vp, vp, vp)
 _decl("tsb_hash_prefix_chunks", st, vp, i64, vp, vp, vp, P(i64))
 _decl("tsb_hash_chunk_digests_device", st, vp, i64, vp, vp, vp, vp)
 _decl("tsb_hash_set_grid", st, C.c_int)
+_decl("tsb_hash_set_tuning", st, C.c_int, C.c_int)
 _decl("tsb_gen_tokens_device", st, vp, u64, i64, vp, vp, vp, vp)
 _decl("tsb_index_create", st, C.c_int, i64, P(vp))
 _decl("tsb_index_destroy", None, vp)

@@ -489,6 +489,14 @@ tsb_status tsb_hash_set_grid(int ctas_per_sm) {
   return TSB_OK;
 }
 
+tsb_status tsb_hash_set_tuning(int prefetch_groups, int fused_chain) {
+  if (prefetch_groups < -1 || prefetch_groups > 64) return fail(TSB_VALIDATION, "hash_set_tuning: prefetch 0..64 groups");
+  if (fused_chain < -1 || fused_chain > 1) return fail(TSB_VALIDATION, "hash_set_tuning: fused_chain 0 or 1");
+  if (prefetch_groups >= 0) tsb::set_hash_prefetch(prefetch_groups);
+  if (fused_chain >= 0) tsb::set_hash_fused(fused_chain);
+  return TSB_OK;
+}
+
 tsb_status tsb_hash_chunk_digests_device(void* stream, int64_t n_req, const int64_t* offsets,
                                          const int32_t* tokens, const int64_t* chunk_offsets, uint64_t* out) {
   if (n_req < 0) return fail(TSB_VALIDATION, "hash_chunk_digests: n_req must be >= 0");

@@ -180,20 +180,38 @@ __device__ __forceinline__ uint64_t tree16x2(uint64_t v0, uint64_t v1, int j) {
   return v;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Per-lane request search (one-time, for the prefetch cursor): first r with co[r + 1] > c.
+__device__ __forceinline__ int64_t lane_request_of(const int64_t* __restrict__ co, int64_t n_req,
+                                                   int64_t c) {
+  int64_t lo = 0, hi = n_req;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (co[mid] <= c) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 // Rotating software pipeline of two rounds: the loads of round u + 2 are issued as soon as round
-// u has been folded, so a warp keeps 1-2 rounds (2 KiB each) in flight while it computes.
-__global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
-    int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
-    const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out) {
+// u has been folded, so a warp keeps 1-2 rounds (2 KiB each) in flight while it computes.  With
+// pf > 0 every lane also prefetches one 128-byte line of the warp's group pf iterations ahead
+// into L2 (32 lines = the group's 4 chunks), so the loads hit L2 and more bytes are in flight
+// than the registers hold.
+template <bool kPf>
+__device__ __forceinline__ void digest_range(int64_t n_req, const int64_t* __restrict__ offsets,
+                                             const int32_t* __restrict__ tokens,
+                                             const int64_t* __restrict__ chunk_offsets,
+                                             uint64_t* __restrict__ out, int pf, int64_t total,
+                                             int64_t c_begin, int64_t c_end) {
   const int lane = threadIdx.x & 31;
   const int half = lane >> 4, j = lane & 15;
-  const int64_t total = chunk_offsets[n_req];
   // The CTA owns a contiguous, equal share of the chunk space; its 8 warps interleave over it in
   // groups of 4 chunks (2 rounds x 2 half-warps), so each CTA streams one region with all its
   // warps on adjacent addresses.
   const int w = threadIdx.x >> 5;
-  const int64_t c_begin = total * blockIdx.x / gridDim.x;
-  const int64_t c_end = total * (blockIdx.x + 1) / gridDim.x;
   const int64_t first = c_begin + 4 * w;
   if (first >= c_end) return;
   constexpr int64_t kStride = 4 * kHashWarps;  // chunks between a warp's consecutive groups
@@ -202,6 +220,16 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
   cur.cb = chunk_offsets[cur.r];
   cur.nb = chunk_offsets[cur.r + 1];
   cur.tb = offsets[cur.r];
+  // prefetch cursor: lane l covers line (l & 7) of chunk (l >> 3) of the group pf iterations on
+  const int64_t pf_off = static_cast<int64_t>(pf) * kStride + (lane >> 3);
+  ReqCursor pcur;
+  if (kPf) {
+    const int64_t pc = min(first + pf_off, total - 1);
+    pcur.r = lane_request_of(chunk_offsets, n_req, pc);
+    pcur.cb = chunk_offsets[pcur.r];
+    pcur.nb = chunk_offsets[pcur.r + 1];
+    pcur.tb = offsets[pcur.r];
+  }
   Leaf f[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
@@ -212,6 +240,10 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
     }
   }
   for (int64_t c = first; c < c_end; c += kStride) {
+    if (kPf) {
+      const int64_t pc = c + pf_off;
+      if (pc < c_end) prefetch_l2(tokens + pcur.base_of(pc, chunk_offsets, offsets) + (lane & 7) * 32);
+    }
     uint64_t v[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -224,7 +256,230 @@ __global__ void __launch_bounds__(kHashThreads, 4) k_chunk_digest(
     }
     const uint64_t d = tree16x2(v[0], v[1], j);
     const int64_t cc = c + 2 * j + half;  // lane 0: round 0's chunk, lane 1: round 1's
-    if (j < 2 && cc < c_end) st_evict_last(out + cc, d);  // keep digests in L2 for k_chain
+    if (j < 2 && cc < c_end) st_evict_last(out + cc, d);  // keep digests in L2 for the chain
+  }
+}
+
+template <bool kPf>
+__global__ void __launch_bounds__(kHashThreads, 3) k_chunk_digest(
+    int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
+    const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out, int pf) {
+  const int64_t total = chunk_offsets[n_req];
+  const int64_t c_begin = total * blockIdx.x / gridDim.x;
+  const int64_t c_end = total * (blockIdx.x + 1) / gridDim.x;
+  digest_range<kPf>(n_req, offsets, tokens, chunk_offsets, out, pf, total, c_begin, c_end);
+}
+
+// ---- Phases 1 + 2 in one kernel -------------------------------------------------------------
+// The CTA's 8 digest warps hand each iteration's 32 consecutive digests to a 9th warp through a
+// shared-memory ring (an mbarrier pair per slot, 16 slots); the chain warp folds them into the
+// per-request chain in chunk order while the digest warps stream on, and writes the chained
+// hashes (one coalesced 256-byte store per iteration).  A request that began in an earlier CTA's
+// range has no known chain value there, so its digests are written raw; k_chain_tail continues
+// those few requests (at most one per range boundary) from the chained value the previous CTA
+// wrote at its range end.
+constexpr int kRing = 16;
+constexpr int kFusedThreads = kHashThreads + 32;
+constexpr uint64_t kChainInit = (kFnvOffset << 32) | (kFnvOffset >> 32);
+
+// ring slot s: full[s] completes when the 8 digest warps have written it (one arrival each),
+// empty[s] when the chain warp has consumed it; parity = (iteration / kRing) & 1.
+struct RingBars {
+  uint64_t full[kRing];
+  uint64_t empty[kRing];
+};
+
+template <bool kPf>
+__device__ __forceinline__ void digest_warp_ring(int64_t n_req, const int64_t* __restrict__ offsets,
+                                                 const int32_t* __restrict__ tokens,
+                                                 const int64_t* __restrict__ chunk_offsets, int pf,
+                                                 int64_t total, int64_t c_begin, int64_t c_end,
+                                                 int64_t iters, uint64_t (*ring)[32],
+                                                 RingBars& bars) {
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4, j = lane & 15;
+  const int w = threadIdx.x >> 5;
+  constexpr int64_t kStride = 4 * kHashWarps;
+  const int64_t first = c_begin + 4 * w;
+  const bool any = first < c_end;
+  ReqCursor cur, pcur;
+  const int64_t pf_off = static_cast<int64_t>(pf) * kStride + (lane >> 3);
+  Leaf f[2];
+  if (any) {
+    cur.r = warp_upper_bound(chunk_offsets, n_req + 1, first) - 1;
+    cur.cb = chunk_offsets[cur.r];
+    cur.nb = chunk_offsets[cur.r + 1];
+    cur.tb = offsets[cur.r];
+    if (kPf) {
+      const int64_t pc = min(first + pf_off, total - 1);
+      pcur.r = lane_request_of(chunk_offsets, n_req, pc);
+      pcur.cb = chunk_offsets[pcur.r];
+      pcur.nb = chunk_offsets[pcur.r + 1];
+      pcur.tb = offsets[pcur.r];
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t cc = first + 2 * u + half;
+      if (cc < c_end) load_leaf(tokens + cur.base_of(cc, chunk_offsets, offsets) + j * 4, f[u]);
+    }
+  }
+  for (int64_t i = 0; i < iters; ++i) {
+    const int64_t c = first + i * kStride;
+    const int slot = static_cast<int>(i % kRing);
+    uint64_t d = 0;
+    if (c < c_end) {
+      if (kPf) {
+        const int64_t pc = c + pf_off;
+        if (pc < c_end) prefetch_l2(tokens + pcur.base_of(pc, chunk_offsets, offsets) + (lane & 7) * 32);
+      }
+      uint64_t v[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        v[u] = fold_leaf(f[u]);
+        const int64_t nc = c + 2 * u + half + kStride;
+        if (nc < c_end) load_leaf(tokens + cur.base_of(nc, chunk_offsets, offsets) + j * 4, f[u]);
+      }
+      d = tree16x2(v[0], v[1], j);
+    }
+    if (i >= kRing) mbar_wait(&bars.empty[slot], static_cast<uint32_t>((i / kRing - 1) & 1));
+    if (j < 2) ring[slot][4 * w + 2 * j + half] = d;  // chunk c + 2j + half of this iteration
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars.full[slot]);
+  }
+}
+
+__device__ __forceinline__ void chain_warp_ring(int64_t n_req, const int64_t* __restrict__ co,
+                                                uint64_t* __restrict__ out, int64_t c_begin,
+                                                int64_t c_end, int64_t iters,
+                                                uint64_t (*ring)[32], RingBars& bars) {
+  const int lane = threadIdx.x & 31;
+  int64_t r = 0, nb = 0, nnb = 0;
+  bool active = false;
+  if (c_begin < c_end) {
+    r = warp_upper_bound(co, n_req + 1, c_begin) - 1;
+    active = co[r] >= c_begin;  // else the request began in an earlier range: raw digests
+    nb = co[r + 1];
+    nnb = co[min(r + 2, n_req)];
+  }
+  uint64_t h = kChainInit;
+  for (int64_t i = 0; i < iters; ++i) {
+    const int slot = static_cast<int>(i % kRing);
+    const int64_t base = c_begin + i * 32;
+    const int n = static_cast<int>(min(c_end - base, int64_t{32}));
+    mbar_wait(&bars.full[slot], static_cast<uint32_t>((i / kRing) & 1));
+    // bit k: a request begins at chunk base + k (nb is the next request's first chunk)
+    uint32_t starts = 0;
+    while (nb < base + n) {
+      starts |= 1u << static_cast<int>(nb - base);
+      ++r;
+      nb = nnb;
+      nnb = co[min(r + 2, n_req)];
+    }
+    const uint64_t* row = ring[slot];
+    uint64_t mine = row[lane];
+    if (starts == 0 && n == 32) {
+      // common case (~3 in 4 iterations): the whole iteration continues one request
+      if (active) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          h = fpair(h, row[k]);
+          mine = lane == k ? h : mine;
+        }
+      }
+    } else {
+      // branch-free: restart the chain at every request start, stop at n
+      bool act = active;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const uint64_t d = row[k];
+        const bool st = (starts >> k) & 1u;
+        h = st ? kChainInit : h;
+        act = act || st;
+        const uint64_t g = fpair(h, d);
+        const bool use = act && k < n;
+        h = use ? g : h;
+        mine = lane == k ? (use ? g : d) : mine;
+      }
+      active = act;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars.empty[slot]);
+    if (lane < n) out[base + lane] = mine;
+  }
+}
+
+template <bool kPf>
+__global__ void __launch_bounds__(kFusedThreads, 3) k_chunk_hash_fused(
+    int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
+    const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out, int pf) {
+  __shared__ uint64_t ring[kRing][32];
+  __shared__ RingBars bars;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kRing; ++k) {
+      mbar_init(&bars.full[k], kHashWarps);
+      mbar_init(&bars.empty[k], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t total = chunk_offsets[n_req];
+  const int64_t c_begin = total * blockIdx.x / gridDim.x;
+  const int64_t c_end = total * (blockIdx.x + 1) / gridDim.x;
+  const int64_t iters = (c_end - c_begin + 31) / 32;
+  if ((threadIdx.x >> 5) == kHashWarps)
+    chain_warp_ring(n_req, chunk_offsets, out, c_begin, c_end, iters, ring, bars);
+  else
+    digest_warp_ring<kPf>(n_req, offsets, tokens, chunk_offsets, pf, total, c_begin, c_end, iters, ring, bars);
+}
+
+// One warp per phase-1 range boundary b: the request holding chunks B_b - 1 and B_b, if it began
+// inside range b - 1 (else an earlier boundary's warp owns it), is continued from out[B_b - 1]
+// (chained by CTA b - 1) through its remaining raw digests, 32 per step: lanes load a block
+// (four blocks in flight) and stage it in shared memory, every lane runs the serial chain over
+// it (broadcast reads), lane k keeps value k, and the block is stored back coalesced.
+constexpr int kTailWarps = 4;
+__global__ void __launch_bounds__(32 * kTailWarps) k_chain_tail(int64_t n_req, const int64_t* __restrict__ co,
+                                                              uint64_t* __restrict__ out, int grid) {
+  __shared__ uint64_t tail_rows[kTailWarps][32];
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kTailWarps + (threadIdx.x >> 5) + 1;
+  if (b >= grid) return;
+  const int64_t total = co[n_req];
+  const int64_t B = total * b / grid, Bp = total * (b - 1) / grid;
+  if (B >= total) return;
+  const int64_t r = warp_upper_bound(co, n_req + 1, B) - 1;  // co[r] <= B < co[r + 1]
+  const int64_t r0 = co[r], end = co[r + 1];
+  if (r0 >= B || r0 < Bp) return;
+  uint64_t* rowb = tail_rows[threadIdx.x >> 5];
+  uint64_t h = out[B - 1];
+  constexpr int kAhead = 4;
+  uint64_t buf[kAhead];
+#pragma unroll
+  for (int a = 0; a < kAhead; ++a) {
+    const int64_t c = B + a * 32 + lane;
+    buf[a] = c < end ? out[c] : 0;
+  }
+  for (int64_t base = B; base < end; base += 32 * kAhead) {
+#pragma unroll
+    for (int a = 0; a < kAhead; ++a) {
+      const int64_t blk = base + a * 32;
+      if (blk < end) {
+        rowb[lane] = buf[a];
+        const int64_t nx = blk + 32 * kAhead + lane;
+        buf[a] = nx < end ? out[nx] : 0;
+        const int n = static_cast<int>(min(end - blk, int64_t{32}));
+        __syncwarp();
+        uint64_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint64_t g = fpair(h, rowb[k]);
+          h = k < n ? g : h;
+          mine = lane == k ? g : mine;
+        }
+        __syncwarp();
+        if (lane < n) out[blk + lane] = mine;
+      }
+    }
   }
 }
 
@@ -323,25 +578,54 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 
 // Phase-1 CTAs per SM (3 shipped; tsb_hash_set_grid for measurement).
 static int g_digest_ctas_per_sm = 3;
+static int g_digest_prefetch = 0;
 void set_hash_grid(int ctas_per_sm) { g_digest_ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : 3; }
+void set_hash_prefetch(int groups) { g_digest_prefetch = groups > 0 ? groups : 0; }
+
+static int g_fused_chain = 0;
+void set_hash_fused(int on) { g_fused_chain = on; }
+
+static void launch_digest(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
+                          const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
+  const int grid = 148 * g_digest_ctas_per_sm;
+  if (g_digest_prefetch > 0)
+    k_chunk_digest<true><<<grid, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, g_digest_prefetch);
+  else
+    k_chunk_digest<false><<<grid, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, 0);
+  count_launch();
+}
+
+static void launch_fused(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
+                         const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
+  const int grid = 148 * g_digest_ctas_per_sm;
+  if (g_digest_prefetch > 0)
+    k_chunk_hash_fused<true><<<grid, kFusedThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out,
+                                                             g_digest_prefetch);
+  else
+    k_chunk_hash_fused<false><<<grid, kFusedThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, 0);
+  count_launch();
+  k_chain_tail<<<ceil_div(grid, kTailWarps), 32 * kTailWarps, 0, st>>>(n_req, chunk_offsets, out, grid);
+  count_launch();
+}
 
 cudaError_t launch_chunk_digests(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                  const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
-  k_chunk_digest<<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
-  count_launch();
+  launch_digest(n_req, offsets, tokens, chunk_offsets, out, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   if (n_req == 0) return cudaSuccess;
-  // persistent phase-1 grid: 4 CTAs of 8 warps per SM (register-limited occupancy)
-  // 3 CTAs of 8 warps per SM (4 measured no faster)
-  k_chunk_digest<<<148 * g_digest_ctas_per_sm, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out);
-  count_launch();
-  k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
-  count_launch();
+  // persistent phase-1 grid: 3 CTAs of 8 warps per SM (4 measured no faster)
+  if (g_fused_chain) {
+    launch_fused(n_req, offsets, tokens, chunk_offsets, out, st);
+  } else {
+    launch_digest(n_req, offsets, tokens, chunk_offsets, out, st);
+    k_chain<<<ceil_div(n_req, 32 * kChainWarps), 32 * kChainWarps, 0, st>>>(n_req, chunk_offsets, out);
+    count_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -111,6 +111,8 @@ cudaError_t launch_order(int64_t n, uint64_t* kp, uint64_t* ka, uint64_t* ki, in
 
 // Prefix hasher (K3) and token generator.
 void set_hash_grid(int ctas_per_sm);
+void set_hash_prefetch(int groups);
+void set_hash_fused(int on);
 cudaError_t launch_chunk_digests(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                                  const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st);
 cudaError_t launch_hash_prefix(int64_t n_req, const int64_t* offsets, const int32_t* tokens,

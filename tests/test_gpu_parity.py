@@ -857,3 +857,28 @@ def test_hash_aligned_layout_and_phase1(oracle):
     hasher.chunk_digests_device(d_off, tok, coff, dig)
     torch.cuda.synchronize()
     assert not np.array_equal(dig.cpu().numpy(), out.cpu().numpy())  # unchained
+
+
+@pytest.mark.parametrize("cps,pf,fused", [(3, 0, 1), (3, 1, 0), (3, 1, 1), (2, 4, 1), (4, 0, 1), (1, 2, 1)])
+def test_hash_tuning_variants_vs_oracle(oracle, cps, pf, fused):
+    """Every K3 tuning (grid, L2 prefetch distance, chain fused into phase 1 with the boundary
+    straddlers chained after) gives the oracle's hashes: a random queue, one request spanning
+    every CTA range, fewer chunks than CTAs, and empty requests at range boundaries."""
+    lib = _capi.lib
+    rng = np.random.default_rng(31 + cps + pf)
+    cases = [rng.integers(0, 4000, 2000),
+             np.array([300, 2_000_000, 0, 0, 700], np.int64),
+             np.array([256, 0, 512, 1, 256 * 3], np.int64),
+             np.concatenate([np.zeros(50, np.int64), rng.integers(0, 600, 3000), np.zeros(50, np.int64)])]
+    try:
+        t.check(lib.tsb_hash_set_grid(cps))
+        t.check(lib.tsb_hash_set_tuning(pf, fused))
+        for lens in cases:
+            lens = lens.astype(np.int64)
+            offs = np.zeros(len(lens) + 1, np.int64)
+            np.cumsum(lens, out=offs[1:])
+            toks = oracle.gen_tokens(9, offs, rng.integers(0, 5, len(lens)), lens // 3)
+            assert np.array_equal(hasher.hash_prefix_chunks(offs, toks), oracle.hash_prefix_chunks(offs, toks))
+    finally:
+        t.check(lib.tsb_hash_set_grid(0))
+        t.check(lib.tsb_hash_set_tuning(0, 0))

@@ -1,0 +1,5 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+timeout 600 python tools/k3_sweep.py > gpurun_out/r02_k3_prefetch.jsonl 2> gpurun_out/k3.err; echo "k3 rc=$?"; tail -3 gpurun_out/k3.err
+cat gpurun_out/r02_k3_prefetch.jsonl

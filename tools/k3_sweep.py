@@ -1,5 +1,5 @@
 """K3 on the configs[4] queue (product generate_workload, loogle, 100K, seed 0): phase 1 alone and
-phase 1 + chain, packed vs 16-byte-aligned request starts, 2-4 CTAs per SM.  CUDA events, mean of
+phase 1 + chain, packed vs 16-byte-aligned request starts, 2-4 CTAs per SM, L2 prefetch distance.  CUDA events, mean of
 10 after 3 warm-ups; against the 7.41 TB/s read-only ceiling.  One JSON line per case."""
 import json
 import sys
@@ -14,6 +14,8 @@ from paper_2603_21257_b200 import _capi, hasher  # noqa: E402
 from paper_2603_21257_b200 import tiersim as t  # noqa: E402
 
 CEIL = 7410.0
+# (CTAs per SM, L2 prefetch distance in warp groups, chain fused into phase 1)
+CASES = [(3, 0, 0), (3, 1, 0), (3, 0, 1), (3, 1, 1), (4, 0, 1), (2, 1, 1)]
 
 
 def timed(fn, reps=10, warm=3):
@@ -49,18 +51,20 @@ def main():
         hasher.gen_tokens_device(0, d_offs, doc, sh, tok)
         out = torch.empty(int(coff[-1]), dtype=torch.int64, device=dev)
         nbytes = int(lens.sum()) * 4 + out.numel() * 8
-        for cps in (2, 3, 4):
+        for cps, pf, fused in CASES:
             t.check(_capi.lib.tsb_hash_set_grid(cps))
+            t.check(_capi.lib.tsb_hash_set_tuning(pf, fused))
             p1 = timed(lambda: hasher.chunk_digests_device(d_offs, tok, coff, out))
             full = timed(lambda: hasher.hash_prefix_chunks_device(d_offs, tok, coff, out))
             h = out.cpu().numpy()
             ref = h if ref is None else ref
-            print(json.dumps({"layout": layout, "ctas_per_sm": cps, "phase1_ms": p1 * 1e3, "total_ms": full * 1e3,
+            print(json.dumps({"layout": layout, "ctas_per_sm": cps, "prefetch_groups": pf, "fused_chain": fused, "phase1_ms": p1 * 1e3, "total_ms": full * 1e3,
                               "phase1_read_ceiling_frac": nbytes / p1 / 1e9 / CEIL,
                               "total_read_ceiling_frac": nbytes / full / 1e9 / CEIL,
                               "hashes_equal_first_case": bool(np.array_equal(h, ref))}), flush=True)
         del tok
     t.check(_capi.lib.tsb_hash_set_grid(0))
+    t.check(_capi.lib.tsb_hash_set_tuning(0, 0))
 
 
 if __name__ == "__main__":
