@@ -576,9 +576,11 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 
 }  // namespace
 
-// Phase-1 CTAs per SM (3 shipped; tsb_hash_set_grid for measurement).
+// Phase-1 CTAs per SM (3 shipped; tsb_hash_set_grid for measurement).  L2 prefetch one warp
+// group ahead is shipped: +2.5-4% on phase 1 over both layouts, deeper prefetch loses
+// (profiles/r02_k3_prefetch_sweep.jsonl).  The fused chain is a measured variant, no faster.
 static int g_digest_ctas_per_sm = 3;
-static int g_digest_prefetch = 0;
+static int g_digest_prefetch = 1;
 void set_hash_grid(int ctas_per_sm) { g_digest_ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : 3; }
 void set_hash_prefetch(int groups) { g_digest_prefetch = groups > 0 ? groups : 0; }
 

@@ -64,7 +64,7 @@ def main():
                               "hashes_equal_first_case": bool(np.array_equal(h, ref))}), flush=True)
         del tok
     t.check(_capi.lib.tsb_hash_set_grid(0))
-    t.check(_capi.lib.tsb_hash_set_tuning(0, 0))
+    t.check(_capi.lib.tsb_hash_set_tuning(1, 0))
 
 
 if __name__ == "__main__":
