@@ -521,9 +521,10 @@ typedef struct {
                            page words differing from tsb_pool_fill_synthetic(verify_seed) */
   int32_t pace_network; /* online mode with an L3 store: a network hop lasts at least
                            transfer_base_latency + bytes / network_bandwidth (engine.cpp:205) */
-  int32_t reuse_l1;     /* batch mode: a chunk whose L2 slot is already resident in another live
-                           request's pages is replicated HBM -> HBM (K8) instead of crossing the
-                           link again; the holder's release waits for the copies */
+  int32_t reuse_l1;     /* a chunk whose L2 slot is already resident in another live request's
+                           pages (its hop issued) is replicated HBM -> HBM (K8) instead of
+                           crossing the link again; the holder's release waits for the copies.
+                           Batch and online modes; TSB_UNSUPPORTED with an L3 store */
 } tsb_stage_options;
 
 typedef struct {

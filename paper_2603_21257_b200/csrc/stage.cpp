@@ -786,6 +786,9 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   const bool use_l3 = s->l3 != nullptr;
   const bool coupled = c->control_mode == 0;
   const bool reactive = c->allocation_mode == 1;
+  const bool reuse = opt->reuse_l1 != 0;
+  if (reuse && use_l3)
+    return fail(TSB_UNSUPPORTED, "stage: reuse_l1 with an L3 store (blocks pass through L2 slots, not pool slots)");
   const int mode = ingest_mode(s, opt);
   const int64_t l2_slot_bytes = tsb_pool_chunk_bytes(s->pool);
   s->trace.clear();
@@ -807,22 +810,34 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     int32_t row = -1, deferred = 0;
     int64_t next_net = 0, next_pcie = 0, net_done = 0, pcie_issued = 0, pcie_done = 0;
     bool arrived = false, admitted = false, compute_ready = false, started = false, finished = false;
+    bool released = false;      // its L1 pages went back to the allocator
+    bool read_by_copy = false;  // reuse_l1: ev_reader guards its pages until K8 has read them
     double arrival = 0.0, admit_t = 0.0;
     cudaEvent_t ev_first = nullptr, ev_resident = nullptr, ev_done = nullptr, ev_begin = nullptr;
+    cudaEvent_t ev_reader = nullptr;
   };
   std::vector<Rt> R(static_cast<size_t>(n));
   double first_arrival = q->arrival[0];
   for (int64_t i = 0; i < n; ++i) first_arrival = std::min(first_arrival, q->arrival[i]);
-  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(4 * n), cudaEventDefault));
+  TSB_TRY(grow_events(s->timing_pool, static_cast<size_t>(5 * n), cudaEventDefault));
   for (int64_t i = 0; i < n; ++i) {
     Rt& r = R[i];
     r.blk.resize(static_cast<size_t>(plans[i].n_chunks));
     r.arrival = q->arrival[i] - first_arrival;
-    r.ev_first = s->timing_pool[4 * i];
-    r.ev_resident = s->timing_pool[4 * i + 1];
-    r.ev_done = s->timing_pool[4 * i + 2];
-    r.ev_begin = s->timing_pool[4 * i + 3];
+    r.ev_first = s->timing_pool[5 * i];
+    r.ev_resident = s->timing_pool[5 * i + 1];
+    r.ev_done = s->timing_pool[5 * i + 2];
+    r.ev_begin = s->timing_pool[5 * i + 3];
+    r.ev_reader = s->timing_pool[5 * i + 4];
   }
+  // reuse_l1: pool slot -> live requests whose pages hold that chunk (hop issued), oldest first.
+  struct Holder {
+    size_t req;
+    int32_t row, chunk;
+  };
+  std::unordered_map<int64_t, std::vector<Holder>> holders;
+  std::vector<size_t> release_wait;  // ComputeDone seen, pages still being read by K8 copies
+  int64_t reused_chunks = 0;
   // Priority keys from the GPU scorer (K4), compared with PriorityKey::operator< on the host.
   std::vector<double> primary(static_cast<size_t>(n));
   std::vector<int64_t> order(static_cast<size_t>(n));
@@ -905,6 +920,18 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     }, &msg);
     return rs == TSB_OK ? TSB_OK : fail(rs, msg);
   };
+  // L1 release at ComputeDone (engine.cpp:280-282): FIFO grants to deferred reservations.
+  auto release_l1 = [&](size_t i) -> tsb_status {
+    Rt& r = R[i];
+    r.released = true;
+    if (r.row < 0 && r.deferred == 0) return TSB_OK;
+    int64_t ng = 0;
+    grants.resize(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
+    TSB_TRY(tsb_l1_release_request(s->l1, plans[i].id, grants.data(), static_cast<int64_t>(grants.size()), &ng));
+    ++releases;
+    for (int64_t g = 0; g < ng; ++g) grant_l1(by_id.at(grants[g].request_id), grants[g].block_index);
+    return TSB_OK;
+  };
 
   tsb_status status = TSB_OK;
   while (finished < static_cast<size_t>(n) && status == TSB_OK) {
@@ -966,15 +993,30 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
           break;
         verify_mismatches += mm;
       }
-      if (r.row >= 0 || r.deferred > 0) {
-        int64_t ng = 0;
-        grants.resize(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
-        if ((status = tsb_l1_release_request(s->l1, plans[i].id, grants.data(),
-                                             static_cast<int64_t>(grants.size()), &ng)) != TSB_OK)
-          break;
-        ++releases;
-        for (int64_t g = 0; g < ng; ++g) grant_l1(by_id.at(grants[g].request_id), grants[g].block_index);
+      if (reuse) {  // its pages stop being a copy source; copies already issued from them finish first
+        for (int64_t ch = 0; ch < plans[i].n_chunks; ++ch) {
+          const auto h = plans[i].slots[ch] >= 0 ? holders.find(plans[i].slots[ch]) : holders.end();
+          if (h == holders.end()) continue;
+          auto& v = h->second;
+          v.erase(std::remove_if(v.begin(), v.end(), [&](const Holder& x) { return x.req == i; }), v.end());
+        }
+        if (r.read_by_copy && !done(r.ev_reader)) {
+          release_wait.push_back(i);
+          continue;
+        }
       }
+      if ((status = release_l1(i)) != TSB_OK) break;
+    }
+    if (status != TSB_OK) break;
+    for (size_t k = 0; k < release_wait.size() && status == TSB_OK;) {  // deferred ComputeDone releases
+      const size_t i = release_wait[k];
+      if (!done(R[i].ev_reader)) {
+        ++k;
+        continue;
+      }
+      release_wait.erase(release_wait.begin() + static_cast<std::ptrdiff_t>(k));
+      status = release_l1(i);
+      progress = true;
     }
     if (status != TSB_OK) break;
     while (admitted_head < admitted.size() && R[admitted[admitted_head]].finished) ++admitted_head;
@@ -1088,18 +1130,28 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
         if (r.next_pcie >= nb) continue;
         if (coupled && r.net_done < nb) continue;
         std::vector<tsb_ingest_item> items;
+        std::vector<tsb_page_copy> copies;
+        std::vector<size_t> copy_from;  // holder request of each copy
         std::vector<int32_t> bl;
         while (r.next_pcie < nb) {
           Blk& b = r.blk[static_cast<size_t>(r.next_pcie)];
           if (!b.net_done || !b.l1_granted) break;
           b.pcie_issued = true;
+          const int32_t ch = static_cast<int32_t>(r.next_pcie);
           const int64_t src = use_l3 ? b.l2_slot : plans[i].slots[r.next_pcie];
-          items.push_back(tsb_ingest_item{src, r.row, static_cast<int32_t>(r.next_pcie)});
-          bl.push_back(static_cast<int32_t>(r.next_pcie));
-          row(4, 1, -1, plans[i].id, static_cast<int32_t>(r.next_pcie), chunk_bytes);
+          const auto h = reuse && src >= 0 ? holders.find(src) : holders.end();
+          if (h != holders.end() && !h->second.empty()) {
+            const Holder& from = h->second.front();
+            copies.push_back(tsb_page_copy{from.row, from.chunk, r.row, ch});
+            copy_from.push_back(from.req);
+          } else {
+            items.push_back(tsb_ingest_item{src, r.row, ch});
+          }
+          bl.push_back(ch);
+          row(4, 1, -1, plans[i].id, ch, chunk_bytes);
           ++r.next_pcie;
         }
-        if (items.empty()) continue;
+        if (bl.empty()) continue;
         if ((status = tsb_l1_sync_block_table(s->l1, stream)) != TSB_OK) break;
         if (r.pcie_issued == 0) {
           const cudaError_t e = cudaEventRecord(r.ev_begin, st);
@@ -1108,8 +1160,29 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
             break;
           }
         }
-        r.pcie_issued += static_cast<int64_t>(items.size());
+        r.pcie_issued += static_cast<int64_t>(bl.size());
         const bool last = r.pcie_issued == nb;
+        if (reuse) {
+          for (int32_t ch : bl)
+            if (plans[i].slots[ch] >= 0) holders[plans[i].slots[ch]].push_back(Holder{i, r.row, ch});
+          // K8 first: its sources were written by ingest calls issued earlier on this stream
+          for (int64_t c0 = 0; c0 < static_cast<int64_t>(copies.size()) && status == TSB_OK; c0 += 65536)
+            status = tsb_l1_copy_chunks(s->l1, copies.data() + c0,
+                                        std::min<int64_t>(65536, static_cast<int64_t>(copies.size()) - c0), 0, L,
+                                        stream);
+          if (status != TSB_OK) break;
+          cudaError_t e = cudaSuccess;
+          for (const size_t h : copy_from) {  // the holders' pages stay until these copies ran
+            if (e == cudaSuccess) e = cudaEventRecord(R[h].ev_reader, st);
+            R[h].read_by_copy = true;
+          }
+          if (e != cudaSuccess) {
+            status = tsb::cuda_fail(e, "stage: reuse reader events");
+            break;
+          }
+          reused_chunks += static_cast<int64_t>(copies.size());
+          bytes_total += static_cast<int64_t>(copies.size()) * chunk_bytes;  // delivered into L1 all the same
+        }
         std::vector<void*> evs;
         if (last) {
           evs.assign(static_cast<size_t>(L), nullptr);
@@ -1128,7 +1201,8 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
           break;
         cudaEvent_t ce = s->call_pool[call_slot++ % 4096];
         cudaError_t e = cudaSuccess;
-        if (last && L == 1) e = cudaEventRecord(r.ev_first, st);
+        if (last && (L == 1 || !copies.empty())) e = cudaEventRecord(r.ev_first, st);
+        if (e == cudaSuccess && last && !copies.empty()) e = cudaEventRecord(r.ev_resident, st);  // covers K8 too
         if (e == cudaSuccess) e = cudaEventRecord(ce, st);
         if (e != cudaSuccess) {
           status = tsb::cuda_fail(e, "stage: ingest call events");
@@ -1173,7 +1247,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     if (finished < static_cast<size_t>(n)) {
       const double t = now();
       if (progress) last_progress = t;
-      const bool in_flight = net_busy || !calls.empty() || compute_busy;
+      const bool in_flight = net_busy || !calls.empty() || compute_busy || !release_wait.empty();
       if (!in_flight && next_arrival >= by_arrival.size() && t - last_progress > 5.0) {
         status = fail(TSB_CAPACITY, "stage: no request can make progress (ledger deadlock)");
         break;
@@ -1197,10 +1271,12 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   }
   cudaStreamSynchronize(st);
   cudaStreamSynchronize(s->compute);
+  for (size_t k = 0; k < release_wait.size() && status == TSB_OK; ++k)  // their readers ran (synced)
+    status = release_l1(release_wait[k]);
   if (status != TSB_OK) {
     const std::string msg = tsb_last_error();
     for (int64_t i = 0; i < n; ++i) {  // hand every L1 reservation back
-      if (!R[i].admitted || R[i].finished) continue;
+      if (!R[i].admitted || R[i].released) continue;
       std::vector<tsb_grant> g(static_cast<size_t>(tsb_l1_deferred(s->l1)) + 1);
       int64_t ng = 0;
       tsb_l1_release_request(s->l1, plans[i].id, g.data(), static_cast<int64_t>(g.size()), &ng);
@@ -1235,6 +1311,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
     stats->verify_mismatches = verify_mismatches;
     stats->net_blocks = net_blocks;
     stats->l2_deferred = l2_deferred;
+    stats->reused_chunks = reused_chunks;
   }
   return TSB_OK;
 }

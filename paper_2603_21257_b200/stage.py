@@ -88,15 +88,16 @@ class LoadStage:
     def run_online(self, queue: QueueArrays, slot_lists: Sequence[Sequence[int]], config: ClusterConfig,
                    models: Optional[CostModelPair] = None, policy: int = PolicyKind.Fifo, mode: int = AUTO,
                    prefill_ctas: int = 0, verify_seed: int = 0, stream=None, pace_network: bool = False,
-                   record_trace: bool = False) -> StageResult:
+                   record_trace: bool = False, reuse_l1: bool = False) -> StageResult:
         """Real-time replay: arrivals at their arrival_time, SimEngine's control loop under
         config.control_mode / allocation_mode (tsb_stage_run_online).  requests['done_ms'] -
         requests['arrival_ms'] is each TTFT.  verify_seed (opt-in, perturbs timing): check every page
         of each request before release.  pace_network: with an L3 store, each network hop lasts at
-        least transfer_base_latency + bytes / network_bandwidth."""
+        least transfer_base_latency + bytes / network_bandwidth.  reuse_l1: a chunk already resident
+        in a live request's pages is replicated HBM -> HBM instead of crossing the link (no L3)."""
         return self.run(queue, slot_lists, config, models, policy, mode, prefill=True, prefill_ctas=prefill_ctas,
                         verify_seed=verify_seed, stream=stream, record_trace=record_trace,
-                        pace_network=pace_network, _fn=lib.tsb_stage_run_online)
+                        pace_network=pace_network, reuse_l1=reuse_l1, _fn=lib.tsb_stage_run_online)
 
     def run(self, queue: QueueArrays, slot_lists: Sequence[Sequence[int]], config: ClusterConfig,
             models: Optional[CostModelPair] = None, policy: int = PolicyKind.Fifo, mode: int = AUTO,

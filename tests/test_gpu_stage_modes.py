@@ -175,6 +175,8 @@ def test_online_errors_and_exclusive_tiers(rig):
         rig["stage"].run_online(q, [[~s for s in sl] for sl in slots], cfg)
     with pytest.raises(t.Unsupported, match="tsb_stage_run_online only"):
         rig["stage"].run(q, slots, cfg)
+    with pytest.raises(t.Unsupported, match="reuse_l1 with an L3 store"):
+        rig["stage"].run_online(q, slots, cfg, reuse_l1=True)
     small = t.ClusterConfig(bytes_per_token=BPT, l2_capacity=2 * SHAPE.chunk_bytes)
     with pytest.raises(t.CapacityError, match="can never fit"):
         rig["stage"].run_online(stream(3, 9), slots_for(stream(3, 9), rig["n_l3"], 2), small)

@@ -119,3 +119,9 @@ def test_random_online_runs_verify(seed):
     assert res.stats["verify_mismatches"] == 0, (seed, mode, layout)
     assert res.stats["bytes"] == sum(len(s) for s in slot_lists) * shape.local_chunk_bytes
     assert l1.reserved() == 0
+    # the same replay with reuse_l1 (host-pool chunks replicated from live holders by K8)
+    res2 = stage.run_online(q, slot_lists, cfg, policy=policy, mode=ingest.MODES[mode], verify_seed=7 + seed,
+                            reuse_l1=True)
+    assert res2.stats["verify_mismatches"] == 0, (seed, "reuse", mode, layout)
+    assert res2.stats["bytes"] == res.stats["bytes"]
+    assert l1.reserved() == 0 and l1.free_pages() == l1.num_pages
