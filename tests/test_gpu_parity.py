@@ -869,7 +869,9 @@ def test_hash_tuning_variants_vs_oracle(oracle, cps, pf, fused):
     cases = [rng.integers(0, 4000, 2000),
              np.array([300, 2_000_000, 0, 0, 700], np.int64),
              np.array([256, 0, 512, 1, 256 * 3], np.int64),
-             np.concatenate([np.zeros(50, np.int64), rng.integers(0, 600, 3000), np.zeros(50, np.int64)])]
+             np.concatenate([np.zeros(50, np.int64), rng.integers(0, 600, 3000), np.zeros(50, np.int64)]),
+             # long requests (>= 256 chunks) among short ones, several in one 32-request window
+             np.where(rng.random(400) < 0.2, rng.integers(256 * 256, 256 * 1200, 400), rng.integers(0, 9000, 400))]
     try:
         t.check(lib.tsb_hash_set_grid(cps))
         t.check(lib.tsb_hash_set_tuning(pf, fused))
