@@ -1,7 +1,8 @@
 // tiersim/engine.hpp — TierLedger of the reference (core/include/tiersim/engine.hpp:22-53), backed by
 // libtsb's tsb::Ledger: identical grant/defer decisions, FIFO grant lists and error messages.
 // The L1 tier with real pages is tiersim::PagedAllocator (tiersim/b200.hpp), which runs the same
-// ledger.  run_simulation (the DES) is out of scope: the real-time path is tiersim::LoadStage.
+// ledger, and config_fingerprint.  run_simulation (the DES) is out of scope: the real-time path is
+// tiersim::LoadStage.
 #pragma once
 
 #include <cstdint>
@@ -9,6 +10,7 @@
 #include <vector>
 
 #include "tiersim/error.hpp"
+#include "tiersim/scheduler.hpp"
 #include "tiersim/types.hpp"
 
 namespace tiersim {
@@ -57,5 +59,11 @@ class TierLedger {
   Tier tier_;
   std::unique_ptr<tsb_ledger, Del> l_;
 };
+
+// config_fingerprint (engine.hpp:68-74): FNV-1a-64 of the config, policy and seed.
+inline std::uint64_t config_fingerprint(const ClusterConfig& config, PolicyKind policy, std::uint64_t seed) {
+  const tsb_cluster c = config.c_abi();
+  return tsb_config_fingerprint(&c, static_cast<int>(policy), seed);
+}
 
 }  // namespace tiersim

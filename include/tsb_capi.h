@@ -68,6 +68,9 @@ typedef struct {
 void tsb_cluster_default(tsb_cluster* out);
 /* ClusterConfig::validate (types.cpp:56-71). */
 tsb_status tsb_cluster_validate(const tsb_cluster* c);
+/* config_fingerprint (engine.hpp:68-74, engine.cpp:500-534): byte-wise FNV-1a-64 over the     */
+/* config fields in declaration order, then the policy and the seed (enums one byte each).    */
+uint64_t tsb_config_fingerprint(const tsb_cluster* c, int policy, uint64_t seed);
 
 /* ------------------------------------------------------------------------------------ */
 /* KV geometry and chunk plan (types.cpp:73-118)                                           */

@@ -137,6 +137,7 @@ _decl("tsb_kernel_launch_count", u64)
 _decl("tsb_current_device", C.c_int)
 _decl("tsb_cluster_default", None, P(Cluster))
 _decl("tsb_cluster_validate", st, P(Cluster))
+_decl("tsb_config_fingerprint", u64, P(Cluster), C.c_int, u64)
 _decl("tsb_kv_bytes_per_token", st, i64, i64, i64, i64, P(i64))
 _decl("tsb_kv_shape_info", st, P(KvShape), P(i64), P(i64), P(i64))
 _decl("tsb_request_validate", st, P(Queue), i64)

@@ -85,6 +85,44 @@ tsb_status tsb_cluster_validate(const tsb_cluster* c) {
   return TSB_OK;
 }
 
+// config_fingerprint (engine.cpp:500-534): byte-wise FNV-1a over the fields in declaration
+// order, each hashed as its in-memory bytes; the three enums are one byte (std::uint8_t).
+}  // extern "C"
+namespace {
+uint64_t fnv1a_bytes(uint64_t h, const void* data, size_t len) {
+  const auto* b = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < len; ++i) {
+    h ^= b[i];
+    h *= tsb::kFnvPrime;
+  }
+  return h;
+}
+template <typename T>
+uint64_t fnv1a_value(uint64_t h, const T& v) {
+  return fnv1a_bytes(h, &v, sizeof(v));
+}
+}  // namespace
+extern "C" {
+
+uint64_t tsb_config_fingerprint(const tsb_cluster* c, int policy, uint64_t seed) {
+  uint64_t h = tsb::kFnvOffset;
+  h = fnv1a_value(h, c->network_bandwidth);
+  h = fnv1a_value(h, c->pcie_bandwidth);
+  h = fnv1a_value(h, c->transfer_base_latency);
+  h = fnv1a_value(h, c->l1_capacity);
+  h = fnv1a_value(h, c->l2_capacity);
+  h = fnv1a_value(h, c->bytes_per_token);
+  h = fnv1a_value(h, c->block_size_tokens);
+  h = fnv1a_value(h, c->compute_base);
+  h = fnv1a_value(h, c->compute_per_token);
+  h = fnv1a_value(h, c->compute_quadratic);
+  h = fnv1a_value(h, static_cast<uint8_t>(c->allocation_mode));
+  h = fnv1a_value(h, static_cast<uint8_t>(c->control_mode));
+  h = fnv1a_value(h, static_cast<uint8_t>(policy));
+  h = fnv1a_value(h, seed);
+  return h;
+}
+
 // ---------------------------------------------------------------------------------------
 // Geometry and plan (types.cpp:73-118)
 // ---------------------------------------------------------------------------------------

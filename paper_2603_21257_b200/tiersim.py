@@ -204,6 +204,11 @@ def _q1(spec: RequestSpec):
     return q, q.struct()
 
 
+def config_fingerprint(config: ClusterConfig, policy: int, seed: int) -> int:
+    """engine.hpp:68-74 / engine.cpp:516-534: FNV-1a-64 of the config fields, policy and seed."""
+    return int(lib.tsb_config_fingerprint(C.byref(config.struct()), int(policy), int(seed)))
+
+
 def kv_bytes_per_token(layers: int, kv_heads: int, head_dim: int, dtype_bytes: int) -> int:
     out = C.c_int64()
     check(lib.tsb_kv_bytes_per_token(layers, kv_heads, head_dim, dtype_bytes, C.byref(out)))

@@ -81,6 +81,12 @@ static void host_cases() {
     const auto st = make_request_state(spec(4, 1.5, 1000, 7, 0.5), cfg);
     EXPECT(st.cached_tokens == 256 && st.compute_tokens == 1000 + 7 - 256 && st.ts.arrival == 1.5);
   });
+  run("config_fingerprint: reference golden (tests/golden/ref_misc.json)", [] {
+    ClusterConfig cfg;
+    EXPECT(config_fingerprint(cfg, PolicyKind::Fifo, 0) == 18430105898594341330ull);
+    cfg.pcie_bandwidth = 55.6e9;
+    EXPECT(config_fingerprint(cfg, PolicyKind::Lstf, 7) == 12797939754527448084ull);
+  });
   run("workload: generate_workload / assign_slos through the kept API", [] {
     WorkloadSpec w;
     w.profile = builtin_profile("loogle");

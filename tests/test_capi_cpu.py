@@ -57,6 +57,23 @@ def test_kv_bytes_per_token_goldens(golden):
     assert t.kv_bytes_per_token(80, 8, 128, 2) == misc["kv_bytes_per_token"]["llama3_70b"]
 
 
+def test_config_fingerprint_matches_reference_golden(golden):
+    """tsb_config_fingerprint == the compiled reference's config_fingerprint (engine.cpp:516-534)
+    on every golden (config, policy, seed), and it separates configs that differ in one field."""
+    misc = json.loads(golden("ref_misc.json"))
+    assert misc["fingerprint"]
+    for fp in misc["fingerprint"]:
+        cfg = dict(fp["cfg"])
+        cfg["allocation_mode"] = t.AllocationMode(cfg["allocation_mode"])
+        cfg["control_mode"] = t.ControlMode(cfg["control_mode"])
+        assert t.config_fingerprint(t.ClusterConfig(**cfg), fp["policy"], int(fp["seed"])) == int(fp["hash"])
+    base = t.ClusterConfig()
+    seen = {t.config_fingerprint(base, 0, 1), t.config_fingerprint(base, 1, 1), t.config_fingerprint(base, 0, 2),
+            t.config_fingerprint(t.ClusterConfig(compute_quadratic=1e-9), 0, 1),
+            t.config_fingerprint(t.ClusterConfig(control_mode=t.ControlMode.Coupled), 0, 1)}
+    assert len(seen) == 5
+
+
 def test_block_plans_match_reference_golden(golden):
     g = golden("ref_plan.npz")
     for (ctx, qry, hit, block), (cached, comp, nb, btok, bbytes) in zip(g["cases"], g["plan"]):
