@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "tiersim/cost_model.hpp"
+#include "tiersim/events.hpp"
 #include "tiersim/scheduler.hpp"
 #include "tiersim/types.hpp"
 
@@ -159,6 +160,18 @@ class LoadStage {
              const ClusterConfig& config, const CostModelPair& models, tsb_stage_options opt,
              void* stream = nullptr) {
     return run_impl(tsb_stage_run, batch, slots, config, models, opt, stream);
+  }
+  /// TraceEvent rows of the last run (opt.record_trace), in seq order: host-clock times for
+  /// arrivals, grants, dispatches and compute completions; CUDA-event times for TransferDone.
+  std::vector<TraceEvent> trace() const {
+    int64_t n = 0;
+    check(tsb_stage_trace(s_.get(), nullptr, 0, &n));
+    std::vector<tsb_trace_row> rows(static_cast<std::size_t>(n));
+    check(tsb_stage_trace(s_.get(), rows.data(), n, &n));
+    std::vector<TraceEvent> out;
+    out.reserve(rows.size());
+    for (const auto& r : rows) out.push_back(trace_event_of(r));
+    return out;
   }
 
  private:

@@ -7,6 +7,7 @@
 #include <filesystem>
 #include <fstream>
 #include <functional>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -80,6 +81,20 @@ static void host_cases() {
     EXPECT(derive_block_plan(spec(3, 0, 28100, 10, 0.0), cfg).empty());
     const auto st = make_request_state(spec(4, 1.5, 1000, 7, 0.5), cfg);
     EXPECT(st.cached_tokens == 256 && st.compute_tokens == 1000 + 7 - 256 && st.ts.arrival == 1.5);
+  });
+  run("events: names and the reference CSV layout", [] {
+    EXPECT(std::string(stage_name(Stage::Pcie)) == "pcie" && std::string(event_kind_name(EventKind::DispatchWake)) == "dispatch_wake");
+    tsb_trace_row row{0.5, 3, 2, -1, 2, 7, 11, 4096};
+    const TraceEvent e = trace_event_of(row);
+    EXPECT(e.kind == EventKind::AllocationGrant && !e.stage && e.tier == Tier::L1 && e.block_index == 7);
+    const auto csv = std::filesystem::temp_directory_path() / "tsb_events_test.csv";
+    write_trace_csv(csv, std::vector<TraceEvent>{e});
+    std::ifstream in(csv);
+    std::string a, b;
+    std::getline(in, a);
+    std::getline(in, b);
+    EXPECT(b == "0.500000000,3,allocation_grant,l1,11,7,4096");
+    std::filesystem::remove(csv);
   });
   run("config_fingerprint: reference golden (tests/golden/ref_misc.json)", [] {
     ClusterConfig cfg;
@@ -324,9 +339,41 @@ static void gpu_cases() {
     opt.mode = TSB_INGEST_AUTO;
     opt.prefill = 1;
     opt.verify_seed = 55;
+    opt.record_trace = 1;
     const auto r = stage.run_online(batch, slots, cfg, cost_models_from_config(cfg), opt);
     EXPECT(r.stats.verify_mismatches == 0 && r.stats.net_blocks == 15 && l1.reserved() == 0);
     EXPECT(calls == 3 * 4);  // every layer of every request went through the hook
+    // the TraceEvent stream (events.hpp): per block one L2 and one L1 grant, one net and one pcie
+    // hop, each dispatched after its grant (trace_checks.hpp:93-143); one compute_done per request
+    const std::vector<TraceEvent> tr = stage.trace();
+    std::map<std::pair<int64_t, int32_t>, std::uint64_t> g1, g2, net, pcie, done;
+    int computes = 0;
+    for (const TraceEvent& e : tr) {
+      const auto key = std::make_pair(e.request_id, e.block_index);
+      if (e.kind == EventKind::AllocationGrant) (*e.tier == Tier::L1 ? g1 : g2)[key] = e.seq;
+      if (e.kind == EventKind::DispatchWake && e.stage == Stage::Net) {
+        EXPECT(g2.count(key) && g2[key] < e.seq && !net.count(key));
+        net[key] = e.seq;
+      }
+      if (e.kind == EventKind::DispatchWake && e.stage == Stage::Pcie) {
+        EXPECT(g1.count(key) && g1[key] < e.seq && !pcie.count(key));
+        pcie[key] = e.seq;
+      }
+      if (e.kind == EventKind::TransferDone && e.stage == Stage::Pcie) done[key] = e.seq;
+      if (e.kind == EventKind::ComputeDone) ++computes;
+    }
+    EXPECT(g1.size() == 15 && g2.size() == 15 && net.size() == 15 && pcie.size() == 15 && done.size() == 15);
+    EXPECT(computes == 3);
+    const auto csv = std::filesystem::temp_directory_path() / "tsb_trace_test.csv";
+    write_trace_csv(csv, tr);
+    std::ifstream in(csv);
+    std::string line;
+    std::getline(in, line);
+    EXPECT(line == "time,seq,kind,stage,request_id,block_index,bytes");
+    std::size_t rows = 0;
+    while (std::getline(in, line)) ++rows;
+    EXPECT(rows == tr.size());
+    std::filesystem::remove(csv);
   });
   run("gpu: prefix hasher", [] {
     std::vector<std::int64_t> off = {0, 600, 1112};

@@ -24,7 +24,7 @@ def build():
 def test_cpp_api_host_cases():
     out = subprocess.run([str(build())], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "0 failures" in out.stdout
+    assert "10 cases, 0 failures" in out.stdout  # every host case ran
 
 
 @pytest.mark.gpu
@@ -32,4 +32,4 @@ def test_cpp_api_host_cases():
 def test_cpp_api_gpu_cases():
     out = subprocess.run([str(build()), "--gpu"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "15 cases, 0 failures" in out.stdout  # every host case plus every gpu case ran
+    assert "17 cases, 0 failures" in out.stdout  # every host case plus every gpu case ran
