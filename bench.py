@@ -653,6 +653,30 @@ def queue_workload(torch, hbm_peak, n=100_000):
                    "phase1_ms": p1 * 1e3, "phase1_read_ceiling_frac": nbytes / p1 / 1e9 / read_ceiling,
                    "hbm_copy_peak_frac": nbytes / secs / 1e9 / hbm_peak, "algorithmic_bytes": int(nbytes),
                    "layout": "16-byte-aligned request starts"}
+    # CPU leg for the hash: the oracle restatement (hash_ref) over the first requests of the same
+    # queue on all host threads and on one, checked equal to the GPU hashes of those requests
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle as po
+
+    k = 4000
+    lens = q.context_tokens[:k]
+    tok_h = tok[: int(offs[k])].cpu().numpy()
+    packed = np.concatenate([tok_h[offs[r]: offs[r] + lens[r]] for r in range(k)])
+    p_offs = np.zeros(k + 1, np.int64)
+    np.cumsum(lens, out=p_offs[1:])
+    threads = os.cpu_count() or 1
+    cpu_hash = {}
+    for th in (threads, 1):
+        t0 = time.perf_counter()
+        h_cpu = po.hash_prefix_chunks(p_offs, packed, threads=th)
+        cpu_hash[th] = time.perf_counter() - t0
+    sample_bytes = int(lens.sum()) * 4 + h_cpu.size * 8
+    res["hash"]["cpu_baseline"] = {
+        "kind": "port", "cores": threads, "cpu_model": cpu_model(),
+        "GBps": sample_bytes / cpu_hash[threads] / 1e9, "GBps_1_thread": sample_bytes / cpu_hash[1] / 1e9,
+        "sample": f"first {k} requests of the queue ({int(lens.sum())} tokens), oracle hash_ref",
+        "equal_to_gpu": bool(np.array_equal(h_cpu, hout[: int(coff[k])].cpu().numpy().view(np.uint64)))}
+    del tok_h, packed
     idx = hasher.PrefixIndex(capacity=1 << int(np.ceil(np.log2(2 * hout.numel()))))
     slots_t = torch.arange(hout.numel(), dtype=torch.int64, device=dev)
     ins_s = timed(lambda: idx.insert_device(hout, slots_t), reps=1, warm=0)
@@ -858,8 +882,11 @@ def run_ours(args):
         while len(times) < 2 or sum(times) < 10.0:
             times.append(cpu_scatter(shp, view, items, bt, num_pages, threads, arena))
         nbytes = len(items) * shp.local_chunk_bytes
+        q1 = max(1, len(items) // 8)  # one thread over an eighth of the sample (same pick order)
+        one = cpu_scatter(shp, view, items[:q1], bt, num_pages, 1, arena)
         line["cpu_baseline"] = {"value": nbytes * len(times) / sum(times) / 1e9, "unit": UNIT, "cores": threads,
                                 "kind": "port", "cpu_model": cpu_model(),
+                                "value_1_thread": q1 * shp.local_chunk_bytes / one / 1e9,
                                 "sample": f"{len(items)} chunks ({nbytes / 1e9:.2f} GB) of the {spec['name']} batch "
                                           f"in FIFO pick order, oracle scatter_ref, {threads} threads, "
                                           f"{len(times)} passes over >= 10 s of CPU work (mean)"}
