@@ -334,12 +334,15 @@ void scorer_free(tsb_scorer* s) {
 tsb_status scorer_reserve(tsb_scorer* s, int64_t n) {
   if (n <= s->capacity) return TSB_OK;
   const int64_t cap = std::max<int64_t>(n, 1024);
+  s->capacity = 0;  // a failed grow leaves no dangling buffer (scorer_free frees what is set)
   for (uint64_t** p : {&s->kp, &s->ka, &s->ki, &s->kp2, &s->ka2, &s->ki2}) {
     cudaFree(*p);
+    *p = nullptr;
     TSB_CUDA_TRY(cudaMalloc(p, sizeof(uint64_t) * cap));
   }
   for (int64_t** p : {&s->idx, &s->idx2}) {
     cudaFree(*p);
+    *p = nullptr;
     TSB_CUDA_TRY(cudaMalloc(p, sizeof(int64_t) * cap));
   }
   s->capacity = cap;
