@@ -508,17 +508,36 @@ def side_workloads(torch, args, ce_peak, hbm_peak, seed, device):
         wl = WORKLOADS[key]()
         pool, desc, _, pseed = make_pool(wl.shape, wl.pool_slots, 1, 0, None, seed, "numa", device)
         for tp in tps:
-            shape = wl.shape.with_rank(tp, 0)
-            m, l1 = stage_pass(torch, wl, shape, pool, pseed, steps, 3, 100)
+            # rank 0 of a tp-way split.  `value`: the rank-local pool `bench.py --gpus tp` gives each
+            # rank (its heads only, contiguous); `shared_pool`: the same rank reading its head slice
+            # out of full chunks (strided copies; the /dev/shm shared-segment deployment)
+            runs = {}
+            for which in (("local", "shared") if tp > 1 else ("local",)):
+                if which == "local" and tp > 1:
+                    p_use, _, shape, p_seed = make_pool(wl.shape, wl.pool_slots, tp, 0, None, seed, "numa", device)
+                else:
+                    p_use, shape, p_seed = pool, wl.shape.with_rank(tp, 0), pseed
+                m, l1 = stage_pass(torch, wl, shape, p_use, p_seed, steps, 3, 100)
+                runs[which] = m
+                del l1
+                if p_use is not pool:
+                    p_use.close()
+                torch.cuda.empty_cache()
+            m = runs["local"]
             link = m["bytes"] * steps / m["dev_s"] / 1e9
             out[f"{wl.name}" + (f"_tp{tp}_rank0" if tp > 1 else "")] = {
                 "config": "configs[0]" if key == "llama8b32k" else f"configs[2] tp{tp} (rank 0 on this GPU)",
                 "value": link, "e2e": m["bytes"] * steps / m["wall_s"] / 1e9, "unit": UNIT,
                 "host_link_frac": link / ce_peak, "bytes_per_step": int(m["bytes"]),
                 "ms_per_step": m["dev_s"] / steps * 1e3, "ttft_load_ms": m["ttft"], "steps": steps,
-                "gpu_launches": m["launches"]}
-            del l1
-            torch.cuda.empty_cache()
+                "gpu_launches": m["launches"],
+                "pool": "rank-local (this rank's heads)" if tp > 1 else "full chunks"}
+            if "shared" in runs:
+                ms = runs["shared"]
+                sl = ms["bytes"] * steps / ms["dev_s"] / 1e9
+                out[f"{wl.name}_tp{tp}_rank0"]["shared_pool"] = {
+                    "value": sl, "e2e": ms["bytes"] * steps / ms["wall_s"] / 1e9, "host_link_frac": sl / ce_peak,
+                    "pool": "full chunks, strided head-slice copies"}
         pool.close()
     out["mixed_trace"] = mixed_workload(torch, ce_peak, device)
     out["queue100k"] = queue_workload(torch, hbm_peak)
