@@ -211,9 +211,8 @@ tsb_status tsb_score_queue(tsb_scorer* s, void* stream, int64_t n, const tsb_que
 /* ------------------------------------------------------------------------------------ */
 /* Measurement knob: phase-1 CTAs per SM (0 = default 3). */
 tsb_status tsb_hash_set_grid(int ctas_per_sm);
-/* Measurement knobs: phase-1 L2 prefetch distance in warp groups (0 = off, default 1; 65..128 */
-/* = one bulk TMA prefetch per group at distance v - 64); chain fused into phase 1 (1) or a    */
-/* separate pass (0, default).  -1 keeps the current setting.                                 */
+/* Measurement knobs: phase-1 L2 prefetch distance in warp groups (0 = off, default 1); chain */
+/* fused into phase 1 (1) or a separate pass (0, default).  -1 keeps the current setting.     */
 tsb_status tsb_hash_set_tuning(int prefetch_groups, int fused_chain);
 /* Phase 1 alone: each full chunk's own digest (no chain) at out[chunk_offsets[r] + c]. */
 tsb_status tsb_hash_chunk_digests_device(void* stream, int64_t n_req, const int64_t* offsets,

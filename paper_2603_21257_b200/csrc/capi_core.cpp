@@ -531,8 +531,7 @@ tsb_status tsb_hash_set_grid(int ctas_per_sm) {
 }
 
 tsb_status tsb_hash_set_tuning(int prefetch_groups, int fused_chain) {
-  if (prefetch_groups < -1 || prefetch_groups > 128)
-    return fail(TSB_VALIDATION, "hash_set_tuning: prefetch 0..64 groups (65..128: bulk prefetch of distance v - 64)");
+  if (prefetch_groups < -1 || prefetch_groups > 64) return fail(TSB_VALIDATION, "hash_set_tuning: prefetch 0..64 groups");
   if (fused_chain < -1 || fused_chain > 1) return fail(TSB_VALIDATION, "hash_set_tuning: fused_chain 0 or 1");
   if (prefetch_groups >= 0) tsb::set_hash_prefetch(prefetch_groups);
   if (fused_chain >= 0) tsb::set_hash_fused(fused_chain);

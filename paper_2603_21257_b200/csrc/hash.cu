@@ -183,10 +183,6 @@ __device__ __forceinline__ uint64_t tree16x2(uint64_t v0, uint64_t v1, int j) {
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
-// One TMA-unit prefetch of `bytes` (multiple of 16, 16-byte aligned) into L2.
-__device__ __forceinline__ void prefetch_bulk_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // Per-lane request search (one-time, for the prefetch cursor): first r with co[r + 1] > c.
 __device__ __forceinline__ int64_t lane_request_of(const int64_t* __restrict__ co, int64_t n_req,
@@ -203,9 +199,8 @@ __device__ __forceinline__ int64_t lane_request_of(const int64_t* __restrict__ c
 // u has been folded, so a warp keeps 1-2 rounds (2 KiB each) in flight while it computes.  With
 // pf > 0 every lane also prefetches one 128-byte line of the warp's group pf iterations ahead
 // into L2 (32 lines = the group's 4 chunks), so the loads hit L2 and more bytes are in flight
-// than the registers hold.  kPf = 2 (measurement variant): lane 0 issues one bulk prefetch of the
-// group's whole chunks (up to 4 KiB, clipped at the request end) through the TMA unit instead.
-template <int kPf>
+// than the registers hold.
+template <bool kPf>
 __device__ __forceinline__ void digest_range(int64_t n_req, const int64_t* __restrict__ offsets,
                                              const int32_t* __restrict__ tokens,
                                              const int64_t* __restrict__ chunk_offsets,
@@ -226,7 +221,7 @@ __device__ __forceinline__ void digest_range(int64_t n_req, const int64_t* __res
   cur.nb = chunk_offsets[cur.r + 1];
   cur.tb = offsets[cur.r];
   // prefetch cursor: lane l covers line (l & 7) of chunk (l >> 3) of the group pf iterations on
-  const int64_t pf_off = static_cast<int64_t>(pf) * kStride + (kPf == 2 ? 0 : (lane >> 3));
+  const int64_t pf_off = static_cast<int64_t>(pf) * kStride + (lane >> 3);
   ReqCursor pcur;
   if (kPf) {
     const int64_t pc = min(first + pf_off, total - 1);
@@ -245,19 +240,9 @@ __device__ __forceinline__ void digest_range(int64_t n_req, const int64_t* __res
     }
   }
   for (int64_t c = first; c < c_end; c += kStride) {
-    if (kPf == 1) {
+    if (kPf) {
       const int64_t pc = c + pf_off;
       if (pc < c_end) prefetch_l2(tokens + pcur.base_of(pc, chunk_offsets, offsets) + (lane & 7) * 32);
-    } else if (kPf == 2) {
-      const int64_t pc = c + pf_off;
-      if (lane == 0 && pc < c_end) {
-        const int64_t base = pcur.base_of(pc, chunk_offsets, offsets);
-        const int64_t nch = min(min(int64_t{4}, c_end - pc), pcur.nb - pc);  // whole chunks of one request
-        const uintptr_t a = reinterpret_cast<uintptr_t>(tokens + base);
-        const uintptr_t a16 = a & ~uintptr_t{15};
-        prefetch_bulk_l2(reinterpret_cast<const void*>(a16),
-                         static_cast<uint32_t>((a + static_cast<uintptr_t>(nch) * 1024 - a16) & ~uintptr_t{15}));
-      }
     }
     uint64_t v[2];
 #pragma unroll
@@ -275,7 +260,7 @@ __device__ __forceinline__ void digest_range(int64_t n_req, const int64_t* __res
   }
 }
 
-template <int kPf>
+template <bool kPf>
 __global__ void __launch_bounds__(kHashThreads, 3) k_chunk_digest(
     int64_t n_req, const int64_t* __restrict__ offsets, const int32_t* __restrict__ tokens,
     const int64_t* __restrict__ chunk_offsets, uint64_t* __restrict__ out, int pf) {
@@ -595,10 +580,9 @@ __global__ void k_gen_tokens(uint64_t seed, const int64_t* __restrict__ offsets,
 // group ahead is shipped: +2.5-4% on phase 1 over both layouts, deeper prefetch loses
 // (profiles/r02_k3_prefetch_sweep.jsonl).  The fused chain is a measured variant, no faster.
 static int g_digest_ctas_per_sm = 3;
-static int g_digest_prefetch = 1;  // 1..64: per-lane line prefetch distance; 65..128: bulk, distance v - 64
+static int g_digest_prefetch = 1;
 void set_hash_grid(int ctas_per_sm) { g_digest_ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : 3; }
 void set_hash_prefetch(int groups) { g_digest_prefetch = groups > 0 ? groups : 0; }
-static int line_prefetch() { return g_digest_prefetch > 64 ? g_digest_prefetch - 64 : g_digest_prefetch; }
 
 static int g_fused_chain = 0;
 void set_hash_fused(int on) { g_fused_chain = on; }
@@ -606,12 +590,10 @@ void set_hash_fused(int on) { g_fused_chain = on; }
 static void launch_digest(int64_t n_req, const int64_t* offsets, const int32_t* tokens,
                           const int64_t* chunk_offsets, uint64_t* out, cudaStream_t st) {
   const int grid = 148 * g_digest_ctas_per_sm;
-  if (g_digest_prefetch > 64)
-    k_chunk_digest<2><<<grid, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, g_digest_prefetch - 64);
-  else if (g_digest_prefetch > 0)
-    k_chunk_digest<1><<<grid, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, g_digest_prefetch);
+  if (g_digest_prefetch > 0)
+    k_chunk_digest<true><<<grid, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, g_digest_prefetch);
   else
-    k_chunk_digest<0><<<grid, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, 0);
+    k_chunk_digest<false><<<grid, kHashThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, 0);
   count_launch();
 }
 
@@ -620,7 +602,7 @@ static void launch_fused(int64_t n_req, const int64_t* offsets, const int32_t* t
   const int grid = 148 * g_digest_ctas_per_sm;
   if (g_digest_prefetch > 0)
     k_chunk_hash_fused<true><<<grid, kFusedThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out,
-                                                             line_prefetch());
+                                                             g_digest_prefetch);
   else
     k_chunk_hash_fused<false><<<grid, kFusedThreads, 0, st>>>(n_req, offsets, tokens, chunk_offsets, out, 0);
   count_launch();

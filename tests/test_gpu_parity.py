@@ -859,7 +859,7 @@ def test_hash_aligned_layout_and_phase1(oracle):
     assert not np.array_equal(dig.cpu().numpy(), out.cpu().numpy())  # unchained
 
 
-@pytest.mark.parametrize("cps,pf,fused", [(3, 0, 0), (3, 0, 1), (3, 1, 0), (3, 1, 1), (2, 4, 1), (4, 0, 1), (1, 2, 1), (3, 66, 0), (1, 65, 0)])
+@pytest.mark.parametrize("cps,pf,fused", [(3, 0, 0), (3, 0, 1), (3, 1, 0), (3, 1, 1), (2, 4, 1), (4, 0, 1), (1, 2, 1)])
 def test_hash_tuning_variants_vs_oracle(oracle, cps, pf, fused):
     """Every K3 tuning (grid, L2 prefetch distance, chain fused into phase 1 with the boundary
     straddlers chained after) gives the oracle's hashes: a random queue, one request spanning
