@@ -21,6 +21,9 @@ from paper_2603_21257_b200 import ingest  # noqa: E402
 from paper_2603_21257_b200 import tiersim as t  # noqa: E402
 from paper_2603_21257_b200.stage import LoadStage  # noqa: E402
 
+# TSB_SOAK=N widens both sweeps N-fold (a soak run; the default keeps the suite at ~1 minute)
+SOAK = max(1, int(__import__("os").environ.get("TSB_SOAK", "1")))
+
 
 def _case(seed):
     rng = np.random.default_rng(seed)
@@ -36,7 +39,7 @@ def _case(seed):
     return rng, full, shape, layout, str(rng.choice(modes)), int(rng.integers(5))
 
 
-@pytest.mark.parametrize("seed", range(64))
+@pytest.mark.parametrize("seed", range(64 * SOAK))
 def test_random_stage_runs_verify(seed):
     rng, full, shape, layout, mode, policy = _case(seed)
     n_slots = int(rng.integers(4, 12))
@@ -90,7 +93,7 @@ def test_random_stage_runs_verify(seed):
     assert l1.reserved() == 0 and l1.free_pages() == num_pages
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(12 * SOAK))
 def test_random_online_runs_verify(seed):
     """The real-time loop (tsb_stage_run_online) over random geometries, layouts and HBM-tier
     chunks: arrivals within ~20 ms, prefill burner on; every page verified before release."""
