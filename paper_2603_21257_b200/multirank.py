@@ -1,9 +1,11 @@
 """One process per GPU: KV-head sharding, the shared L2 pool segment, and max-over-ranks timing.
 
 The ingest path shards by KV head, TP-style: rank r of N keeps heads
-[r*H/N, (r+1)*H/N) of every (layer, K/V, token), reads only that slice from the box's one pinned
-pool over its own host link, and never exchanges data with other ranks -- torch.distributed is
-used for barriers and for the max-over-ranks reduction of timings only.
+[r*H/N, (r+1)*H/N) of every (layer, K/V, token) and reads only that slice over its own host link
+-- from a rank-local pinned pool on its GPU's NUMA node holding just those heads (the default,
+bench.py make_pool), or strided out of full chunks in one /dev/shm segment shared by all ranks
+(SharedSegment).  Ranks never exchange data: torch.distributed is used for barriers and for the
+max-over-ranks reduction of timings only.
 """
 from __future__ import annotations
 
