@@ -800,7 +800,7 @@ def run_ours(args):
                "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(k2_alg), "launch_us": k2_s * 1e6,
                "share_of_step": None}
     roofline = {"bound": "host_link",
-                "kernel": "L2->L1 hop: copy engines (cudaMemcpyBatchAsync into the HBM staging ring) + K2 paged "
+                "kernel": "L2->L1 hop: copy engines (cudaMemcpy2DAsync per run of consecutive pool slots into the HBM staging ring) + K2 paged "
                           "scatter; achieved = this GPU's payload bytes over the link / CUDA-event time of the passes",
                 "achieved": link_rate, "peak": ce_peak, "unit": "GB/s", "frac": link_rate / ce_peak,
                 "traffic": None, "peak_source": "live pinned 1 GiB cudaMemcpy H2D, best of 5, this box",

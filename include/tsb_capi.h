@@ -431,10 +431,10 @@ typedef enum {
                               strided cudaMemcpy3DAsync per run of consecutive slots per
                               group.  K2 runs on an internal greatest-priority stream */
   TSB_INGEST_CE_DIRECT = 4 /* copy engines straight into the pages, no SM work at all: one
-                              cudaMemcpyBatchAsync entry per (layer, K|V, run of consecutive
-                              pages); for full-head chunks into flash-attn / NHD pages (the
-                              page segment is contiguous on both sides), else UNSUPPORTED.
-                              What the stage uses while a prefill shares the SMs */
+                              cudaMemcpy3DAsync per (item, run of consecutive pages) covering
+                              K|V x the layers up to the next requested fence; for full-head
+                              chunks into flash-attn / NHD pages (the page segment is
+                              contiguous on both sides), else UNSUPPORTED */
 } tsb_ingest_mode;
 
 /* One pcie_dispatch with real bytes (engine.cpp:427-446; PcieDone engine.cpp:258-272).
@@ -492,11 +492,11 @@ tsb_status tsb_l1_copy_chunks(tsb_l1* l1, const tsb_page_copy* items, int64_t n_
 tsb_status tsb_ingest_set_grid(int zerocopy_ctas, int bulk_ctas, int scatter_ctas);
 /* K2 implementation: 0 = SM 16-byte load/store warps (default), 1 = cp.async.bulk ring. */
 tsb_status tsb_ingest_set_scatter(int impl, int ctas);
-/* CE copy strategy: 0 = one cudaMemcpyAsync per (item, layer), 1 = one cudaMemcpy2DAsync per
- * run of consecutive pool slots, 2 = one cudaMemcpyBatchAsync per staging group (default:
- * 99.6% of the CE peak for any slot order, measured on B200).  Full-head shapes only;
- * head-sharded shapes always use one 3D copy per consecutive-slot run.
- * staging_bytes: HBM staging ring size (0 = default 512 MiB). */
+/* CE copy strategy: 0 = one cudaMemcpyAsync per (item, layer span), 1 = one cudaMemcpy2DAsync
+ * per run of consecutive pool slots (default).  Full-head shapes only; head-sharded shapes
+ * always use one 3D copy per consecutive-slot run.  (The batched-memcpy entry points are not
+ * used: they are closed on this GPU pool after GPU faults.)
+ * staging_bytes: HBM staging ring size (0 = default 1 GiB, two halves). */
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes);
 
 /* ------------------------------------------------------------------------------------ */

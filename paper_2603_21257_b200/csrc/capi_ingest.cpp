@@ -39,7 +39,7 @@ struct Knobs {
   int bulk_ctas = 64;
   int scatter_ctas = 148 * 32;  // HBM-source grid (K2, K1 over device pools): r01 K1 sweep
   int scatter_impl = 0;  // K2: 0 = SM load/store warps, 1 = bulk-copy (TMA engine)
-  int ce_variant = 2;
+  int ce_variant = 1;  // 0 = one cudaMemcpyAsync per item, 1 = one 2D copy per run of consecutive slots
   int64_t staging_bytes = 1ll << 30;  // 2 x 512 MiB: one K2 launch per layer of a 460-chunk request
 };
 Knobs g_knobs;
@@ -872,23 +872,6 @@ tsb_status ce_copy_layers(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it, 
         TSB_CUDA_TRY(cudaMemcpyAsync(stage + k * span, base + it[k].src_slot * src.chunk_bytes, span,
                                      cudaMemcpyHostToDevice, l->ce_stream));
       return TSB_OK;
-    case 2: {
-      std::vector<void*> dst(n), srcp(n);
-      std::vector<size_t> sz(n, static_cast<size_t>(span));
-      for (int64_t k = 0; k < n; ++k) {
-        dst[k] = stage + k * span;
-        srcp[k] = const_cast<uint8_t*>(base + it[k].src_slot * src.chunk_bytes);
-      }
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      attr.srcLocHint.type = cudaMemLocationTypeHost;
-      attr.dstLocHint.type = cudaMemLocationTypeDevice;
-      attr.dstLocHint.id = l->device;
-      size_t idx = 0, fail_idx = 0;
-      TSB_CUDA_TRY(cudaMemcpyBatchAsync(dst.data(), srcp.data(), sz.data(), static_cast<size_t>(n),
-                                        &attr, &idx, 1, &fail_idx, l->ce_stream));
-      return TSB_OK;
-    }
     default: {  // one 2D copy per run of consecutive pool slots (pitch = chunk bytes)
       int64_t k = 0;
       while (k < n) {
@@ -970,11 +953,13 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
   return TSB_OK;
 }
 
-// CE-direct: the copy engines write the pages themselves.  For full-head chunks a (layer, K|V,
-// page j) segment is P contiguous token rows in the chunk and one contiguous page plane, so one
-// batched-memcpy entry moves it; consecutive pages of a chunk that landed on consecutive page ids
-// (flash-attn planes) merge into one entry.  Measured on B200 (profiles/r02_ce_direct_probe.jsonl):
-// 32 KiB entries run at 54.5 GB/s, 512 KiB at 54.7 -- with every SM busy or not.
+// CE-direct: the copy engines write the pages themselves (no SM work).  For full-head chunks a
+// (layer, K|V, page j) segment is P contiguous token rows in the chunk and one contiguous page
+// plane; consecutive pages of a chunk that landed on consecutive page ids (flash-attn planes)
+// merge into one run.  One 3D copy moves a run for K and V (y, pitch = the K|V stride) of every
+// layer up to the next requested fence (z, slice = the layer stride), so a fresh allocator's
+// chunk costs one call per fence span.  The batched-memcpy entry points are closed on this pool
+// (they raised GPU faults); copies are plain per-call cudaMemcpy3DAsync / cudaMemcpyAsync.
 bool ce_direct_ok(const tsb_l1* l, const tsb_pool* pool) {
   return pool->location == TSB_POOL_HOST && l->shape.tp_size == 1 && l->layout != TSB_LAYOUT_FLASHINFER_HND;
 }
@@ -990,50 +975,48 @@ tsb_status ingest_ce_direct(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it
   const tsb::IngestGeom g = make_geom(l, 0, 1);
   const int64_t ppc = l->ppc, seg = g.seg_bytes;
   const bool planes = l->layout == TSB_LAYOUT_FLASH_ATTN;  // consecutive pages are contiguous
-  std::vector<void*> dst, src;
-  std::vector<size_t> sz;
-  dst.reserve(8192);
-  src.reserve(8192);
-  sz.reserve(8192);
-  auto flush = [&]() -> tsb_status {
-    if (dst.empty()) return TSB_OK;
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.srcLocHint.type = cudaMemLocationTypeHost;
-    attr.dstLocHint.type = cudaMemLocationTypeDevice;
-    attr.dstLocHint.id = l->device;
-    size_t attr_idx = 0, fail_idx = 0;
-    TSB_CUDA_TRY(cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), dst.size(), &attr, &attr_idx, 1, &fail_idx,
-                                      l->ce_stream));
-    dst.clear();
-    src.clear();
-    sz.clear();
-    return TSB_OK;
-  };
-  for (int64_t layer = lo; layer < hi; ++layer) {
+  int max_pitch = 0;
+  TSB_CUDA_TRY(cudaDeviceGetAttribute(&max_pitch, cudaDevAttrMaxPitch, l->device));
+  // 3D copies need both K|V strides within the copy engines' pitch limit; else one copy per
+  // (layer, K|V, run).
+  const bool use_3d = g.kv_dst <= max_pitch && g.kv_src <= max_pitch;
+  int64_t layer = lo;
+  while (layer < hi) {
+    int64_t span_end = layer + 1;  // exclusive: the layers up to and including the next fence
+    while (span_end < hi && !(layer_events && layer_events[span_end - 1 - lo])) ++span_end;
+    const int64_t nl = span_end - layer;
     for (int64_t i = 0; i < n_items; ++i) {
       const tsb_ingest_item& it = items_host[i];
       const int32_t* pages = l->bt_host + it.bt_row * l->stride + static_cast<int64_t>(it.chunk_index) * ppc;
       const uint8_t* chunk = pool->host + it.src_slot * g.chunk_bytes + layer * g.layer_src;
-      for (int64_t kv = 0; kv < 2; ++kv) {
-        int64_t j = 0;
-        while (j < ppc) {
-          int64_t e = j + 1;  // extend over consecutive page ids (contiguous in flash-attn planes)
-          while (planes && e < ppc && pages[e] == pages[e - 1] + 1) ++e;
-          dst.push_back(l->arena + layer * g.layer_dst + kv * g.kv_dst + static_cast<int64_t>(pages[j]) * g.page_dst);
-          src.push_back(const_cast<uint8_t*>(chunk + kv * g.kv_src + j * g.P * g.row));
-          sz.push_back(static_cast<size_t>((e - j) * seg));
-          j = e;
+      int64_t j = 0;
+      while (j < ppc) {
+        int64_t e = j + 1;  // extend over consecutive page ids (contiguous in flash-attn planes)
+        while (planes && e < ppc && pages[e] == pages[e - 1] + 1) ++e;
+        const size_t width = static_cast<size_t>((e - j) * seg);
+        const uint8_t* src = chunk + j * g.P * g.row;
+        uint8_t* dst = l->arena + layer * g.layer_dst + static_cast<int64_t>(pages[j]) * g.page_dst;
+        if (use_3d) {
+          cudaMemcpy3DParms p{};
+          p.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(src), static_cast<size_t>(g.kv_src), width,
+                                         static_cast<size_t>(g.layer_src / g.kv_src));
+          p.dstPtr = make_cudaPitchedPtr(dst, static_cast<size_t>(g.kv_dst), width,
+                                         static_cast<size_t>(g.layer_dst / g.kv_dst));
+          p.extent = make_cudaExtent(width, 2, static_cast<size_t>(nl));
+          p.kind = cudaMemcpyHostToDevice;
+          TSB_CUDA_TRY(cudaMemcpy3DAsync(&p, l->ce_stream));
+        } else {
+          for (int64_t ly = 0; ly < nl; ++ly)
+            for (int64_t kv = 0; kv < 2; ++kv)
+              TSB_CUDA_TRY(cudaMemcpyAsync(dst + ly * g.layer_dst + kv * g.kv_dst, src + ly * g.layer_src + kv * g.kv_src,
+                                           width, cudaMemcpyHostToDevice, l->ce_stream));
         }
+        j = e;
       }
-      if (dst.size() >= 8192) TSB_TRY(flush());
     }
-    if (layer_events && layer_events[layer - lo]) {
-      TSB_TRY(flush());
-      TSB_TRY(record_fence(l, layer_events[layer - lo], l->ce_stream));
-    }
+    layer = span_end;
+    if (layer_events && layer_events[layer - 1 - lo]) TSB_TRY(record_fence(l, layer_events[layer - 1 - lo], l->ce_stream));
   }
-  TSB_TRY(flush());
   TSB_CUDA_TRY(cudaEventRecord(l->ev_k2_done, l->ce_stream));
   TSB_CUDA_TRY(cudaStreamWaitEvent(st, l->ev_k2_done, 0));
   return TSB_OK;
@@ -1238,7 +1221,7 @@ tsb_status tsb_ingest_resolve_mode(const tsb_l1* l, const tsb_pool* pool,
 }
 
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes) {
-  if (variant < 0 || variant > 2) return fail(TSB_VALIDATION, "ingest_set_ce: variant must be 0, 1 or 2");
+  if (variant < 0 || variant > 1) return fail(TSB_VALIDATION, "ingest_set_ce: variant must be 0 or 1");
   g_knobs.ce_variant = variant;
   g_knobs.staging_bytes = staging_bytes > 0 ? staging_bytes : (1ll << 30);
   return TSB_OK;

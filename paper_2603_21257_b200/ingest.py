@@ -371,6 +371,6 @@ def resolve_mode(l1: PagedKVCache, pool: ChunkPool, items=None, mode: int = AUTO
     return out.value
 
 
-def set_ce(variant: int = 2, staging_bytes: int = 0):
-    """CE copy strategy: 0 per-item memcpy, 1 2D per consecutive-slot run, 2 batch API (default)."""
+def set_ce(variant: int = 1, staging_bytes: int = 0):
+    """CE copy strategy: 0 per-item memcpy, 1 2D copy per consecutive-slot run (default)."""
     check(lib.tsb_ingest_set_ce(variant, staging_bytes))

@@ -120,8 +120,8 @@ if __name__ == "__main__":
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
     bench_ce_peak()
-    bench_ingest(ingest.LLAMA31_8B, 128, ["ce"], per_layer=True, ce_variants=(0, 1, 2))
-    bench_ingest(ingest.LLAMA31_8B, 128, ["ce"], per_layer=True, ce_variants=(0, 1, 2),
+    bench_ingest(ingest.LLAMA31_8B, 128, ["ce"], per_layer=True, ce_variants=(0, 1))
+    bench_ingest(ingest.LLAMA31_8B, 128, ["ce"], per_layer=True, ce_variants=(0, 1),
                  slots=np.random.default_rng(0).permutation(128))
     bench_ingest(ingest.LLAMA31_8B, 128, ["bulk", "zerocopy", "ce"], per_layer=False)
     bench_ingest(ingest.QWEN25_32B, 460, ["ce", "bulk"], per_layer=True)

@@ -1,8 +1,9 @@
 // Probe: can the copy engines scatter chunks straight into pages (no K2, no SMs)?
-// cudaMemcpyBatchAsync with one entry per (layer, K|V, page) segment -- 32 KiB contiguous on both
-// sides for full-head chunks -- to randomly permuted page destinations, vs one 1 MiB entry per
-// (chunk, layer) into a staging buffer (the current CE+K2 path's copy side).  Also under a
-// concurrent SM-saturating kernel (stand-in for prefill) to show the copy engines are unaffected.
+// One cudaMemcpyAsync per (layer, K|V, page run) segment -- 32 KiB contiguous on both sides per
+// page for full-head chunks -- to randomly permuted page destinations, 32 KiB (fully fragmented
+// pages) to 1 MiB (a chunk's 16 pages on consecutive ids, K and V).  Also under a concurrent
+// SM-saturating kernel (stand-in for prefill) to show the copy engines are unaffected.
+// (r02 first ran this with the batched-memcpy entry point, since closed on this pool.)
 // Probe only; not product code.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ce_direct_probe ce_direct_probe.cu
 #include <cuda_runtime.h>
@@ -39,11 +40,6 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.srcLocHint.type = cudaMemLocationTypeHost;
-  attr.dstLocHint.type = cudaMemLocationTypeDevice;
-  attr.dstLocHint.id = 0;
   std::mt19937_64 rng(1);
   for (size_t seg : {size_t(32) << 10, size_t(64) << 10, size_t(256) << 10, size_t(1) << 20}) {
     const size_t n = bytes / seg;
@@ -51,7 +47,6 @@ int main(int argc, char** argv) {
     std::iota(perm.begin(), perm.end(), 0);
     std::shuffle(perm.begin(), perm.end(), rng);
     std::vector<void*> dst(n), src(n);
-    std::vector<size_t> sz(n, seg);
     for (size_t i = 0; i < n; ++i) {
       src[i] = h + i * seg;
       dst[i] = d + perm[i] * seg;
@@ -61,13 +56,7 @@ int main(int argc, char** argv) {
       for (int rep = 0; rep < 4; ++rep) {
         if (busy) burn<<<148 * 8, 256, 0, sb>>>(sink, 1 << 22);  // ~tens of ms of full-GPU FMA
         CK(cudaEventRecord(a, s));
-        // batches of <= 4096 entries per call (a staging-group-sized call)
-        for (size_t i0 = 0; i0 < n; i0 += 4096) {
-          const size_t k = std::min<size_t>(4096, n - i0);
-          size_t attr_idx = 0, fail_idx = 0;
-          CK(cudaMemcpyBatchAsync(dst.data() + i0, src.data() + i0, sz.data() + i0, k, &attr, &attr_idx, 1, &fail_idx,
-                                  s));
-        }
+        for (size_t i = 0; i < n; ++i) CK(cudaMemcpyAsync(dst[i], src[i], seg, cudaMemcpyHostToDevice, s));
         CK(cudaEventRecord(b, s));
         CK(cudaEventSynchronize(b));
         CK(cudaStreamSynchronize(sb));
@@ -75,7 +64,7 @@ int main(int argc, char** argv) {
         CK(cudaEventElapsedTime(&ms, a, b));
         best = std::min(best, ms);
       }
-      printf("{\"probe\": \"ce_batch_scatter\", \"segment_bytes\": %zu, \"entries\": %zu, \"sm_busy\": %d, "
+      printf("{\"probe\": \"ce_percall_scatter\", \"segment_bytes\": %zu, \"entries\": %zu, \"sm_busy\": %d, "
              "\"GBps\": %.2f}\n", seg, n, busy, bytes / (best * 1e-3) / 1e9);
     }
   }

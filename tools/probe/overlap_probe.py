@@ -58,17 +58,18 @@ def main():
         for _ in range(k):
             wr.run(q, (kv[0], kv[1]))
 
-    def ingest_once(mode):
+    def ingest_once(mode, fenced):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evs = [torch.cuda.Event() for _ in range(shape.layers)] if fenced else None
         a.record(ing)
-        ingest.ingest(l1, pool, items, mode=mode, stream=ing)
+        ingest.ingest(l1, pool, items, mode=mode, stream=ing, layer_events=evs)
         b.record(ing)
         b.synchronize()
         return n * shape.chunk_bytes / (a.elapsed_time(b) * 1e-3) / 1e9
 
-    for mode_name in ("ce_direct", "ce"):
+    for mode_name, fenced in (("ce_direct", False), ("ce_direct", True), ("ce", False), ("ce", True)):
         mode = ingest.MODES[mode_name]
-        ingest_once(mode)
+        ingest_once(mode, fenced)
         for load in ("none", "gemm", "attention", "both"):
             torch.cuda.synchronize()
             with torch.cuda.stream(comp):
@@ -76,10 +77,11 @@ def main():
                     gemms(60)
                 if load in ("attention", "both"):
                     attn(40)
-            gbs = ingest_once(mode)
+            gbs = ingest_once(mode, fenced)
             busy = not comp.query()
             torch.cuda.synchronize()
-            print(json.dumps({"probe": "ingest_under_prefill", "mode": mode_name, "concurrent": load, "GBps": round(gbs, 2),
+            print(json.dumps({"probe": "ingest_under_prefill", "mode": mode_name, "per_layer_fences": fenced,
+                              "concurrent": load, "GBps": round(gbs, 2),
                               "prefill_still_running_at_end": busy}), flush=True)
 
 
