@@ -241,14 +241,11 @@ tsb_status grow_events(std::vector<cudaEvent_t>& v, size_t n, unsigned flags) {
   return TSB_OK;
 }
 
-// The ingest mode a run uses: while a prefill shares the GPU (K6 or a consumer hook) and the
-// caller left the choice to AUTO, the copy engines write the pages directly when the geometry
-// allows -- ingest then takes no SM time from prefill and prefill cannot stall it.
-int ingest_mode(const tsb_stage* s, const tsb_stage_options* opt) {
-  if (opt->mode == TSB_INGEST_AUTO && (opt->prefill || s->hook) && tsb_ingest_ce_direct_supported(s->l1, s->pool))
-    return TSB_INGEST_CE_DIRECT;
-  return opt->mode;
-}
+// The ingest mode a run uses: the caller's choice; AUTO resolves per call (CE + K2 for host
+// pools).  While a prefill shares the GPU the stage keeps CE + K2: with per-layer fences it holds
+// 54.4-55.0 GB/s beside GEMMs and attention, where CE-direct's per-call page copies reach 43-45
+// (repo:profiles/r02_overlap_probe_percall.jsonl).
+int ingest_mode(const tsb_stage*, const tsb_stage_options* opt) { return opt->mode; }
 
 // Enqueues a request's prefill on the compute stream: for each layer, wait on its fence (may be
 // null = no wait), then the caller's hook or the K6 burner for that layer's share of `secs`.

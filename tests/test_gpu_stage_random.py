@@ -35,7 +35,7 @@ def _case(seed):
                           dtype_bytes=int(rng.choice([1, 2])), chunk_tokens=chunk, page_tokens=page)
     shape = full.with_rank(tp, int(rng.integers(tp)))
     layout = int(rng.integers(3))
-    modes = ["auto", "ce", "zerocopy", "bulk"]
+    modes = ["auto", "ce", "zerocopy", "bulk"] + (["ce_direct"] if tp == 1 and layout != 2 else [])
     return rng, full, shape, layout, str(rng.choice(modes)), int(rng.integers(5))
 
 
@@ -85,7 +85,7 @@ def test_random_stage_runs_verify(seed):
     want = po.sort_order(pr, q.arrival, q.id)
     assert list(np.argsort(res.requests["pick_position"])) == list(want)
     # the same batch with reuse_l1 (K8 replication from live holders) and a K6 prefill sharing the GPU
-    # (AUTO then resolves to CE-direct where the geometry allows)
+    # (AUTO resolves per call as without the prefill: CE + K2 for host pools)
     res2 = stage.run(q, slot_lists, cfg, policy=policy, verify_seed=1000 + seed, reuse_l1=True, prefill=True,
                      layer_events=bool(seed % 2))
     assert res2.stats["verify_mismatches"] == 0, (seed, "reuse", layout)
