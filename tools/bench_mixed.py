@@ -125,6 +125,8 @@ def main():
                     help="k6: the calibrated timer; real: PagedPrefill (FlashInfer paged attention over the "
                          "ingested pages + Llama-3.1-8B-sized bf16 GEMMs per layer) as the stage's prefill hook")
     ap.add_argument("--n", type=int, default=48)
+    ap.add_argument("--mode", default="auto", choices=["auto", "ce", "ce_direct", "zerocopy", "bulk"],
+                    help="the stage's ingest mode (AUTO: CE + K2 for the host pool)")
     ap.add_argument("--profile", default="", help="write a kineto (CUPTI) timeline summary of the overlapped run here")
     args = ap.parse_args()
     shape = ingest.LLAMA31_8B
@@ -146,7 +148,7 @@ def main():
     stage = LoadStage(l1, pool)
     out = {"workload": f"configs[3]: {n} requests, 2K-128K prefixes (lognormal mean 24K, cv 1.0), hit in "
                        f"{{0.25,0.5,0.75,0.9,1.0}}, Llama-3.1-8B KV, L1 {num_pages * shape.page_bytes / 2**30:.0f} GiB",
-           "chunks": int(sum(plans)), "bytes": int(sum(plans) * shape.local_chunk_bytes)}
+           "chunks": int(sum(plans)), "bytes": int(sum(plans) * shape.local_chunk_bytes), "ingest_mode": args.mode}
     stage.run(q, slots, cfg, verify_seed=5)  # warm-up + full parity check
     consumer = None
     if args.consumer == "real":
@@ -165,7 +167,7 @@ def main():
             stage.set_prefill_hook(None)
         if consumer is not None:
             consumer.host_s = consumer.host_max_s = consumer.plan_s = 0.0
-        r = stage.run(q, slots, cfg, **kw)
+        r = stage.run(q, slots, cfg, mode=ingest.MODES[args.mode], **kw)
         if consumer is not None:
             stage.set_prefill_hook(consumer)
         req = r.requests
@@ -194,7 +196,7 @@ def main():
         from torch.profiler import ProfilerActivity, profile
 
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            stage.run(q, slots, cfg, prefill=True, layer_events=True)
+            stage.run(q, slots, cfg, prefill=True, layer_events=True, mode=ingest.MODES[args.mode])
             torch.cuda.synchronize()
         out["timeline"] = timeline_summary(prof, args.profile)
 
