@@ -127,10 +127,13 @@ def main():
     ap.add_argument("--n", type=int, default=48)
     ap.add_argument("--mode", default="auto", choices=["auto", "ce", "ce_direct", "zerocopy", "bulk"],
                     help="the stage's ingest mode (AUTO: CE + K2 for the host pool)")
+    ap.add_argument("--k2-ctas", type=int, default=0, help="K2 grid (0 = default 148 x 32)")
     ap.add_argument("--profile", default="", help="write a kineto (CUPTI) timeline summary of the overlapped run here")
     args = ap.parse_args()
     shape = ingest.LLAMA31_8B
     n = args.n
+    if args.k2_ctas:
+        ingest.set_grid(scatter_ctas=args.k2_ctas)
     q = mixed_batch(n, 0)
     cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(32, 8, 128, 2),
                           compute_per_token=args.compute_per_token)
@@ -148,7 +151,8 @@ def main():
     stage = LoadStage(l1, pool)
     out = {"workload": f"configs[3]: {n} requests, 2K-128K prefixes (lognormal mean 24K, cv 1.0), hit in "
                        f"{{0.25,0.5,0.75,0.9,1.0}}, Llama-3.1-8B KV, L1 {num_pages * shape.page_bytes / 2**30:.0f} GiB",
-           "chunks": int(sum(plans)), "bytes": int(sum(plans) * shape.local_chunk_bytes), "ingest_mode": args.mode}
+           "chunks": int(sum(plans)), "bytes": int(sum(plans) * shape.local_chunk_bytes), "ingest_mode": args.mode,
+           "k2_ctas": args.k2_ctas or 148 * 32}
     stage.run(q, slots, cfg, verify_seed=5)  # warm-up + full parity check
     consumer = None
     if args.consumer == "real":
