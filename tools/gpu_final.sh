@@ -13,3 +13,4 @@ nproc > gpurun_out/final_platform.txt; lscpu | grep -E "Model name|NUMA|Socket|T
 nvidia-smi --query-gpu=name,clocks.max.sm,clocks.sm,power.limit,pcie.link.gen.current,pcie.link.width.current --format=csv >> gpurun_out/final_platform.txt
 bash tools/ncu_r02.sh
 bash tools/sanitize_r02.sh
+timeout 900 python bench.py --gpus 2 --one-device --workload llama70b32k --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/final_bench_2rank_onedevice.json 2> gpurun_out/final_bench_2rank_onedevice.err; echo "2-rank one-device rc=$?"
