@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -128,12 +129,15 @@ def main():
     ap.add_argument("--mode", default="auto", choices=["auto", "ce", "ce_direct", "zerocopy", "bulk"],
                     help="the stage's ingest mode (AUTO: CE + K2 for the host pool)")
     ap.add_argument("--k2-ctas", type=int, default=0, help="K2 grid (0 = default 148 x 32)")
+    ap.add_argument("--staging-mib", type=int, default=0, help="CE staging ring, both halves (0 = default 1024)")
     ap.add_argument("--profile", default="", help="write a kineto (CUPTI) timeline summary of the overlapped run here")
     args = ap.parse_args()
     shape = ingest.LLAMA31_8B
     n = args.n
     if args.k2_ctas:
         ingest.set_grid(scatter_ctas=args.k2_ctas)
+    if args.staging_mib:
+        ingest.set_ce(1, args.staging_mib << 20)
     q = mixed_batch(n, 0)
     cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(32, 8, 128, 2),
                           compute_per_token=args.compute_per_token)
@@ -152,7 +156,8 @@ def main():
     out = {"workload": f"configs[3]: {n} requests, 2K-128K prefixes (lognormal mean 24K, cv 1.0), hit in "
                        f"{{0.25,0.5,0.75,0.9,1.0}}, Llama-3.1-8B KV, L1 {num_pages * shape.page_bytes / 2**30:.0f} GiB",
            "chunks": int(sum(plans)), "bytes": int(sum(plans) * shape.local_chunk_bytes), "ingest_mode": args.mode,
-           "k2_ctas": args.k2_ctas or 148 * 32}
+           "k2_ctas": args.k2_ctas or 148 * 32, "staging_mib": args.staging_mib or 1024,
+           "max_connections": os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "default")}
     stage.run(q, slots, cfg, verify_seed=5)  # warm-up + full parity check
     consumer = None
     if args.consumer == "real":
