@@ -170,10 +170,20 @@ def make_pool(shape_full, n_slots, world, rank, dist, seed, kind, device):
         seg.unlink()  # every rank has mapped and registered it: nothing outlives the run
         return pool, "shared /dev/shm segment of full chunks, cudaHostRegister'ed by every rank", \
             shape_full.with_rank(world, rank), seed
+    def create_numa(shape):
+        # mbind can be refused (a container's seccomp policy): place the pages by first touch then
+        try:
+            return ingest.ChunkPool.create_numa(shape, n_slots, node)
+        except Exception as e:  # noqa: BLE001
+            if node < 0:
+                raise
+            print(f"[bench] NUMA binding to node {node} refused ({e}); default placement", file=sys.stderr)
+            return ingest.ChunkPool.create_numa(shape, n_slots, -1)
+
     if world > 1:
         local = ingest.KVShape(shape_full.layers, shape_full.kv_heads // world, shape_full.head_dim,
                                shape_full.dtype_bytes, shape_full.chunk_tokens, shape_full.page_tokens)
-        pool = ingest.ChunkPool.create_numa(local, n_slots, node)
+        pool = create_numa(local)
         pool.fill_synthetic(seed + rank)
         return pool, f"rank-local pinned pool of this rank's KV heads on NUMA node {pool.numa_node} " \
                      f"(GPU's node {node}; tsb_pool_create_numa)", local, seed + rank
@@ -181,7 +191,7 @@ def make_pool(shape_full, n_slots, world, rank, dist, seed, kind, device):
         pool = ingest.ChunkPool(shape_full, n_slots)
         desc = "cudaHostAlloc portable|mapped"
     else:
-        pool = ingest.ChunkPool.create_numa(shape_full, n_slots, node)
+        pool = create_numa(shape_full)
         desc = f"pinned pool on NUMA node {pool.numa_node} (GPU's node {node}; tsb_pool_create_numa)"
     pool.fill_synthetic(seed)
     return pool, desc, shape_full, seed
