@@ -498,6 +498,11 @@ tsb_status tsb_ingest_set_scatter(int impl, int ctas);
  * used: they are closed on this GPU pool after GPU faults.)
  * staging_bytes: HBM staging ring size (0 = default 1 GiB, two halves). */
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes);
+/* Per-L1 cap on one CE staging group (bytes of one half of the ring a group may fill; 0 = the
+ * whole half).  Smaller groups shorten each copy-engine wait that a scatter launch sits behind;
+ * the load stage sets it while a prefill shares the GPU (tsb_stage_options.prefill or a hook). */
+tsb_status tsb_l1_set_ce_group_bytes(tsb_l1* l1, int64_t bytes);
+int64_t tsb_l1_ce_group_bytes(const tsb_l1* l1);
 
 /* ------------------------------------------------------------------------------------ */
 /* Load stage: the real-time L2->L1 dispatcher.  Follows SimEngine's dispatch semantics    */

@@ -215,6 +215,8 @@ _decl("tsb_l1_sync_block_table", st, vp, vp)
 _decl("tsb_ingest", st, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_device", st, vp, vp, vp, i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_set_ce", st, C.c_int, i64)
+_decl("tsb_l1_set_ce_group_bytes", st, vp, i64)
+_decl("tsb_l1_ce_group_bytes", i64, vp)
 _decl("tsb_ingest_tiered", st, vp, vp, vp, P(IngestItem), i64, i64, i64, C.c_int, vp, P(vp))
 _decl("tsb_ingest_ce_direct_supported", C.c_int, vp, vp)
 _decl("tsb_ingest_resolve_mode", st, vp, vp, P(IngestItem), i64, C.c_int, P(C.c_int))

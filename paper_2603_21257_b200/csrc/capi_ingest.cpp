@@ -391,6 +391,7 @@ struct tsb_l1 {
   UploadRing ring_items;
   uint8_t* staging = nullptr;  // CE staging (lazy)
   int64_t staging_bytes = 0;
+  int64_t group_cap = 0;       // CE staging-group cap in bytes (0: one half of the ring)
   cudaStream_t ce_stream = nullptr;
   cudaStream_t k2_stream = nullptr;  // K2 at the greatest stream priority: ahead of prefill kernels
   cudaEvent_t ev_k2_done = nullptr;
@@ -913,7 +914,9 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
   const int64_t lb = make_staged_geom(l, lo).layer_src;
   const int64_t half = l->staging_bytes / 2;
   if (lb > half) return fail(TSB_UNSUPPORTED, "ingest CE: one chunk layer exceeds the staging ring");
-  const int64_t items_per_half = half / lb;
+  // A group fills at most `cap` bytes of its half (at least one item-layer).
+  const int64_t cap = l->group_cap > 0 ? std::max(lb, std::min(half, l->group_cap)) : half;
+  const int64_t items_per_half = cap / lb;
   // Host reads are ordered after the work already queued on `st` (stream semantics).
   TSB_CUDA_TRY(cudaEventRecord(l->ev_fence, st));
   TSB_CUDA_TRY(cudaStreamWaitEvent(l->ce_stream, l->ev_fence, 0));
@@ -927,7 +930,7 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
       while (span_end < hi && !layer_events[span_end - 1 - lo]) ++span_end;
     }
     const int64_t nl = n_items <= items_per_half
-                           ? std::max<int64_t>(1, std::min(span_end - layer, half / (n_items * lb)))
+                           ? std::max<int64_t>(1, std::min(span_end - layer, cap / (n_items * lb)))
                            : 1;
     const int64_t per_group = n_items <= items_per_half ? n_items : items_per_half;
     const tsb::IngestGeom g = make_staged_geom(l, layer, nl);
@@ -1234,6 +1237,15 @@ tsb_status tsb_ingest_resolve_mode(const tsb_l1* l, const tsb_pool* pool,
   *resolved = resolve_mode(l, pool, mode, items, n_items);
   return TSB_OK;
 }
+
+tsb_status tsb_l1_set_ce_group_bytes(tsb_l1* l, int64_t bytes) {
+  if (!l) return fail(TSB_VALIDATION, "l1_set_ce_group_bytes: null L1");
+  if (bytes < 0) return fail(TSB_VALIDATION, "l1_set_ce_group_bytes: bytes must be >= 0");
+  l->group_cap = bytes;
+  return TSB_OK;
+}
+
+int64_t tsb_l1_ce_group_bytes(const tsb_l1* l) { return l ? l->group_cap : 0; }
 
 tsb_status tsb_ingest_set_ce(int variant, int64_t staging_bytes) {
   if (variant < 0 || variant > 1) return fail(TSB_VALIDATION, "ingest_set_ce: variant must be 0 or 1");

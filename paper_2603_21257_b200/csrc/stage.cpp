@@ -247,6 +247,24 @@ tsb_status grow_events(std::vector<cudaEvent_t>& v, size_t n, unsigned flags) {
 // (repo:profiles/r02_overlap_probe_percall.jsonl).
 int ingest_mode(const tsb_stage*, const tsb_stage_options* opt) { return opt->mode; }
 
+// While a prefill shares the GPU, the stage caps CE staging groups at 128 MiB (unless the caller
+// set a cap on the L1): with K6 at 4 us/token, 512 MiB groups delay the prefill start of each
+// request (mean TTFT 865 vs 842 ms, DES error 8.5% vs 2.9%) at the same ingest rate and the same
+// real-consumer TTFT; 64 MiB groups start to cost link rate (repo:profiles/r02_ce_group_under_prefill.jsonl).
+constexpr int64_t kPrefillGroupBytes = 128ll << 20;
+
+class GroupCapScope {
+ public:
+  GroupCapScope(tsb_l1* l1, bool prefill) : l1_(l1), prev_(tsb_l1_ce_group_bytes(l1)) {
+    if (prefill && prev_ == 0) tsb_l1_set_ce_group_bytes(l1_, kPrefillGroupBytes);
+  }
+  ~GroupCapScope() { tsb_l1_set_ce_group_bytes(l1_, prev_); }
+
+ private:
+  tsb_l1* l1_;
+  int64_t prev_;
+};
+
 // Enqueues a request's prefill on the compute stream: for each layer, wait on its fence (may be
 // null = no wait), then the caller's hook or the K6 burner for that layer's share of `secs`.
 tsb_status enqueue_prefill(tsb_stage* s, int64_t q_index, int32_t bt_row, double secs,
@@ -442,6 +460,7 @@ tsb_status tsb_stage_run(tsb_stage* s, int64_t n, const tsb_queue* q, const tsb_
     return fail(TSB_UNSUPPORTED, "stage: the L3 network stage runs in tsb_stage_run_online only");
   const bool coupled = c->control_mode == 0;
   const int mode = ingest_mode(s, opt);
+  GroupCapScope group_cap(s->l1, opt->prefill || s->hook);
   s->trace.clear();
   s->seq = 0;
   auto row = [&](double t, int kind, int stg, int tier, int64_t rid, int32_t blk, int64_t bytes) {
@@ -787,6 +806,7 @@ tsb_status tsb_stage_run_online(tsb_stage* s, int64_t n, const tsb_queue* q,
   if (reuse && use_l3)
     return fail(TSB_UNSUPPORTED, "stage: reuse_l1 with an L3 store (blocks pass through L2 slots, not pool slots)");
   const int mode = ingest_mode(s, opt);
+  GroupCapScope group_cap(s->l1, opt->prefill || s->hook);
   const int64_t l2_slot_bytes = tsb_pool_chunk_bytes(s->pool);
   s->trace.clear();
   s->seq = 0;

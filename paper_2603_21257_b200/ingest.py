@@ -232,6 +232,15 @@ class PagedKVCache:
         self.layout = layout
 
     @property
+    def ce_group_bytes(self) -> int:
+        """Cap on one CE staging group (0: half of the staging ring; tsb_l1_set_ce_group_bytes)."""
+        return int(lib.tsb_l1_ce_group_bytes(self.handle))
+
+    @ce_group_bytes.setter
+    def ce_group_bytes(self, nbytes: int):
+        check(lib.tsb_l1_set_ce_group_bytes(self.handle, int(nbytes)))
+
+    @property
     def handle(self):
         return self._h
 

@@ -644,6 +644,26 @@ def test_ce_layer_groups_with_subranges_and_fences(oracle, tp):
 
 
 @pytest.mark.parametrize("tp", [(1, 0), (4, 1)])
+def test_ce_group_cap_bit_exact(oracle, tp):
+    """A per-L1 CE group cap of 3 item-layers (what the stage applies, at 128 MiB, while a prefill
+    runs): groups of 3 items per layer inside the 1 GiB ring, with per-layer fences."""
+    shape = SMALL.with_rank(*tp)
+    lb = 2 * shape.chunk_tokens * shape.heads_local * shape.head_dim * shape.dtype_bytes
+    pool, l1, items = build_scenario(shape)
+    assert l1.ce_group_bytes == 0
+    l1.ce_group_bytes = 3 * lb
+    assert l1.ce_group_bytes == 3 * lb
+    evs = [torch.cuda.Event() for _ in range(shape.layers)]
+    ingest.ingest(l1, pool, items, mode=ingest.CE, layer_events=evs)
+    torch.cuda.synchronize()
+    with pytest.raises(t.ValidationError):
+        l1.ce_group_bytes = -1
+    l1.ce_group_bytes = 0
+    want = oracle.scatter_ref(shape, pool.slot_view(0, pool.n_slots), items, l1.block_table(), l1.num_pages)
+    assert np.array_equal(l1.arena.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("tp", [(1, 0), (4, 1)])
 def test_ce_small_staging_splits_items(oracle, tp):
     """A staging half that holds 3 item-layers: CE splits the items of each layer into groups of 3
     (no layer grouping), ping-ponging the two halves many times per call."""

@@ -172,6 +172,11 @@ def test_stage_synthetic_prefill_overlap():
     assert np.all(r["done_ms"] >= r["resident_ms"])
     prefill_s = cfg.compute_base + cfg.compute_per_token * 500
     assert r["done_ms"].max() * 1e-3 >= 6 * prefill_s * 0.9
+    # the stage's 128 MiB CE group cap under a prefill is scoped to the run; a caller's cap stays
+    assert l1.ce_group_bytes == 0
+    l1.ce_group_bytes = 3 << 20
+    res = stage.run(q, slots, cfg, mode=ingest.CE, layer_events=True, prefill=True, verify_seed=2)
+    assert res.stats["verify_mismatches"] == 0 and l1.ce_group_bytes == 3 << 20
 
 
 @pytest.mark.parametrize("layer_events", [False, True])
