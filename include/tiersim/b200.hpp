@@ -96,6 +96,10 @@ class PagedAllocator {
   std::int64_t capacity() const { return tsb_l1_capacity(l_.get()); }
   std::int64_t reserved() const { return tsb_l1_reserved(l_.get()); }
   std::int64_t page_bytes() const { return tsb_l1_page_bytes(l_.get()); }
+  /// Cap on one copy-engine staging group (0: half of the ring; the load stage applies 128 MiB
+  /// while a prefill shares the GPU unless a cap is set here).
+  void set_ce_group_bytes(std::int64_t bytes) { check(tsb_l1_set_ce_group_bytes(l_.get(), bytes)); }
+  std::int64_t ce_group_bytes() const { return tsb_l1_ce_group_bytes(l_.get()); }
   void* layer(std::int64_t l) { return tsb_l1_layer_ptr(l_.get(), l); }
   const int32_t* block_table() const { return tsb_l1_block_table_host(l_.get()); }
   tsb_l1* handle() { return l_.get(); }

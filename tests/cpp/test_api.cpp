@@ -287,6 +287,13 @@ static void gpu_cases() {
     const auto r = stage.run(batch, slots, cfg, cost_models_from_config(cfg), opt);
     EXPECT(r.stats.verify_mismatches == 0 && r.stats.deferred_chunks > 0 && l1.reserved() == 0);
     EXPECT(r.stats.bytes == 9 * 256 * cfg.bytes_per_token);
+    // one item-layer per copy-engine group (the knob the stage sets itself under a prefill)
+    l1.set_ce_group_bytes(2 * 256 * 8 * 128 * 2);
+    EXPECT(l1.ce_group_bytes() == 2 * 256 * 8 * 128 * 2);
+    opt.mode = TSB_INGEST_CE;
+    opt.verify_seed = 78;
+    const auto r2 = stage.run(batch, slots, cfg, cost_models_from_config(cfg), opt);
+    EXPECT(r2.stats.verify_mismatches == 0 && l1.reserved() == 0);
   });
   run("gpu: pick_next drain == schedule_order, keys computed once per request", [] {
     std::vector<RequestSpec> q;
