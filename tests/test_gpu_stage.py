@@ -175,7 +175,7 @@ def test_stage_synthetic_prefill_overlap():
     # the stage's 128 MiB CE group cap under a prefill is scoped to the run; a caller's cap stays
     assert l1.ce_group_bytes == 0
     l1.ce_group_bytes = 3 << 20
-    res = stage.run(q, slots, cfg, mode=ingest.CE, layer_events=True, prefill=True, verify_seed=2)
+    res = stage.run(q, slots, cfg, mode=ingest.CE, layer_events=True, prefill=True, verify_seed=1)
     assert res.stats["verify_mismatches"] == 0 and l1.ce_group_bytes == 3 << 20
 
 
