@@ -291,7 +291,7 @@ static void gpu_cases() {
     l1.set_ce_group_bytes(2 * 256 * 8 * 128 * 2);
     EXPECT(l1.ce_group_bytes() == 2 * 256 * 8 * 128 * 2);
     opt.mode = TSB_INGEST_CE;
-    opt.verify_seed = 78;
+    opt.verify_seed = 77;  // the pools hold seed 77
     const auto r2 = stage.run(batch, slots, cfg, cost_models_from_config(cfg), opt);
     EXPECT(r2.stats.verify_mismatches == 0 && l1.reserved() == 0);
   });
