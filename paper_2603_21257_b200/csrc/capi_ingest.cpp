@@ -959,9 +959,10 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
 // CE-direct: the copy engines write the pages themselves (no SM work).  For full-head chunks a
 // (layer, K|V, page j) segment is P contiguous token rows in the chunk and one contiguous page
 // plane; consecutive pages of a chunk that landed on consecutive page ids (flash-attn planes)
-// merge into one run.  One 3D copy moves a run for K and V (y, pitch = the K|V stride) of every
-// layer up to the next requested fence (z, slice = the layer stride), so a fresh allocator's
-// chunk costs one call per fence span.  The batched-memcpy entry points are closed on this pool
+// merge into one run, and runs that advance by constant strides on both sides (a document's
+// chunks in consecutive slots on consecutive pages) merge into one 2D copy per (layer, K|V).
+// A lone run moves K and V (y, pitch = the K|V stride) of every layer up to the next requested
+// fence (z, slice = the layer stride) in one 3D copy.  The batched-memcpy entry points are closed on this pool
 // (they raised GPU faults); copies are plain per-call cudaMemcpy3DAsync / cudaMemcpyAsync.
 bool ce_direct_ok(const tsb_l1* l, const tsb_pool* pool) {
   return pool->location == TSB_POOL_HOST && l->shape.tp_size == 1 && l->layout != TSB_LAYOUT_FLASHINFER_HND;
@@ -980,41 +981,81 @@ tsb_status ingest_ce_direct(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* it
   const bool planes = l->layout == TSB_LAYOUT_FLASH_ATTN;  // consecutive pages are contiguous
   int max_pitch = 0;
   TSB_CUDA_TRY(cudaDeviceGetAttribute(&max_pitch, cudaDevAttrMaxPitch, l->device));
-  // 3D copies need both K|V strides within the copy engines' pitch limit; else one copy per
-  // (layer, K|V, run).
+  // Runs of one layer's K plane (V and the other layers sit at fixed offsets): (item, pages j..e)
+  // with consecutive page ids.  Runs of equal width whose source and destination both advance by
+  // a constant stride form a strip -- e.g. the chunks of a document in consecutive slots landing
+  // on consecutive pages -- and a strip is one 2D copy per (layer, K|V).
+  struct Run {
+    int64_t src, dst, width;  // byte offsets: pool slot area, arena (layer 0, K)
+  };
+  std::vector<Run> runs;
+  runs.reserve(static_cast<size_t>(n_items));
+  for (int64_t i = 0; i < n_items; ++i) {
+    const tsb_ingest_item& it = items_host[i];
+    const int32_t* pages = l->bt_host + it.bt_row * l->stride + static_cast<int64_t>(it.chunk_index) * ppc;
+    int64_t j = 0;
+    while (j < ppc) {
+      int64_t e = j + 1;
+      while (planes && e < ppc && pages[e] == pages[e - 1] + 1) ++e;
+      runs.push_back(Run{it.src_slot * g.chunk_bytes + j * g.P * g.row, static_cast<int64_t>(pages[j]) * g.page_dst,
+                         (e - j) * seg});
+      j = e;
+    }
+  }
+  struct Strip {
+    size_t first, count;
+    int64_t spitch, dpitch;
+  };
+  std::vector<Strip> strips;
+  for (size_t k = 0; k < runs.size();) {
+    Strip sp{k, 1, 0, 0};
+    if (k + 1 < runs.size() && runs[k + 1].width == runs[k].width) {
+      sp.spitch = runs[k + 1].src - runs[k].src;
+      sp.dpitch = runs[k + 1].dst - runs[k].dst;
+      if (sp.spitch >= runs[k].width && sp.dpitch >= runs[k].width && sp.spitch <= max_pitch && sp.dpitch <= max_pitch) {
+        sp.count = 2;
+        while (k + sp.count < runs.size() && runs[k + sp.count].width == runs[k].width &&
+               runs[k + sp.count].src - runs[k + sp.count - 1].src == sp.spitch &&
+               runs[k + sp.count].dst - runs[k + sp.count - 1].dst == sp.dpitch)
+          ++sp.count;
+      }
+    }
+    strips.push_back(sp);
+    k += sp.count;
+  }
+  // A single run moves K|V x the span's layers in one 3D copy when both K|V strides are within
+  // the copy engines' pitch limit.
   const bool use_3d = g.kv_dst <= max_pitch && g.kv_src <= max_pitch;
   int64_t layer = lo;
   while (layer < hi) {
     int64_t span_end = layer + 1;  // exclusive: the layers up to and including the next fence
     while (span_end < hi && !(layer_events && layer_events[span_end - 1 - lo])) ++span_end;
     const int64_t nl = span_end - layer;
-    for (int64_t i = 0; i < n_items; ++i) {
-      const tsb_ingest_item& it = items_host[i];
-      const int32_t* pages = l->bt_host + it.bt_row * l->stride + static_cast<int64_t>(it.chunk_index) * ppc;
-      const uint8_t* chunk = pool->host + it.src_slot * g.chunk_bytes + layer * g.layer_src;
-      int64_t j = 0;
-      while (j < ppc) {
-        int64_t e = j + 1;  // extend over consecutive page ids (contiguous in flash-attn planes)
-        while (planes && e < ppc && pages[e] == pages[e - 1] + 1) ++e;
-        const size_t width = static_cast<size_t>((e - j) * seg);
-        const uint8_t* src = chunk + j * g.P * g.row;
-        uint8_t* dst = l->arena + layer * g.layer_dst + static_cast<int64_t>(pages[j]) * g.page_dst;
-        if (use_3d) {
-          cudaMemcpy3DParms p{};
-          p.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(src), static_cast<size_t>(g.kv_src), width,
-                                         static_cast<size_t>(g.layer_src / g.kv_src));
-          p.dstPtr = make_cudaPitchedPtr(dst, static_cast<size_t>(g.kv_dst), width,
-                                         static_cast<size_t>(g.layer_dst / g.kv_dst));
-          p.extent = make_cudaExtent(width, 2, static_cast<size_t>(nl));
-          p.kind = cudaMemcpyHostToDevice;
-          TSB_CUDA_TRY(cudaMemcpy3DAsync(&p, l->ce_stream));
-        } else {
-          for (int64_t ly = 0; ly < nl; ++ly)
-            for (int64_t kv = 0; kv < 2; ++kv)
-              TSB_CUDA_TRY(cudaMemcpyAsync(dst + ly * g.layer_dst + kv * g.kv_dst, src + ly * g.layer_src + kv * g.kv_src,
-                                           width, cudaMemcpyHostToDevice, l->ce_stream));
-        }
-        j = e;
+    for (const Strip& sp : strips) {
+      const Run& r = runs[sp.first];
+      const uint8_t* src = pool->host + layer * g.layer_src + r.src;
+      uint8_t* dst = l->arena + layer * g.layer_dst + r.dst;
+      const auto width = static_cast<size_t>(r.width);
+      if (sp.count > 1) {
+        for (int64_t ly = 0; ly < nl; ++ly)
+          for (int64_t kv = 0; kv < 2; ++kv)
+            TSB_CUDA_TRY(cudaMemcpy2DAsync(dst + ly * g.layer_dst + kv * g.kv_dst, static_cast<size_t>(sp.dpitch),
+                                           src + ly * g.layer_src + kv * g.kv_src, static_cast<size_t>(sp.spitch),
+                                           width, sp.count, cudaMemcpyHostToDevice, l->ce_stream));
+      } else if (use_3d) {
+        cudaMemcpy3DParms p{};
+        p.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(src), static_cast<size_t>(g.kv_src), width,
+                                       static_cast<size_t>(g.layer_src / g.kv_src));
+        p.dstPtr = make_cudaPitchedPtr(dst, static_cast<size_t>(g.kv_dst), width,
+                                       static_cast<size_t>(g.layer_dst / g.kv_dst));
+        p.extent = make_cudaExtent(width, 2, static_cast<size_t>(nl));
+        p.kind = cudaMemcpyHostToDevice;
+        TSB_CUDA_TRY(cudaMemcpy3DAsync(&p, l->ce_stream));
+      } else {
+        for (int64_t ly = 0; ly < nl; ++ly)
+          for (int64_t kv = 0; kv < 2; ++kv)
+            TSB_CUDA_TRY(cudaMemcpyAsync(dst + ly * g.layer_dst + kv * g.kv_dst, src + ly * g.layer_src + kv * g.kv_src,
+                                         width, cudaMemcpyHostToDevice, l->ce_stream));
       }
     }
     layer = span_end;
@@ -1148,7 +1189,8 @@ tsb_status tsb_ingest(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items, i
   // call is free (each names its own pages; fences cover the whole call), so host-pool calls that
   // may go through the copy engines are issued in slot order.
   std::vector<tsb_ingest_item> by_slot;
-  if (pool->location == TSB_POOL_HOST && n_items > 1 && (mode == TSB_INGEST_AUTO || mode == TSB_INGEST_CE)) {
+  if (pool->location == TSB_POOL_HOST && n_items > 1 &&
+      (mode == TSB_INGEST_AUTO || mode == TSB_INGEST_CE || mode == TSB_INGEST_CE_DIRECT)) {
     bool ordered = true;
     for (int64_t k = 1; k < n_items && ordered; ++k) ordered = items[k].src_slot >= items[k - 1].src_slot;
     if (!ordered) {
