@@ -243,8 +243,8 @@ tsb_status grow_events(std::vector<cudaEvent_t>& v, size_t n, unsigned flags) {
 
 // The ingest mode a run uses: the caller's choice; AUTO resolves per call (CE + K2 for host
 // pools).  While a prefill shares the GPU the stage keeps CE + K2: with per-layer fences it holds
-// 54.4-55.0 GB/s beside GEMMs and attention, where CE-direct's per-call page copies reach 43-45
-// (repo:profiles/r02_overlap_probe_percall.jsonl).
+// 54.8-55.1 GB/s beside GEMMs and attention, and the real consumer runs 1% faster beside it than
+// beside CE-direct's page writes (repo:profiles/r02_stage_mode_ab_strips.jsonl).
 int ingest_mode(const tsb_stage*, const tsb_stage_options* opt) { return opt->mode; }
 
 // While a prefill shares the GPU, the stage caps CE staging groups at 128 MiB (unless the caller
