@@ -126,6 +126,9 @@ def main():
                     help="k6: the calibrated timer; real: PagedPrefill (FlashInfer paged attention over the "
                          "ingested pages + Llama-3.1-8B-sized bf16 GEMMs per layer) as the stage's prefill hook")
     ap.add_argument("--n", type=int, default=48)
+    ap.add_argument("--uniform", default="", metavar="CTX:HIT",
+                    help="instead of the mixed trace: n requests of CTX tokens at hit ratio HIT (e.g. 32768:0.9, "
+                         "ingest and prefill of one request about equal on B200)")
     ap.add_argument("--mode", default="auto", choices=["auto", "ce", "ce_direct", "zerocopy", "bulk"],
                     help="the stage's ingest mode (AUTO: CE + K2 for the host pool)")
     ap.add_argument("--k2-ctas", type=int, default=0, help="K2 grid (0 = default 148 x 32)")
@@ -138,7 +141,13 @@ def main():
         ingest.set_grid(scatter_ctas=args.k2_ctas)
     if args.staging_mib:
         ingest.set_ce(1, args.staging_mib << 20)
-    q = mixed_batch(n, 0)
+    if args.uniform:
+        u_ctx, u_hit = args.uniform.split(":")
+        q = mixed_batch(n, 0)
+        q.context_tokens[:] = int(u_ctx)
+        q.cache_hit_ratio[:] = float(u_hit)
+    else:
+        q = mixed_batch(n, 0)
     cfg = t.ClusterConfig(bytes_per_token=t.kv_bytes_per_token(32, 8, 128, 2),
                           compute_per_token=args.compute_per_token)
     plans = [int(np.floor(q.context_tokens[i] * q.cache_hit_ratio[i] / 256)) for i in range(n)]
@@ -153,8 +162,9 @@ def main():
     num_pages = 40 * 1024  # 80 GiB of L1 (80 GB GPU of the paper's setup, SPEC defaults)
     l1 = ingest.PagedKVCache(shape, num_pages, max_rows=n + 1, max_chunks=max(plans) + 1)
     stage = LoadStage(l1, pool)
-    out = {"workload": f"configs[3]: {n} requests, 2K-128K prefixes (lognormal mean 24K, cv 1.0), hit in "
-                       f"{{0.25,0.5,0.75,0.9,1.0}}, Llama-3.1-8B KV, L1 {num_pages * shape.page_bytes / 2**30:.0f} GiB",
+    desc = (f"{n} requests of {args.uniform.split(':')[0]} tokens at hit {args.uniform.split(':')[1]}" if args.uniform
+            else f"configs[3]: {n} requests, 2K-128K prefixes (lognormal mean 24K, cv 1.0), hit in {{0.25,0.5,0.75,0.9,1.0}}")
+    out = {"workload": f"{desc}, Llama-3.1-8B KV, L1 {num_pages * shape.page_bytes / 2**30:.0f} GiB",
            "chunks": int(sum(plans)), "bytes": int(sum(plans) * shape.local_chunk_bytes), "ingest_mode": args.mode,
            "k2_ctas": args.k2_ctas or 148 * 32, "staging_mib": args.staging_mib or 1024,
            "max_connections": os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "default")}
