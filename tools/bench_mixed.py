@@ -250,9 +250,11 @@ def main():
             # the real consumer's own cost: fit (compute tokens, prefill seconds) of the serial run
             from paper_2603_21257_b200 import calibrate
 
-            fit = t.fit_linear((x.tokens, x.seconds) for x in calibrate.compute_samples(runs["serial_prefill"]["_req"]))
-            out["sim_vs_real_calibrated"] = {"mode": "DES with T_comp fitted to this run's prefills (fit_linear)",
-                                             **des(fit.model.intercept, fit.model.slope)}
+            samples = calibrate.compute_samples(runs["serial_prefill"]["_req"])
+            if len({x.tokens for x in samples}) > 1:  # a uniform batch has one token count: no fit
+                fit = t.fit_linear((x.tokens, x.seconds) for x in samples)
+                out["sim_vs_real_calibrated"] = {"mode": "DES with T_comp fitted to this run's prefills (fit_linear)",
+                                                 **des(fit.model.intercept, fit.model.slope)}
     print(json.dumps(out), flush=True)
 
 
