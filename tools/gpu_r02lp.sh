@@ -4,7 +4,8 @@
 set -u
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-for u in 32768:0.9 65536:0.95 131072:0.98 16384:0.8; do
-  tag=$(echo $u | tr ':.' '__')
-  timeout 900 python tools/bench_mixed.py --consumer real --n 12 --uniform $u > gpurun_out/lp_real_${tag}.json 2> gpurun_out/lp_real_${tag}.err; echo "real $u rc=$?"
+for spec in 12:32768:0.97 12:32768:0.98 8:65536:0.985 12:32768:0.9 8:131072:0.98; do
+  n=${spec%%:*}; u=${spec#*:}
+  tag=$(echo $spec | tr ':.' '__')
+  timeout 900 python tools/bench_mixed.py --consumer real --n $n --uniform $u > gpurun_out/lp2_real_${tag}.json 2> gpurun_out/lp2_real_${tag}.err; echo "real $spec rc=$?"
 done
