@@ -74,6 +74,19 @@ class PagedPrefill:
                            torch.zeros(1, dtype=torch.int32, pin_memory=True)) for _ in range(wrappers)]
         self.slot_of = {}
         self.next = 0
+        # With a wrapper per request the attention is planned here, before any ingest: a plan
+        # uploads its metadata with small host-to-device copies, and issued during the run those
+        # copies queue behind the bulk KV copies on the copy engine -- the request's prefill could
+        # not start before its last layer landed, defeating the per-layer fences
+        # (repo:profiles/r02_layer_pipelining.jsonl).  The page list is then a device buffer that
+        # layer 0 fills from the device block table with a kernel, no copy engine involved.
+        self.bt_dev = l1.block_table_device()
+        self.preplanned = queue.n <= wrappers
+        if self.preplanned:
+            for i in range(queue.n):
+                if self.nb[i] > 0:
+                    self._plan_static(i, i)
+            torch.cuda.synchronize(dev)
         self.flops = 0.0
         self.calls = 0
         self.host_s = 0.0       # host time spent inside the hook (enqueueing)
@@ -87,6 +100,16 @@ class PagedPrefill:
         gemm = 2 * ct * (hidden * self.w_qkv.shape[1] + self.w_o.shape[0] * hidden + hidden * 2 * inter + inter * hidden)
         attn = 4 * ct * kv * self.Hq * self.D
         return float(self.l1.shape.layers * (gemm + attn))
+
+    def _plan_static(self, q_index: int, k: int):
+        """Plan request q_index on wrapper k with dev_pages[k] as its page list (filled later)."""
+        n_pages = self.nb[q_index] * self.l1.shape.pages_per_chunk
+        qo, kvp, last = self.host_meta[k]
+        qo[1], kvp[1], last[0] = self.ct[q_index], n_pages, self.l1.shape.page_tokens
+        self.wrappers[k].plan(qo, kvp, self.dev_pages[k][:n_pages], last, self.Hq, self.Hkv, self.D,
+                              self.l1.shape.page_tokens, causal=False, q_data_type=torch.bfloat16,
+                              kv_data_type=torch.bfloat16)
+        self.slot_of[q_index] = k
 
     def _plan(self, q_index: int, bt_row: int):
         k = self.next % len(self.wrappers)
@@ -121,7 +144,12 @@ class PagedPrefill:
                 return
             if layer == 0 and self.nb[q_index] > 0:
                 t0 = time.perf_counter()
-                self._plan(q_index, bt_row)
+                if self.preplanned:  # the request's pages, device block table -> its page list
+                    n_pages = self.nb[q_index] * self.l1.shape.pages_per_chunk
+                    k = self.slot_of[q_index]
+                    torch.add(self.bt_dev[bt_row, :n_pages], 0, out=self.dev_pages[k][:n_pages])
+                else:
+                    self._plan(q_index, bt_row)
                 self.plan_s += time.perf_counter() - t0
             x = self.x[:ct]
             qkv = x @ self.w_qkv
@@ -140,7 +168,7 @@ class PagedPrefill:
                 gu = hb @ self.w_gu
                 a = torch.nn.functional.silu(gu[:, :inter]) * gu[:, inter:]
                 hb.copy_(a @ self.w_down)
-            if layer == self.l1.shape.layers - 1 and self.nb[q_index] > 0:
+            if layer == self.l1.shape.layers - 1 and self.nb[q_index] > 0 and not self.preplanned:
                 ev = torch.cuda.Event()
                 ev.record(stream)
                 self.done[self.slot_of[q_index]] = ev

@@ -287,6 +287,17 @@ class PagedKVCache:
     def sync_block_table(self, stream=None):
         check(lib.tsb_l1_sync_block_table(self._h, _stream(stream)))
 
+    def block_table_device(self) -> torch.Tensor:
+        """The device block table [max_rows, stride] int32 (a view; rows are uploaded by
+        sync_block_table / the load stage ahead of the ingest that reads them)."""
+        ptr = lib.tsb_l1_block_table_device(self._h)
+
+        class _View:  # __cuda_array_interface__ over memory the L1 object owns
+            __cuda_array_interface__ = {"shape": (self.max_rows, self.stride), "typestr": "<i4",
+                                        "data": (ptr, False), "version": 3, "strides": None}
+
+        return torch.as_tensor(_View(), device=torch.device("cuda", self.device))
+
     def layer(self, layer: int, dtype=torch.bfloat16) -> torch.Tensor:
         """One layer in the consumer's layout: flash-attn [2, pages, P, H_local, D]; FlashInfer NHD
         [pages, 2, P, H_local, D]; FlashInfer HND [pages, 2, H_local, P, D]."""
