@@ -30,7 +30,7 @@ from .tiersim import ClusterConfig, QueueArrays
 class PagedPrefill:
     def __init__(self, l1: PagedKVCache, queue: QueueArrays, config: ClusterConfig, hidden: int = 4096,
                  q_heads: int = 32, intermediate: int = 14336, token_block: int = 8192, wrappers: int = 0,
-                 seed: int = 0):
+                 seed: int = 0, preplan: Optional[bool] = None):
         import flashinfer
 
         self.l1, self.queue, self.config = l1, queue, config
@@ -81,7 +81,7 @@ class PagedPrefill:
         # (repo:profiles/r02_layer_pipelining.jsonl).  The page list is then a device buffer that
         # layer 0 fills from the device block table with a kernel, no copy engine involved.
         self.bt_dev = l1.block_table_device()
-        self.preplanned = queue.n <= wrappers
+        self.preplanned = queue.n <= wrappers if preplan is None else (preplan and queue.n <= wrappers)
         if self.preplanned:
             for i in range(queue.n):
                 if self.nb[i] > 0:

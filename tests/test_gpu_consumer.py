@@ -78,11 +78,14 @@ def test_flashinfer_paged_decode_reads_ingested_pages(mode, layout):
             torch.testing.assert_close(out[b].float(), want, atol=2e-2, rtol=2e-2)
 
 
+@pytest.mark.parametrize("preplan", [True, False])
 @pytest.mark.parametrize("layout", ["flash_attn", "flashinfer_nhd"])
-def test_real_prefill_consumer_as_stage_hook(layout):
+def test_real_prefill_consumer_as_stage_hook(layout, preplan):
     """PagedPrefill (FlashInfer paged prefill + bf16 GEMMs per layer) runs as the stage's prefill
     hook, gated on per-layer fences: every page is verified, the consumer's last-layer attention
-    equals attention over the source chunks, and ComputeDone follows residency."""
+    equals attention over the source chunks, and ComputeDone follows residency.  preplan: attention
+    planned before the run with the page list filled on device from the device block table (the
+    default when every request has a wrapper), or planned at layer 0 from the host mirror."""
     pytest.importorskip("flashinfer")
     from paper_2603_21257_b200.consumer import PagedPrefill
     from paper_2603_21257_b200.stage import LoadStage
@@ -96,10 +99,14 @@ def test_real_prefill_consumer_as_stage_hook(layout):
                       cache_hit_ratio=[1.0], flags=np.zeros(1, np.uint8))
     slots = [[3, 9, 4, 0, 12, 7]]
     stage = LoadStage(l1, pool)
-    cons = PagedPrefill(l1, q, cfg, hidden=1024, intermediate=2048, wrappers=2)
+    cons = PagedPrefill(l1, q, cfg, hidden=1024, intermediate=2048, wrappers=2, preplan=preplan)
+    assert cons.preplanned == preplan
     stage.set_prefill_hook(cons)
     res = stage.run(q, slots, cfg, prefill=True, layer_events=True, verify_seed=11)
     assert res.stats["verify_mismatches"] == 0 and cons.calls == shape.layers
+    l1.sync_block_table()  # rows released at ComputeDone reach the device copy
+    torch.cuda.synchronize()
+    assert torch.equal(l1.block_table_device().cpu(), torch.from_numpy(l1.block_table().copy()))
     r = res.requests
     assert r["done_ms"][0] >= r["resident_ms"][0] >= r["first_layer_ms"][0]
     # the consumer's last layer: o = attention(q, cached K/V of layer L-1) -- against the source chunks
