@@ -23,10 +23,13 @@ from .tiersim import (ClusterConfig, CostModelPair, LinearCostModel, LinearFit, 
 
 
 def ingest_samples(requests: np.ndarray) -> list[TokenSample]:
-    """(cached tokens, seconds of the request's L2 -> L1 hops) per request that moved chunks."""
+    """(cached tokens, seconds of the request's L2 -> L1 hops) per request that moved chunks.
+    Requests with a deferred chunk reservation are left out: their span from first hop to
+    residency includes the wait for pages that a release granted later, which the reference
+    models as TierLedger deferral (engine.cpp:38-49), not as transfer time (engine.cpp:206-207)."""
     out = []
     for r in requests:
-        if r["chunks"] > 0:
+        if r["chunks"] > 0 and r["deferred_chunks"] == 0:
             out.append(TokenSample(int(r["cached_tokens"]), float(r["resident_ms"] - r["ingest_begin_ms"]) * 1e-3))
     return out
 

@@ -44,7 +44,8 @@ def test_fit_of_csv_samples_equals_reference(tmp_path, ref_lib):
 
 def test_calibration_from_stage_requests(tmp_path):
     """The request rows a stage run returns -> CSVs -> fitted models (no device: synthetic rows)."""
-    dt = np.dtype([("pick_position", np.int32), ("chunks", np.int64), ("cached_tokens", np.int64), ("compute_tokens", np.int64),
+    dt = np.dtype([("pick_position", np.int32), ("deferred_chunks", np.int32), ("chunks", np.int64),
+                   ("cached_tokens", np.int64), ("compute_tokens", np.int64),
                    ("ingest_begin_ms", np.float64), ("resident_ms", np.float64), ("done_ms", np.float64)])
     n = 40
     rows = np.zeros(n, dt)
@@ -55,6 +56,9 @@ def test_calibration_from_stage_requests(tmp_path):
     rows["ingest_begin_ms"] = np.arange(n) * 100.0
     rows["resident_ms"] = rows["ingest_begin_ms"] + (2.4e-6 * rows["cached_tokens"] + 5e-4) * 1e3
     rows["pick_position"] = np.arange(n)
+    # a request whose reservation waited for a release: its span includes the wait, not a T_load sample
+    rows["deferred_chunks"][3] = 5
+    rows["resident_ms"][3] += 500.0
     # prefills queue on one compute stream: request k starts at max(resident_k, done_{k-1})
     prev = 0.0
     for k in range(n):
@@ -70,4 +74,4 @@ def test_calibration_from_stage_requests(tmp_path):
     assert abs(cal.models.load.slope - 2.4e-6) / 2.4e-6 < 1e-9 and abs(cal.models.load.intercept - 5e-4) < 1e-12
     assert abs(cal.models.comp.slope - 1e-5) / 1e-5 < 1e-9 and abs(cal.models.comp.intercept - 2e-3) < 1e-12
     assert cal.default.load.slope == t.cost_models_from_config(cfg).load.slope
-    assert len(t.read_samples_csv(cal.load_csv)) == int((rows["chunks"] > 0).sum())
+    assert len(t.read_samples_csv(cal.load_csv)) == int(((rows["chunks"] > 0) & (rows["deferred_chunks"] == 0)).sum())

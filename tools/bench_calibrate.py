@@ -95,7 +95,11 @@ def main():
                    "comp": {"slope": cal.models.comp.slope, "intercept": cal.models.comp.intercept}},
            "default": {"load": {"slope": cal.default.load.slope, "intercept": cal.default.load.intercept},
                        "comp": {"slope": cal.default.comp.slope, "intercept": cal.default.comp.intercept}},
-           "samples_csv": [cal.load_csv, cal.comp_csv]}
+           "samples_csv": [cal.load_csv, cal.comp_csv],
+           "load_samples": {"used": sum(int(((r.requests["chunks"] > 0) & (r.requests["deferred_chunks"] == 0)).sum())
+                                        for r in cal_runs),
+                            "left_out_deferred": sum(int(((r.requests["chunks"] > 0) & (r.requests["deferred_chunks"] > 0)).sum())
+                                                     for r in cal_runs)}}
     # 2. static orders under both models
     sc = BatchScorer(0)
     orders = {}
