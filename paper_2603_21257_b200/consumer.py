@@ -56,12 +56,13 @@ class PagedPrefill:
         self.o_buf = torch.empty_like(self.q_buf)
         layout = "HND" if l1.layout == LAYOUT_FLASHINFER_HND else "NHD"
         self.kv_tuple = l1.layout == LAYOUT_FLASH_ATTN
-        # A ring of wrappers: each holds one request's plan (host pinned staging + device
-        # metadata); a wrapper is re-planned only after the prefill that used it has finished.
-        # Default: one per request up to 32, so planning never waits on the GPU.
-        wrappers = wrappers or max(2, min(32, queue.n))
-        self.wrappers = [flashinfer.BatchPrefillWithPagedKVCacheWrapper(
-            torch.empty(128 << 20, dtype=torch.uint8, device=dev), layout) for _ in range(wrappers)]
+        # A wrapper per request up to 128 (each holds one request's plan: 8 MiB of device and of
+        # pinned metadata); beyond that a ring whose wrappers are re-planned once the prefill that
+        # used them has finished.  The 128 MiB split-k float workspace is shared: every run is
+        # serialized on the one compute stream.
+        wrappers = wrappers or max(2, min(128, queue.n))
+        self.float_ws = torch.empty(128 << 20, dtype=torch.uint8, device=dev)
+        self.wrappers = [flashinfer.BatchPrefillWithPagedKVCacheWrapper(self.float_ws, layout) for _ in range(wrappers)]
         self.done = [None] * wrappers
         # per wrapper: pinned staging of the page list (copied async) + host indptr tensors; all
         # reused only after the prefill that used them has finished, so nothing here syncs the
