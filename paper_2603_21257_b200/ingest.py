@@ -289,7 +289,8 @@ class PagedKVCache:
 
     def block_table_device(self) -> torch.Tensor:
         """The device block table [max_rows, stride] int32 (a view; rows are uploaded by
-        sync_block_table / the load stage ahead of the ingest that reads them)."""
+        sync_block_table / the load stage ahead of the ingest that reads them).  The view aliases
+        memory the L1 owns: keep this PagedKVCache alive while it is used."""
         ptr = lib.tsb_l1_block_table_device(self._h)
 
         class _View:  # __cuda_array_interface__ over memory the L1 object owns
