@@ -962,8 +962,8 @@ tsb_status ingest_ce(tsb_l1* l, tsb_pool* pool, const tsb_ingest_item* items_dev
 // merge into one run, and runs that advance by constant strides on both sides (a document's
 // chunks in consecutive slots on consecutive pages) merge into one 2D copy per (layer, K|V).
 // A lone run moves K and V (y, pitch = the K|V stride) of every layer up to the next requested
-// fence (z, slice = the layer stride) in one 3D copy.  The batched-memcpy entry points are closed on this pool
-// (they raised GPU faults); copies are plain per-call cudaMemcpy3DAsync / cudaMemcpyAsync.
+// fence (z, slice = the layer stride) in one 3D copy.  The batched-memcpy entry points are closed
+// on this GPU pool (they raised GPU faults), so every copy is a plain per-call 2D / 3D / 1D copy.
 bool ce_direct_ok(const tsb_l1* l, const tsb_pool* pool) {
   return pool->location == TSB_POOL_HOST && l->shape.tp_size == 1 && l->layout != TSB_LAYOUT_FLASHINFER_HND;
 }

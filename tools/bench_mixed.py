@@ -76,9 +76,9 @@ def stage_overlap(req, layer_events):
 
 
 def timeline_summary(prof, path):
-    """From a kineto (CUPTI) trace of one overlapped run: busy time of the ingest kernels (K2; the
-    batched host->device copies are not reported as memcpy activity by CUPTI), of the prefill
-    kernels, the ingest window [first K2 start, last K2 end], and how much prefill ran inside it."""
+    """From a kineto (CUPTI) trace of one overlapped run: busy time of the ingest kernels (K2), of
+    the host->device copies, of the prefill kernels, the ingest window [first K2 start, last K2 end],
+    and how much prefill ran inside it."""
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
     spans = {"ingest": [], "prefill": [], "memcpy": []}
     for e in ev:
