@@ -52,6 +52,9 @@ def main():
     ap.add_argument("--l1-gib", type=int, default=24)
     ap.add_argument("--compute-per-token", type=float, default=4e-6)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--consumer", choices=["k6", "real"], default="k6",
+                    help="real: PagedPrefill (FlashInfer paged prefill + Llama-8B GEMMs) as the prefill hook; "
+                         "the DES then uses T_comp fitted to a serial batch pass of the same consumer")
     args = ap.parse_args()
     import pyoracle as po
 
@@ -79,10 +82,23 @@ def main():
     stage.run(q, cal_slots, base)
     r = stage.run(q, cal_slots, base)
     link = r.stats["bytes"] / (r.requests["resident_ms"].max() * 1e-3)
+    comp_base, comp_tok, compute_desc = 2e-3, args.compute_per_token, f"K6 {args.compute_per_token:g} s/token + 2 ms"
+    if args.consumer == "real":
+        from paper_2603_21257_b200 import calibrate
+        from paper_2603_21257_b200.consumer import PagedPrefill
+
+        consumer = PagedPrefill(l1, q, base)
+        stage.set_prefill_hook(consumer)
+        stage.run(q, cal_slots, base, prefill=True)  # JIT + warm-up
+        fit = t.fit_linear((x.tokens, x.seconds) for x in
+                           calibrate.compute_samples(stage.run(q, cal_slots, base, prefill=True).requests))
+        comp_base, comp_tok = fit.model.intercept, fit.model.slope
+        compute_desc = (f"PagedPrefill (FlashInfer + Llama-3.1-8B GEMMs); DES T_comp fitted: {comp_tok:.3e} s/token + "
+                        f"{comp_base * 1e3:.2f} ms")
     stage.set_l3(l3, copy_threads=8)
     box = t.ClusterConfig(bytes_per_token=bpt, l1_capacity=num_pages * shape.page_bytes,
-                          l2_capacity=args.l2_slots * shape.chunk_bytes, compute_base=2e-3,
-                          compute_per_token=args.compute_per_token, network_bandwidth=args.net_gbps * 1e9,
+                          l2_capacity=args.l2_slots * shape.chunk_bytes, compute_base=comp_base,
+                          compute_per_token=comp_tok, network_bandwidth=args.net_gbps * 1e9,
                           pcie_bandwidth=link)
     t.assign_slos_queue(q, box, [2.0, 4.0, 8.0], 7)
     dl = q.deadline - q.arrival
@@ -90,7 +106,7 @@ def main():
                        "{0.25,0.5,0.75,1.0}, contexts capped at 64K, 6 shared documents in L3, Llama-3.1-8B KV",
            "tiers": {"l3_to_l2": f"host copy threads paced to {args.net_gbps} GB/s", "l2_slots": args.l2_slots,
                      "l1_gib": args.l1_gib, "l2_to_l1_measured_GBps": link / 1e9},
-           "compute": f"K6 {args.compute_per_token:g} s/token + 2 ms", "runs": {}}
+           "compute": compute_desc, "runs": {}}
     first = True
     for control in (t.ControlMode.Decoupled, t.ControlMode.Coupled):
         for pol in (t.PolicyKind.Fifo, t.PolicyKind.SjfCost, t.PolicyKind.Edf, t.PolicyKind.Lstf):
