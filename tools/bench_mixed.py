@@ -42,10 +42,12 @@ def mixed_batch(n, seed, block=256):
 
 def stage_overlap(req, layer_events):
     """Device-clock spans from the stage's own CUDA events: ingest of request k is
-    [ingest_begin, resident]; its prefill runs on the one compute stream after the previous prefill,
-    from its first layer (layer-pipelined) or its residency (serial) to done.  Reports how long the
-    link and the prefill were busy at the same time, and how many prefills began before their own
-    request was fully resident (layer pipelining at work)."""
+    [ingest_begin, resident]; its prefill window is taken from the earliest it may start (its first
+    layer when layer-pipelined, its residency when serial, and not before the previous prefill's
+    end) to done.  Reports how long the link and those windows overlap, and how many requests were
+    eligible to start prefill before they were fully resident.  These are inferred from the fences,
+    not observed: whether prefill kernels actually ran early shows in the kineto timeline (--profile)
+    and in the TTFT itself."""
     def union(iv):
         out = []
         for a, b in sorted(iv):
@@ -71,7 +73,7 @@ def stage_overlap(req, layer_events):
         for c, d in up:
             both += max(0.0, min(b, d) - max(a, c))
     return {"link_busy_ms": sum(b - a for a, b in ui), "prefill_busy_ms": sum(b - a for a, b in up),
-            "link_and_prefill_concurrent_ms": both, "prefills_started_before_own_residency": early,
+            "link_and_prefill_concurrent_ms": both, "prefills_eligible_before_own_residency": early,
             "source": "stage CUDA events (ingest_begin / first_layer / resident / done per request)"}
 
 
