@@ -47,10 +47,12 @@ cudaError_t launch_ingest_ldg(const IngestGeom& g, const uint8_t* src, uint8_t* 
 // [slot][L][2][C]) and this rank's first head (HND maps) or first u64 column (NHD maps).
 constexpr int kBulkSmem = 200 * 1024;
 constexpr int kTmaMaxStages = 16;
-// Ring depth per CTA: ~96 KiB of segments (6..16 stages, within kBulkSmem), so small head-shard
-// segments run 2-3 rings per SM and full-head 32 KiB segments one 6-deep ring.
+// Ring depth per CTA: ~96 KiB of segments (6..16 stages, within kBulkSmem), ~64 KiB for head-
+// shard segments of <= 8 KiB so three rings share an SM (TP4's 8 KiB segments: 0.876 -> 0.902
+// of HBM, TP8 unchanged; repo:profiles/r02_k1b_ring_sweep.jsonl).  Full-head 32 KiB segments run
+// one 6-deep ring per SM.
 inline int tma_ring_stages(int64_t seg_bytes) {
-  int64_t st = 98304 / seg_bytes;
+  int64_t st = (seg_bytes <= 8192 ? 65536 : 98304) / seg_bytes;
   st = st < 6 ? 6 : st > kTmaMaxStages ? kTmaMaxStages : st;
   while (st > 2 && st * seg_bytes > kBulkSmem) --st;
   return static_cast<int>(st);
