@@ -1,5 +1,6 @@
 #!/bin/bash
 # Round 2: K1b ring size (bytes of segment buffers per CTA ring; CTAs per SM follow) over the
+# (TSB_K1B_RING was a one-off switch in kernels.h, removed once 64 KiB rings for <= 8 KiB segments shipped)
 # peer-tier shapes -- default 96 KiB vs 64 / 48 / 128 KiB.
 set -u
 mkdir -p gpurun_out
