@@ -761,7 +761,9 @@ tsb::IngestGeom make_geom(const tsb_l1* l, int64_t layer_lo, int64_t layer_hi) {
     g.page_dst = 2 * g.seg_bytes;
   }
   g.head_bytes = s.head_dim * s.dtype_bytes;
-  g.hnd = l->layout == TSB_LAYOUT_FLASHINFER_HND ? 1 : 0;
+  // With one local head, HND pages [2][1][P][D] are byte-identical to NHD [2][P][1][D]: take the
+  // NHD addressing (contiguous page planes; K1 / K1b / K2 skip the per-row head transpose).
+  g.hnd = l->layout == TSB_LAYOUT_FLASHINFER_HND && Hl > 1 ? 1 : 0;
   g.bt_stride = l->stride;
   g.layer_lo = static_cast<int32_t>(layer_lo);
   g.n_layers = static_cast<int32_t>(layer_hi - layer_lo);
