@@ -46,21 +46,20 @@ __device__ __forceinline__ SegAddr seg_addr(const IngestGeom& g, const uint8_t* 
   return a;
 }
 
-// Destination byte offset of 16-byte vector v of a segment (P token rows of vpr vectors): NHD
-// pages keep the source order; HND pages ([H_local][P][D]) move each head's row of token t to
-// head * P * D*E + t * D*E.
-template <bool kHnd>
-__device__ __forceinline__ int64_t seg_dst_off(const IngestGeom& g, int v, int vpr, int vph) {
-  if (!kHnd) return static_cast<int64_t>(v) * 16;
-  // 32-bit index math (64-bit division would dominate the store path): vph = vectors per head row
-  const int t = v / vpr, c = v - t * vpr;
-  const int h = c / vph, w = c - h * vph;
-  return (static_cast<int64_t>(h) * g.P + t) * g.head_bytes + w * 16;
-}
-
 // K1 / K2: one warp per segment, 16-byte streaming loads, U loads in flight per lane before
 // the stores.  Source may be mapped host memory (K1, zero-copy over PCIe) or an HBM staging
-// buffer (K2).
+// buffer (K2).  NHD pages keep the source order.  HND pages ([H_local][P][D]) are walked in
+// destination order: the stores are contiguous and the loads gather each head's row of token t
+// (walking in source order with transposed stores measured 0.93 of HBM at TP2/TP4 vs 0.95-0.96,
+// repo:profiles/r02_k1_hnd_walk.jsonl).
+__device__ __forceinline__ int64_t hnd_src_off(const IngestGeom& g, int v, int vph) {
+  // destination order [h][t][w] -> source [t][h][w] (32-bit index math)
+  const int per_head = static_cast<int>(g.P) * vph;
+  const int h = v / per_head, rem = v - h * per_head;
+  const int t = rem / vph, w = rem - t * vph;
+  return static_cast<int64_t>(t) * g.row + static_cast<int64_t>(h) * g.head_bytes + w * 16;
+}
+
 template <bool kContig, int U, bool kHnd>
 __global__ void __launch_bounds__(256) k_ingest_ldg(IngestGeom g, const uint8_t* __restrict__ src,
                                                     uint8_t* __restrict__ arena,
@@ -82,15 +81,16 @@ __global__ void __launch_bounds__(256) k_ingest_ldg(IngestGeom g, const uint8_t*
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32;
         if (v < nvec) {
-          const int64_t off = kContig ? static_cast<int64_t>(v) * 16
-                                      : (v / vpr) * g.row + (v % vpr) * 16;
+          const int64_t off = kHnd      ? hnd_src_off(g, v, vph)
+                              : kContig ? static_cast<int64_t>(v) * 16
+                                        : (v / vpr) * g.row + (v % vpr) * 16;
           buf[u] = ld_stream(a.src + off);
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32;
-        if (v < nvec) st_stream(a.dst + seg_dst_off<kHnd>(g, v, vpr, vph), buf[u]);
+        if (v < nvec) st_stream(a.dst + static_cast<int64_t>(v) * 16, buf[u]);
       }
     }
   }
