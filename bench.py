@@ -21,7 +21,8 @@ data-path collective).  Without torchrun, --gpus N > 1 launches the N ranks itse
   hbm_tier : the same step with the pool held in HBM (the peer-HBM tier's K1 path), not the
              headline
   workloads: driver-visible lines for configs[0] (Llama-8B 32K), configs[2] (70B, rank 0 of a
-             tp 1/2/4/8 head split on this GPU) and configs[4] (100K-request scorer + hasher)
+             tp 1/2/4/8 head split on this GPU), configs[3] (mixed trace, K6 prefill), the real
+             consumer's layer pipelining (f1) and configs[4] (100K-request scorer + hasher)
   cpu_baseline : the oracle's scatter_ref (port) on the host cores, bounded sample (rank 0, N=1)
 """
 from __future__ import annotations
