@@ -1,7 +1,7 @@
 """Small, single-purpose workloads for ncu (one GPU, short):  python tools/prof_targets.py <what>
 
 what: scorer | hash | index | ingest-ce | ingest-bulk | ingest-zerocopy | ingest-tp8 | ingest-hbm | ingest-hbm-tp8 |
-      bulk-hbm | bulk-hbm-tp8 | bulk-hbm-tp8-hnd | ingest-ce-direct
+      bulk-hbm | bulk-hbm-tp8 | bulk-hbm-tp8-hnd | ingest-ce-direct | ingest-hbm-tp4-hnd
 """
 from __future__ import annotations
 
@@ -50,11 +50,11 @@ def ingest_hbm_bulk(shape, n_chunks, layout=0, reps=2):
     assert ingest.verify_synthetic(l1, pool, items, 3) == 0
 
 
-def ingest_hbm(shape, n_chunks, reps=2):
+def ingest_hbm(shape, n_chunks, reps=2, layout=0):
     """K1 over an HBM-resident pool as the stage issues it: layer 0 alone, then layers [1, L)."""
     pool = ingest.ChunkPool.create_device(shape, n_chunks)
     pool.fill_synthetic(3)
-    l1 = ingest.PagedKVCache(shape, n_chunks * shape.pages_per_chunk, 1, n_chunks)
+    l1 = ingest.PagedKVCache(shape, n_chunks * shape.pages_per_chunk, 1, n_chunks, layout=layout)
     cb = shape.page_bytes * shape.pages_per_chunk
     for c in range(n_chunks):
         g, row = l1.request(1, c, cb)
@@ -111,5 +111,7 @@ if __name__ == "__main__":
         ingest_once(ingest.LLAMA31_8B, 128, ingest.CE_DIRECT)
     elif what == "ingest-hbm-tp8":
         ingest_hbm(ingest.LLAMA3_70B.with_rank(8, 7), 128)
+    elif what == "ingest-hbm-tp4-hnd":
+        ingest_hbm(ingest.LLAMA3_70B.with_rank(4, 1), 128, layout=ingest.LAYOUT_FLASHINFER_HND)
     else:
         raise SystemExit(__doc__)
