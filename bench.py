@@ -556,8 +556,6 @@ def side_workloads(torch, args, ce_peak, hbm_peak, seed, device):
     except Exception as e:  # noqa: BLE001  the third-party consumer (FlashInfer JIT) failed: no
         # fallback, the sub-line reports why and the contract line stands
         out["layer_pipelining"] = {"skipped": f"real consumer unavailable: {type(e).__name__}: {e}"}
-        torch.cuda.synchronize()
-        torch.cuda.empty_cache()
     out["queue100k"] = queue_workload(torch, hbm_peak)
     return out
 
